@@ -1,0 +1,80 @@
+// Shared helpers for libairg (B200 / sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <cstdarg>
+#include <cmath>
+#include "../../include/airg.h"
+
+namespace airg {
+
+// Thread-local last-error text, surfaced by airg_last_error().
+void set_error(const char* fmt, ...);
+
+#define AIRG_CUDA(call)                                                          \
+  do {                                                                           \
+    cudaError_t _e = (call);                                                     \
+    if (_e != cudaSuccess) {                                                     \
+      ::airg::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call,              \
+                        cudaGetErrorString(_e));                                 \
+      return AIRG_ERR_CUDA;                                                      \
+    }                                                                            \
+  } while (0)
+
+#define AIRG_LAUNCH_CHECK()                                                      \
+  do {                                                                           \
+    cudaError_t _e = cudaGetLastError();                                         \
+    if (_e != cudaSuccess) {                                                     \
+      ::airg::set_error("%s:%d launch: %s", __FILE__, __LINE__,                  \
+                        cudaGetErrorString(_e));                                 \
+      return AIRG_ERR_CUDA;                                                      \
+    }                                                                            \
+  } while (0)
+
+#define AIRG_TRY(call)                                                           \
+  do {                                                                           \
+    int _s = (call);                                                             \
+    if (_s != AIRG_OK) return _s;                                                \
+  } while (0)
+
+constexpr int kNumSMs = 148;
+
+inline int blocks_for(long long n, int threads, long long cap = 148LL * 64) {
+  long long b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return (int)b;
+}
+
+// Exact (non-contracted) fp64 arithmetic: scipy's sparsetools and numpy
+// accumulate with separate multiply and add roundings.
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v, unsigned mask = 0xffffffffu) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Scratch memory from the stream-ordered pool (freed by the caller of alloc).
+template <typename T>
+inline int scratch(T** p, size_t count, cudaStream_t s) {
+  if (count == 0) count = 1;
+  AIRG_CUDA(cudaMallocAsync((void**)p, count * sizeof(T), s));
+  return AIRG_OK;
+}
+inline void release(void* p, cudaStream_t s) {
+  if (p) cudaFreeAsync(p, s);
+}
+
+}  // namespace airg

@@ -1,0 +1,945 @@
+// Solve-path kernels: SpMV family with fused epilogues, polynomial apply
+// (Horner / Neumann / factored Newton), the V-cycle plan and the Richardson
+// driver.  ref: /root/reference/pkg/src/airmg/solve.py:89-167,
+// polynomial.py:295-369, sparse.py:206-212.
+#include "airg_common.cuh"
+#include <vector>
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <mutex>
+
+namespace airg {
+
+static thread_local std::string g_err;
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+// ---------------------------------------------------------------------------
+// SpMV with a fused epilogue:
+//   out[omap ? omap[i] : i] = alpha * (A (xs*x))_i + beta * v[vmap ? vmap[i] : i]
+//   (+ optional out2[omap..] += same value, + optional sum of squares)
+// VS lanes cooperate on one row (VS = 1 .. 32).
+// ---------------------------------------------------------------------------
+struct Epi {
+  double* out;
+  const int* omap;
+  double alpha;
+  double beta;
+  const double* v;  // may be null
+  const int* vmap;
+  double* acc;      // optional: acc[o] += value
+  double* partial;  // optional: per-block sum of squares of value
+};
+
+template <int VS>
+__global__ void __launch_bounds__(256) spmv_vec_kernel(int nrows, const int* __restrict__ ptr,
+                                                       const int* __restrict__ col,
+                                                       const double* __restrict__ val,
+                                                       const double* __restrict__ x, double xs,
+                                                       Epi ep) {
+  const int lane = threadIdx.x & (VS - 1);
+  const long long row = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / VS;
+  double s = 0.0;
+  if (row < nrows) {
+    const int b = __ldg(ptr + row), e = __ldg(ptr + row + 1);
+    int k = b + lane;
+    // two independent accumulators for MLP on long rows
+    double s2 = 0.0;
+    for (; k + VS < e; k += 2 * VS) {
+      s = fma(__ldg(val + k), xs * __ldg(x + __ldg(col + k)), s);
+      s2 = fma(__ldg(val + k + VS), xs * __ldg(x + __ldg(col + k + VS)), s2);
+    }
+    if (k < e) s = fma(__ldg(val + k), xs * __ldg(x + __ldg(col + k)), s);
+    s += s2;
+  }
+  if (VS > 1) {
+#pragma unroll
+    for (int o = VS / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  }
+  double sq = 0.0;
+  if (lane == 0 && row < nrows) {
+    double r = ep.alpha * s;
+    if (ep.v) r = fma(ep.beta, ep.v[ep.vmap ? ep.vmap[row] : row], r);
+    const long long o = ep.omap ? ep.omap[row] : row;
+    if (ep.out) ep.out[o] = r;
+    if (ep.acc) ep.acc[o] += r;
+    sq = r * r;
+  }
+  if (ep.partial) {
+    __shared__ double red[32];
+    sq = warp_sum(sq);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      double t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+      t = warp_sum(t);
+      if (threadIdx.x == 0) ep.partial[blockIdx.x] = t;
+    }
+  }
+}
+
+// Bitwise scipy csr_matvec: s = 0; s = s + a*x (separate roundings) in column order.
+__global__ void spmv_exact_kernel(int nrows, const int* __restrict__ ptr,
+                                  const int* __restrict__ col, const double* __restrict__ val,
+                                  const double* __restrict__ x, double* __restrict__ y) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nrows;
+       i += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = ptr[i]; k < ptr[i + 1]; ++k) s = add_rn(s, mul_rn(val[k], x[col[k]]));
+    y[i] = s;
+  }
+}
+
+static int pick_vs(long long nnz, int nrows) {
+  double mean = nrows > 0 ? (double)nnz / nrows : 0.0;
+  if (mean <= 2.5) return 1;
+  if (mean <= 5) return 2;
+  if (mean <= 10) return 4;
+  if (mean <= 20) return 8;
+  if (mean <= 40) return 16;
+  return 32;
+}
+
+// Host-side launcher shared by every solve-path SpMV.
+struct Csr {
+  int nrows = 0, ncols = 0;
+  long long nnz = 0;
+  const int* ptr = nullptr;
+  const int* col = nullptr;
+  const double* val = nullptr;
+  int vs = 1;
+};
+
+static long long g_launches = 0;
+
+static int launch_spmv(const Csr& A, const double* x, double xs, const Epi& ep, cudaStream_t s) {
+  if (A.nrows == 0) return AIRG_OK;
+  const int threads = 256;
+  const long long groups = (long long)A.nrows * A.vs;
+  const int blocks = (int)((groups + threads - 1) / threads);
+#define AIRG_SPMV_CASE(V) \
+  case V: spmv_vec_kernel<V><<<blocks, threads, 0, s>>>(A.nrows, A.ptr, A.col, A.val, x, xs, ep); break;
+  switch (A.vs) {
+    AIRG_SPMV_CASE(1)
+    AIRG_SPMV_CASE(2)
+    AIRG_SPMV_CASE(4)
+    AIRG_SPMV_CASE(8)
+    AIRG_SPMV_CASE(16)
+    AIRG_SPMV_CASE(32)
+    default: set_error("bad vector width"); return AIRG_ERR_ARG;
+  }
+#undef AIRG_SPMV_CASE
+  ++g_launches;
+  AIRG_LAUNCH_CHECK();
+  return AIRG_OK;
+}
+
+static int spmv_blocks(const Csr& A) {
+  return (int)(((long long)A.nrows * A.vs + 255) / 256);
+}
+
+// out[omap(i)] = a * x[xmap(i)] + b * y[i]   (elementwise helpers)
+__global__ void axpby_kernel(long long n, double* __restrict__ out, const int* __restrict__ omap,
+                             double a, const double* __restrict__ x, const int* __restrict__ xmap,
+                             double b, const double* __restrict__ y) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double r = a * x[xmap ? xmap[i] : i];
+    if (y) r = fma(b, y[i], r);
+    out[omap ? omap[i] : i] = r;
+  }
+}
+
+static int launch_axpby(long long n, double* out, const int* omap, double a, const double* x,
+                        const int* xmap, double b, const double* y, cudaStream_t s) {
+  if (n == 0) return AIRG_OK;
+  axpby_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, out, omap, a, x, xmap, b, y);
+  ++g_launches;
+  AIRG_LAUNCH_CHECK();
+  return AIRG_OK;
+}
+
+// Neumann step: t_new = t - ds .* (A t); acc += t_new.
+__global__ void neumann_step_kernel(int n, const int* __restrict__ ptr, const int* __restrict__ col,
+                                    const double* __restrict__ val, const double* __restrict__ ds,
+                                    const double* __restrict__ t, double* __restrict__ tn,
+                                    double* __restrict__ acc) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = ptr[i]; k < ptr[i + 1]; ++k) s = fma(val[k], t[col[k]], s);
+    double v = t[i] - ds[i] * s;
+    tn[i] = v;
+    acc[i] += v;
+  }
+}
+
+// Deterministic sum of per-block partials -> sqrt into out[0].
+__global__ void finish_norm_kernel(int nparts, const double* __restrict__ parts,
+                                   double* __restrict__ out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += parts[i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) out[0] = sqrt(t);
+  }
+}
+
+__global__ void sumsq_kernel(long long n, const double* __restrict__ x, double* __restrict__ parts) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    s = fma(x[i], x[i], s);
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) parts[blockIdx.x] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Factored Newton application (polynomial.py:312-355) in ONE CTA: the
+// per-root max|u| rescale is a block-wide reduction, so the whole root
+// sequence runs without leaving the SM.  Vectors live in global memory
+// (L1/L2 resident for coarse grids); u, w, z, x are caller scratch.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double block_max(double v, double* red) {
+  v = warp_max(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    t = warp_max(t);
+    if (threadIdx.x == 0) red[32] = t;
+  }
+  __syncthreads();
+  double r = red[32];
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ double row_dot(const int* __restrict__ ptr, const int* __restrict__ col,
+                                          const double* __restrict__ val, const double* x, int i) {
+  double s = 0.0;
+  for (int k = ptr[i]; k < ptr[i + 1]; ++k) s = fma(val[k], x[col[k]], s);
+  return s;
+}
+
+__global__ void __launch_bounds__(1024) newton_cta_kernel(
+    int n, const int* __restrict__ ptr, const int* __restrict__ col, const double* __restrict__ val,
+    const double* __restrict__ b, double* x, double* u, double* w, double* z, int nunits,
+    const int* __restrict__ utype, const double* __restrict__ up1, const double* __restrict__ up2) {
+  __shared__ double red[33];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    u[i] = b[i];
+    x[i] = 0.0;
+  }
+  __syncthreads();
+  double scale = 1.0;
+  for (int k = 0; k < nunits; ++k) {
+    double lmax = 0.0;
+    if (utype[k] == 0) {
+      const double t = up1[k];
+      const double sc = scale / t;
+      int bad = 0;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) bad |= !isfinite(sc * u[i]);
+      if (__syncthreads_or(bad)) break;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] = row_dot(ptr, col, val, u, i);
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double ui = u[i];
+        x[i] += sc * ui;
+        const double un = ui - w[i] / t;
+        u[i] = un;
+        lmax = fmax(lmax, fabs(un));
+      }
+    } else {
+      const double two_a = up1[k], m2 = up2[k];
+      const double sc = scale / m2;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] = row_dot(ptr, col, val, u, i);
+      __syncthreads();
+      int bad = 0;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) bad |= !isfinite(sc * (two_a * u[i] - w[i]));
+      if (__syncthreads_or(bad)) break;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        x[i] += sc * (two_a * u[i] - w[i]);
+        z[i] = row_dot(ptr, col, val, w, i);
+      }
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double un = u[i] + (z[i] - two_a * w[i]) / m2;
+        u[i] = un;
+        lmax = fmax(lmax, fabs(un));
+      }
+    }
+    const double nrm = block_max(lmax, red);  // also orders the u writes above
+    if (nrm == 0.0) break;
+    if (nrm > 1e150 || nrm < 1e-150) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) u[i] /= nrm;
+      scale *= nrm;
+      __syncthreads();
+      if (!isfinite(scale) || scale == 0.0) break;
+    }
+  }
+}
+
+// Multi-CTA Newton for large coarse grids: host loop over roots with the
+// scale / stop state kept on the device.
+struct NewtonState {
+  double scale;
+  int stop;
+  double nrm;
+};
+
+__global__ void newton_init_kernel(int n, const double* __restrict__ b, double* u, double* x,
+                                   NewtonState* st) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    u[i] = b[i];
+    x[i] = 0.0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->scale = 1.0;
+    st->stop = 0;
+    st->nrm = 0.0;
+  }
+}
+
+// flags[0] = any nonfinite delta; partial max in parts
+__global__ void newton_check_kernel(int n, int type, double p1, double p2, const double* u,
+                                    const double* w, const NewtonState* st, int* flag) {
+  if (st->stop) return;
+  const double sc = st->scale / (type == 0 ? p1 : p2);
+  int bad = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    bad |= type == 0 ? !isfinite(sc * u[i]) : !isfinite(sc * (p1 * u[i] - w[i]));
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+__global__ void newton_rowspmv_kernel(int n, const int* __restrict__ ptr, const int* __restrict__ col,
+                                      const double* __restrict__ val, const double* in, double* out,
+                                      const NewtonState* st, const int* flag) {
+  if (st->stop || *flag) return;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = row_dot(ptr, col, val, in, (int)i);
+}
+
+__global__ void newton_update_kernel(int n, int type, double p1, double p2, double* x, double* u,
+                                     const double* w, const double* z, const NewtonState* st,
+                                     const int* flag, double* parts) {
+  __shared__ double red[33];
+  if (st->stop || *flag) return;
+  const double sc = st->scale / (type == 0 ? p1 : p2);
+  double lmax = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double un;
+    if (type == 0) {
+      x[i] += sc * u[i];
+      un = u[i] - w[i] / p1;
+    } else {
+      x[i] += sc * (p1 * u[i] - w[i]);
+      un = u[i] + (z[i] - p1 * w[i]) / p2;
+    }
+    u[i] = un;
+    lmax = fmax(lmax, fabs(un));
+  }
+  lmax = block_max(lmax, red);
+  if (threadIdx.x == 0) parts[blockIdx.x] = lmax;
+}
+
+__global__ void newton_rescale_kernel(int n, int nparts, const double* parts, double* u,
+                                      NewtonState* st, int* flag) {
+  // single block: reduce partial maxima, decide, rescale
+  __shared__ double red[33];
+  __shared__ int act;
+  if (st->stop) return;
+  if (*flag) {
+    if (threadIdx.x == 0) st->stop = 1;
+    return;
+  }
+  double m = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) m = fmax(m, parts[i]);
+  m = block_max(m, red);
+  if (threadIdx.x == 0) {
+    act = 0;
+    if (m == 0.0) st->stop = 1;
+    else if (m > 1e150 || m < 1e-150) act = 1;
+    st->nrm = m;
+  }
+  __syncthreads();
+  if (act) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) u[i] /= m;
+    if (threadIdx.x == 0) {
+      double sc = st->scale * m;
+      st->scale = sc;
+      if (!isfinite(sc) || sc == 0.0) st->stop = 1;
+    }
+  }
+}
+
+__global__ void neumann_scale_kernel(int n, const double* __restrict__ ds, const double* __restrict__ b,
+                                     double* __restrict__ t, double* __restrict__ acc) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double v = ds[i] * b[i];
+    t[i] = v;
+    acc[i] = v;
+  }
+}
+
+int neumann_scale(int n, const double* ds, const double* b, double* t, double* acc,
+                  cudaStream_t s) {
+  neumann_scale_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, ds, b, t, acc);
+  ++g_launches;
+  AIRG_LAUNCH_CHECK();
+  return AIRG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Polynomial operator (device-side description used by the plan)
+// ---------------------------------------------------------------------------
+struct Poly {
+  int kind = 0;  // 0 coeff (Horner), 1 newton, 2 neumann
+  std::vector<double> coef;
+  std::vector<int> utype;
+  std::vector<double> p1, p2;
+  const double* diag_scale = nullptr;
+  int* d_utype = nullptr;
+  double* d_p1 = nullptr;
+  double* d_p2 = nullptr;
+};
+
+constexpr int kNewtonCtaMax = 16384;  // single-CTA Newton up to this many rows
+
+struct Work {
+  double* buf = nullptr;
+  size_t cap = 0;
+};
+
+// y = q(A) b using scratch t0..t3 (each n doubles).  ymap: optional scatter
+// of the result (y[ymap[i]] = ...).  Only the Horner path supports ymap; the
+// caller handles others.
+static int poly_apply_dev(const Poly& p, const Csr& A, const double* b, double* y, double* t0,
+                          double* t1, double* t2, double* t3, int* iflag, double* parts,
+                          NewtonState* nst, cudaStream_t s) {
+  const int n = A.nrows;
+  if (n == 0) return AIRG_OK;
+  if (p.kind == 0) {
+    const int d = (int)p.coef.size() - 1;
+    if (d < 0) {
+      set_error("empty coefficient polynomial");
+      return AIRG_ERR_ARG;
+    }
+    if (d == 0) return launch_axpby(n, y, nullptr, p.coef[0], b, nullptr, 0.0, nullptr, s);
+    // y_1 = A (c_d b) + c_{d-1} b ; y_{j} = A y_{j-1} + c_j b
+    const double* cur = b;
+    double xs = p.coef[d];
+    double* bufs[2] = {t0, t1};
+    for (int j = d - 1; j >= 0; --j) {
+      double* dst = (j == 0) ? y : bufs[j & 1];
+      Epi ep{dst, nullptr, 1.0, p.coef[j], b, nullptr, nullptr, nullptr};
+      AIRG_TRY(launch_spmv(A, cur, xs, ep, s));
+      cur = dst;
+      xs = 1.0;
+    }
+    return AIRG_OK;
+  }
+  if (p.kind == 2) {
+    // t = ds*b; acc = t; repeat: t = t - ds*(A t); acc += t
+    const int order = (int)p.coef.size() - 1;
+    const int thr = 256;
+    AIRG_TRY(neumann_scale(n, p.diag_scale, b, t0, y, s));
+    double* cur = t0;
+    double* nxt = t1;
+    for (int it = 0; it < order; ++it) {
+      neumann_step_kernel<<<blocks_for(n, thr), thr, 0, s>>>(n, A.ptr, A.col, A.val, p.diag_scale,
+                                                            cur, nxt, y);
+      ++g_launches;
+      AIRG_LAUNCH_CHECK();
+      std::swap(cur, nxt);
+    }
+    return AIRG_OK;
+  }
+  // Newton
+  const int nunits = (int)p.utype.size();
+  if (n <= kNewtonCtaMax) {
+    newton_cta_kernel<<<1, 1024, 0, s>>>(n, A.ptr, A.col, A.val, b, y, t0, t1, t2, nunits,
+                                         p.d_utype, p.d_p1, p.d_p2);
+    ++g_launches;
+    AIRG_LAUNCH_CHECK();
+    return AIRG_OK;
+  }
+  const int thr = 256;
+  const int nb = blocks_for(n, thr, 148 * 8);
+  newton_init_kernel<<<nb, thr, 0, s>>>(n, b, t0, y, nst);
+  ++g_launches;
+  for (int k = 0; k < nunits; ++k) {
+    const int ty = p.utype[k];
+    AIRG_CUDA(cudaMemsetAsync(iflag, 0, sizeof(int), s));
+    if (ty == 1) {
+      newton_rowspmv_kernel<<<nb, thr, 0, s>>>(n, A.ptr, A.col, A.val, t0, t1, nst, iflag);
+      ++g_launches;
+    }
+    newton_check_kernel<<<nb, thr, 0, s>>>(n, ty, p.p1[k], p.p2[k], t0, t1, nst, iflag);
+    ++g_launches;
+    if (ty == 0) {
+      newton_rowspmv_kernel<<<nb, thr, 0, s>>>(n, A.ptr, A.col, A.val, t0, t1, nst, iflag);
+    } else {
+      newton_rowspmv_kernel<<<nb, thr, 0, s>>>(n, A.ptr, A.col, A.val, t1, t2, nst, iflag);
+    }
+    ++g_launches;
+    newton_update_kernel<<<nb, thr, 0, s>>>(n, ty, p.p1[k], p.p2[k], y, t0, t1, t2, nst, iflag,
+                                            parts);
+    newton_rescale_kernel<<<1, 1024, 0, s>>>(n, nb, parts, t0, nst, iflag);
+    g_launches += 2;
+  }
+  AIRG_LAUNCH_CHECK();
+  return AIRG_OK;
+}
+
+static int build_poly(Poly& p, int kind, int ncoef, const double* coef_h, int nunits,
+                      const int* type_h, const double* p1_h, const double* p2_h,
+                      const double* diag_scale) {
+  p.kind = kind;
+  p.diag_scale = diag_scale;
+  if (kind == 0 || kind == 2) {
+    if (ncoef < 1 || !coef_h) {
+      set_error("coefficient polynomial needs >= 1 coefficient");
+      return AIRG_ERR_ARG;
+    }
+    p.coef.assign(coef_h, coef_h + ncoef);
+    if (kind == 2 && !diag_scale) {
+      set_error("neumann polynomial needs diag_scale");
+      return AIRG_ERR_ARG;
+    }
+    return AIRG_OK;
+  }
+  if (kind != 1) {
+    set_error("unknown polynomial kind %d", kind);
+    return AIRG_ERR_ARG;
+  }
+  p.utype.assign(type_h, type_h + nunits);
+  p.p1.assign(p1_h, p1_h + nunits);
+  p.p2.assign(p2_h, p2_h + nunits);
+  if (nunits > 0) {
+    AIRG_CUDA(cudaMalloc(&p.d_utype, nunits * sizeof(int)));
+    AIRG_CUDA(cudaMalloc(&p.d_p1, nunits * sizeof(double)));
+    AIRG_CUDA(cudaMalloc(&p.d_p2, nunits * sizeof(double)));
+    AIRG_CUDA(cudaMemcpy(p.d_utype, type_h, nunits * sizeof(int), cudaMemcpyHostToDevice));
+    AIRG_CUDA(cudaMemcpy(p.d_p1, p1_h, nunits * sizeof(double), cudaMemcpyHostToDevice));
+    AIRG_CUDA(cudaMemcpy(p.d_p2, p2_h, nunits * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  return AIRG_OK;
+}
+
+static void free_poly(Poly& p) {
+  if (p.d_utype) cudaFree(p.d_utype);
+  if (p.d_p1) cudaFree(p.d_p1);
+  if (p.d_p2) cudaFree(p.d_p2);
+  p.d_utype = nullptr;
+  p.d_p1 = p.d_p2 = nullptr;
+}
+
+static Csr make_csr(int nrows, int ncols, const int* ptr, const int* col, const double* val,
+                    long long nnz) {
+  Csr c;
+  c.nrows = nrows;
+  c.ncols = ncols;
+  c.ptr = ptr;
+  c.col = col;
+  c.val = val;
+  c.nnz = nnz;
+  c.vs = pick_vs(nnz, nrows);
+  return c;
+}
+
+static long long read_nnz(const int* ptr, int nrows) {
+  int v = 0;
+  if (nrows > 0) cudaMemcpy(&v, ptr + nrows, sizeof(int), cudaMemcpyDeviceToHost);
+  return v;
+}
+
+}  // namespace airg
+
+using namespace airg;
+
+// ---------------------------------------------------------------------------
+// Plan
+// ---------------------------------------------------------------------------
+struct LevelOps {
+  int n = 0, n_f = 0, n_c = 0;
+  Csr R, Afc, Aff, Asm;
+  bool has_asm = false;
+  const int* f_idx = nullptr;
+  const int* c_idx = nullptr;
+  Poly sm;
+  // work vectors (owned)
+  double* rc = nullptr;   // n_c : restricted residual (input of the next level)
+  double* ec = nullptr;   // n_c : coarse error (output of the next level)
+  double* rhs = nullptr;  // n_f
+  double* ef = nullptr;   // n_f
+  double* t0 = nullptr;   // n_f
+  double* t1 = nullptr;   // n_f
+  double* t2 = nullptr;   // n_f (extra smooths)
+};
+
+struct airg_plan {
+  int nlevels = 0;
+  std::vector<LevelOps> lv;
+  Csr top;
+  Csr coarse;
+  Poly coarse_poly;
+  double *cw0 = nullptr, *cw1 = nullptr, *cw2 = nullptr, *cw3 = nullptr;  // coarse scratch
+  double* r = nullptr;  // top residual
+  double* e = nullptr;  // top error
+  double* parts = nullptr;
+  double* norm_d = nullptr;
+  double* norm_h = nullptr;  // pinned
+  int* iflag = nullptr;
+  NewtonState* nst = nullptr;
+  int nparts_cap = 0;
+  long long launches = 0;
+  bool ready_top = false, ready_coarse = false;
+};
+
+static int alloc_vec(double** p, long long n) {
+  AIRG_CUDA(cudaMalloc(p, (n > 0 ? n : 1) * sizeof(double)));
+  return AIRG_OK;
+}
+
+extern "C" {
+
+int airg_version(void) { return 1; }
+
+int airg_last_error(char* buf, int len) {
+  if (!buf || len <= 0) return (int)airg::g_err.size();
+  snprintf(buf, len, "%s", airg::g_err.c_str());
+  return (int)airg::g_err.size();
+}
+
+int airg_sm_count(void) {
+  int dev = 0, v = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+  return v;
+}
+
+int airg_spmv(int nrows, const int32_t* ptr, const int32_t* col, const double* val,
+              const double* x, double* y, int exact, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (nrows < 0) {
+    set_error("negative row count");
+    return AIRG_ERR_ARG;
+  }
+  if (nrows == 0) return AIRG_OK;
+  if (exact) {
+    spmv_exact_kernel<<<blocks_for(nrows, 128), 128, 0, s>>>(nrows, ptr, col, val, x, y);
+    AIRG_LAUNCH_CHECK();
+    return AIRG_OK;
+  }
+  Csr A = make_csr(nrows, 0, ptr, col, val, read_nnz(ptr, nrows));
+  Epi ep{y, nullptr, 1.0, 0.0, nullptr, nullptr, nullptr, nullptr};
+  return launch_spmv(A, x, 1.0, ep, s);
+}
+
+int airg_norm2(int n, const double* x, double* out_h, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nb = blocks_for(n, 256, 1024);
+  double* parts = nullptr;
+  double* d = nullptr;
+  AIRG_TRY(scratch(&parts, nb + 1, s));
+  d = parts + nb;
+  sumsq_kernel<<<nb, 256, 0, s>>>(n, x, parts);
+  finish_norm_kernel<<<1, 1024, 0, s>>>(nb, parts, d);
+  AIRG_LAUNCH_CHECK();
+  AIRG_CUDA(cudaMemcpyAsync(out_h, d, sizeof(double), cudaMemcpyDeviceToHost, s));
+  AIRG_CUDA(cudaStreamSynchronize(s));
+  release(parts, s);
+  return AIRG_OK;
+}
+
+int airg_poly_apply(int kind, int n, const int32_t* ptr, const int32_t* col, const double* val,
+                    int ncoef, const double* coef_h, int nunits, const int32_t* type_h,
+                    const double* p1_h, const double* p2_h, const double* diag_scale,
+                    const double* b, double* y, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  Poly p;
+  AIRG_TRY(build_poly(p, kind, ncoef, coef_h, nunits, type_h, p1_h, p2_h, diag_scale));
+  Csr A = make_csr(n, n, ptr, col, val, read_nnz(ptr, n));
+  double* w = nullptr;
+  const int nb = blocks_for(n, 256, 148 * 8);
+  AIRG_TRY(scratch(&w, 4LL * (n > 0 ? n : 1) + nb + 8, s));
+  double* parts = w + 4LL * (n > 0 ? n : 1);
+  int* iflag = (int*)(parts + nb);
+  NewtonState* nst = (NewtonState*)(parts + nb + 2);
+  const size_t nn = n > 0 ? n : 1;
+  int st = poly_apply_dev(p, A, b, y, w, w + nn, w + 2 * nn, w + 3 * nn, iflag, parts, nst, s);
+  release(w, s);
+  cudaStreamSynchronize(s);
+  free_poly(p);
+  return st;
+}
+
+int airg_plan_create(int nlevels, airg_plan** out) {
+  if (nlevels < 0 || !out) {
+    set_error("bad plan arguments");
+    return AIRG_ERR_ARG;
+  }
+  airg_plan* p = new airg_plan();
+  p->nlevels = nlevels;
+  p->lv.resize(nlevels);
+  AIRG_CUDA(cudaMallocHost(&p->norm_h, sizeof(double)));
+  AIRG_CUDA(cudaMalloc(&p->norm_d, sizeof(double)));
+  AIRG_CUDA(cudaMalloc(&p->iflag, sizeof(int)));
+  AIRG_CUDA(cudaMalloc(&p->nst, sizeof(NewtonState)));
+  *out = p;
+  return AIRG_OK;
+}
+
+int airg_plan_destroy(airg_plan* p) {
+  if (!p) return AIRG_OK;
+  for (auto& L : p->lv) {
+    for (double* q : {L.rc, L.ec, L.rhs, L.ef, L.t0, L.t1, L.t2})
+      if (q) cudaFree(q);
+    free_poly(L.sm);
+  }
+  free_poly(p->coarse_poly);
+  for (double* q : {p->cw0, p->cw1, p->cw2, p->cw3, p->r, p->e, p->parts, p->norm_d})
+    if (q) cudaFree(q);
+  if (p->iflag) cudaFree(p->iflag);
+  if (p->nst) cudaFree(p->nst);
+  if (p->norm_h) cudaFreeHost(p->norm_h);
+  delete p;
+  return AIRG_OK;
+}
+
+int airg_plan_set_top(airg_plan* p, int n, const int32_t* ptr, const int32_t* col,
+                      const double* val) {
+  p->top = make_csr(n, n, ptr, col, val, read_nnz(ptr, n));
+  AIRG_TRY(alloc_vec(&p->r, n));
+  AIRG_TRY(alloc_vec(&p->e, n));
+  const int nb = (int)((p->top.nrows * (long long)p->top.vs + 255) / 256);
+  p->nparts_cap = std::max(nb, 148 * 8);
+  AIRG_TRY(alloc_vec(&p->parts, p->nparts_cap));
+  p->ready_top = true;
+  return AIRG_OK;
+}
+
+int airg_plan_set_level(airg_plan* p, int level, int n, int n_f, int n_c, const int32_t* R_ptr,
+                        const int32_t* R_col, const double* R_val, const int32_t* Afc_ptr,
+                        const int32_t* Afc_col, const double* Afc_val, const int32_t* Aff_ptr,
+                        const int32_t* Aff_col, const double* Aff_val, const int32_t* f_idx,
+                        const int32_t* c_idx, int kind, int ncoef, const double* coef_h,
+                        const double* diag_scale, int64_t asm_nnz, const int32_t* asm_ptr,
+                        const int32_t* asm_col, const double* asm_val) {
+  if (level < 0 || level >= p->nlevels || n_f + n_c != n) {
+    set_error("bad level %d (n=%d n_f=%d n_c=%d)", level, n, n_f, n_c);
+    return AIRG_ERR_ARG;
+  }
+  LevelOps& L = p->lv[level];
+  L.n = n;
+  L.n_f = n_f;
+  L.n_c = n_c;
+  L.R = make_csr(n_c, n, R_ptr, R_col, R_val, read_nnz(R_ptr, n_c));
+  L.Afc = make_csr(n_f, n_c, Afc_ptr, Afc_col, Afc_val, read_nnz(Afc_ptr, n_f));
+  L.Aff = make_csr(n_f, n_f, Aff_ptr, Aff_col, Aff_val, read_nnz(Aff_ptr, n_f));
+  L.has_asm = asm_nnz >= 0;
+  if (L.has_asm) L.Asm = make_csr(n_f, n_f, asm_ptr, asm_col, asm_val, asm_nnz);
+  L.f_idx = f_idx;
+  L.c_idx = c_idx;
+  AIRG_TRY(build_poly(L.sm, kind, ncoef, coef_h, 0, nullptr, nullptr, nullptr, diag_scale));
+  AIRG_TRY(alloc_vec(&L.rc, n_c));
+  AIRG_TRY(alloc_vec(&L.ec, n_c));
+  AIRG_TRY(alloc_vec(&L.rhs, n_f));
+  AIRG_TRY(alloc_vec(&L.ef, n_f));
+  AIRG_TRY(alloc_vec(&L.t0, n_f));
+  AIRG_TRY(alloc_vec(&L.t1, n_f));
+  AIRG_TRY(alloc_vec(&L.t2, n_f));
+  return AIRG_OK;
+}
+
+int airg_plan_set_coarse(airg_plan* p, int n, const int32_t* ptr, const int32_t* col,
+                         const double* val, int kind, int ncoef, const double* coef_h, int nunits,
+                         const int32_t* type_h, const double* p1_h, const double* p2_h,
+                         const double* diag_scale) {
+  p->coarse = make_csr(n, n, ptr, col, val, read_nnz(ptr, n));
+  AIRG_TRY(build_poly(p->coarse_poly, kind, ncoef, coef_h, nunits, type_h, p1_h, p2_h,
+                      diag_scale));
+  AIRG_TRY(alloc_vec(&p->cw0, n));
+  AIRG_TRY(alloc_vec(&p->cw1, n));
+  AIRG_TRY(alloc_vec(&p->cw2, n));
+  AIRG_TRY(alloc_vec(&p->cw3, n));
+  if (!p->parts) {
+    p->nparts_cap = 148 * 8;
+    AIRG_TRY(alloc_vec(&p->parts, p->nparts_cap));
+  }
+  p->ready_coarse = true;
+  return AIRG_OK;
+}
+
+}  // extern "C"
+
+// smoother application on one level: ef = q(A_ff) rhs  (or assembled SpMV)
+static int smooth_level(airg_plan* p, LevelOps& L, const double* rhs, double* out, cudaStream_t s) {
+  if (L.has_asm) {
+    Epi ep{out, nullptr, 1.0, 0.0, nullptr, nullptr, nullptr, nullptr};
+    return launch_spmv(L.Asm, rhs, 1.0, ep, s);
+  }
+  return poly_apply_dev(L.sm, L.Aff, rhs, out, L.t0, L.t1, L.t2, L.t2, p->iflag, p->parts, p->nst,
+                        s);
+}
+
+// V-cycle from `level` with residual r (size n_level) -> e (size n_level).
+static int vcycle_rec(airg_plan* p, int level, const double* r, double* e, int fits,
+                      cudaStream_t s) {
+  if (level == p->nlevels) {
+    if (!p->ready_coarse) {
+      set_error("plan has no coarse solver");
+      return AIRG_ERR_ARG;
+    }
+    return poly_apply_dev(p->coarse_poly, p->coarse, r, e, p->cw0, p->cw1, p->cw2, p->cw3,
+                          p->iflag, p->parts, p->nst, s);
+  }
+  LevelOps& L = p->lv[level];
+  // r_c = R r
+  {
+    Epi ep{L.rc, nullptr, 1.0, 0.0, nullptr, nullptr, nullptr, nullptr};
+    AIRG_TRY(launch_spmv(L.R, r, 1.0, ep, s));
+  }
+  AIRG_TRY(vcycle_rec(p, level + 1, L.rc, L.ec, fits, s));
+  // rhs = r[f] - A_fc e_c
+  {
+    Epi ep{L.rhs, nullptr, -1.0, 1.0, r, L.f_idx, nullptr, nullptr};
+    AIRG_TRY(launch_spmv(L.Afc, L.ec, 1.0, ep, s));
+  }
+  AIRG_TRY(smooth_level(p, L, L.rhs, L.ef, s));
+  for (int it = 1; it < fits; ++it) {
+    // t1 = rhs - A_ff ef ; ef += q(A_ff) t1
+    Epi ep{L.t1, nullptr, -1.0, 1.0, L.rhs, nullptr, nullptr, nullptr};
+    AIRG_TRY(launch_spmv(L.Aff, L.ef, 1.0, ep, s));
+    double* tmp = nullptr;
+    AIRG_TRY(scratch(&tmp, 2 * (size_t)(L.n_f > 0 ? L.n_f : 1), s));
+    AIRG_CUDA(cudaMemcpyAsync(tmp, L.t1, L.n_f * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    double* corr = tmp + (L.n_f > 0 ? L.n_f : 1);
+    AIRG_TRY(smooth_level(p, L, tmp, corr, s));
+    AIRG_TRY(launch_axpby(L.n_f, L.ef, nullptr, 1.0, corr, nullptr, 1.0, L.ef, s));
+    release(tmp, s);
+  }
+  // scatter e[f] = ef, e[c] = ec
+  AIRG_TRY(launch_axpby(L.n_f, e, L.f_idx, 1.0, L.ef, nullptr, 0.0, nullptr, s));
+  AIRG_TRY(launch_axpby(L.n_c, e, L.c_idx, 1.0, L.ec, nullptr, 0.0, nullptr, s));
+  return AIRG_OK;
+}
+
+extern "C" {
+
+int airg_plan_vcycle(airg_plan* p, int level, const double* r, double* e, int f_smooth_its,
+                     void* stream) {
+  if (level < 0 || level > p->nlevels) {
+    set_error("level %d out of range", level);
+    return AIRG_ERR_ARG;
+  }
+  return vcycle_rec(p, level, r, e, f_smooth_its < 1 ? 1 : f_smooth_its, (cudaStream_t)stream);
+}
+
+int64_t airg_plan_launches(airg_plan* p) { return p ? p->launches : 0; }
+
+}  // extern "C"
+
+// r = b - A x, with deterministic norm into p->norm_h (synchronous)
+static int residual_norm(airg_plan* p, const double* b, const double* x, double* rnorm,
+                         cudaStream_t s) {
+  const Csr& A = p->top;
+  const int nb = spmv_blocks(A);
+  double* parts = p->parts;
+  if (nb > p->nparts_cap) {
+    set_error("partials buffer too small");
+    return AIRG_ERR_ARG;
+  }
+  Epi ep{p->r, nullptr, -1.0, 1.0, b, nullptr, nullptr, parts};
+  AIRG_TRY(launch_spmv(A, x, 1.0, ep, s));
+  finish_norm_kernel<<<1, 1024, 0, s>>>(nb, parts, p->norm_d);
+  ++g_launches;
+  AIRG_LAUNCH_CHECK();
+  AIRG_CUDA(cudaMemcpyAsync(p->norm_h, p->norm_d, sizeof(double), cudaMemcpyDeviceToHost, s));
+  AIRG_CUDA(cudaStreamSynchronize(s));
+  *rnorm = *p->norm_h;
+  return AIRG_OK;
+}
+
+extern "C" int airg_plan_richardson(airg_plan* p, const double* b, double* x, double rtol,
+                                    double atol, int max_iters, int f_smooth_its,
+                                    double* history, int* iterations, int* converged,
+                                    void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!p->ready_top) {
+    set_error("plan has no top matrix");
+    return AIRG_ERR_ARG;
+  }
+  const long long l0 = g_launches;
+  const int n = p->top.nrows;
+  double bnorm = 0.0, rnorm = 0.0;
+  {
+    // ||b|| with the same fixed-order reduction
+    const int nb = blocks_for(n, 256, 1024);
+    sumsq_kernel<<<nb, 256, 0, s>>>(n, b, p->parts);
+    finish_norm_kernel<<<1, 1024, 0, s>>>(nb, p->parts, p->norm_d);
+    g_launches += 2;
+    AIRG_LAUNCH_CHECK();
+    AIRG_CUDA(cudaMemcpyAsync(p->norm_h, p->norm_d, sizeof(double), cudaMemcpyDeviceToHost, s));
+    AIRG_CUDA(cudaStreamSynchronize(s));
+    bnorm = *p->norm_h;
+  }
+  AIRG_TRY(residual_norm(p, b, x, &rnorm, s));
+  history[0] = rnorm;
+  const double ref = bnorm > 0 ? bnorm : rnorm;
+  const double thr = std::max(rtol * ref, atol);
+  *iterations = 0;
+  *converged = 0;
+  if (!std::isfinite(rnorm)) {
+    set_error("non-finite residual at iteration 0");
+    return AIRG_ERR_DIVERGED;
+  }
+  bool conv = rnorm <= thr;
+  int its = 0;
+  while (!conv && its < max_iters) {
+    AIRG_TRY(vcycle_rec(p, 0, p->r, p->e, f_smooth_its < 1 ? 1 : f_smooth_its, s));
+    AIRG_TRY(launch_axpby(n, x, nullptr, 1.0, p->e, nullptr, 1.0, x, s));
+    AIRG_TRY(residual_norm(p, b, x, &rnorm, s));
+    ++its;
+    history[its] = rnorm;
+    *iterations = its;
+    if (!std::isfinite(rnorm)) {
+      set_error("non-finite residual at iteration %d", its);
+      p->launches = g_launches - l0;
+      return AIRG_ERR_DIVERGED;
+    }
+    if (rnorm > 1e8 * history[0]) {
+      set_error("residual grew by more than 1e+08 at iteration %d", its);
+      p->launches = g_launches - l0;
+      return AIRG_ERR_DIVERGED;
+    }
+    conv = rnorm <= thr;
+  }
+  *converged = conv ? 1 : 0;
+  p->launches = g_launches - l0;
+  return AIRG_OK;
+}

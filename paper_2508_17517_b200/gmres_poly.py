@@ -1,0 +1,178 @@
+"""GMRES polynomial approximate inverses (ref: polynomial.py:25-431).
+
+The Krylov basis (SpMVs, MGS dot products, norms) is built on the GPU; the
+(order+2) x (order+1) Hessenberg block comes back to the host, where the
+O(m^3) dense algebra (least squares, SVD, eigenvalues, Leja ordering) runs in
+numpy -- the control plane, exactly the routines the reference calls.
+Application (Horner / factored Newton / Neumann) is a device kernel chain.
+"""
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib as L
+from .csr import VAL, empty, to_dev
+
+KIND_CODE = {'arnoldi_coeff': 0, 'newton_roots': 1, 'neumann': 2}
+
+
+@dataclass(frozen=True)
+class PolySolver:
+    """Fixed polynomial approximation of a matrix inverse (polynomial.py:40-58)."""
+
+    kind: str
+    order: int
+    effective_order: int
+    coeffs: np.ndarray = None
+    roots: np.ndarray = None
+    diag_scale: object = None       # device fp64 tensor (neumann)
+    residual_history: tuple = None
+
+
+def newton_units(roots):
+    """Encode Leja-ordered roots as units: real theta -> (0, theta, 0); a
+    conjugate pair (a +- bi) -> (1, 2a, |theta|^2) (polynomial.py:324-345)."""
+    types, p1, p2 = [], [], []
+    i = 0
+    while i < len(roots):
+        th = roots[i]
+        if th.imag == 0:
+            types.append(0)
+            p1.append(th.real)
+            p2.append(0.0)
+            i += 1
+        else:
+            types.append(1)
+            p1.append(2.0 * th.real)
+            p2.append((th * np.conj(th)).real)
+            i += 2
+    return (np.array(types, dtype=np.int32), np.array(p1, dtype=np.float64),
+            np.array(p2, dtype=np.float64))
+
+
+def poly_args(p):
+    """(kind, ncoef, coef_h, nunits, type_h, p1_h, p2_h, diag_scale_tensor, keepalive)."""
+    code = KIND_CODE.get(p.kind)
+    if code is None:
+        raise ValueError(f'unknown polynomial kind {p.kind!r}')
+    if code == 1:
+        t, a, b = newton_units(p.roots)
+        return code, 0, None, len(t), t, a, b, None, (t, a, b)
+    c = np.ascontiguousarray(p.coeffs, dtype=np.float64)
+    ds = p.diag_scale if code == 2 else None
+    return code, len(c), c, 0, None, None, None, ds, (c,)
+
+
+def apply_matrix_free(p, A, b):
+    """q(A) b with SpMVs and vector updates only (polynomial.py:358-369)."""
+    b = to_dev(b, VAL)
+    if A.nrows != A.ncols or b.numel() != A.ncols:
+        raise ValueError('solver, matrix and vector shapes disagree')
+    code, nc, c, nu, t, a1, a2, ds, keep = poly_args(p)
+    y = empty(A.nrows, VAL)
+    L.call('airg_poly_apply', code, A.nrows, L.ptr(A.row_offsets), L.ptr(A.col_indices),
+           L.ptr(A.values), nc, L.hptr(c), nu, L.hptr(t), L.hptr(a1), L.hptr(a2), L.ptr(ds),
+           L.ptr(b), L.ptr(y), L.stream_handle())
+    del keep
+    return y
+
+
+# ---------------------------------------------------------------------------
+# host-side dense algebra on the device-built Hessenberg block
+# ---------------------------------------------------------------------------
+
+def _lsq(H, k, beta):
+    rhs = np.zeros(H.shape[0])
+    rhs[0] = beta
+    y, *_ = np.linalg.lstsq(H[:k + 1, :k], rhs[:k + 1], rcond=None)
+    return y, np.linalg.norm(rhs[:k + 1] - H[:k + 1, :k] @ y)
+
+
+def _history(H, k, beta):
+    return tuple(float(_lsq(H, j, beta)[1]) for j in range(1, k + 1))
+
+
+def coeffs_from_hessenberg(H, k, beta, order):
+    """Monomial GMRES-polynomial coefficients with the noise-limited order
+    choice (polynomial.py:148-170)."""
+    hist = _history(H, k, beta)
+    Cb = np.zeros((k, k))
+    Cb[0, 0] = 1.0
+    scale = max(np.linalg.norm(H[:j + 2, j]) for j in range(k))
+    powers = scale ** np.arange(k)
+    growth = np.empty(k)
+    growth[0] = 1.0
+    for j in range(k - 1):
+        sh = np.zeros(k)
+        sh[1:j + 2] = Cb[:j + 1, j]
+        Cb[:, j + 1] = (sh - Cb[:, :j + 1] @ H[:j + 1, j]) / H[j + 1, j]
+        growth[j + 1] = np.abs(Cb[:, j + 1]) @ powers
+    noise = np.finfo(np.float64).eps * np.maximum.accumulate(growth) * beta
+    k_use = int(np.argmin(np.maximum(hist, noise))) + 1
+    y, _ = _lsq(H, k_use, beta)
+    return PolySolver('arnoldi_coeff', order, k_use - 1, coeffs=(Cb[:k_use, :k_use] @ y) / beta,
+                      residual_history=hist)
+
+
+def roots_from_hessenberg(H, k, beta, order, added_root_tol=1e-4):
+    """Harmonic Ritz values, Leja order, stability copies (polynomial.py:173-279)."""
+    while True:
+        Hk = H[:k, :k]
+        sv = np.linalg.svd(Hk, compute_uv=False)
+        rank = int(np.sum(sv > 1e-12 * sv[0])) if sv[0] > 0 else 0
+        if rank == 0:
+            raise ValueError('matrix is numerically zero on the Krylov space')
+        if rank == k:
+            break
+        k = rank
+    hs = H[k, k - 1] if H.shape[0] > k else 0.0
+    ek = np.zeros(k)
+    ek[-1] = 1.0
+    try:
+        f = np.linalg.solve(Hk.T, ek)
+    except np.linalg.LinAlgError:
+        f, *_ = np.linalg.lstsq(Hk.T, ek, rcond=None)
+    M = Hk.copy()
+    M[:, -1] += (hs * hs) * f
+    theta = np.linalg.eigvals(M)
+    if np.any(np.abs(theta) == 0):
+        raise ValueError('zero harmonic Ritz value; residual polynomial is degenerate')
+    real = [complex(t) for t in theta[theta.imag == 0]]
+    upper = np.sort_complex(theta[theta.imag > 0])
+    if len(upper) != np.count_nonzero(theta.imag < 0):
+        raise ValueError('complex roots of a real matrix must come in conjugate pairs')
+    pool = [(t,) for t in real] + [(t, np.conj(t)) for t in upper]
+    pool.sort(key=lambda u: max(abs(t) for t in u), reverse=True)
+    seq = [pool.pop(0)]
+    placed = list(seq[0])
+    while pool:
+        score = [sum(math.log(max(abs(t - q), 1e-300)) for t in u for q in placed) for u in pool]
+        u = pool.pop(int(np.argmax(score)))
+        seq.append(u)
+        placed.extend(u)
+    out, seen = [], []
+    for u in seq:
+        reps = 1
+        if added_root_tol > 0 and any(abs(t - q) < added_root_tol * max(abs(t), abs(q))
+                                      for t in u for q in seen):
+            reps = 2
+        for _ in range(reps):
+            out.extend(u)
+        seen.extend(u)
+    return PolySolver('newton_roots', order, k - 1, roots=np.array(out, dtype=np.complex128),
+                      residual_history=_history(H, k, beta))
+
+
+def export_diagnostics(p):
+    """JSON-serialisable description (polynomial.py:419-431)."""
+    return {
+        'kind': p.kind,
+        'order': p.order,
+        'effective_order': p.effective_order,
+        'coeffs': None if p.coeffs is None else [float(c) for c in p.coeffs],
+        'roots': None if p.roots is None else [[float(r.real), float(r.imag)] for r in p.roots],
+        'generating_residual_history':
+            None if p.residual_history is None else list(p.residual_history),
+    }

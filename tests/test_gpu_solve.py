@@ -1,0 +1,141 @@
+"""GPU parity of the solve path on identical operators (oracle hierarchy
+uploaded to HBM): SpMV, polynomial application, V-cycle and Richardson.
+
+Tolerances: SpMV exact mode is bitwise; the fast (FMA, vector) kernels and
+the solve agree with the oracle to 1e-10 relative (north_star tolerance)."""
+
+import numpy as np
+import pytest
+
+from oracle import airg_oracle as O
+from tests.gpu_util import dev_csr, dev_poly, rel, upload_hierarchy
+
+pytestmark = pytest.mark.gpu
+
+PI4 = (float(np.cos(np.pi / 4)), float(np.sin(np.pi / 4)))
+HARD = (float(np.sqrt(2 / 3)), float(np.sqrt(1 / 3)))
+
+
+@pytest.fixture(scope='module')
+def G():
+    import paper_2508_17517_b200 as G
+    return G
+
+
+@pytest.fixture(scope='module')
+def hier64():
+    A = O.advection_2d(64, 64, *PI4)
+    return O.setup(A, O.Cfg(poly_order=4), keep_level_matrices=True)
+
+
+def test_spmv_exact_bitwise_on_every_level_operator(G, hier64):
+    rng = np.random.default_rng(0)
+    mats = [hier64.top_A, hier64.coarsest_A]
+    for L in hier64.levels:
+        mats += [L.R, L.A_fc, L.A_ff, L.A, L.P]
+    for M in mats:
+        x = rng.standard_normal(M.ncols)
+        want = O.spmv(M, x)
+        got = G.spmv(dev_csr(M), x, exact=True).cpu().numpy()
+        assert got.tobytes() == want.tobytes()
+        fast = G.spmv(dev_csr(M), x).cpu().numpy()
+        assert np.allclose(fast, want, rtol=1e-12, atol=1e-12 * np.abs(want).max())
+
+
+def test_spmv_empty_and_ragged(G):
+    A = O.from_triplets(5, 7, [0, 0, 3, 3, 3], [1, 6, 0, 2, 5], [1.0, -2.0, 3.0, 0.0, 4.0])
+    x = np.arange(7, dtype=np.float64) + 0.5
+    assert np.array_equal(G.spmv(dev_csr(A), x, exact=True).cpu().numpy(), O.spmv(A, x))
+    Z = O.from_triplets(0, 3, [], [], [])
+    assert G.spmv(dev_csr(Z), np.ones(3)).numel() == 0
+    with pytest.raises(ValueError):
+        G.spmv(dev_csr(A), np.ones(3))
+
+
+def test_poly_apply_kinds_match_oracle(G, hier64):
+    rng = np.random.default_rng(1)
+    L = hier64.levels[2]
+    b = rng.standard_normal(L.A_ff.nrows)
+    got = G.apply_matrix_free(dev_poly(L.smoother), dev_csr(L.A_ff), b).cpu().numpy()
+    assert rel(got, O.apply_poly(L.smoother, L.A_ff, b)) < 1e-12
+    C = hier64.coarsest_A
+    bc = rng.standard_normal(C.nrows)
+    got = G.apply_matrix_free(dev_poly(hier64.coarse_solver), dev_csr(C), bc).cpu().numpy()
+    want = O.apply_poly(hier64.coarse_solver, C, bc)
+    assert np.max(np.abs(got - want)) <= 1e-10 * np.max(np.abs(want))
+    nm = O.neumann_poly(L.A_ff, 3)
+    got = G.apply_matrix_free(dev_poly(nm), dev_csr(L.A_ff), b).cpu().numpy()
+    assert rel(got, O.apply_poly(nm, L.A_ff, b)) < 1e-12
+
+
+def test_newton_rescale_and_early_exit(G):
+    """Wide-spectrum high-order Newton: rescaling / underflow exit semantics
+    (polynomial.py:331-353) must match."""
+    n = 200
+    d = np.linspace(1.0, 1e4, n)
+    A = O.from_triplets(n, n, np.arange(n), np.arange(n), d)
+    p = O.gmres_poly_newton(A, 80, 3)
+    b = np.random.default_rng(2).standard_normal(n)
+    want = O.apply_poly(p, A, b)
+    got = G.apply_matrix_free(dev_poly(p), dev_csr(A), b).cpu().numpy()
+    assert np.all(np.isfinite(got))
+    assert np.max(np.abs(got - want)) <= 1e-9 * np.max(np.abs(want))
+
+
+def test_vcycle_every_level(G, hier64):
+    H = upload_hierarchy(hier64)
+    rng = np.random.default_rng(3)
+    for lev in range(len(hier64.levels) + 1):
+        n = hier64.levels[lev].n if lev < len(hier64.levels) else hier64.coarsest_A.nrows
+        r = rng.standard_normal(n)
+        want = O.vcycle(hier64, lev, r)
+        got = G.vcycle(H, lev, r, G.SolveConfig()).cpu().numpy()
+        assert np.max(np.abs(got - want)) <= 1e-10 * np.max(np.abs(want)), lev
+
+
+@pytest.mark.parametrize('nx,ny,v,order,its', [
+    (64, 64, PI4, 4, 1), (128, 128, PI4, 4, 1), (128, 128, PI4, 6, 1), (48, 40, HARD, 6, 1),
+    (96, 64, PI4, 3, 2)])
+def test_richardson_matches_oracle(G, nx, ny, v, order, its):
+    A = O.advection_2d(nx, ny, *v)
+    Hh = O.setup(A, O.Cfg(poly_order=order))
+    x_o, hist_o, conv_o, its_o = O.richardson(Hh, np.zeros(A.nrows), np.ones(A.nrows),
+                                              f_smooth_its=its)
+    H = upload_hierarchy(Hh)
+    x, st = G.richardson_solve(H, np.zeros(A.nrows), np.ones(A.nrows),
+                               G.SolveConfig(f_smooth_its=its))
+    assert st.iterations == its_o and st.converged == conv_o
+    assert rel(st.residual_history, hist_o) < 1e-10
+    x = x.cpu().numpy()
+    assert np.max(np.abs(x - x_o)) <= 1e-10 * max(np.max(np.abs(x_o)), 1e-300) + 1e-14
+
+
+def test_assembled_smoother_path(G):
+    A = O.advection_2d(48, 48, *PI4)
+    Hh = O.setup(A, O.Cfg(poly_order=3, matrix_free_polys=False))
+    x_o, hist_o, _, its_o = O.richardson(Hh, np.zeros(A.nrows), np.ones(A.nrows))
+    H = upload_hierarchy(Hh)
+    x, st = G.richardson_solve(H, np.zeros(A.nrows), np.ones(A.nrows), G.SolveConfig())
+    assert st.iterations == its_o
+    assert rel(st.residual_history, hist_o) < 1e-10
+
+
+def test_divergence_guard(G):
+    A = O.advection_2d(32, 32, *PI4)
+    Hh = O.setup(A, O.Cfg(poly_order=2))
+    H = upload_hierarchy(Hh)
+    bad = O._mk(A.nrows, A.ncols, A.ptr, A.col, -50.0 * A.val)
+    H.top_A = dev_csr(bad)
+    H._plan = None
+    with pytest.raises(G.DivergenceError) as ei:
+        G.richardson_solve(H, np.zeros(A.nrows), np.ones(A.nrows), G.SolveConfig(max_iters=50))
+    assert ei.value.iteration >= 1
+
+
+def test_solve_bitwise_deterministic(G):
+    A = O.advection_2d(64, 64, *PI4)
+    H = upload_hierarchy(O.setup(A, O.Cfg(poly_order=4)))
+    x1, s1 = G.richardson_solve(H, np.zeros(A.nrows), np.ones(A.nrows), G.SolveConfig())
+    x2, s2 = G.richardson_solve(H, np.zeros(A.nrows), np.ones(A.nrows), G.SolveConfig())
+    assert s1.residual_history == s2.residual_history
+    assert x1.cpu().numpy().tobytes() == x2.cpu().numpy().tobytes()
