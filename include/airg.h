@@ -92,6 +92,110 @@ int airg_plan_richardson(airg_plan* plan, const double* b, double* x, double rto
 /* Number of kernel launches issued by the last airg_plan_richardson call. */
 int64_t airg_plan_launches(airg_plan* plan);
 
+/* ---- variable-size CSR results (setup path) ------------------------------
+ * Producers return an opaque airg_csr_result held in library scratch;
+ * airg_result_info gives its shape, the caller allocates ptr[nrows+1],
+ * col[nnz], val[nnz] and airg_result_take copies them out and frees the
+ * result (val may be NULL to drop values). */
+typedef struct airg_csr_result airg_csr_result;
+int airg_result_info(airg_csr_result* r, int32_t* nrows_h, int32_t* ncols_h, int64_t* nnz_h);
+int airg_result_take(airg_csr_result* r, int32_t* ptr, int32_t* col, double* val, void* stream);
+int airg_result_free(airg_csr_result* r);
+
+/* numpy Generator(PCG64(SeedSequence(seed))) stream: out[i] = a + b*random()_i
+ * (a=0,b=1: .random(n); a=-1,b=2: .uniform(-1,1,n)); the 128-bit state and
+ * increment come from the host's SeedSequence.  ref: polynomial.py:61-65,
+ * splitting.py:119 */
+int airg_pcg64_fill(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                    int64_t n, double a, double b, double* out, void* stream);
+
+/* Random unit vector: uniform(-1, 1, n) / ||.|| (norm_h may be NULL).
+ * ref: polynomial.py:61-65 */
+int airg_random_unit(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                     int64_t n, double* out, double* norm_h, void* stream);
+/* Main diagonal (structurally missing entries are 0).  ref: sparse.py:360-367 */
+int airg_diagonal(int n, const int32_t* p, const int32_t* c, const double* v, double* d,
+                  void* stream);
+
+/* 2-D upwind advection stencil (nnz = n + [vx>0](nx-1)ny + [vy>0]nx(ny-1)).
+ * ref: problems.py:48-85 */
+int airg_advection_2d(int nx, int ny, double vx, double vy, int32_t* ptr, int32_t* col,
+                      double* val, void* stream);
+
+/* ---- CF splitting (splitting.py:86-238) --------------------------------- */
+/* S and pattern(S + S^T) with unit values.  ref: splitting.py:86-109 */
+int airg_strength(int n, const int32_t* ptr, const int32_t* col, const double* val, int64_t nnz,
+                  double theta, airg_csr_result** S_out, airg_csr_result** closure_out,
+                  void* stream);
+/* Luby rounds on a symmetric closure; labels int8 F=0 / C=1; max_loops<0 =
+ * unlimited.  ref: splitting.py:127-159 */
+int airg_pmisr(int n, const int32_t* cptr, const int32_t* ccol, uint64_t state_hi,
+               uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int max_loops,
+               int8_t* labels, int32_t* loops_h, void* stream);
+/* strength + closure + PMISR fused (closure never leaves the library). */
+int airg_cf_pmisr(int n, const int32_t* ptr, const int32_t* col, const double* val, int64_t nnz,
+                  double theta, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                  uint64_t inc_lo, int max_loops, int8_t* labels, int32_t* loops_h, void* stream);
+/* One DDC pass, labels updated in place; stats_h[6] = n_f_before, converted,
+ * ratio_min, ratio_max, ratio_mean, cut.  ref: splitting.py:162-207 */
+int airg_ddc_pass(int n, const int32_t* ptr, const int32_t* col, const double* val, int8_t* labels,
+                  double fraction, int nbins, double* stats_h, void* stream);
+/* pos[i] = rank of i inside its class; f_idx / c_idx = sorted index sets
+ * (any of the three may be NULL).  ref: splitting.py:53-58 (CFSplit.from_labels) */
+int airg_split_index(int n, const int8_t* labels, int32_t* pos, int32_t* f_idx, int32_t* c_idx,
+                     int32_t* nf_h, void* stream);
+/* F rows without a C coupling become C.  ref: hierarchy.py:289-305 */
+int airg_repair_split(int n, const int32_t* ptr, const int32_t* col, int8_t* labels,
+                      int32_t* changed_h, void* stream);
+/* One-point prolongator column per row (coarse numbering).  ref: hierarchy.py:250-278 */
+int airg_prolong_onepoint(int n, const int32_t* ptr, const int32_t* col, const double* val,
+                          const int8_t* labels, const int32_t* pos, int32_t* pcol, void* stream);
+
+/* ---- sparse products (sparse.py:222-352, polynomial.py:372-416) ---------- */
+/* C = A B (m x k times k x n), structural pattern with cancellation zeros
+ * kept, entries summed k-ascending with separate roundings (== scipy
+ * csr_matmat); negate=1 stores -C (hierarchy.py:200-202,236). */
+int airg_spgemm(int m, int k, int n, const int32_t* Ap, const int32_t* Ac, const double* Av,
+                const int32_t* Bp, const int32_t* Bc, const double* Bv, int negate,
+                airg_csr_result** out, void* stream);
+/* A B restricted to the stored positions of pattern P.  ref: sparse.py:243-263 */
+int airg_spgemm_masked(int m, int k, int n, const int32_t* Ap, const int32_t* Ac, const double* Av,
+                       const int32_t* Bp, const int32_t* Bc, const double* Bv, const int32_t* Pp,
+                       const int32_t* Pc, airg_csr_result** out, void* stream);
+/* sum_k c_k mask(A^k), mask = pattern(A) + diagonal, exact zeros pruned.
+ * ref: polynomial.py:372-416 (arnoldi_coeff kind) */
+int airg_poly_assemble(int n, const int32_t* Ap, const int32_t* Ac, const double* Av, int ncoef,
+                       const double* coef_h, airg_csr_result** out, void* stream);
+/* Row-relative drop (+ sequential lump onto the diagonal); changed_h = any
+ * entry dropped.  ref: sparse.py:307-352 */
+int airg_drop_lump(int m, int ncols, const int32_t* p, const int32_t* c, const double* v,
+                   double tol, int lump, airg_csr_result** out, int32_t* changed_h, void* stream);
+/* Galerkin coarse matrix drop_and_lump(R (A P), a_drop, lump) with the
+ * one-point P given as pcol[n]; the drop/lump runs in the numeric epilogue.
+ * ref: hierarchy.py:281-286 */
+int airg_galerkin(int n, int nc, const int32_t* Rp, const int32_t* Rc, const double* Rv,
+                  const int32_t* Ap, const int32_t* Ac, const double* Av, const int32_t* pcol,
+                  double a_drop, int lump, airg_csr_result** out, void* stream);
+/* A[rows, cols] with colmap[old col] = new col or -1.  ref: sparse.py:278-304 */
+int airg_extract(int nr_sel, const int32_t* rows, const int32_t* p, const int32_t* c,
+                 const double* v, const int32_t* colmap, int ncols_sel, airg_csr_result** out,
+                 void* stream);
+/* map[i] = labels[i] == which ? pos[i] : -1 */
+int airg_label_colmap(int n, const int8_t* labels, int which, const int32_t* pos, int32_t* map,
+                      void* stream);
+/* R = [Z | I] scattered into the fine ordering.  ref: hierarchy.py:239-244 */
+int airg_restriction(int n, int nc, const int32_t* zp, const int32_t* zc, const double* zv,
+                     const int32_t* f_idx, const int32_t* c_idx, airg_csr_result** out,
+                     void* stream);
+
+/* ---- Krylov (polynomial.py:68-110) --------------------------------------
+ * MGS Arnoldi from start vector b (device), m = min(order+1, n) steps, one
+ * reorthogonalisation sweep when ||w|| < 0.7 ||A v||, lucky breakdown at
+ * h_{j+1,j} <= 1e-14 max column norm.  H_h receives the (m+1) x m block
+ * (row-major), k_h the achieved dimension, beta_h = ||b||. */
+int airg_arnoldi(int n, const int32_t* p, const int32_t* c, const double* v, const double* b,
+                 int m, double* H_h, int32_t* k_h, double* beta_h, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -121,6 +121,40 @@ sig('airg_plan_set_coarse', vp, i32, vp, vp, vp, C.c_int, C.c_int, vp, C.c_int, 
 sig('airg_plan_vcycle', vp, C.c_int, vp, vp, C.c_int, vp)
 sig('airg_plan_richardson', vp, vp, vp, f64, f64, C.c_int, C.c_int, vp, vp, vp, vp)
 sig('airg_plan_launches', vp, ret=i64)
+u64 = C.c_uint64
+pp = C.POINTER(vp)
+sig('airg_result_info', vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i64))
+sig('airg_result_take', vp, vp, vp, vp, vp)
+sig('airg_result_free', vp)
+sig('airg_pcg64_fill', u64, u64, u64, u64, i64, f64, f64, vp, vp)
+sig('airg_random_unit', u64, u64, u64, u64, i64, vp, vp, vp)
+sig('airg_diagonal', i32, vp, vp, vp, vp, vp)
+sig('airg_advection_2d', i32, i32, f64, f64, vp, vp, vp, vp)
+sig('airg_strength', i32, vp, vp, vp, i64, f64, pp, pp, vp)
+sig('airg_pmisr', i32, vp, vp, u64, u64, u64, u64, C.c_int, vp, C.POINTER(i32), vp)
+sig('airg_cf_pmisr', i32, vp, vp, vp, i64, f64, u64, u64, u64, u64, C.c_int, vp, C.POINTER(i32),
+    vp)
+sig('airg_ddc_pass', i32, vp, vp, vp, vp, f64, C.c_int, vp, vp)
+sig('airg_split_index', i32, vp, vp, vp, vp, C.POINTER(i32), vp)
+sig('airg_repair_split', i32, vp, vp, vp, C.POINTER(i32), vp)
+sig('airg_prolong_onepoint', i32, vp, vp, vp, vp, vp, vp, vp)
+sig('airg_spgemm', i32, i32, i32, vp, vp, vp, vp, vp, vp, C.c_int, pp, vp)
+sig('airg_spgemm_masked', i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, pp, vp)
+sig('airg_poly_assemble', i32, vp, vp, vp, C.c_int, vp, pp, vp)
+sig('airg_drop_lump', i32, i32, vp, vp, vp, f64, C.c_int, pp, C.POINTER(i32), vp)
+sig('airg_galerkin', i32, i32, vp, vp, vp, vp, vp, vp, vp, f64, C.c_int, pp, vp)
+sig('airg_extract', i32, vp, vp, vp, vp, vp, i32, pp, vp)
+sig('airg_label_colmap', i32, vp, C.c_int, vp, vp, vp)
+sig('airg_restriction', i32, i32, vp, vp, vp, vp, vp, pp, vp)
+sig('airg_arnoldi', i32, vp, vp, vp, vp, C.c_int, vp, C.POINTER(i32), C.POINTER(f64), vp)
+
+
+def pcg_params(seed):
+    """(state_hi, state_lo, inc_hi, inc_lo) of numpy's PCG64(SeedSequence(seed))."""
+    st = np.random.PCG64(np.random.SeedSequence(seed)).state['state']
+    s, inc = int(st['state']), int(st['inc'])
+    m = (1 << 64) - 1
+    return s >> 64, s & m, inc >> 64, inc & m
 
 
 def as_f64(a):

@@ -212,3 +212,236 @@ def resolve_truncate_start(cfg, n_top):
     if n_top <= reach:
         return 0
     return int(np.ceil(np.log2(n_top / reach))) + 2
+
+
+# ---------------------------------------------------------------------------
+# level operators
+# ---------------------------------------------------------------------------
+
+def _colmaps(split):
+    """Device column maps old -> F position / C position (-1 elsewhere)."""
+    from . import _lib as L
+    from .csr import IDX, empty
+    n = split.n
+    fmap, cmap = empty(n, IDX), empty(n, IDX)
+    L.call('airg_label_colmap', n, L.ptr(split.labels), 0, L.ptr(split.pos), L.ptr(fmap),
+           L.stream_handle())
+    L.call('airg_label_colmap', n, L.ptr(split.labels), 1, L.ptr(split.pos), L.ptr(cmap),
+           L.stream_handle())
+    return fmap, cmap
+
+
+def _smoother_for(A_ff, cfg, seed):
+    from .gmres_poly import gmres_poly_arnoldi, neumann_poly
+    if cfg.inverse_type == 'arnoldi':
+        return gmres_poly_arnoldi(A_ff, cfg.poly_order, seed)
+    return neumann_poly(A_ff, cfg.poly_order)
+
+
+def build_restriction(A, split, cfg, level=0, timings=None, return_assembled=False,
+                      smoother=None):
+    """R = [Z I] with Z = -A_cf Ahat_ff, Ahat the fixed-sparsity polynomial
+    (hierarchy.py:211-247).  ``smoother`` injects a precomputed polynomial."""
+    import ctypes as C
+    from . import _lib as L
+    from .csr import drop_and_lump, extract_mapped, spgemm, take
+    from .gmres_poly import assemble_fixed_sparsity
+    with _Timer(timings, 'extract'):
+        fmap, cmap = _colmaps(split)
+        A_ff = extract_mapped(A, split.f_idx, fmap, split.n_f)
+        A_fc = extract_mapped(A, split.f_idx, cmap, split.n_c)
+        A_cf = extract_mapped(A, split.c_idx, fmap, split.n_f)
+    with _Timer(timings, 'polynomial'):
+        if smoother is None:
+            smoother = _smoother_for(A_ff, cfg, derive_seed(cfg.seed, level, SEED_SMOOTHER))
+        assembled = assemble_fixed_sparsity(smoother, A_ff)
+    with _Timer(timings, 'spgemm_R'):
+        Z = spgemm(A_cf, assembled, negate=True)
+    with _Timer(timings, 'drop'):
+        Z = drop_and_lump(Z, cfg.r_drop, lump=False)
+    with _Timer(timings, 'spgemm_R'):
+        r = C.c_void_p()
+        L.call('airg_restriction', A.nrows, split.n_c, L.ptr(Z.row_offsets),
+               L.ptr(Z.col_indices), L.ptr(Z.values), L.ptr(split.f_idx), L.ptr(split.c_idx),
+               C.byref(r), L.stream_handle())
+        R = take(r)
+    if return_assembled:
+        return R, A_ff, A_fc, smoother, assembled
+    return R, A_ff, A_fc, smoother
+
+
+def _prolong_cols(A, split):
+    from . import _lib as L
+    from .csr import IDX, empty
+    pcol = empty(split.n, IDX)
+    L.call('airg_prolong_onepoint', split.n, L.ptr(A.row_offsets), L.ptr(A.col_indices),
+           L.ptr(A.values), L.ptr(split.labels), L.ptr(split.pos), L.ptr(pcol), L.stream_handle())
+    return pcol
+
+
+def build_prolongation(A, split, pcol=None):
+    """One-point classical prolongator P = [W; I] (hierarchy.py:250-278)."""
+    import torch
+    from .csr import IDX, VAL, SparseMatrix
+    n = split.n
+    if split.n_f == 0:
+        return SparseMatrix.identity(n)
+    if pcol is None:
+        pcol = _prolong_cols(A, split)
+    dev = pcol.device
+    return SparseMatrix(n, split.n_c, torch.arange(n + 1, dtype=IDX, device=dev), pcol,
+                        torch.ones(n, dtype=VAL, device=dev))
+
+
+def coarse_matrix(A, R, P, cfg, timings=None):
+    """drop_and_lump(R (A P), a_drop, lump) with the drop fused into the
+    numeric SpGEMM epilogue (hierarchy.py:281-286)."""
+    import ctypes as C
+    from . import _lib as L
+    from .csr import spgemm, take
+    with _Timer(timings, 'spgemm_coarse'):
+        if P.nnz == P.nrows and A.nrows == P.nrows:
+            r = C.c_void_p()
+            L.call('airg_galerkin', A.nrows, R.nrows, L.ptr(R.row_offsets), L.ptr(R.col_indices),
+                   L.ptr(R.values), L.ptr(A.row_offsets), L.ptr(A.col_indices), L.ptr(A.values),
+                   L.ptr(P.col_indices), float(cfg.a_drop), 1 if cfg.lump else 0, C.byref(r),
+                   L.stream_handle())
+            return take(r)
+        from .csr import drop_and_lump
+        return drop_and_lump(spgemm(R, spgemm(A, P)), cfg.a_drop, cfg.lump)
+
+
+def _repair_split(A, split):
+    """F points without a C coupling become C (hierarchy.py:289-305)."""
+    import ctypes as C
+    from . import _lib as L
+    from .cfsplit import CFSplit
+    if split.n_f == 0:
+        return split
+    lab = split.labels.clone()
+    ch = C.c_int32()
+    L.call('airg_repair_split', split.n, L.ptr(A.row_offsets), L.ptr(A.col_indices), L.ptr(lab),
+           C.byref(ch), L.stream_handle())
+    if ch.value == 0:
+        return split
+    return CFSplit.from_labels(lab)
+
+
+def _build_coarse_solver(A, cfg, level):
+    from .gmres_poly import gmres_poly_arnoldi, gmres_poly_newton, neumann_poly
+    seed = derive_seed(cfg.seed, level, SEED_COARSE_POLY)
+    kind = cfg.coarsest_inverse_type
+    if kind == 'newton':
+        return gmres_poly_newton(A, cfg.coarsest_poly_order, seed)
+    if kind == 'arnoldi':
+        return gmres_poly_arnoldi(A, cfg.coarsest_poly_order, seed)
+    return neumann_poly(A, cfg.coarsest_poly_order)
+
+
+def try_truncate(A, cfg, level, start_level=None, solver=None):
+    """Tentative high-order coarse solver test (hierarchy.py:336-362)."""
+    from .csr import norm2, random_unit_vector, spmv
+    from .gmres_poly import apply_matrix_free
+    if start_level is None:
+        start_level = resolve_truncate_start(cfg, A.nrows)
+    if cfg.auto_truncate_tol is None or level < start_level:
+        return None
+    if solver is None:
+        try:
+            solver = _build_coarse_solver(A, cfg, level)
+        except (ValueError, np.linalg.LinAlgError) as exc:
+            _log.warning('tentative coarse solver failed at level %d: %s', level, exc)
+            return None
+    rhs = random_unit_vector(A.nrows, derive_seed(cfg.seed, level, SEED_TRUNC_RHS))
+    x = apply_matrix_free(solver, A, rhs)
+    residual = norm2(rhs - spmv(A, x)) / norm2(rhs)
+    if np.isfinite(residual) and residual <= cfg.auto_truncate_tol:
+        return solver
+    return None
+
+
+def setup(A, cfg, poly_inject=None, keep_level_matrices=False):
+    """Build the multigrid hierarchy on the GPU (hierarchy.py:365-448).
+
+    ``poly_inject`` (test hook, not in the reference API): dict mapping
+    ('smoother', level) / ('coarse', level) to PolySolver objects used instead
+    of recomputing them -- coefficient injection, SURVEY.md 8(c).
+    The recorded polynomials of a run are in ``H.polys``.
+    """
+    from .cfsplit import cf_split
+    from .csr import SparseMatrix, to_dev, IDX, VAL
+    cfg.validate()
+    if not isinstance(A, SparseMatrix):
+        raise TypeError('setup expects a paper_2508_17517_b200.SparseMatrix')
+    if A.nrows != A.ncols:
+        raise ValueError('require a square matrix')
+    if A.nrows == 0:
+        raise ValueError('require a non-empty matrix')
+    inj = poly_inject or {}
+    polys = {}
+    timings = {phase: 0.0 for phase in SETUP_PHASES}
+    truncate_start = resolve_truncate_start(cfg, A.nrows)
+    levels = []
+    current = A
+    level = 0
+    truncated_at = None
+    coarse_solver = None
+
+    def coarse_here(M, lev):
+        with _Timer(timings, 'truncation'):
+            s = inj.get(('coarse', lev)) or _build_coarse_solver(M, cfg, lev)
+        polys[('coarse', lev)] = s
+        return s
+
+    while True:
+        if current.nrows <= cfg.min_coarse_size:
+            coarse_solver = coarse_here(current, level)
+            break
+        if level >= cfg.max_levels:
+            _log.warning('level budget (%d) exhausted at %d unknowns; building the coarse '
+                         'solver here', cfg.max_levels, current.nrows)
+            coarse_solver = coarse_here(current, level)
+            break
+        with _Timer(timings, 'truncation'):
+            cand = None
+            if cfg.auto_truncate_tol is not None and level >= truncate_start:
+                cand = try_truncate(current, cfg, level, start_level=truncate_start,
+                                    solver=inj.get(('coarse', level)))
+        if cand is not None:
+            coarse_solver = cand
+            polys[('coarse', level)] = cand
+            truncated_at = level
+            break
+        with _Timer(timings, 'cf_split'):
+            split, ddc_stats = cf_split(current, cfg.strong_threshold, cfg.ddc_fraction,
+                                        cfg.ddc_its, derive_seed(cfg.seed, level, SEED_SPLIT),
+                                        nbins=cfg.ddc_bins)
+        if split.n_c == split.n:
+            raise ValueError(f'splitting produced no F points at level {level}')
+        if split.n_c > 0:
+            with _Timer(timings, 'cf_split'):
+                split = _repair_split(current, split)
+        if split.n_c == 0 or split.n_f == 0:
+            _log.info('level %d needs no further reduction; building the coarse solver '
+                      'directly', level)
+            coarse_solver = coarse_here(current, level)
+            break
+        R, A_ff, A_fc, smoother, assembled = build_restriction(
+            current, split, cfg, level=level, timings=timings, return_assembled=True,
+            smoother=inj.get(('smoother', level)))
+        polys[('smoother', level)] = smoother
+        with _Timer(timings, 'prolongator'):
+            P = build_prolongation(current, split)
+        coarse = coarse_matrix(current, R, P, cfg, timings=timings)
+        levels.append(Level(R=R, P=P, A_ff=A_ff, A_fc=A_fc, f_smoother=smoother, split=split,
+                            n=current.nrows, nnz_A=current.nnz,
+                            f_smoother_assembled=None if cfg.matrix_free_polys else assembled,
+                            ddc_stats=tuple(ddc_stats)))
+        if keep_level_matrices:
+            levels[-1].A = current
+        current = coarse
+        level += 1
+    H = Hierarchy(levels=levels, coarsest_A=current, coarse_solver=coarse_solver, top_A=A,
+                  truncated_at=truncated_at, config=cfg, setup_breakdown=timings)
+    H.polys = polys
+    return finalize_complexities(H)

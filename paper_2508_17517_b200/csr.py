@@ -7,6 +7,7 @@ int32 row offsets / int32 columns / fp64 values (torch tensors used only as
 device buffers); every operation is an sm_100a kernel in libairg.so.
 """
 
+import ctypes as C
 from dataclasses import dataclass
 
 import numpy as np
@@ -165,3 +166,119 @@ def norm2(x):
     out = np.zeros(1)
     L.call('airg_norm2', x.numel(), L.ptr(x), L.hptr(out), L.stream_handle())
     return float(out[0])
+
+
+# ---------------------------------------------------------------------------
+# variable-size results
+# ---------------------------------------------------------------------------
+
+def new_result():
+    return C.c_void_p()
+
+
+def take(res, values=True):
+    """Copy a library-held airg_csr_result into fresh device tensors."""
+    nr, nc, nnz = C.c_int32(), C.c_int32(), C.c_int64()
+    L.call('airg_result_info', res, C.byref(nr), C.byref(nc), C.byref(nnz))
+    p = empty(nr.value + 1, IDX)
+    c = empty(nnz.value, IDX)
+    v = empty(nnz.value, VAL) if values else None
+    L.call('airg_result_take', res, L.ptr(p), L.ptr(c), L.ptr(v), L.stream_handle())
+    if v is None:
+        v = torch.ones(nnz.value, dtype=VAL, device=p.device)
+    return SparseMatrix(nr.value, nc.value, p, c, v)
+
+
+def _args(A):
+    return L.ptr(A.row_offsets), L.ptr(A.col_indices), L.ptr(A.values)
+
+
+def spgemm(A, B, negate=False):
+    """Structural product, cancellation zeros kept (sparse.py:222-240)."""
+    if A.ncols != B.nrows:
+        raise ValueError(f'cannot multiply {A.nrows}x{A.ncols} by {B.nrows}x{B.ncols}')
+    r = new_result()
+    L.call('airg_spgemm', A.nrows, A.ncols, B.ncols, *_args(A), *_args(B), 1 if negate else 0,
+           C.byref(r), L.stream_handle())
+    return take(r)
+
+
+def spgemm_fixed_sparsity(A, B, pattern):
+    """A @ B restricted to the stored positions of ``pattern`` (sparse.py:243-263)."""
+    if A.ncols != B.nrows:
+        raise ValueError(f'cannot multiply {A.nrows}x{A.ncols} by {B.nrows}x{B.ncols}')
+    if pattern.nrows != A.nrows or pattern.ncols != B.ncols:
+        raise ValueError('pattern shape must match the product shape')
+    r = new_result()
+    L.call('airg_spgemm_masked', A.nrows, A.ncols, B.ncols, *_args(A), *_args(B),
+           L.ptr(pattern.row_offsets), L.ptr(pattern.col_indices), C.byref(r), L.stream_handle())
+    return take(r)
+
+
+def _index_set(idx, limit, name):
+    t = to_dev(idx, IDX)
+    if t.dim() != 1:
+        raise ValueError(f'{name} index set must be one-dimensional')
+    if t.numel():
+        h = t.cpu().numpy()
+        if h[0] < 0 or h[-1] >= limit:
+            raise ValueError(f'{name} index out of range for dimension {limit}')
+        if np.any(np.diff(h) <= 0):
+            raise ValueError(f'{name} index set must be strictly increasing')
+    return t
+
+
+def extract_mapped(A, rows, colmap, ncols):
+    """A[rows, :] with columns renumbered through ``colmap`` (-1 drops)."""
+    r = new_result()
+    L.call('airg_extract', int(rows.numel()), L.ptr(rows), *_args(A), L.ptr(colmap), int(ncols),
+           C.byref(r), L.stream_handle())
+    return take(r)
+
+
+def extract(A, rows, cols):
+    """Submatrix A[rows, cols], renumbered, entry order kept (sparse.py:278-304)."""
+    rows = _index_set(rows, A.nrows, 'row')
+    cols = _index_set(cols, A.ncols, 'column')
+    colmap = torch.full((A.ncols,), -1, dtype=IDX, device=rows.device)
+    colmap[cols.long()] = torch.arange(cols.numel(), dtype=IDX, device=rows.device)
+    return extract_mapped(A, rows, colmap, cols.numel())
+
+
+def drop_and_lump(A, rel_tol, lump):
+    """Row-relative drop, optional sequential lump onto the diagonal (sparse.py:307-352)."""
+    if rel_tol < 0:
+        raise ValueError('rel_tol must be non-negative')
+    if lump and A.nrows != A.ncols:
+        raise ValueError('lumping requires a square matrix')
+    if rel_tol == 0 or A.nnz == 0:
+        return A
+    r = new_result()
+    changed = C.c_int32()
+    L.call('airg_drop_lump', A.nrows, A.ncols, *_args(A), float(rel_tol), 1 if lump else 0,
+           C.byref(r), C.byref(changed), L.stream_handle())
+    out = take(r)
+    return out if changed.value else A
+
+
+def diagonal(A):
+    """Main diagonal as a device vector (sparse.py:360-367)."""
+    n = min(A.nrows, A.ncols)
+    d = empty(n, VAL)
+    L.call('airg_diagonal', n, *_args(A), L.ptr(d), L.stream_handle())
+    return d
+
+
+def pcg_vector(seed, n, a, b):
+    """out[i] = a + b * Generator(PCG64(SeedSequence(seed))).random()_i, on the GPU."""
+    out = empty(n, VAL)
+    L.call('airg_pcg64_fill', *L.pcg_params(seed), int(n), float(a), float(b), L.ptr(out),
+           L.stream_handle())
+    return out
+
+
+def random_unit_vector(n, seed):
+    """uniform(-1, 1, n) normalised (polynomial.py:61-65), generated on the GPU."""
+    out = empty(n, VAL)
+    L.call('airg_random_unit', *L.pcg_params(seed), int(n), L.ptr(out), None, L.stream_handle())
+    return out

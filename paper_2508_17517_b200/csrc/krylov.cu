@@ -1,0 +1,302 @@
+// Arnoldi (modified Gram-Schmidt with one selective reorthogonalisation
+// sweep and the lucky-breakdown rule) for the GMRES-polynomial setup.
+// ref: polynomial.py:61-110 (_random_unit_vector, _arnoldi)
+//
+// Small operators (coarse grids, n <= kArnoldiCta) run the whole Krylov
+// recurrence inside ONE CTA: V lives in global memory (L2-resident), every
+// dot product is a block reduction, no host round trips.  Large operators
+// use a device-resident multi-kernel path: SpMV, fixed-order dot partials,
+// axpy; the reorthogonalisation / breakdown decisions are taken on the host
+// from 2 scalars per step.
+#include "setup_common.cuh"
+#include <vector>
+#include <cmath>
+
+namespace airg {
+
+constexpr int kArnoldiCta = 32768;
+
+__device__ double block_sum(double v, double* red) {
+  v = warp_sum(v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[32] = t;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+__device__ __forceinline__ double rowdot(const int* __restrict__ p, const int* __restrict__ c,
+                                         const double* __restrict__ v, const double* x, int i) {
+  double s = 0.0;
+  for (int k = p[i]; k < p[i + 1]; ++k) s = fma(v[k], x[c[k]], s);
+  return s;
+}
+
+// H is (m+1) x m row-major.  info[0] = k, info[1] = error code, dinfo[0] = beta
+__global__ void __launch_bounds__(1024) arnoldi_cta_kernel(int n, const int* __restrict__ p,
+                                                           const int* __restrict__ c,
+                                                           const double* __restrict__ v,
+                                                           const double* __restrict__ b, int m,
+                                                           double* V, double* w, double* H,
+                                                           int* info, double* dinfo) {
+  __shared__ double red[33];
+  double sq = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sq = fma(b[i], b[i], sq);
+  const double beta = sqrt(block_sum(sq, red));
+  if (threadIdx.x == 0) {
+    dinfo[0] = beta;
+    info[0] = m;
+    info[1] = 0;
+  }
+  if (beta == 0.0) {
+    if (threadIdx.x == 0) info[1] = 1;
+    return;
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) V[i] = b[i] / beta;
+  for (int i = threadIdx.x; i < (m + 1) * m; i += blockDim.x) H[i] = 0.0;
+  __syncthreads();
+  double hmax = 0.0;
+  int k = m;
+  for (int j = 0; j < m; ++j) {
+    const double* Vj = V + (size_t)j * n;
+    sq = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const double t = rowdot(p, c, v, Vj, i);
+      w[i] = t;
+      sq = fma(t, t, sq);
+    }
+    const double before = sqrt(block_sum(sq, red));
+    double hn = 0.0;
+    for (int sweep = 0; sweep < 2; ++sweep) {
+      for (int q = 0; q <= j; ++q) {
+        const double* Vq = V + (size_t)q * n;
+        double d = 0.0;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) d = fma(Vq[i], w[i], d);
+        const double h = block_sum(d, red);
+        if (threadIdx.x == 0) H[q * m + j] += h;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] -= h * Vq[i];
+      }
+      sq = 0.0;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) sq = fma(w[i], w[i], sq);
+      hn = sqrt(block_sum(sq, red));
+      if (!(sweep == 0 && hn < 0.7 * before)) break;  // "twice is enough"
+    }
+    __syncthreads();
+    double cn = 0.0;
+    if (threadIdx.x == 0) {
+      H[(j + 1) * m + j] = hn;
+      for (int q = 0; q <= j + 1; ++q) cn = fma(H[q * m + j], H[q * m + j], cn);
+      red[32] = sqrt(cn);
+    }
+    __syncthreads();
+    hmax = fmax(hmax, red[32]);
+    __syncthreads();
+    if (hn <= 1e-14 * hmax) {
+      if (threadIdx.x == 0) H[(j + 1) * m + j] = 0.0;
+      k = j + 1;
+      break;
+    }
+    double* Vn = V + (size_t)(j + 1) * n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) Vn[i] = w[i] / hn;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) info[0] = k;
+}
+
+// ---- multi-kernel path ----------------------------------------------------
+__global__ void dot_partial_kernel(long long n, const double* __restrict__ x, const double* __restrict__ y,
+                                   double* __restrict__ parts) {
+  __shared__ double red[33];
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    s = fma(x[i], y[i], s);
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) parts[blockIdx.x] = s;
+}
+
+// out = sum(parts) (+ optional accumulate into *acc), fixed order
+__global__ void dot_finish_kernel(int np, const double* __restrict__ parts, double* out, double* acc) {
+  __shared__ double red[33];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) s += parts[i];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) {
+    *out = s;
+    if (acc) *acc += s;
+  }
+}
+
+__global__ void axpy_dev_kernel(long long n, const double* __restrict__ hptr, const double* __restrict__ x,
+                                double* __restrict__ y) {
+  const double h = *hptr;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    y[i] -= h * x[i];
+}
+
+__global__ void scale_div_kernel(long long n, const double* __restrict__ x, double d, double* __restrict__ y) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    y[i] = x[i] / d;
+}
+
+__global__ void spmv_rows_kernel(int n, const int* __restrict__ p, const int* __restrict__ c,
+                                 const double* __restrict__ v, const double* __restrict__ x,
+                                 double* __restrict__ y) {
+  // warp per row (rows of coarse operators are long)
+  const int lane = threadIdx.x & 31;
+  for (long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; r < n;
+       r += ((long long)gridDim.x * blockDim.x) >> 5) {
+    double s = 0.0;
+    for (int k = p[r] + lane; k < p[r + 1]; k += 32) s = fma(v[k], x[c[k]], s);
+    s = warp_sum(s);
+    if (lane == 0) y[r] = s;
+  }
+}
+
+struct DotCtx {
+  double* parts;
+  int np;
+};
+
+static int dev_dot(long long n, const double* x, const double* y, double* out, double* acc,
+                   const DotCtx& d, cudaStream_t s) {
+  dot_partial_kernel<<<d.np, 256, 0, s>>>(n, x, y, d.parts);
+  dot_finish_kernel<<<1, 256, 0, s>>>(d.np, d.parts, out, acc);
+  AIRG_LAUNCH_CHECK();
+  return AIRG_OK;
+}
+
+static int arnoldi_multi(int n, const int* p, const int* c, const double* v, const double* b, int m,
+                         double* H_h, int* k_h, double* beta_h, cudaStream_t s) {
+  double *V = nullptr, *w = nullptr, *sc = nullptr, *Hd = nullptr;
+  const int np = blocks_for(n, 256, 148 * 4);
+  AIRG_TRY(scratch(&V, (size_t)(m + 1) * n, s));
+  AIRG_TRY(scratch(&w, n, s));
+  AIRG_TRY(scratch(&sc, np + 8, s));
+  AIRG_TRY(scratch(&Hd, (size_t)(m + 1) * m, s));
+  AIRG_CUDA(cudaMemsetAsync(Hd, 0, (size_t)(m + 1) * m * sizeof(double), s));
+  DotCtx d{sc + 8, np};
+  double* scal = sc;  // [0] scratch scalar
+  auto host_scalar = [&](double* dptr, double* out) -> int {
+    AIRG_CUDA(cudaMemcpyAsync(out, dptr, sizeof(double), cudaMemcpyDeviceToHost, s));
+    AIRG_CUDA(cudaStreamSynchronize(s));
+    return AIRG_OK;
+  };
+  double bb = 0;
+  AIRG_TRY(dev_dot(n, b, b, scal, nullptr, d, s));
+  AIRG_TRY(host_scalar(scal, &bb));
+  const double beta = std::sqrt(bb);
+  *beta_h = beta;
+  if (beta == 0.0) {
+    set_error("cannot build a Krylov space from a zero vector");
+    return AIRG_ERR_VALUE;
+  }
+  const int nb = blocks_for(n, 256);
+  scale_div_kernel<<<nb, 256, 0, s>>>(n, b, beta, V);
+  double hmax = 0.0;
+  int k = m;
+  std::vector<double> Hh((size_t)(m + 1) * m, 0.0);
+  for (int j = 0; j < m; ++j) {
+    const double* Vj = V + (size_t)j * n;
+    spmv_rows_kernel<<<blocks_for((long long)n * 32, 256), 256, 0, s>>>(n, p, c, v, Vj, w);
+    AIRG_LAUNCH_CHECK();
+    double before2 = 0, hn2 = 0;
+    AIRG_TRY(dev_dot(n, w, w, scal, nullptr, d, s));
+    AIRG_TRY(host_scalar(scal, &before2));
+    const double before = std::sqrt(before2);
+    double hn = 0.0;
+    for (int sweep = 0; sweep < 2; ++sweep) {
+      for (int q = 0; q <= j; ++q) {
+        const double* Vq = V + (size_t)q * n;
+        AIRG_TRY(dev_dot(n, Vq, w, scal + 1, Hd + q * m + j, d, s));
+        axpy_dev_kernel<<<nb, 256, 0, s>>>(n, scal + 1, Vq, w);
+      }
+      AIRG_TRY(dev_dot(n, w, w, scal, nullptr, d, s));
+      AIRG_TRY(host_scalar(scal, &hn2));
+      hn = std::sqrt(hn2);
+      if (!(sweep == 0 && hn < 0.7 * before)) break;
+    }
+    AIRG_CUDA(cudaMemcpyAsync(Hh.data(), Hd, Hh.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    AIRG_CUDA(cudaStreamSynchronize(s));
+    Hh[(size_t)(j + 1) * m + j] = hn;
+    double cn = 0.0;
+    for (int q = 0; q <= j + 1; ++q) cn += Hh[(size_t)q * m + j] * Hh[(size_t)q * m + j];
+    hmax = std::max(hmax, std::sqrt(cn));
+    AIRG_CUDA(cudaMemcpyAsync(Hd + (size_t)(j + 1) * m + j, &Hh[(size_t)(j + 1) * m + j], sizeof(double),
+                              cudaMemcpyHostToDevice, s));
+    if (hn <= 1e-14 * hmax) {
+      Hh[(size_t)(j + 1) * m + j] = 0.0;
+      k = j + 1;
+      break;
+    }
+    scale_div_kernel<<<nb, 256, 0, s>>>(n, w, hn, V + (size_t)(j + 1) * n);
+    AIRG_LAUNCH_CHECK();
+  }
+  AIRG_CUDA(cudaStreamSynchronize(s));
+  for (size_t i = 0; i < Hh.size(); ++i) H_h[i] = Hh[i];
+  *k_h = k;
+  release(V, s);
+  release(w, s);
+  release(sc, s);
+  release(Hd, s);
+  return AIRG_OK;
+}
+
+}  // namespace airg
+
+using namespace airg;
+
+extern "C" int airg_arnoldi(int n, const int32_t* p, const int32_t* c, const double* v,
+                            const double* b, int m, double* H_h, int32_t* k_h, double* beta_h,
+                            void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (m < 1 || n < 1) {
+    set_error("Arnoldi needs m >= 1 and n >= 1");
+    return AIRG_ERR_VALUE;
+  }
+  if (m > n) m = n;
+  int st = AIRG_OK;
+  if (n <= kArnoldiCta) {
+    double *V = nullptr, *w = nullptr, *H = nullptr, *dinfo = nullptr;
+    int* info = nullptr;
+    AIRG_TRY(scratch(&V, (size_t)(m + 1) * n, s));
+    AIRG_TRY(scratch(&w, n, s));
+    AIRG_TRY(scratch(&H, (size_t)(m + 1) * m, s));
+    AIRG_TRY(scratch(&dinfo, 1, s));
+    AIRG_TRY(scratch(&info, 2, s));
+    const int thr = n <= 4096 ? 256 : 1024;
+    arnoldi_cta_kernel<<<1, thr, 0, s>>>(n, p, c, v, b, m, V, w, H, info, dinfo);
+    AIRG_LAUNCH_CHECK();
+    int hi[2];
+    AIRG_CUDA(cudaMemcpyAsync(H_h, H, (size_t)(m + 1) * m * sizeof(double), cudaMemcpyDeviceToHost, s));
+    AIRG_CUDA(cudaMemcpyAsync(hi, info, sizeof hi, cudaMemcpyDeviceToHost, s));
+    AIRG_CUDA(cudaMemcpyAsync(beta_h, dinfo, sizeof(double), cudaMemcpyDeviceToHost, s));
+    AIRG_CUDA(cudaStreamSynchronize(s));
+    for (void* q : {(void*)V, (void*)w, (void*)H, (void*)dinfo, (void*)info}) release(q, s);
+    if (hi[1]) {
+      set_error("cannot build a Krylov space from a zero vector");
+      return AIRG_ERR_VALUE;
+    }
+    *k_h = hi[0];
+  } else {
+    st = arnoldi_multi(n, p, c, v, b, m, H_h, k_h, beta_h, s);
+    if (st != AIRG_OK) return st;
+  }
+  // numerically zero on the Krylov space? (polynomial.py:108-109)
+  const int k = *k_h;
+  double mx = 0.0;
+  for (int i = 0; i <= k; ++i)
+    for (int j = 0; j < k; ++j) mx = std::max(mx, std::fabs(H_h[(size_t)i * m + j]));
+  if (mx == 0.0) {
+    set_error("matrix is numerically zero on the Krylov space");
+    return AIRG_ERR_VALUE;
+  }
+  return AIRG_OK;
+}

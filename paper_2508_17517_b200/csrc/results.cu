@@ -1,0 +1,264 @@
+// Result handles, scans, PCG64 streams and the advection problem generator.
+// ref: problems.py:48-99 (generator), splitting.py:119 / polynomial.py:63 (PCG64)
+#include "setup_common.cuh"
+
+namespace airg {
+
+int scan_counts(const int* in, int* out, int n, long long* total_h, cudaStream_t s) {
+  // out[0] = 0, out[i+1] = sum(in[0..i])
+  void* tmp = nullptr;
+  size_t bytes = 0;
+  AIRG_CUDA(cudaMemsetAsync(out, 0, sizeof(int), s));
+  if (n > 0) {
+    AIRG_CUDA(cub::DeviceScan::InclusiveSum(tmp, bytes, in, out + 1, n, s));
+    AIRG_CUDA(cudaMallocAsync(&tmp, bytes, s));
+    AIRG_CUDA(cub::DeviceScan::InclusiveSum(tmp, bytes, in, out + 1, n, s));
+    cudaFreeAsync(tmp, s);
+  }
+  if (total_h) {
+    int t = 0;
+    AIRG_CUDA(cudaMemcpyAsync(&t, out + n, sizeof(int), cudaMemcpyDeviceToHost, s));
+    AIRG_CUDA(cudaStreamSynchronize(s));
+    *total_h = t;
+  }
+  return AIRG_OK;
+}
+
+int scan_counts64(const long long* in, long long* out, int n, long long* total_h, cudaStream_t s) {
+  void* tmp = nullptr;
+  size_t bytes = 0;
+  AIRG_CUDA(cudaMemsetAsync(out, 0, sizeof(long long), s));
+  if (n > 0) {
+    AIRG_CUDA(cub::DeviceScan::InclusiveSum(tmp, bytes, in, out + 1, n, s));
+    AIRG_CUDA(cudaMallocAsync(&tmp, bytes, s));
+    AIRG_CUDA(cub::DeviceScan::InclusiveSum(tmp, bytes, in, out + 1, n, s));
+    cudaFreeAsync(tmp, s);
+  }
+  if (total_h) {
+    long long t = 0;
+    AIRG_CUDA(cudaMemcpyAsync(&t, out + n, sizeof(long long), cudaMemcpyDeviceToHost, s));
+    AIRG_CUDA(cudaStreamSynchronize(s));
+    *total_h = t;
+  }
+  return AIRG_OK;
+}
+
+airg_csr_result* new_result(int nrows, int ncols, cudaStream_t s) {
+  airg_csr_result* r = new airg_csr_result();
+  r->nrows = nrows;
+  r->ncols = ncols;
+  r->stream = s;
+  if (cudaMallocAsync((void**)&r->ptr, (size_t)(nrows + 1) * sizeof(int), s) != cudaSuccess) {
+    delete r;
+    set_error("out of device memory (result ptr)");
+    return nullptr;
+  }
+  return r;
+}
+
+int result_alloc_entries(airg_csr_result* r, long long nnz, bool values) {
+  r->nnz = nnz;
+  AIRG_CUDA(cudaMallocAsync((void**)&r->col, (size_t)(nnz > 0 ? nnz : 1) * sizeof(int), r->stream));
+  if (values)
+    AIRG_CUDA(cudaMallocAsync((void**)&r->val, (size_t)(nnz > 0 ? nnz : 1) * sizeof(double),
+                              r->stream));
+  return AIRG_OK;
+}
+
+__global__ void pcg_fill_kernel(u128 s0, u128 inc, long long n, long long chunk, double a, double b,
+                                double* __restrict__ out) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long i0 = t * chunk;
+  if (i0 >= n) return;
+  long long i1 = i0 + chunk < n ? i0 + chunk : n;
+  u128 st = pcg_jump(s0, inc, (unsigned long long)i0);
+  for (long long i = i0; i < i1; ++i) {
+    st = pcg_step(st, inc);  // numpy steps first, then outputs the new state
+    out[i] = add_rn(a, mul_rn(b, pcg_out_double(st)));
+  }
+}
+
+int pcg64_fill(u128 s0, u128 inc, long long n, double a, double b, double* out, cudaStream_t s) {
+  if (n <= 0) return AIRG_OK;
+  const long long chunk = 64;
+  const long long threads = (n + chunk - 1) / chunk;
+  pcg_fill_kernel<<<(int)((threads + 255) / 256), 256, 0, s>>>(s0, inc, n, chunk, a, b, out);
+  AIRG_LAUNCH_CHECK();
+  return AIRG_OK;
+}
+
+// 2-D upwind stencil, rows in column order: south (-vy), west (-vx), diag (vx+vy)
+__global__ void advection_kernel(int nx, int ny, double vx, double vy, int* __restrict__ ptr,
+                                 int* __restrict__ col, double* __restrict__ val) {
+  const long long n = (long long)nx * ny;
+  const double dg = add_rn(vx, vy);
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long i = idx % nx, j = idx / nx;
+    long long before = idx;
+    if (vx > 0) before += j * (nx - 1) + (i > 0 ? i - 1 : 0);
+    if (vy > 0) before += idx - nx > 0 ? idx - nx : 0;
+    long long k = before;
+    ptr[idx] = (int)before;
+    if (vy > 0 && j > 0) {
+      col[k] = (int)(idx - nx);
+      val[k] = -vy;
+      ++k;
+    }
+    if (vx > 0 && i > 0) {
+      col[k] = (int)(idx - 1);
+      val[k] = -vx;
+      ++k;
+    }
+    col[k] = (int)idx;
+    val[k] = dg;
+    ++k;
+    if (idx == n - 1) ptr[n] = (int)k;
+  }
+}
+
+}  // namespace airg
+
+using namespace airg;
+
+extern "C" {
+
+int airg_result_info(airg_csr_result* r, int32_t* nrows_h, int32_t* ncols_h, int64_t* nnz_h) {
+  if (!r) {
+    set_error("null result");
+    return AIRG_ERR_ARG;
+  }
+  *nrows_h = r->nrows;
+  *ncols_h = r->ncols;
+  *nnz_h = r->nnz;
+  return AIRG_OK;
+}
+
+int airg_result_take(airg_csr_result* r, int32_t* ptr, int32_t* col, double* val, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!r) {
+    set_error("null result");
+    return AIRG_ERR_ARG;
+  }
+  if (r->stream != s) AIRG_CUDA(cudaStreamSynchronize(r->stream));
+  AIRG_CUDA(cudaMemcpyAsync(ptr, r->ptr, (size_t)(r->nrows + 1) * sizeof(int),
+                            cudaMemcpyDeviceToDevice, s));
+  if (r->nnz > 0) {
+    AIRG_CUDA(cudaMemcpyAsync(col, r->col, (size_t)r->nnz * sizeof(int), cudaMemcpyDeviceToDevice, s));
+    if (val) {
+      if (r->val)
+        AIRG_CUDA(cudaMemcpyAsync(val, r->val, (size_t)r->nnz * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, s));
+      else
+        AIRG_CUDA(cudaMemsetAsync(val, 0, (size_t)r->nnz * sizeof(double), s));
+    }
+  }
+  release(r->ptr, s);
+  release(r->col, s);
+  release(r->val, s);
+  delete r;
+  return AIRG_OK;
+}
+
+int airg_result_free(airg_csr_result* r) {
+  if (!r) return AIRG_OK;
+  release(r->ptr, r->stream);
+  release(r->col, r->stream);
+  release(r->val, r->stream);
+  delete r;
+  return AIRG_OK;
+}
+
+int airg_pcg64_fill(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                    int64_t n, double a, double b, double* out, void* stream) {
+  u128 s0 = {state_lo, state_hi}, inc = {inc_lo, inc_hi};
+  return pcg64_fill(s0, inc, n, a, b, out, (cudaStream_t)stream);
+}
+
+int airg_advection_2d(int nx, int ny, double vx, double vy, int32_t* ptr, int32_t* col,
+                      double* val, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (nx < 1 || ny < 1) {
+    set_error("require nx >= 1 and ny >= 1");
+    return AIRG_ERR_VALUE;
+  }
+  const long long n = (long long)nx * ny;
+  advection_kernel<<<blocks_for(n, 256), 256, 0, s>>>(nx, ny, vx, vy, ptr, col, val);
+  AIRG_LAUNCH_CHECK();
+  return AIRG_OK;
+}
+
+}  // extern "C"
+
+namespace airg {
+__global__ void diagonal_kernel(int n, const int* __restrict__ p, const int* __restrict__ c,
+                                const double* __restrict__ v, double* __restrict__ d) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double x = 0.0;
+    for (int k = p[i]; k < p[i + 1]; ++k)
+      if (c[k] == i) x = v[k];
+    d[i] = x;
+  }
+}
+
+__global__ void sumsq_det_kernel(long long n, const double* __restrict__ x, double* __restrict__ parts) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    s = fma(x[i], x[i], s);
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) parts[blockIdx.x] = t;
+  }
+}
+
+__global__ void div_by_norm_kernel(long long n, int np, const double* __restrict__ parts,
+                                   double* __restrict__ x, double* __restrict__ nrm_out) {
+  __shared__ double nrm;
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < np; ++i) s += parts[i];
+    nrm = sqrt(s);
+    if (blockIdx.x == 0) *nrm_out = nrm;
+  }
+  __syncthreads();
+  const double d = nrm;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    x[i] = x[i] / d;
+}
+}  // namespace airg
+
+extern "C" int airg_diagonal(int n, const int32_t* p, const int32_t* c, const double* v, double* d,
+                             void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n > 0) diagonal_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, p, c, v, d);
+  AIRG_LAUNCH_CHECK();
+  return AIRG_OK;
+}
+
+extern "C" int airg_random_unit(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                                uint64_t inc_lo, int64_t n, double* out, double* norm_h,
+                                void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  u128 s0 = {state_lo, state_hi}, inc = {inc_lo, inc_hi};
+  AIRG_TRY(pcg64_fill(s0, inc, n, -1.0, 2.0, out, s));
+  const int np = blocks_for(n, 256, 512);
+  double* parts = nullptr;
+  AIRG_TRY(scratch(&parts, np + 1, s));
+  sumsq_det_kernel<<<np, 256, 0, s>>>(n, out, parts);
+  div_by_norm_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, np, parts, out, parts + np);
+  AIRG_LAUNCH_CHECK();
+  if (norm_h) {
+    AIRG_CUDA(cudaMemcpyAsync(norm_h, parts + np, sizeof(double), cudaMemcpyDeviceToHost, s));
+    AIRG_CUDA(cudaStreamSynchronize(s));
+  }
+  release(parts, s);
+  return AIRG_OK;
+}

@@ -67,6 +67,8 @@ def poly_args(p):
 
 def apply_matrix_free(p, A, b):
     """q(A) b with SpMVs and vector updates only (polynomial.py:358-369)."""
+    if p.kind not in KIND_CODE:
+        raise ValueError(f'unknown polynomial kind {p.kind!r}')
     b = to_dev(b, VAL)
     if A.nrows != A.ncols or b.numel() != A.ncols:
         raise ValueError('solver, matrix and vector shapes disagree')
@@ -163,6 +165,76 @@ def roots_from_hessenberg(H, k, beta, order, added_root_tol=1e-4):
         seen.extend(u)
     return PolySolver('newton_roots', order, k - 1, roots=np.array(out, dtype=np.complex128),
                       residual_history=_history(H, k, beta))
+
+
+def hessenberg(A, m, b):
+    """Device Arnoldi (polynomial.py:68-110): returns (H (m+1) x m, k, beta)."""
+    import ctypes as C
+    n = A.nrows
+    m = min(m, n)
+    H = np.zeros((m + 1, m))
+    k = C.c_int32()
+    beta = C.c_double()
+    L.call('airg_arnoldi', n, L.ptr(A.row_offsets), L.ptr(A.col_indices), L.ptr(A.values),
+           L.ptr(b), m, L.hptr(H), C.byref(k), C.byref(beta), L.stream_handle())
+    k = k.value
+    return H[:k + 1, :k].copy(), k, beta.value
+
+
+def gmres_poly_arnoldi(A, order, seed):
+    """Minimum-residual polynomial in monomial form (polynomial.py:126-170)."""
+    from .csr import random_unit_vector
+    if A.nrows != A.ncols:
+        raise ValueError('require a square matrix')
+    if order < 0:
+        raise ValueError('order must be non-negative')
+    b = random_unit_vector(A.nrows, seed)
+    H, k, beta = hessenberg(A, order + 1, b)
+    return coeffs_from_hessenberg(H, k, beta, order)
+
+
+def gmres_poly_newton(A, order, seed, added_root_tol=1e-4):
+    """Minimum-residual polynomial in factored Newton form (polynomial.py:257-279)."""
+    from .csr import random_unit_vector
+    if A.nrows != A.ncols:
+        raise ValueError('require a square matrix')
+    if order < 1:
+        raise ValueError('order must be at least 1')
+    b = random_unit_vector(A.nrows, seed)
+    H, k, beta = hessenberg(A, order + 1, b)
+    return roots_from_hessenberg(H, k, beta, order, added_root_tol)
+
+
+def neumann_poly(A, order):
+    """Truncated Neumann series sum_k (I - D^-1 A)^k D^-1 (polynomial.py:282-292)."""
+    from .csr import diagonal
+    if A.nrows != A.ncols:
+        raise ValueError('require a square matrix')
+    if order < 0:
+        raise ValueError('order must be non-negative')
+    d = diagonal(A)
+    if bool((d == 0).any()):
+        raise ValueError('Neumann polynomial requires a nonzero diagonal')
+    return PolySolver('neumann', order, order, coeffs=np.ones(order + 1), diag_scale=1.0 / d)
+
+
+def assemble_fixed_sparsity(p, A):
+    """sum_k c_k mask(A^k), mask = pattern(A) + diagonal (polynomial.py:372-416)."""
+    import ctypes as C
+    from .csr import take
+    if p.kind == 'newton_roots':
+        raise ValueError('fixed-sparsity assembly is defined for coefficient forms only, not '
+                         'newton_roots')
+    if A.nrows != A.ncols:
+        raise ValueError('require a square matrix')
+    if p.kind != 'arnoldi_coeff':
+        raise ValueError('fixed-sparsity assembly of the neumann kind is not implemented on '
+                         'the device')
+    c = np.ascontiguousarray(p.coeffs, dtype=np.float64)
+    r = C.c_void_p()
+    L.call('airg_poly_assemble', A.nrows, L.ptr(A.row_offsets), L.ptr(A.col_indices),
+           L.ptr(A.values), len(c), L.hptr(c), C.byref(r), L.stream_handle())
+    return take(r)
 
 
 def export_diagnostics(p):
