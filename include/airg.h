@@ -53,7 +53,7 @@ int airg_norm2(int n, const double* x, double* out_h, void* stream);
 int airg_poly_apply(int kind, int n, const int32_t* ptr, const int32_t* col, const double* val,
                     int ncoef, const double* coef_h, int nunits, const int32_t* type_h,
                     const double* p1_h, const double* p2_h, const double* diag_scale,
-                    const double* b, double* y, void* stream);
+                    const double* b, double* y, int exact, void* stream);
 
 /* ---- V-cycle / Richardson plan (solve.py:95-167) ------------------------
  * A plan holds device pointers to the retained operators of a hierarchy
@@ -89,6 +89,10 @@ int airg_plan_vcycle(airg_plan* plan, int level, const double* r, double* e,
 int airg_plan_richardson(airg_plan* plan, const double* b, double* x, double rtol,
                          double atol, int max_iters, int f_smooth_its, double* history_h,
                          int* iterations_h, int* converged_h, void* stream);
+/* exact=1: every solve kernel follows the reference's arithmetic order
+ * (sequential row sums, separate mul/add roundings) so x is bitwise the
+ * reference's for the same hierarchy; exact=0 (default): vector SpMV + FMA. */
+int airg_plan_set_exact(airg_plan* plan, int exact);
 /* Number of kernel launches issued by the last airg_plan_richardson call. */
 int64_t airg_plan_launches(airg_plan* plan);
 

@@ -111,7 +111,8 @@ sig('airg_sm_count')
 sig('airg_spmv', i32, vp, vp, vp, vp, vp, C.c_int, vp)
 sig('airg_norm2', i32, vp, vp, vp)
 sig('airg_poly_apply', C.c_int, i32, vp, vp, vp, C.c_int, vp, C.c_int, vp, vp, vp, vp, vp, vp,
-    vp)
+    C.c_int, vp)
+sig('airg_plan_set_exact', vp, C.c_int)
 sig('airg_plan_create', C.c_int, C.POINTER(vp))
 sig('airg_plan_destroy', vp)
 sig('airg_plan_set_top', vp, i32, vp, vp, vp)

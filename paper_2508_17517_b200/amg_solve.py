@@ -112,11 +112,12 @@ class Plan:
         return int(L.load().airg_plan_launches(self.h))
 
 
-def plan_for(H):
+def plan_for(H, exact=False):
     p = getattr(H, '_plan', None)
     if p is None:
         p = Plan(H)
         H._plan = p
+    L.call('airg_plan_set_exact', p.h, 1 if exact else 0)
     return p
 
 
@@ -126,8 +127,9 @@ def _level_size(H, level):
     return H.levels[level].n
 
 
-def vcycle(H, level, r, cfg):
-    """Error estimate for A_level e = r from one V-cycle (solve.py:95-110)."""
+def vcycle(H, level, r, cfg, exact=False):
+    """Error estimate for A_level e = r from one V-cycle (solve.py:95-110).
+    ``exact=True`` runs the reference-order arithmetic (parity mode)."""
     if level < 0 or level > len(H.levels):
         raise ValueError(f'level {level} out of range')
     n = _level_size(H, level)
@@ -135,22 +137,25 @@ def vcycle(H, level, r, cfg):
     if r.numel() != n:
         raise ValueError('residual has wrong length for this level')
     e = empty(n, VAL)
-    L.call('airg_plan_vcycle', plan_for(H).h, level, L.ptr(r), L.ptr(e), cfg.f_smooth_its,
+    L.call('airg_plan_vcycle', plan_for(H, exact).h, level, L.ptr(r), L.ptr(e), cfg.f_smooth_its,
            L.stream_handle())
     return e
 
 
-def richardson_solve(H, b, x0, cfg):
+def richardson_solve(H, b, x0, cfg, exact=False):
     """Undamped Richardson iteration preconditioned by one V-cycle
     (solve.py:113-167).  ``b``/``x0`` may be numpy or device tensors; ``x`` is
-    returned as a device tensor."""
+    returned as a device tensor.  ``exact=True`` selects the parity mode in
+    which every kernel follows the reference's arithmetic order (x is then
+    bitwise the reference's for the same hierarchy); the default is the fast
+    vector/FMA path."""
     cfg.validate()
     A = H.top_A
     b = to_dev(b, VAL)
     x = to_dev(x0, VAL).clone()
     if b.numel() != A.nrows or x.numel() != A.nrows:
         raise ValueError('right-hand side or initial guess has wrong length')
-    plan = plan_for(H)
+    plan = plan_for(H, exact)
     hist = np.zeros(cfg.max_iters + 1)
     its = C.c_int(0)
     conv = C.c_int(0)

@@ -38,7 +38,16 @@ struct Epi {
   double* partial;  // optional: per-block sum of squares of value
 };
 
-template <int VS>
+template <bool E>
+__device__ __forceinline__ double madd(double a, double b, double c) {
+  return E ? add_rn(c, mul_rn(a, b)) : fma(a, b, c);
+}
+template <bool E>
+__device__ __forceinline__ double mul(double a, double b) {
+  return E ? mul_rn(a, b) : a * b;
+}
+
+template <int VS, bool E>
 __global__ void __launch_bounds__(256) spmv_vec_kernel(int nrows, const int* __restrict__ ptr,
                                                        const int* __restrict__ col,
                                                        const double* __restrict__ val,
@@ -47,7 +56,11 @@ __global__ void __launch_bounds__(256) spmv_vec_kernel(int nrows, const int* __r
   const int lane = threadIdx.x & (VS - 1);
   const long long row = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / VS;
   double s = 0.0;
-  if (row < nrows) {
+  if (E && row < nrows) {
+    // reference order: s = 0; s = s + a*x, column order, separate roundings
+    const int b = __ldg(ptr + row), e = __ldg(ptr + row + 1);
+    for (int k = b; k < e; ++k) s = add_rn(s, mul_rn(__ldg(val + k), mul_rn(xs, __ldg(x + __ldg(col + k)))));
+  } else if (row < nrows) {
     const int b = __ldg(ptr + row), e = __ldg(ptr + row + 1);
     int k = b + lane;
     // two independent accumulators for MLP on long rows
@@ -65,8 +78,8 @@ __global__ void __launch_bounds__(256) spmv_vec_kernel(int nrows, const int* __r
   }
   double sq = 0.0;
   if (lane == 0 && row < nrows) {
-    double r = ep.alpha * s;
-    if (ep.v) r = fma(ep.beta, ep.v[ep.vmap ? ep.vmap[row] : row], r);
+    double r = mul<E>(ep.alpha, s);
+    if (ep.v) r = madd<E>(ep.beta, ep.v[ep.vmap ? ep.vmap[row] : row], r);
     const long long o = ep.omap ? ep.omap[row] : row;
     if (ep.out) ep.out[o] = r;
     if (ep.acc) ep.acc[o] += r;
@@ -119,13 +132,21 @@ struct Csr {
 
 static long long g_launches = 0;
 
-static int launch_spmv(const Csr& A, const double* x, double xs, const Epi& ep, cudaStream_t s) {
+static int launch_spmv(const Csr& A, const double* x, double xs, const Epi& ep, cudaStream_t s,
+                       bool exact = false) {
   if (A.nrows == 0) return AIRG_OK;
   const int threads = 256;
+  if (exact) {
+    spmv_vec_kernel<1, true><<<(A.nrows + threads - 1) / threads, threads, 0, s>>>(
+        A.nrows, A.ptr, A.col, A.val, x, xs, ep);
+    ++g_launches;
+    AIRG_LAUNCH_CHECK();
+    return AIRG_OK;
+  }
   const long long groups = (long long)A.nrows * A.vs;
   const int blocks = (int)((groups + threads - 1) / threads);
 #define AIRG_SPMV_CASE(V) \
-  case V: spmv_vec_kernel<V><<<blocks, threads, 0, s>>>(A.nrows, A.ptr, A.col, A.val, x, xs, ep); break;
+  case V: spmv_vec_kernel<V, false><<<blocks, threads, 0, s>>>(A.nrows, A.ptr, A.col, A.val, x, xs, ep); break;
   switch (A.vs) {
     AIRG_SPMV_CASE(1)
     AIRG_SPMV_CASE(2)
@@ -146,27 +167,31 @@ static int spmv_blocks(const Csr& A) {
 }
 
 // out[omap(i)] = a * x[xmap(i)] + b * y[i]   (elementwise helpers)
+template <bool E>
 __global__ void axpby_kernel(long long n, double* __restrict__ out, const int* __restrict__ omap,
                              double a, const double* __restrict__ x, const int* __restrict__ xmap,
                              double b, const double* __restrict__ y) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
-    double r = a * x[xmap ? xmap[i] : i];
-    if (y) r = fma(b, y[i], r);
+    double r = mul<E>(a, x[xmap ? xmap[i] : i]);
+    if (y) r = madd<E>(b, y[i], r);
     out[omap ? omap[i] : i] = r;
   }
 }
 
 static int launch_axpby(long long n, double* out, const int* omap, double a, const double* x,
-                        const int* xmap, double b, const double* y, cudaStream_t s) {
+                        const int* xmap, double b, const double* y, cudaStream_t s,
+                        bool exact = false) {
   if (n == 0) return AIRG_OK;
-  axpby_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, out, omap, a, x, xmap, b, y);
+  if (exact) axpby_kernel<true><<<blocks_for(n, 256), 256, 0, s>>>(n, out, omap, a, x, xmap, b, y);
+  else axpby_kernel<false><<<blocks_for(n, 256), 256, 0, s>>>(n, out, omap, a, x, xmap, b, y);
   ++g_launches;
   AIRG_LAUNCH_CHECK();
   return AIRG_OK;
 }
 
 // Neumann step: t_new = t - ds .* (A t); acc += t_new.
+template <bool E>
 __global__ void neumann_step_kernel(int n, const int* __restrict__ ptr, const int* __restrict__ col,
                                     const double* __restrict__ val, const double* __restrict__ ds,
                                     const double* __restrict__ t, double* __restrict__ tn,
@@ -174,10 +199,10 @@ __global__ void neumann_step_kernel(int n, const int* __restrict__ ptr, const in
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     double s = 0.0;
-    for (int k = ptr[i]; k < ptr[i + 1]; ++k) s = fma(val[k], t[col[k]], s);
-    double v = t[i] - ds[i] * s;
+    for (int k = ptr[i]; k < ptr[i + 1]; ++k) s = madd<E>(val[k], t[col[k]], s);
+    double v = E ? sub_rn(t[i], mul_rn(ds[i], s)) : t[i] - ds[i] * s;
     tn[i] = v;
-    acc[i] += v;
+    acc[i] = E ? add_rn(acc[i], v) : acc[i] + v;
   }
 }
 
@@ -234,13 +259,15 @@ __device__ __forceinline__ double block_max(double v, double* red) {
   return r;
 }
 
+template <bool E>
 __device__ __forceinline__ double row_dot(const int* __restrict__ ptr, const int* __restrict__ col,
                                           const double* __restrict__ val, const double* x, int i) {
   double s = 0.0;
-  for (int k = ptr[i]; k < ptr[i + 1]; ++k) s = fma(val[k], x[col[k]], s);
+  for (int k = ptr[i]; k < ptr[i + 1]; ++k) s = madd<E>(val[k], x[col[k]], s);
   return s;
 }
 
+template <bool E>
 __global__ void __launch_bounds__(1024) newton_cta_kernel(
     int n, const int* __restrict__ ptr, const int* __restrict__ col, const double* __restrict__ val,
     const double* __restrict__ b, double* x, double* u, double* w, double* z, int nunits,
@@ -260,29 +287,32 @@ __global__ void __launch_bounds__(1024) newton_cta_kernel(
       int bad = 0;
       for (int i = threadIdx.x; i < n; i += blockDim.x) bad |= !isfinite(sc * u[i]);
       if (__syncthreads_or(bad)) break;
-      for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] = row_dot(ptr, col, val, u, i);
+      for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] = row_dot<E>(ptr, col, val, u, i);
       __syncthreads();
       for (int i = threadIdx.x; i < n; i += blockDim.x) {
         const double ui = u[i];
-        x[i] += sc * ui;
-        const double un = ui - w[i] / t;
+        x[i] = E ? add_rn(x[i], mul_rn(sc, ui)) : x[i] + sc * ui;
+        const double un = E ? sub_rn(ui, __ddiv_rn(w[i], t)) : ui - w[i] / t;
         u[i] = un;
         lmax = fmax(lmax, fabs(un));
       }
     } else {
       const double two_a = up1[k], m2 = up2[k];
       const double sc = scale / m2;
-      for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] = row_dot(ptr, col, val, u, i);
+      for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] = row_dot<E>(ptr, col, val, u, i);
       __syncthreads();
       int bad = 0;
-      for (int i = threadIdx.x; i < n; i += blockDim.x) bad |= !isfinite(sc * (two_a * u[i] - w[i]));
+      for (int i = threadIdx.x; i < n; i += blockDim.x)
+        bad |= !isfinite(mul<E>(sc, E ? sub_rn(mul_rn(two_a, u[i]), w[i]) : two_a * u[i] - w[i]));
       if (__syncthreads_or(bad)) break;
       for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        x[i] += sc * (two_a * u[i] - w[i]);
-        z[i] = row_dot(ptr, col, val, w, i);
+        if (E) x[i] = add_rn(x[i], mul_rn(sc, sub_rn(mul_rn(two_a, u[i]), w[i])));
+        else x[i] += sc * (two_a * u[i] - w[i]);
+        z[i] = row_dot<E>(ptr, col, val, w, i);
       }
       for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const double un = u[i] + (z[i] - two_a * w[i]) / m2;
+        const double un = E ? add_rn(u[i], __ddiv_rn(sub_rn(z[i], mul_rn(two_a, w[i])), m2))
+                            : u[i] + (z[i] - two_a * w[i]) / m2;
         u[i] = un;
         lmax = fmax(lmax, fabs(un));
       }
@@ -332,15 +362,17 @@ __global__ void newton_check_kernel(int n, int type, double p1, double p2, const
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
+template <bool E>
 __global__ void newton_rowspmv_kernel(int n, const int* __restrict__ ptr, const int* __restrict__ col,
                                       const double* __restrict__ val, const double* in, double* out,
                                       const NewtonState* st, const int* flag) {
   if (st->stop || *flag) return;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
-    out[i] = row_dot(ptr, col, val, in, (int)i);
+    out[i] = row_dot<E>(ptr, col, val, in, (int)i);
 }
 
+template <bool E>
 __global__ void newton_update_kernel(int n, int type, double p1, double p2, double* x, double* u,
                                      const double* w, const double* z, const NewtonState* st,
                                      const int* flag, double* parts) {
@@ -351,7 +383,15 @@ __global__ void newton_update_kernel(int n, int type, double p1, double p2, doub
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     double un;
-    if (type == 0) {
+    if (E) {
+      if (type == 0) {
+        x[i] = add_rn(x[i], mul_rn(sc, u[i]));
+        un = sub_rn(u[i], __ddiv_rn(w[i], p1));
+      } else {
+        x[i] = add_rn(x[i], mul_rn(sc, sub_rn(mul_rn(p1, u[i]), w[i])));
+        un = add_rn(u[i], __ddiv_rn(sub_rn(z[i], mul_rn(p1, w[i])), p2));
+      }
+    } else if (type == 0) {
       x[i] += sc * u[i];
       un = u[i] - w[i] / p1;
     } else {
@@ -434,12 +474,46 @@ struct Work {
   size_t cap = 0;
 };
 
+template <bool E>
+static int newton_multi(const Poly& p, const Csr& A, const double* b, double* y, double* t0,
+                        double* t1, double* t2, int* iflag, double* parts, NewtonState* nst,
+                        cudaStream_t s) {
+  const int n = A.nrows;
+  const int nunits = (int)p.utype.size();
+  const int thr = 256;
+  const int nb = blocks_for(n, thr, 148 * 8);
+  newton_init_kernel<<<nb, thr, 0, s>>>(n, b, t0, y, nst);
+  ++g_launches;
+  for (int k = 0; k < nunits; ++k) {
+    const int ty = p.utype[k];
+    AIRG_CUDA(cudaMemsetAsync(iflag, 0, sizeof(int), s));
+    if (ty == 1) {
+      newton_rowspmv_kernel<E><<<nb, thr, 0, s>>>(n, A.ptr, A.col, A.val, t0, t1, nst, iflag);
+      ++g_launches;
+    }
+    newton_check_kernel<<<nb, thr, 0, s>>>(n, ty, p.p1[k], p.p2[k], t0, t1, nst, iflag);
+    ++g_launches;
+    if (ty == 0) {
+      newton_rowspmv_kernel<E><<<nb, thr, 0, s>>>(n, A.ptr, A.col, A.val, t0, t1, nst, iflag);
+    } else {
+      newton_rowspmv_kernel<E><<<nb, thr, 0, s>>>(n, A.ptr, A.col, A.val, t1, t2, nst, iflag);
+    }
+    ++g_launches;
+    newton_update_kernel<E><<<nb, thr, 0, s>>>(n, ty, p.p1[k], p.p2[k], y, t0, t1, t2, nst, iflag,
+                                            parts);
+    newton_rescale_kernel<<<1, 1024, 0, s>>>(n, nb, parts, t0, nst, iflag);
+    g_launches += 2;
+  }
+  AIRG_LAUNCH_CHECK();
+  return AIRG_OK;
+}
+
 // y = q(A) b using scratch t0..t3 (each n doubles).  ymap: optional scatter
 // of the result (y[ymap[i]] = ...).  Only the Horner path supports ymap; the
 // caller handles others.
 static int poly_apply_dev(const Poly& p, const Csr& A, const double* b, double* y, double* t0,
                           double* t1, double* t2, double* t3, int* iflag, double* parts,
-                          NewtonState* nst, cudaStream_t s) {
+                          NewtonState* nst, cudaStream_t s, bool exact) {
   const int n = A.nrows;
   if (n == 0) return AIRG_OK;
   if (p.kind == 0) {
@@ -448,7 +522,7 @@ static int poly_apply_dev(const Poly& p, const Csr& A, const double* b, double* 
       set_error("empty coefficient polynomial");
       return AIRG_ERR_ARG;
     }
-    if (d == 0) return launch_axpby(n, y, nullptr, p.coef[0], b, nullptr, 0.0, nullptr, s);
+    if (d == 0) return launch_axpby(n, y, nullptr, p.coef[0], b, nullptr, 0.0, nullptr, s, exact);
     // y_1 = A (c_d b) + c_{d-1} b ; y_{j} = A y_{j-1} + c_j b
     const double* cur = b;
     double xs = p.coef[d];
@@ -456,7 +530,7 @@ static int poly_apply_dev(const Poly& p, const Csr& A, const double* b, double* 
     for (int j = d - 1; j >= 0; --j) {
       double* dst = (j == 0) ? y : bufs[j & 1];
       Epi ep{dst, nullptr, 1.0, p.coef[j], b, nullptr, nullptr, nullptr};
-      AIRG_TRY(launch_spmv(A, cur, xs, ep, s));
+      AIRG_TRY(launch_spmv(A, cur, xs, ep, s, exact));
       cur = dst;
       xs = 1.0;
     }
@@ -470,8 +544,12 @@ static int poly_apply_dev(const Poly& p, const Csr& A, const double* b, double* 
     double* cur = t0;
     double* nxt = t1;
     for (int it = 0; it < order; ++it) {
-      neumann_step_kernel<<<blocks_for(n, thr), thr, 0, s>>>(n, A.ptr, A.col, A.val, p.diag_scale,
-                                                            cur, nxt, y);
+      if (exact)
+        neumann_step_kernel<true><<<blocks_for(n, thr), thr, 0, s>>>(n, A.ptr, A.col, A.val,
+                                                                   p.diag_scale, cur, nxt, y);
+      else
+        neumann_step_kernel<false><<<blocks_for(n, thr), thr, 0, s>>>(n, A.ptr, A.col, A.val,
+                                                                    p.diag_scale, cur, nxt, y);
       ++g_launches;
       AIRG_LAUNCH_CHECK();
       std::swap(cur, nxt);
@@ -481,38 +559,18 @@ static int poly_apply_dev(const Poly& p, const Csr& A, const double* b, double* 
   // Newton
   const int nunits = (int)p.utype.size();
   if (n <= kNewtonCtaMax) {
-    newton_cta_kernel<<<1, 1024, 0, s>>>(n, A.ptr, A.col, A.val, b, y, t0, t1, t2, nunits,
-                                         p.d_utype, p.d_p1, p.d_p2);
+    if (exact)
+      newton_cta_kernel<true><<<1, 1024, 0, s>>>(n, A.ptr, A.col, A.val, b, y, t0, t1, t2, nunits,
+                                                 p.d_utype, p.d_p1, p.d_p2);
+    else
+      newton_cta_kernel<false><<<1, 1024, 0, s>>>(n, A.ptr, A.col, A.val, b, y, t0, t1, t2, nunits,
+                                                  p.d_utype, p.d_p1, p.d_p2);
     ++g_launches;
     AIRG_LAUNCH_CHECK();
     return AIRG_OK;
   }
-  const int thr = 256;
-  const int nb = blocks_for(n, thr, 148 * 8);
-  newton_init_kernel<<<nb, thr, 0, s>>>(n, b, t0, y, nst);
-  ++g_launches;
-  for (int k = 0; k < nunits; ++k) {
-    const int ty = p.utype[k];
-    AIRG_CUDA(cudaMemsetAsync(iflag, 0, sizeof(int), s));
-    if (ty == 1) {
-      newton_rowspmv_kernel<<<nb, thr, 0, s>>>(n, A.ptr, A.col, A.val, t0, t1, nst, iflag);
-      ++g_launches;
-    }
-    newton_check_kernel<<<nb, thr, 0, s>>>(n, ty, p.p1[k], p.p2[k], t0, t1, nst, iflag);
-    ++g_launches;
-    if (ty == 0) {
-      newton_rowspmv_kernel<<<nb, thr, 0, s>>>(n, A.ptr, A.col, A.val, t0, t1, nst, iflag);
-    } else {
-      newton_rowspmv_kernel<<<nb, thr, 0, s>>>(n, A.ptr, A.col, A.val, t1, t2, nst, iflag);
-    }
-    ++g_launches;
-    newton_update_kernel<<<nb, thr, 0, s>>>(n, ty, p.p1[k], p.p2[k], y, t0, t1, t2, nst, iflag,
-                                            parts);
-    newton_rescale_kernel<<<1, 1024, 0, s>>>(n, nb, parts, t0, nst, iflag);
-    g_launches += 2;
-  }
-  AIRG_LAUNCH_CHECK();
-  return AIRG_OK;
+  return exact ? newton_multi<true>(p, A, b, y, t0, t1, t2, iflag, parts, nst, s)
+               : newton_multi<false>(p, A, b, y, t0, t1, t2, iflag, parts, nst, s);
 }
 
 static int build_poly(Poly& p, int kind, int ncoef, const double* coef_h, int nunits,
@@ -618,6 +676,7 @@ struct airg_plan {
   int nparts_cap = 0;
   long long launches = 0;
   bool ready_top = false, ready_coarse = false;
+  bool exact = false;  // reference arithmetic order (parity mode)
 };
 
 static int alloc_vec(double** p, long long n) {
@@ -679,7 +738,7 @@ int airg_norm2(int n, const double* x, double* out_h, void* stream) {
 int airg_poly_apply(int kind, int n, const int32_t* ptr, const int32_t* col, const double* val,
                     int ncoef, const double* coef_h, int nunits, const int32_t* type_h,
                     const double* p1_h, const double* p2_h, const double* diag_scale,
-                    const double* b, double* y, void* stream) {
+                    const double* b, double* y, int exact, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   Poly p;
   AIRG_TRY(build_poly(p, kind, ncoef, coef_h, nunits, type_h, p1_h, p2_h, diag_scale));
@@ -691,7 +750,8 @@ int airg_poly_apply(int kind, int n, const int32_t* ptr, const int32_t* col, con
   int* iflag = (int*)(parts + nb);
   NewtonState* nst = (NewtonState*)(parts + nb + 2);
   const size_t nn = n > 0 ? n : 1;
-  int st = poly_apply_dev(p, A, b, y, w, w + nn, w + 2 * nn, w + 3 * nn, iflag, parts, nst, s);
+  int st = poly_apply_dev(p, A, b, y, w, w + nn, w + 2 * nn, w + 3 * nn, iflag, parts, nst, s,
+                          exact != 0);
   release(w, s);
   cudaStreamSynchronize(s);
   free_poly(p);
@@ -801,10 +861,10 @@ int airg_plan_set_coarse(airg_plan* p, int n, const int32_t* ptr, const int32_t*
 static int smooth_level(airg_plan* p, LevelOps& L, const double* rhs, double* out, cudaStream_t s) {
   if (L.has_asm) {
     Epi ep{out, nullptr, 1.0, 0.0, nullptr, nullptr, nullptr, nullptr};
-    return launch_spmv(L.Asm, rhs, 1.0, ep, s);
+    return launch_spmv(L.Asm, rhs, 1.0, ep, s, p->exact);
   }
   return poly_apply_dev(L.sm, L.Aff, rhs, out, L.t0, L.t1, L.t2, L.t2, p->iflag, p->parts, p->nst,
-                        s);
+                        s, p->exact);
 }
 
 // V-cycle from `level` with residual r (size n_level) -> e (size n_level).
@@ -816,36 +876,36 @@ static int vcycle_rec(airg_plan* p, int level, const double* r, double* e, int f
       return AIRG_ERR_ARG;
     }
     return poly_apply_dev(p->coarse_poly, p->coarse, r, e, p->cw0, p->cw1, p->cw2, p->cw3,
-                          p->iflag, p->parts, p->nst, s);
+                          p->iflag, p->parts, p->nst, s, p->exact);
   }
   LevelOps& L = p->lv[level];
   // r_c = R r
   {
     Epi ep{L.rc, nullptr, 1.0, 0.0, nullptr, nullptr, nullptr, nullptr};
-    AIRG_TRY(launch_spmv(L.R, r, 1.0, ep, s));
+    AIRG_TRY(launch_spmv(L.R, r, 1.0, ep, s, p->exact));
   }
   AIRG_TRY(vcycle_rec(p, level + 1, L.rc, L.ec, fits, s));
   // rhs = r[f] - A_fc e_c
   {
     Epi ep{L.rhs, nullptr, -1.0, 1.0, r, L.f_idx, nullptr, nullptr};
-    AIRG_TRY(launch_spmv(L.Afc, L.ec, 1.0, ep, s));
+    AIRG_TRY(launch_spmv(L.Afc, L.ec, 1.0, ep, s, p->exact));
   }
   AIRG_TRY(smooth_level(p, L, L.rhs, L.ef, s));
   for (int it = 1; it < fits; ++it) {
     // t1 = rhs - A_ff ef ; ef += q(A_ff) t1
     Epi ep{L.t1, nullptr, -1.0, 1.0, L.rhs, nullptr, nullptr, nullptr};
-    AIRG_TRY(launch_spmv(L.Aff, L.ef, 1.0, ep, s));
+    AIRG_TRY(launch_spmv(L.Aff, L.ef, 1.0, ep, s, p->exact));
     double* tmp = nullptr;
     AIRG_TRY(scratch(&tmp, 2 * (size_t)(L.n_f > 0 ? L.n_f : 1), s));
     AIRG_CUDA(cudaMemcpyAsync(tmp, L.t1, L.n_f * sizeof(double), cudaMemcpyDeviceToDevice, s));
     double* corr = tmp + (L.n_f > 0 ? L.n_f : 1);
     AIRG_TRY(smooth_level(p, L, tmp, corr, s));
-    AIRG_TRY(launch_axpby(L.n_f, L.ef, nullptr, 1.0, corr, nullptr, 1.0, L.ef, s));
+    AIRG_TRY(launch_axpby(L.n_f, L.ef, nullptr, 1.0, L.ef, nullptr, 1.0, corr, s, p->exact));
     release(tmp, s);
   }
   // scatter e[f] = ef, e[c] = ec
-  AIRG_TRY(launch_axpby(L.n_f, e, L.f_idx, 1.0, L.ef, nullptr, 0.0, nullptr, s));
-  AIRG_TRY(launch_axpby(L.n_c, e, L.c_idx, 1.0, L.ec, nullptr, 0.0, nullptr, s));
+  AIRG_TRY(launch_axpby(L.n_f, e, L.f_idx, 1.0, L.ef, nullptr, 0.0, nullptr, s, p->exact));
+  AIRG_TRY(launch_axpby(L.n_c, e, L.c_idx, 1.0, L.ec, nullptr, 0.0, nullptr, s, p->exact));
   return AIRG_OK;
 }
 
@@ -862,20 +922,25 @@ int airg_plan_vcycle(airg_plan* p, int level, const double* r, double* e, int f_
 
 int64_t airg_plan_launches(airg_plan* p) { return p ? p->launches : 0; }
 
+int airg_plan_set_exact(airg_plan* p, int exact) {
+  p->exact = exact != 0;
+  return AIRG_OK;
+}
+
 }  // extern "C"
 
 // r = b - A x, with deterministic norm into p->norm_h (synchronous)
 static int residual_norm(airg_plan* p, const double* b, const double* x, double* rnorm,
                          cudaStream_t s) {
   const Csr& A = p->top;
-  const int nb = spmv_blocks(A);
+  const int nb = p->exact ? (A.nrows + 255) / 256 : spmv_blocks(A);  // blocks of the launch below
   double* parts = p->parts;
   if (nb > p->nparts_cap) {
     set_error("partials buffer too small");
     return AIRG_ERR_ARG;
   }
   Epi ep{p->r, nullptr, -1.0, 1.0, b, nullptr, nullptr, parts};
-  AIRG_TRY(launch_spmv(A, x, 1.0, ep, s));
+  AIRG_TRY(launch_spmv(A, x, 1.0, ep, s, p->exact));
   finish_norm_kernel<<<1, 1024, 0, s>>>(nb, parts, p->norm_d);
   ++g_launches;
   AIRG_LAUNCH_CHECK();
@@ -922,7 +987,7 @@ extern "C" int airg_plan_richardson(airg_plan* p, const double* b, double* x, do
   int its = 0;
   while (!conv && its < max_iters) {
     AIRG_TRY(vcycle_rec(p, 0, p->r, p->e, f_smooth_its < 1 ? 1 : f_smooth_its, s));
-    AIRG_TRY(launch_axpby(n, x, nullptr, 1.0, p->e, nullptr, 1.0, x, s));
+    AIRG_TRY(launch_axpby(n, x, nullptr, 1.0, x, nullptr, 1.0, p->e, s, p->exact));
     AIRG_TRY(residual_norm(p, b, x, &rnorm, s));
     ++its;
     history[its] = rnorm;

@@ -65,8 +65,9 @@ def poly_args(p):
     return code, len(c), c, 0, None, None, None, ds, (c,)
 
 
-def apply_matrix_free(p, A, b):
-    """q(A) b with SpMVs and vector updates only (polynomial.py:358-369)."""
+def apply_matrix_free(p, A, b, exact=False):
+    """q(A) b with SpMVs and vector updates only (polynomial.py:358-369).
+    ``exact=True`` follows the reference's arithmetic order bit for bit."""
     if p.kind not in KIND_CODE:
         raise ValueError(f'unknown polynomial kind {p.kind!r}')
     b = to_dev(b, VAL)
@@ -76,7 +77,7 @@ def apply_matrix_free(p, A, b):
     y = empty(A.nrows, VAL)
     L.call('airg_poly_apply', code, A.nrows, L.ptr(A.row_offsets), L.ptr(A.col_indices),
            L.ptr(A.values), nc, L.hptr(c), nu, L.hptr(t), L.hptr(a1), L.hptr(a2), L.ptr(ds),
-           L.ptr(b), L.ptr(y), L.stream_handle())
+           L.ptr(b), L.ptr(y), 1 if exact else 0, L.stream_handle())
     del keep
     return y
 

@@ -110,6 +110,25 @@ def test_richardson_matches_oracle(G, nx, ny, v, order, its):
     assert np.max(np.abs(x - x_o)) <= 1e-10 * max(np.max(np.abs(x_o)), 1e-300) + 1e-14
 
 
+@pytest.mark.parametrize('nx,ny,v,order,its', [(64, 64, PI4, 4, 1), (48, 40, HARD, 6, 2)])
+def test_richardson_exact_mode_bitwise(G, nx, ny, v, order, its):
+    """Parity mode: every kernel follows the reference's arithmetic order, so
+    x is bitwise the oracle's (== scipy/numpy) on the same hierarchy."""
+    A = O.advection_2d(nx, ny, *v)
+    Hh = O.setup(A, O.Cfg(poly_order=order))
+    x_o, hist_o, _, its_o = O.richardson(Hh, np.zeros(A.nrows), np.ones(A.nrows),
+                                         f_smooth_its=its)
+    H = upload_hierarchy(Hh)
+    x, st = G.richardson_solve(H, np.zeros(A.nrows), np.ones(A.nrows),
+                               G.SolveConfig(f_smooth_its=its), exact=True)
+    assert st.iterations == its_o
+    assert x.cpu().numpy().tobytes() == x_o.tobytes()
+    assert rel(st.residual_history, hist_o) < 1e-13
+    r = np.random.default_rng(4).standard_normal(A.nrows)
+    e = G.vcycle(H, 0, r, G.SolveConfig(), exact=True).cpu().numpy()
+    assert e.tobytes() == O.vcycle(Hh, 0, r).tobytes()
+
+
 def test_assembled_smoother_path(G):
     A = O.advection_2d(48, 48, *PI4)
     Hh = O.setup(A, O.Cfg(poly_order=3, matrix_free_polys=False))
