@@ -66,9 +66,25 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
+// Keep freed scratch mapped in the stream-ordered pool: with the default
+// release threshold (0) every synchronisation unmaps it and the next large
+// cudaMallocAsync pays for re-mapping GBs of HBM.
+inline void keep_pool_warm() {
+  static thread_local int done_dev = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    unsigned long long thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done_dev = dev;
+}
+
 // Scratch memory from the stream-ordered pool (freed by the caller of alloc).
 template <typename T>
 inline int scratch(T** p, size_t count, cudaStream_t s) {
+  keep_pool_warm();
   if (count == 0) count = 1;
   AIRG_CUDA(cudaMallocAsync((void**)p, count * sizeof(T), s));
   return AIRG_OK;

@@ -1,0 +1,265 @@
+// Row-wise Gustavson SpGEMM core, bit-exact with scipy's csr_matmat.
+//
+// Pass 1 (count): warp per row, shared-memory open-addressing key set.
+// Pass 2 (numeric + structure): warp per row, key -> slot table with an fp64
+//   accumulator per slot; the A row is walked in order and lanes split ONE B
+//   row at a time (distinct output columns), so every output entry receives
+//   its k contributions in ascending order with separate mul/add roundings.
+//   The occupied slots are compacted and bitonic-sorted by column in shared
+//   memory and written once (optionally negated, or through the fused
+//   drop_and_lump epilogue).
+// Latency: A-row metadata (k, a_ik, B row bounds) is fetched 32 entries at a
+// time, one per lane, and the first 32 entries of the next B row are loaded
+// before the current one is processed.
+#pragma once
+#include "setup_common.cuh"
+
+namespace airg {
+
+constexpr int kEmpty = -1;
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ unsigned hash_of(int key, int bits) {
+  return ((unsigned)key * 0x9E3779B1u) >> (32 - bits);
+}
+
+// returns 1 when newly inserted, 0 when present, 1<<20 when the table is full
+__device__ __forceinline__ int set_insert(int* keys, int bits, int key) {
+  const unsigned mask = (1u << bits) - 1u;
+  unsigned h = hash_of(key, bits);
+  for (unsigned probe = 0; probe <= mask; ++probe) {
+    const int prev = atomicCAS(keys + h, kEmpty, key);
+    if (prev == kEmpty) return 1;
+    if (prev == key) return 0;
+    h = (h + 1u) & mask;
+  }
+  return 1 << 20;
+}
+
+// slot of key (inserting it); the table always has room in pass 2
+__device__ __forceinline__ int slot_of(int* keys, int bits, int key) {
+  const unsigned mask = (1u << bits) - 1u;
+  unsigned h = hash_of(key, bits);
+  while (true) {
+    const int cur = keys[h];
+    if (cur == key) return (int)h;
+    if (cur == kEmpty) {
+      const int prev = atomicCAS(keys + h, kEmpty, key);
+      if (prev == kEmpty || prev == key) return (int)h;
+    }
+    h = (h + 1u) & mask;
+  }
+}
+
+__device__ __forceinline__ int map_find(const int* keys, const int* vals, int bits, int key) {
+  const unsigned mask = (1u << bits) - 1u;
+  unsigned h = hash_of(key, bits);
+  while (true) {
+    const int k = keys[h];
+    if (k == key) return vals[h];
+    if (k == kEmpty) return -1;
+    h = (h + 1u) & mask;
+  }
+}
+
+__device__ __forceinline__ void map_insert(int* keys, int* vals, int bits, int key, int v) {
+  const unsigned mask = (1u << bits) - 1u;
+  unsigned h = hash_of(key, bits);
+  while (true) {
+    const int prev = atomicCAS(keys + h, kEmpty, key);
+    if (prev == kEmpty || prev == key) {
+      vals[h] = v;
+      return;
+    }
+    h = (h + 1u) & mask;
+  }
+}
+
+// warp-wide bitonic sort of buf[0..P) ascending (P power of two); optional payload
+template <typename V>
+__device__ void warp_bitonic(int* buf, V* pay, int P, int lane) {
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = lane; i < P; i += 32) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const int a = buf[i], b = buf[ixj];
+          const bool up = (i & k) == 0;
+          if ((a > b) == up) {
+            buf[i] = b;
+            buf[ixj] = a;
+            if (pay) {
+              const V t = pay[i];
+              pay[i] = pay[ixj];
+              pay[ixj] = t;
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+__host__ __device__ __forceinline__ int ceil_log2(long long x) {
+  int b = 0;
+  while ((1ll << b) < x) ++b;
+  return b;
+}
+
+// Walk the products of A row `row` with B: f(a_ik, col, b_kj) per product,
+// lanes split one B row, rows in A order; SYNC orders successive B rows.
+template <bool SYNC, bool VALUES, class F>
+__device__ __forceinline__ void walk_products(const int* __restrict__ Ap, const int* __restrict__ Ac,
+                                              const double* __restrict__ Av,
+                                              const int* __restrict__ Bp, const int* __restrict__ Bc,
+                                              const double* __restrict__ Bv, int row, int lane,
+                                              F& f) {
+  const int ab = Ap[row], ae = Ap[row + 1];
+  for (int base = ab; base < ae; base += 32) {
+    const int kk = base + lane;
+    int bb = 0, be = 0;
+    double av = 0.0;
+    if (kk < ae) {
+      const int k = Ac[kk];
+      if (VALUES) av = Av[kk];
+      bb = Bp[k];
+      be = Bp[k + 1];
+    }
+    const int cnt = min(32, ae - base);
+    int cb = __shfl_sync(kFull, bb, 0), ce = __shfl_sync(kFull, be, 0);
+    int pc = cb + lane < ce ? Bc[cb + lane] : -1;
+    double pv = (VALUES && cb + lane < ce) ? Bv[cb + lane] : 0.0;
+    for (int t = 0; t < cnt; ++t) {
+      const double a = VALUES ? __shfl_sync(kFull, av, t) : 0.0;
+      const int tb = cb, te = ce;
+      const int c0 = pc;
+      const double v0 = pv;
+      if (t + 1 < cnt) {  // prefetch the head of the next B row
+        cb = __shfl_sync(kFull, bb, t + 1);
+        ce = __shfl_sync(kFull, be, t + 1);
+        pc = cb + lane < ce ? Bc[cb + lane] : -1;
+        if (VALUES) pv = cb + lane < ce ? Bv[cb + lane] : 0.0;
+      }
+      if (c0 >= 0) f(a, c0, v0);
+      for (int jb = tb + 32; jb < te; jb += 96) {
+        int cc[3];
+        double vv[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const int jj = jb + 32 * q + lane;
+          cc[q] = jj < te ? Bc[jj] : -1;
+          vv[q] = (VALUES && jj < te) ? Bv[jj] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          if (cc[q] >= 0) f(a, cc[q], vv[q]);
+      }
+      if (SYNC) __syncwarp();
+    }
+  }
+}
+
+struct CountOp {
+  int* keys;
+  int bits;
+  int added;
+  __device__ __forceinline__ void operator()(double, int c, double) { added += set_insert(keys, bits, c); }
+};
+
+struct AccOp {
+  int* keys;
+  double* acc;
+  int bits;
+  __device__ __forceinline__ void operator()(double a, int c, double v) {
+    const int s = slot_of(keys, bits, c);
+    acc[s] = add_rn(acc[s], mul_rn(a, v));
+  }
+};
+
+// In-place compaction of occupied slots (keys + payload) to [0, n).
+template <typename V>
+__device__ __forceinline__ int compact_slots(int* keys, V* pay, int T, int lane) {
+  int wpos = 0;
+  for (int base = 0; base < T; base += 32) {
+    const int k = keys[base + lane];
+    V v{};
+    if (pay) v = pay[base + lane];
+    const bool occ = k != kEmpty;
+    const unsigned bal = __ballot_sync(kFull, occ);
+    __syncwarp();
+    if (occ) {
+      const int d = wpos + __popc(bal & ((1u << lane) - 1u));
+      keys[d] = k;
+      if (pay) pay[d] = v;
+    }
+    wpos += __popc(bal);
+    __syncwarp();
+  }
+  return wpos;
+}
+
+// drop_and_lump (sparse.py:307-352) of one sorted row held in (col, val)[0..n):
+// keep = diagonal | |v| >= tol*max|v|; dropped values summed sequentially in
+// column order onto the diagonal (inserted when absent and the sum != 0).
+// Writes kept entries to out_col/out_val[o...]; returns the written count.
+__device__ static int drop_lump_row(const int* col, const double* val, int n, int row, double tol, int lump,
+                             int* __restrict__ out_col, double* __restrict__ out_val, long long o,
+                             int lane, int* any_drop) {
+  double mx = 0.0;
+  int dpos = -1;
+  for (int i = lane; i < n; i += 32) {
+    mx = fmax(mx, fabs(val[i]));
+    if (col[i] == row) dpos = i;
+  }
+  mx = warp_max(mx);
+  dpos = __reduce_max_sync(kFull, dpos);
+  const double thr = mul_rn(tol, mx);
+  double lumped = 0.0;
+  int ndrop = 0;
+  if (lane == 0) {
+    for (int i = 0; i < n; ++i) {
+      const double x = val[i];
+      if (i != dpos && !(fabs(x) >= thr)) {
+        lumped = add_rn(lumped, x);
+        ++ndrop;
+      }
+    }
+    if (ndrop && any_drop) atomicOr(any_drop, 1);
+  }
+  lumped = __shfl_sync(kFull, lumped, 0);
+  ndrop = __shfl_sync(kFull, ndrop, 0);
+  const bool insert = lump && ndrop > 0 && dpos < 0 && lumped != 0.0;
+  int written = 0, before = 0;
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    bool keep = false;
+    double x = 0.0;
+    int cc = 0;
+    if (i < n) {
+      x = val[i];
+      cc = col[i];
+      keep = i == dpos || fabs(x) >= thr;
+      if (i == dpos && lump && ndrop > 0) x = add_rn(x, lumped);
+    }
+    const unsigned bal = __ballot_sync(kFull, keep);
+    before += __popc(__ballot_sync(kFull, keep && cc < row));
+    if (keep) {
+      int dst = written + __popc(bal & ((1u << lane) - 1u));
+      if (insert && cc > row) ++dst;
+      out_col[o + dst] = cc;
+      out_val[o + dst] = x;
+    }
+    written += __popc(bal);
+  }
+  if (insert) {
+    if (lane == 0) {
+      out_col[o + before] = row;
+      out_val[o + before] = lumped;
+    }
+    ++written;
+  }
+  return written;
+}
+
+}  // namespace airg

@@ -1,0 +1,479 @@
+// General SpGEMM (Z = -A_cf Ahat, A P, R (A P)) and the fused Galerkin
+// product with drop/lump.  Kernel design in spgemm_core.cuh.
+// ref: sparse.py:222-240 (spgemm), hierarchy.py:281-286 (coarse_matrix)
+#include "spgemm_core.cuh"
+#include <vector>
+#include <algorithm>
+
+namespace airg {
+
+// ---- row classification ------------------------------------------------------
+__global__ void product_ub_kernel(int m, const int* __restrict__ Ap, const int* __restrict__ Ac,
+                                  const int* __restrict__ Bp, long long* __restrict__ ub) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x) {
+    long long s = 0;
+    for (int k = Ap[i]; k < Ap[i + 1]; ++k) {
+      const int c = Ac[k];
+      s += Bp[c + 1] - Bp[c];
+    }
+    ub[i] = s;
+  }
+}
+
+__global__ void rowlen_kernel(int m, const int* __restrict__ ptr, long long* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = ptr[i + 1] - ptr[i];
+}
+
+constexpr int kMaxCls = 8;
+
+// block-aggregated append of row ids to per-class lists (lists[c*m + ...])
+__global__ void classify_kernel(int m, const long long* __restrict__ size, const long long* __restrict__ th,
+                                int ncls, int* __restrict__ lists, int* __restrict__ counts) {
+  __shared__ int scnt[kMaxCls], sbase[kMaxCls];
+  if (threadIdx.x < ncls) scnt[threadIdx.x] = 0;
+  __syncthreads();
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  int c = 0, slot = 0;
+  if (i < m) {
+    const long long v = size[i];
+    while (c < ncls - 1 && v > th[c]) ++c;
+    slot = atomicAdd(scnt + c, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < ncls) sbase[threadIdx.x] = atomicAdd(counts + threadIdx.x, scnt[threadIdx.x]);
+  __syncthreads();
+  if (i < m) lists[(long long)c * m + sbase[c] + slot] = (int)i;
+}
+
+struct Classes {
+  std::vector<int> count;
+  int* lists = nullptr;
+  int m = 0;
+  const int* list(int c) const { return lists + (long long)c * m; }
+};
+
+static int classify(int m, const long long* size, const std::vector<long long>& th, Classes& out,
+                    cudaStream_t s) {
+  const int ncls = (int)th.size() + 1;
+  long long* dth = nullptr;
+  int* cnt = nullptr;
+  AIRG_TRY(scratch(&out.lists, (size_t)ncls * (m > 0 ? m : 1), s));
+  AIRG_TRY(scratch(&dth, th.size() + 1, s));
+  AIRG_TRY(scratch(&cnt, ncls, s));
+  if (!th.empty())
+    AIRG_CUDA(cudaMemcpyAsync(dth, th.data(), th.size() * sizeof(long long), cudaMemcpyHostToDevice, s));
+  AIRG_CUDA(cudaMemsetAsync(cnt, 0, ncls * sizeof(int), s));
+  if (m > 0) classify_kernel<<<(m + 255) / 256, 256, 0, s>>>(m, size, dth, ncls, out.lists, cnt);
+  AIRG_LAUNCH_CHECK();
+  out.count.assign(ncls, 0);
+  AIRG_CUDA(cudaMemcpyAsync(out.count.data(), cnt, ncls * sizeof(int), cudaMemcpyDeviceToHost, s));
+  AIRG_CUDA(cudaStreamSynchronize(s));
+  out.m = m;
+  release(dth, s);
+  release(cnt, s);
+  return AIRG_OK;
+}
+
+// ---- pass 1: structural count -------------------------------------------------
+struct CountArgs {
+  const int *Ap, *Ac, *Bp, *Bc;
+  const int* rows;
+  int nrows;
+  int bits;  // shared tables (log2 slots); global tables when gtab != nullptr
+  int limit;
+  int* cnt;
+  int* ovf_rows;
+  int* ovf_n;
+  int* gtab;
+  const long long* goff;
+  const int* gbits;
+};
+
+struct CountCheckOp {
+  int* keys;
+  int bits;
+  int added;
+  __device__ __forceinline__ void operator()(double, int c, double) { added += set_insert(keys, bits, c); }
+};
+
+__global__ void __launch_bounds__(256) spgemm_count_kernel(CountArgs a) {
+  extern __shared__ int smem[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (long long t = (long long)blockIdx.x * nw + w; t < a.nrows; t += (long long)gridDim.x * nw) {
+    const int row = a.rows[t];
+    int* keys;
+    int bits;
+    if (a.gtab) {
+      keys = a.gtab + a.goff[t];
+      bits = a.gbits[t];
+    } else {
+      keys = smem + (size_t)w * (1 << a.bits);
+      bits = a.bits;
+    }
+    const int T = 1 << bits;
+    for (int i = lane; i < T; i += 32) keys[i] = kEmpty;
+    __syncwarp();
+    // walk in chunks of A entries so an overflowing row bails out early
+    CountCheckOp op{keys, bits, 0};
+    const int ab = a.Ap[row], ae = a.Ap[row + 1];
+    bool ovf = false;
+    for (int base = ab; base < ae && !ovf; base += 32) {
+      // B-row bounds of 32 A entries at once (one per lane)
+      int bb = 0, be = 0;
+      if (base + lane < ae) {
+        const int k = a.Ac[base + lane];
+        bb = a.Bp[k];
+        be = a.Bp[k + 1];
+      }
+      const int cnt = min(32, ae - base);
+      for (int t = 0; t < cnt; ++t) {
+        const int tb = __shfl_sync(kFull, bb, t), te = __shfl_sync(kFull, be, t);
+        for (int jb = tb; jb < te; jb += 128) {
+          int cc[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int jj = jb + 32 * q + lane;
+            cc[q] = jj < te ? a.Bc[jj] : -1;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (cc[q] >= 0) op(0.0, cc[q], 0.0);
+        }
+      }
+      if (!a.gtab) ovf = warp_sum(op.added) > a.limit;
+    }
+    const int n = warp_sum(op.added);
+    if (ovf || (!a.gtab && n > a.limit)) {
+      if (lane == 0) a.ovf_rows[atomicAdd(a.ovf_n, 1)] = row;
+    } else if (lane == 0) {
+      a.cnt[row] = n;
+    }
+    __syncwarp();
+  }
+}
+
+// ---- pass 2: numeric + structure --------------------------------------------------
+struct NumArgs {
+  const int *Ap, *Ac;
+  const double* Av;
+  const int *Bp, *Bc;
+  const double* Bv;
+  const int* rows;
+  int nrows;
+  int bits;
+  const int* Cp;
+  int* Cc;
+  double* Cv;
+  int negate;
+  int mode;  // 0 plain, 1 fused drop/lump into raw offsets
+  double tol;
+  int lump;
+  int* out_cnt;
+  int* any_drop;
+  int* gkeys;
+  double* gacc;
+  const long long* goff;
+  const int* gbits;
+};
+
+__global__ void __launch_bounds__(256) spgemm_numeric_kernel(NumArgs a) {
+  extern __shared__ double smd[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (long long t = (long long)blockIdx.x * nw + w; t < a.nrows; t += (long long)gridDim.x * nw) {
+    const int row = a.rows[t];
+    int bits;
+    int* keys;
+    double* acc;
+    if (a.gkeys) {
+      bits = a.gbits[t];
+      keys = a.gkeys + a.goff[t];
+      acc = a.gacc + a.goff[t];
+    } else {
+      bits = a.bits;
+      const int T = 1 << bits;
+      acc = smd + (size_t)w * T * 3 / 2;  // T doubles + T ints per warp
+      keys = (int*)(acc + T);
+    }
+    const int T = 1 << bits;
+    for (int i = lane; i < T; i += 32) {
+      keys[i] = kEmpty;
+      acc[i] = 0.0;
+    }
+    __syncwarp();
+    AccOp op{keys, acc, bits};
+    walk_products<true, true>(a.Ap, a.Ac, a.Av, a.Bp, a.Bc, a.Bv, row, lane, op);
+    __syncwarp();
+    const int n = compact_slots(keys, acc, T, lane);
+    int P = 1;
+    while (P < n) P <<= 1;
+    for (int i = n + lane; i < P; i += 32) keys[i] = 0x7fffffff;
+    __syncwarp();
+    warp_bitonic(keys, acc, P, lane);
+    const int o = a.Cp[row];
+    if (a.mode == 0) {
+      for (int i = lane; i < n; i += 32) {
+        a.Cc[o + i] = keys[i];
+        const double v = acc[i];
+        a.Cv[o + i] = a.negate ? -v : v;
+      }
+    } else {
+      const int wr = drop_lump_row(keys, acc, n, row, a.tol, a.lump, a.Cc, a.Cv, (long long)o + row,
+                                   lane, a.any_drop);
+      if (lane == 0) a.out_cnt[row] = wr;
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void compact_raw_kernel(int m, const int* __restrict__ rawp, const int* __restrict__ optr,
+                                   const int* __restrict__ icol, const double* __restrict__ ival,
+                                   int* __restrict__ ocol, double* __restrict__ oval) {
+  const int lane = threadIdx.x & 31;
+  for (long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; r < m;
+       r += ((long long)gridDim.x * blockDim.x) >> 5) {
+    const long long src = (long long)rawp[r] + r;
+    const int dst = optr[r], n = optr[r + 1] - dst;
+    for (int i = lane; i < n; i += 32) {
+      ocol[dst + i] = icol[src + i];
+      oval[dst + i] = ival[src + i];
+    }
+  }
+}
+
+__global__ void iota_kernel(int n, int* __restrict__ p) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i <= n;
+       i += (long long)gridDim.x * blockDim.x)
+    p[i] = (int)i;
+}
+
+__global__ void ones_kernel(long long n, double* __restrict__ v) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    v[i] = 1.0;
+}
+
+struct Mat {
+  int nrows, ncols;
+  const int* p;
+  const int* c;
+  const double* v;
+};
+
+static int set_smem(const void* fn, size_t shm) {
+  if (shm > 48 * 1024)
+    AIRG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+  return AIRG_OK;
+}
+
+// global-memory tables for rows beyond the shared-memory classes
+struct GlobalTables {
+  int* rows = nullptr;
+  int* bits = nullptr;
+  long long* off = nullptr;
+  int* keys = nullptr;
+  double* acc = nullptr;
+  int n = 0;
+  void free(cudaStream_t s) {
+    for (void* q : {(void*)rows, (void*)bits, (void*)off, (void*)keys, (void*)acc}) release(q, s);
+  }
+};
+
+// sizes: per-row key counts to hold (table = pow2 >= 2*size)
+static int make_tables(const std::vector<int>& rows, const std::vector<long long>& sizes, bool values,
+                       GlobalTables& g, cudaStream_t s) {
+  const int n = (int)rows.size();
+  g.n = n;
+  if (!n) return AIRG_OK;
+  std::vector<long long> off(n);
+  std::vector<int> bits(n);
+  long long tot = 0;
+  for (int i = 0; i < n; ++i) {
+    bits[i] = std::max(5, ceil_log2(2 * std::max(1ll, sizes[i])));
+    off[i] = tot;
+    tot += 1ll << bits[i];
+  }
+  AIRG_TRY(scratch(&g.rows, n, s));
+  AIRG_TRY(scratch(&g.bits, n, s));
+  AIRG_TRY(scratch(&g.off, n, s));
+  AIRG_TRY(scratch(&g.keys, tot, s));
+  if (values) AIRG_TRY(scratch(&g.acc, tot, s));
+  AIRG_CUDA(cudaMemcpyAsync(g.rows, rows.data(), n * sizeof(int), cudaMemcpyHostToDevice, s));
+  AIRG_CUDA(cudaMemcpyAsync(g.bits, bits.data(), n * sizeof(int), cudaMemcpyHostToDevice, s));
+  AIRG_CUDA(cudaMemcpyAsync(g.off, off.data(), n * sizeof(long long), cudaMemcpyHostToDevice, s));
+  return AIRG_OK;
+}
+
+static int gather_ll(const long long* d, const std::vector<int>& rows, std::vector<long long>& out,
+                     cudaStream_t s, int m) {
+  std::vector<long long> all(m);
+  AIRG_CUDA(cudaMemcpyAsync(all.data(), d, m * sizeof(long long), cudaMemcpyDeviceToHost, s));
+  AIRG_CUDA(cudaStreamSynchronize(s));
+  out.resize(rows.size());
+  for (size_t i = 0; i < rows.size(); ++i) out[i] = all[rows[i]];
+  return AIRG_OK;
+}
+
+// C = A B (mode 0, optionally negated) or drop_and_lump(A B) (mode 1).
+static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double tol, int lump,
+                       airg_csr_result** out, cudaStream_t s) {
+  const int m = A.nrows;
+  long long *ub = nullptr, *rl = nullptr;
+  int *cnt = nullptr, *Cp = nullptr;
+  AIRG_TRY(scratch(&ub, m, s));
+  AIRG_TRY(scratch(&cnt, m + 1, s));
+  AIRG_TRY(scratch(&Cp, m + 1, s));
+  if (m > 0) product_ub_kernel<<<blocks_for(m, 256), 256, 0, s>>>(m, A.p, A.c, B.p, ub);
+  AIRG_LAUNCH_CHECK();
+  // ---- pass 1 ----
+  {
+    Classes cl;
+    AIRG_TRY(classify(m, ub, {64, 512}, cl, s));
+    int *ovf_rows = nullptr, *ovf_n = nullptr;
+    AIRG_TRY(scratch(&ovf_rows, m > 0 ? m : 1, s));
+    AIRG_TRY(scratch(&ovf_n, 1, s));
+    AIRG_CUDA(cudaMemsetAsync(ovf_n, 0, sizeof(int), s));
+    const int cbits[3] = {7, 10, 12}, cwarps[3] = {8, 8, 4};
+    for (int c = 0; c < 3; ++c) {
+      const int nr = cl.count[c];
+      if (!nr) continue;
+      const size_t shm = (size_t)cwarps[c] * (1 << cbits[c]) * sizeof(int);
+      AIRG_TRY(set_smem((const void*)spgemm_count_kernel, shm));
+      CountArgs a{A.p, A.c, B.p, B.c, cl.list(c), nr, cbits[c], (1 << cbits[c]) * 3 / 4, cnt,
+                  ovf_rows, ovf_n, nullptr, nullptr, nullptr};
+      spgemm_count_kernel<<<blocks_for(nr, cwarps[c], 148 * 32), cwarps[c] * 32, shm, s>>>(a);
+      AIRG_LAUNCH_CHECK();
+    }
+    int novf = 0;
+    AIRG_CUDA(cudaMemcpyAsync(&novf, ovf_n, sizeof(int), cudaMemcpyDeviceToHost, s));
+    AIRG_CUDA(cudaStreamSynchronize(s));
+    if (novf) {
+      std::vector<int> rows(novf);
+      AIRG_CUDA(cudaMemcpyAsync(rows.data(), ovf_rows, novf * sizeof(int), cudaMemcpyDeviceToHost, s));
+      std::vector<long long> sizes;
+      AIRG_TRY(gather_ll(ub, rows, sizes, s, m));
+      GlobalTables g;
+      AIRG_TRY(make_tables(rows, sizes, false, g, s));
+      CountArgs a{A.p, A.c, B.p, B.c, g.rows, novf, 0, 0x7fffffff, cnt, ovf_rows, ovf_n, g.keys,
+                  g.off, g.bits};
+      spgemm_count_kernel<<<blocks_for(novf, 4), 128, 0, s>>>(a);
+      AIRG_LAUNCH_CHECK();
+      AIRG_CUDA(cudaStreamSynchronize(s));
+      g.free(s);
+    }
+    release(ovf_rows, s);
+    release(ovf_n, s);
+    release(cl.lists, s);
+  }
+  long long nnz = 0;
+  AIRG_TRY(scan_counts(cnt, Cp, m, &nnz, s));
+  // ---- pass 2 ----
+  airg_csr_result* r = new airg_csr_result();
+  r->nrows = m;
+  r->ncols = B.ncols;
+  r->stream = s;
+  int* ocol = nullptr;
+  double* oval = nullptr;
+  int* anyd = nullptr;
+  const long long cap = mode == 1 ? nnz + m : nnz;
+  AIRG_TRY(scratch(&ocol, cap, s));
+  AIRG_TRY(scratch(&oval, cap, s));
+  AIRG_TRY(scratch(&anyd, 1, s));
+  AIRG_CUDA(cudaMemsetAsync(anyd, 0, sizeof(int), s));
+  AIRG_TRY(scratch(&rl, m, s));
+  if (m > 0) rowlen_kernel<<<blocks_for(m, 256), 256, 0, s>>>(m, Cp, rl);
+  {
+    Classes cl;
+    AIRG_TRY(classify(m, rl, {32, 128, 512, 1024, 2048}, cl, s));
+    const int cbits[5] = {6, 8, 10, 11, 12}, cwarps[5] = {8, 8, 8, 4, 2};
+    for (int c = 0; c < 5; ++c) {
+      const int nr = cl.count[c];
+      if (!nr) continue;
+      const size_t shm = (size_t)cwarps[c] * (1 << cbits[c]) * 12;
+      AIRG_TRY(set_smem((const void*)spgemm_numeric_kernel, shm));
+      NumArgs a{A.p, A.c, A.v, B.p, B.c, B.v, cl.list(c), nr, cbits[c], Cp, ocol, oval, negate,
+                mode, tol, lump, cnt, anyd, nullptr, nullptr, nullptr, nullptr};
+      spgemm_numeric_kernel<<<blocks_for(nr, cwarps[c], 148 * 32), cwarps[c] * 32, shm, s>>>(a);
+      AIRG_LAUNCH_CHECK();
+    }
+    const int nr = cl.count[5];
+    if (nr) {
+      std::vector<int> rows(nr);
+      AIRG_CUDA(cudaMemcpyAsync(rows.data(), cl.list(5), nr * sizeof(int), cudaMemcpyDeviceToHost, s));
+      std::vector<long long> sizes;
+      AIRG_TRY(gather_ll(rl, rows, sizes, s, m));
+      GlobalTables g;
+      AIRG_TRY(make_tables(rows, sizes, true, g, s));
+      NumArgs a{A.p, A.c, A.v, B.p, B.c, B.v, g.rows, nr, 0, Cp, ocol, oval, negate, mode, tol, lump,
+                cnt, anyd, g.keys, g.acc, g.off, g.bits};
+      spgemm_numeric_kernel<<<blocks_for(nr, 4), 128, 0, s>>>(a);
+      AIRG_LAUNCH_CHECK();
+      AIRG_CUDA(cudaStreamSynchronize(s));
+      g.free(s);
+    }
+    release(cl.lists, s);
+  }
+  if (mode == 0) {
+    r->ptr = Cp;
+    r->col = ocol;
+    r->val = oval;
+    r->nnz = nnz;
+  } else {
+    AIRG_CUDA(cudaMallocAsync((void**)&r->ptr, (size_t)(m + 1) * sizeof(int), s));
+    long long fn = 0;
+    AIRG_TRY(scan_counts(cnt, r->ptr, m, &fn, s));
+    AIRG_TRY(result_alloc_entries(r, fn, true));
+    if (m > 0)
+      compact_raw_kernel<<<blocks_for((long long)m * 32, 256), 256, 0, s>>>(m, Cp, r->ptr, ocol, oval,
+                                                                           r->col, r->val);
+    AIRG_LAUNCH_CHECK();
+    release(ocol, s);
+    release(oval, s);
+    release(Cp, s);
+  }
+  release(anyd, s);
+  release(ub, s);
+  release(rl, s);
+  release(cnt, s);
+  *out = r;
+  return AIRG_OK;
+}
+
+}  // namespace airg
+
+using namespace airg;
+
+extern "C" {
+
+int airg_spgemm(int m, int k, int n, const int32_t* Ap, const int32_t* Ac, const double* Av,
+                const int32_t* Bp, const int32_t* Bc, const double* Bv, int negate,
+                airg_csr_result** out, void* stream) {
+  Mat A{m, k, Ap, Ac, Av}, B{k, n, Bp, Bc, Bv};
+  return spgemm_rows(A, B, negate, 0, 0.0, 0, out, (cudaStream_t)stream);
+}
+
+int airg_galerkin(int n, int nc, const int32_t* Rp, const int32_t* Rc, const double* Rv,
+                  const int32_t* Ap, const int32_t* Ac, const double* Av, const int32_t* pcol,
+                  double a_drop, int lump, airg_csr_result** out, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  int* Pp = nullptr;
+  double* Pv = nullptr;
+  AIRG_TRY(scratch(&Pp, n + 1, s));
+  AIRG_TRY(scratch(&Pv, n, s));
+  iota_kernel<<<blocks_for(n + 1, 256), 256, 0, s>>>(n, Pp);
+  ones_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, Pv);
+  AIRG_LAUNCH_CHECK();
+  Mat A{n, n, Ap, Ac, Av}, P{n, nc, Pp, pcol, Pv};
+  airg_csr_result* AP = nullptr;
+  AIRG_TRY(spgemm_rows(A, P, 0, 0, 0.0, 0, &AP, s));
+  Mat R{nc, n, Rp, Rc, Rv}, APm{n, nc, AP->ptr, AP->col, AP->val};
+  AIRG_TRY(spgemm_rows(R, APm, 0, a_drop == 0.0 ? 0 : 1, a_drop, lump, out, s));
+  airg_result_free(AP);
+  release(Pp, s);
+  release(Pv, s);
+  return AIRG_OK;
+}
+
+}  // extern "C"
