@@ -1,0 +1,354 @@
+"""AIRG setup + solve benchmark (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = the hot path over one synthetic problem: ``setup(A, SetupConfig())``
+followed by ``richardson_solve`` to rtol 1e-10 (b = 0, x0 = 1), exactly the
+reference's benchmark run (cli.py:220-259).  Workload = BASELINE.json
+configs[1]: 2D upwind advection, 2048 x 2048 (4.19M DOFs), theta = pi/4,
+default AIRG config (order-6 GMRES polynomial smoothers, order-100 Newton
+coarse solver, automatic truncation).
+
+value = DOFs / (setup s + solve s) summed over ranks (each rank owns one
+2048^2 problem -- weak scaling; the domain-decomposed single problem is not
+implemented yet).  Inputs are resident in HBM before the
+timed region; every level operator of the hierarchy (> 1 GB) exceeds L2.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ('AIRG setup+solve throughput, rtol 1e-10 (DOFs / (setup s + solve s)); '
+          'solve V-cycle HBM GB/s in roofline')
+PI4 = (float(np.cos(np.pi / 4)), float(np.sin(np.pi / 4)))
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument('--gpus', type=int, default=1)
+    ap.add_argument('--steps', type=int, default=5)
+    ap.add_argument('--warmup', type=int, default=3)
+    ap.add_argument('--impl', default='ours', choices=['ours', 'reference'])
+    ap.add_argument('--nx', type=int, default=2048)
+    ap.add_argument('--order', type=int, default=6)
+    ap.add_argument('--cpu-nx', type=int, default=256, help='CPU baseline sample grid')
+    ap.add_argument('--no-cpu', action='store_true')
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get('RANK', 0)), int(os.environ.get('WORLD_SIZE', 1)),
+            int(os.environ.get('LOCAL_RANK', 0)))
+
+
+# ---------------------------------------------------------------------------
+# CPU side: the oracle port of the reference (numpy/scipy, same kernels)
+# ---------------------------------------------------------------------------
+
+def cpu_run(nx, order):
+    """Reference-style run on the host: setup then two solves, the second
+    timed (cli.py:220-259).  Returns (setup_s, solve_s, its)."""
+    from oracle import airg_oracle as O
+    A = O.advection_2d(nx, nx, *PI4)
+    t0 = time.perf_counter()
+    H = O.setup(A, O.Cfg(poly_order=order))
+    t1 = time.perf_counter()
+    O.richardson(H, np.zeros(A.nrows), np.ones(A.nrows))
+    t2 = time.perf_counter()
+    _, hist, conv, its = O.richardson(H, np.zeros(A.nrows), np.ones(A.nrows))
+    t3 = time.perf_counter()
+    return t1 - t0, t3 - t2, its
+
+
+def cpu_cores_note():
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [f"{i.get('internal_api')}:{i.get('num_threads')}" for i in threadpool_info()]
+    except Exception:
+        blas = []
+    return os.cpu_count(), blas
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return 0
+    setup_s, solve_s, its = [], [], 0
+    for i in range(args.warmup + args.steps):
+        a, b, its = cpu_run(args.cpu_nx, args.order)
+        if i >= args.warmup:
+            setup_s.append(a)
+            solve_s.append(b)
+    t = float(np.mean(setup_s) + np.mean(solve_s))
+    n = args.cpu_nx * args.cpu_nx
+    ncpu, blas = cpu_cores_note()
+    v = n / t
+    line = {
+        'impl': 'reference', 'metric': METRIC, 'value': v, 'unit': 'DOF/s',
+        'n_gpus': world, 'steps': args.steps, 'warmup': args.warmup, 'ms_per_step': t * 1e3,
+        'higher_is_better': True, 'scaling': 'weak', 'vs_baseline': None, 'dtype': 'f64',
+        'data': 'synthetic (2D upwind advection stencil, b=0, x0=1)',
+        'config': {'workload': f'AIRG pi/4 advection {args.nx}x{args.nx} order {args.order}',
+                   'sample': f'{args.cpu_nx}x{args.cpu_nx}', 'rtol': 1e-10},
+        'setup_s': float(np.mean(setup_s)), 'solve_s': float(np.mean(solve_s)), 'iterations': its,
+        'cpu_baseline': {'value': v, 'unit': 'DOF/s', 'cores': 1, 'kind': 'port',
+                         'sample': f'{args.cpu_nx}^2 of the {args.nx}^2 workload (oracle/airg_oracle.py '
+                                   f'= numpy/scipy restatement of airmg; scipy sparse kernels are '
+                                   f'single-threaded, BLAS-1 dots use {blas}; host has {ncpu} cpus)'},
+        'e2e': {'value': v, 'unit': 'DOF/s', 'h2d_bytes_per_step': 0, 'd2h_bytes_per_step': 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU side
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        if os.environ.get('AIRG_BENCH_NO_CLOCKS'):
+            return self
+        q = ('clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,'
+             'clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,'
+             'clocks_event_reasons.sw_power_cap')
+        try:
+            self.proc = subprocess.Popen(['nvidia-smi', '-i', str(self.index), f'--query-gpu={q}',
+                                          '--format=csv,noheader,nounits', '-lms', '1000'],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(',')])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                pass
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace('.', '').isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace('.', '').isdigit()]
+        names = ['hw_slowdown', 'hw_thermal_slowdown', 'sw_thermal_slowdown', 'sw_power_cap']
+        reasons = set()
+        for r in self.rows:
+            for nm, v in zip(names, r[3:7]):
+                if v.strip().lower() == 'active':
+                    reasons.add(nm)
+        return {'sm_mhz': float(np.median(sm)) if sm else None,
+                'sm_max_mhz': max(mx) if mx else None, 'reasons': sorted(reasons),
+                'samples': len(sm)}
+
+
+def count_launches(step):
+    """Kernel launches of one step (CUPTI via torch.profiler), untimed."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        step()
+        torch.cuda.synchronize()
+    n = 0
+    mine = 0
+    for e in prof.events():
+        if e.device_type.name == 'CUDA' and not e.name.startswith('Memcpy') \
+                and not e.name.startswith('Memset'):
+            n += 1
+            if 'airg' in e.name:
+                mine += 1
+    return n, mine
+
+
+def ours_arm(args, rank, world, local):
+    import torch
+    import paper_2508_17517_b200 as G
+    from paper_2508_17517_b200.amg_solve import count_cycle_bytes, plan_for
+    from paper_2508_17517_b200 import _lib as L
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group('nccl', device_id=torch.device('cuda', local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    nx = args.nx
+    n = nx * nx
+    cfg = G.SetupConfig(poly_order=args.order)
+    scfg = G.SolveConfig()
+    A, b = G.build_advection_2d(G.AdvectionProblem(nx=nx, ny=nx, vx=PI4[0], vy=PI4[1]))
+    x0 = torch.ones(n, dtype=torch.float64, device='cuda')
+    info = {}
+
+    def step():
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record()
+        H = G.setup(A, cfg)
+        ev[1].record()
+        x, st = G.richardson_solve(H, b, x0, scfg)
+        ev[2].record()
+        info['H'], info['st'], info['ev'] = H, st, ev
+        return H
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    setup_ms, solve_ms = [], []
+    with ClockSampler(local) as clk:
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        start.record()
+        for _ in range(args.steps):
+            step()
+            ev = info['ev']
+            ev[2].synchronize()
+            setup_ms.append(ev[0].elapsed_time(ev[1]))
+            solve_ms.append(ev[1].elapsed_time(ev[2]))
+        stop.record()
+        barrier()
+    ms = start.elapsed_time(stop) / args.steps
+    if dist is not None:
+        t = torch.tensor([ms], device='cuda')
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    H, st = info['H'], info['st']
+
+    # ---- roofline: one V-cycle (the solve's kernel chain), CUDA events ----
+    plan = plan_for(H)
+    r = torch.randn(n, dtype=torch.float64, device='cuda')
+    e = torch.empty_like(r)
+    for _ in range(3):
+        L.call('airg_plan_vcycle', plan.h, 0, L.ptr(r), L.ptr(e), 1, L.stream_handle())
+    nv = 20
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(nv):
+        L.call('airg_plan_vcycle', plan.h, 0, L.ptr(r), L.ptr(e), 1, L.stream_handle())
+    e1.record()
+    torch.cuda.synchronize()
+    vms = e0.elapsed_time(e1) / nv
+    vbytes = count_cycle_bytes(H, include_top=False)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, 'MEASURED_PEAKS.json')))
+    except Exception:
+        pass
+    peak = float(peaks.get('hbm_gbs', 6650.0))
+    achieved = vbytes / (vms * 1e-3) / 1e9
+
+    # ---- e2e through the public API with pinned host buffers ----
+    Ap, Ac, Av = (t.cpu().pin_memory() for t in (A.row_offsets, A.col_indices, A.values))
+    bh = torch.zeros(n, dtype=torch.float64).pin_memory()
+    xh = torch.ones(n, dtype=torch.float64).pin_memory()
+    xout = torch.empty(n, dtype=torch.float64).pin_memory()
+    h2d = (Ap.numel() * 4 + Ac.numel() * 4 + Av.numel() * 8 + 16 * n)
+    d2h = 8 * n
+
+    def e2e_step():
+        Ad = G.SparseMatrix(n, n, Ap.to('cuda', non_blocking=True), Ac.to('cuda', non_blocking=True),
+                            Av.to('cuda', non_blocking=True))
+        Hh = G.setup(Ad, cfg)
+        x, _ = G.richardson_solve(Hh, bh.to('cuda', non_blocking=True),
+                                  xh.to('cuda', non_blocking=True), scfg)
+        xout.copy_(x, non_blocking=True)
+
+    e2e_step()
+    k_e2e = max(1, min(args.steps, 3))
+    barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    for _ in range(k_e2e):
+        e2e_step()
+    f1.record()
+    barrier()
+    e2e_ms = f0.elapsed_time(f1) / k_e2e
+    if dist is not None:
+        t = torch.tensor([e2e_ms], device='cuda')
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    launches, mine = count_launches(step)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        a, bs, its = cpu_run(args.cpu_nx, args.order)
+        ncpu, blas = cpu_cores_note()
+        cpu = {'value': args.cpu_nx ** 2 / (a + bs), 'unit': 'DOF/s', 'cores': 1, 'kind': 'port',
+               'sample': f'one setup + timed second solve at {args.cpu_nx}^2 (of the {nx}^2 '
+                         f'workload) with oracle/airg_oracle.py (numpy/scipy restatement of airmg; '
+                         f'scipy sparse kernels single-threaded; BLAS {blas}; {ncpu} host cpus); '
+                         f'setup {a:.2f} s, solve {bs:.3f} s, {its} its'}
+
+    if rank == 0:
+        line = {
+            'metric': METRIC, 'value': world * n / (ms * 1e-3), 'unit': 'DOF/s', 'n_gpus': world,
+            'steps': args.steps, 'warmup': args.warmup, 'ms_per_step': ms,
+            'higher_is_better': True, 'scaling': 'weak', 'vs_baseline': None, 'dtype': 'f64',
+            'data': 'synthetic (2D upwind advection stencil generated on device, b=0, x0=1)',
+            'config': {'workload': f'AIRG pi/4 advection {nx}x{nx} per GPU, order {args.order}, '
+                                   'default SetupConfig (BASELINE.json configs[1])',
+                       'dofs_per_gpu': n, 'rtol': 1e-10,
+                       'parallelism': f'{world} independent per-rank problems (weak scaling)',
+                       'l2': 'hierarchy operators (>1 GB) exceed the 126 MB L2'},
+            'setup_s': float(np.mean(setup_ms)) / 1e3, 'solve_s': float(np.mean(solve_ms)) / 1e3,
+            'iterations': st.iterations, 'levels': H.num_levels,
+            'truncated_at': H.truncated_at, 'cycle_complexity': H.cycle_complexity,
+            'setup_breakdown_s': {k: round(v, 4) for k, v in H.setup_breakdown.items()},
+            'vcycle_ms': vms,
+            'roofline': {'bound': 'hbm', 'achieved': achieved, 'peak': peak, 'unit': 'GB/s',
+                         'frac': achieved / peak, 'traffic': None,
+                         'kernel': 'one V-cycle (R/A_fc/A_ff SpMV chains + Newton coarse solve); '
+                                   f'algorithmic bytes {vbytes} (count_cycle_bytes)',
+                         'peak_source': 'MEASURED_PEAKS.json hbm_gbs' if peaks else 'fallback'},
+            'e2e': {'value': world * n / (e2e_ms * 1e-3), 'unit': 'DOF/s',
+                    'h2d_bytes_per_step': int(h2d), 'd2h_bytes_per_step': int(d2h),
+                    'ms_per_step': e2e_ms},
+            'gpu_launches': int(mine * args.steps),
+            'gpu_launches_all_kernels_per_step': int(launches),
+            'clocks': clk.summary(),
+            'cpu_baseline': cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == 'reference':
+        return reference_arm(args, rank, world)
+    return ours_arm(args, rank, world, local)
+
+
+if __name__ == '__main__':
+    sys.exit(main())

@@ -93,4 +93,16 @@ inline void release(void* p, cudaStream_t s) {
   if (p) cudaFreeAsync(p, s);
 }
 
+// Long-lived plan buffers: pool-backed (no device-wide sync on free).
+template <typename T>
+inline cudaError_t dmalloc(T** p, size_t bytes) {
+  keep_pool_warm();
+  cudaError_t e = cudaMallocAsync((void**)p, bytes ? bytes : 1, 0);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+  return e;
+}
+inline void dfree(void* p) {
+  if (p) cudaFreeAsync(p, 0);
+}
+
 }  // namespace airg

@@ -598,9 +598,9 @@ static int build_poly(Poly& p, int kind, int ncoef, const double* coef_h, int nu
   p.p1.assign(p1_h, p1_h + nunits);
   p.p2.assign(p2_h, p2_h + nunits);
   if (nunits > 0) {
-    AIRG_CUDA(cudaMalloc(&p.d_utype, nunits * sizeof(int)));
-    AIRG_CUDA(cudaMalloc(&p.d_p1, nunits * sizeof(double)));
-    AIRG_CUDA(cudaMalloc(&p.d_p2, nunits * sizeof(double)));
+    AIRG_CUDA(dmalloc(&p.d_utype, nunits * sizeof(int)));
+    AIRG_CUDA(dmalloc(&p.d_p1, nunits * sizeof(double)));
+    AIRG_CUDA(dmalloc(&p.d_p2, nunits * sizeof(double)));
     AIRG_CUDA(cudaMemcpy(p.d_utype, type_h, nunits * sizeof(int), cudaMemcpyHostToDevice));
     AIRG_CUDA(cudaMemcpy(p.d_p1, p1_h, nunits * sizeof(double), cudaMemcpyHostToDevice));
     AIRG_CUDA(cudaMemcpy(p.d_p2, p2_h, nunits * sizeof(double), cudaMemcpyHostToDevice));
@@ -609,9 +609,9 @@ static int build_poly(Poly& p, int kind, int ncoef, const double* coef_h, int nu
 }
 
 static void free_poly(Poly& p) {
-  if (p.d_utype) cudaFree(p.d_utype);
-  if (p.d_p1) cudaFree(p.d_p1);
-  if (p.d_p2) cudaFree(p.d_p2);
+  if (p.d_utype) dfree(p.d_utype);
+  if (p.d_p1) dfree(p.d_p1);
+  if (p.d_p2) dfree(p.d_p2);
   p.d_utype = nullptr;
   p.d_p1 = p.d_p2 = nullptr;
 }
@@ -670,7 +670,8 @@ struct airg_plan {
   double* e = nullptr;  // top error
   double* parts = nullptr;
   double* norm_d = nullptr;
-  double* norm_h = nullptr;  // pinned
+  double* norm_h = nullptr;
+  double norm_hv = 0.0;
   int* iflag = nullptr;
   NewtonState* nst = nullptr;
   int nparts_cap = 0;
@@ -680,7 +681,7 @@ struct airg_plan {
 };
 
 static int alloc_vec(double** p, long long n) {
-  AIRG_CUDA(cudaMalloc(p, (n > 0 ? n : 1) * sizeof(double)));
+  AIRG_CUDA(dmalloc(p, (n > 0 ? n : 1) * sizeof(double)));
   return AIRG_OK;
 }
 
@@ -766,10 +767,10 @@ int airg_plan_create(int nlevels, airg_plan** out) {
   airg_plan* p = new airg_plan();
   p->nlevels = nlevels;
   p->lv.resize(nlevels);
-  AIRG_CUDA(cudaMallocHost(&p->norm_h, sizeof(double)));
-  AIRG_CUDA(cudaMalloc(&p->norm_d, sizeof(double)));
-  AIRG_CUDA(cudaMalloc(&p->iflag, sizeof(int)));
-  AIRG_CUDA(cudaMalloc(&p->nst, sizeof(NewtonState)));
+  p->norm_h = &p->norm_hv;
+  AIRG_CUDA(dmalloc(&p->norm_d, sizeof(double)));
+  AIRG_CUDA(dmalloc(&p->iflag, sizeof(int)));
+  AIRG_CUDA(dmalloc(&p->nst, sizeof(NewtonState)));
   *out = p;
   return AIRG_OK;
 }
@@ -778,15 +779,15 @@ int airg_plan_destroy(airg_plan* p) {
   if (!p) return AIRG_OK;
   for (auto& L : p->lv) {
     for (double* q : {L.rc, L.ec, L.rhs, L.ef, L.t0, L.t1, L.t2})
-      if (q) cudaFree(q);
+      if (q) dfree(q);
     free_poly(L.sm);
   }
   free_poly(p->coarse_poly);
   for (double* q : {p->cw0, p->cw1, p->cw2, p->cw3, p->r, p->e, p->parts, p->norm_d})
-    if (q) cudaFree(q);
-  if (p->iflag) cudaFree(p->iflag);
-  if (p->nst) cudaFree(p->nst);
-  if (p->norm_h) cudaFreeHost(p->norm_h);
+    if (q) dfree(q);
+  if (p->iflag) dfree(p->iflag);
+  if (p->nst) dfree(p->nst);
+
   delete p;
   return AIRG_OK;
 }
