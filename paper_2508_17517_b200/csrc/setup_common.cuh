@@ -16,6 +16,45 @@ struct airg_csr_result {
 
 namespace airg {
 
+// Fork / join of a few side streams so independent launches (per row-size
+// class) overlap instead of running back to back with small grids.
+struct Fork {
+  static constexpr int K = 4;
+  cudaStream_t st[K];
+  cudaEvent_t ev0, evs[K];
+  int begin(cudaStream_t s) {
+    static thread_local int dev_init = -1;
+    static thread_local cudaStream_t ss[K];
+    static thread_local cudaEvent_t e0, es[K];
+    int dev = 0;
+    AIRG_CUDA(cudaGetDevice(&dev));
+    if (dev_init != dev) {
+      for (int i = 0; i < K; ++i) {
+        AIRG_CUDA(cudaStreamCreateWithFlags(&ss[i], cudaStreamNonBlocking));
+        AIRG_CUDA(cudaEventCreateWithFlags(&es[i], cudaEventDisableTiming));
+      }
+      AIRG_CUDA(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+      dev_init = dev;
+    }
+    ev0 = e0;
+    for (int i = 0; i < K; ++i) {
+      st[i] = ss[i];
+      evs[i] = es[i];
+    }
+    AIRG_CUDA(cudaEventRecord(ev0, s));
+    for (int i = 0; i < K; ++i) AIRG_CUDA(cudaStreamWaitEvent(st[i], ev0, 0));
+    return AIRG_OK;
+  }
+  cudaStream_t stream(int c) const { return st[c % K]; }
+  int end(cudaStream_t s) {
+    for (int i = 0; i < K; ++i) {
+      AIRG_CUDA(cudaEventRecord(evs[i], st[i]));
+      AIRG_CUDA(cudaStreamWaitEvent(s, evs[i], 0));
+    }
+    return AIRG_OK;
+  }
+};
+
 // exclusive scan of `in` (n entries) into out[0..n] (out[n] = total); returns total on host.
 int scan_counts(const int* in, int* out, int n, long long* total_h, cudaStream_t s);
 // same for 64-bit counts

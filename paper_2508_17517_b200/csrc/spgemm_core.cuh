@@ -101,6 +101,80 @@ __device__ void warp_bitonic(int* buf, V* pay, int P, int lane) {
   }
 }
 
+// Warp-level stable LSD radix sort of (k, v)[0..n) by k (8-bit digits of
+// k - min k), ping-ponging through (k2, v2)[0..n); cnt = 256 ints of scratch.
+// The sorted result is left in (k, v).
+template <typename V>
+__device__ void warp_radix_sort(int* k, V* v, int* k2, V* v2, int n, int* cnt, int lane) {
+  int mn = 0x7fffffff, mx = -0x7fffffff - 1;
+  for (int i = lane; i < n; i += 32) {
+    mn = min(mn, k[i]);
+    mx = max(mx, k[i]);
+  }
+  mn = __reduce_min_sync(kFull, mn);
+  mx = __reduce_max_sync(kFull, mx);
+  const unsigned span = (unsigned)(mx - mn);
+  const int bits = span ? 32 - __clz(span) : 0;
+  const int passes = (bits + 7) / 8;
+  int *src = k, *dst = k2;
+  V *vs = v, *vd = v2;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int p = 0; p < passes; ++p) {
+    const int sh = 8 * p;
+    for (int i = lane; i < 256; i += 32) cnt[i] = 0;
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) atomicAdd(cnt + ((((unsigned)(src[i] - mn)) >> sh) & 255u), 1);
+    __syncwarp();
+    // exclusive scan of the 256 counters: 8 per lane
+    int loc[8], s = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      loc[j] = s;
+      s += cnt[lane * 8 + j];
+    }
+    int inc = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const int excl = inc - s;
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) cnt[lane * 8 + j] = excl + loc[j];
+    __syncwarp();
+    for (int base = 0; base < n; base += 32) {
+      const int i = base + lane;
+      const bool ok = i < n;
+      const int key = ok ? src[i] : 0;
+      const int d = ok ? (int)((((unsigned)(key - mn)) >> sh) & 255u) : 256 + lane;
+      const unsigned peers = __match_any_sync(kFull, d);
+      int off = 0;
+      if (ok) {
+        off = cnt[d] + __popc(peers & lt);
+        dst[off] = key;
+        vd[off] = vs[i];
+      }
+      __syncwarp();
+      if (ok && lane == __ffs(peers) - 1) cnt[d] += __popc(peers);
+      __syncwarp();
+    }
+    int* tk = src;
+    src = dst;
+    dst = tk;
+    V* tv = vs;
+    vs = vd;
+    vd = tv;
+  }
+  if (src != k) {
+    for (int i = lane; i < n; i += 32) {
+      k[i] = src[i];
+      v[i] = vs[i];
+    }
+    __syncwarp();
+  }
+}
+
 __host__ __device__ __forceinline__ int ceil_log2(long long x) {
   int b = 0;
   while ((1ll << b) < x) ++b;

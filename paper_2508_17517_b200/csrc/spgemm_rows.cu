@@ -187,15 +187,18 @@ __global__ void __launch_bounds__(256) spgemm_numeric_kernel(NumArgs a) {
     int bits;
     int* keys;
     double* acc;
+    int* cnt;
     if (a.gkeys) {
       bits = a.gbits[t];
       keys = a.gkeys + a.goff[t];
       acc = a.gacc + a.goff[t];
+      cnt = keys + (1 << bits) - 256;  // global tables are sized >= 2n + 256
     } else {
       bits = a.bits;
       const int T = 1 << bits;
-      acc = smd + (size_t)w * T * 3 / 2;  // T doubles + T ints per warp
+      acc = smd + (size_t)w * ((size_t)T * 3 / 2 + 128);  // T doubles + T ints + 256 ints
       keys = (int*)(acc + T);
+      cnt = keys + T;
     }
     const int T = 1 << bits;
     for (int i = lane; i < T; i += 32) {
@@ -207,11 +210,15 @@ __global__ void __launch_bounds__(256) spgemm_numeric_kernel(NumArgs a) {
     walk_products<true, true>(a.Ap, a.Ac, a.Av, a.Bp, a.Bc, a.Bv, row, lane, op);
     __syncwarp();
     const int n = compact_slots(keys, acc, T, lane);
-    int P = 1;
-    while (P < n) P <<= 1;
-    for (int i = n + lane; i < P; i += 32) keys[i] = 0x7fffffff;
-    __syncwarp();
-    warp_bitonic(keys, acc, P, lane);
+    if (n <= 64) {
+      int P = 1;
+      while (P < n) P <<= 1;
+      for (int i = n + lane; i < P; i += 32) keys[i] = 0x7fffffff;
+      __syncwarp();
+      warp_bitonic(keys, acc, P, lane);
+    } else {
+      warp_radix_sort(keys, acc, keys + n, acc + n, n, cnt, lane);
+    }
     const int o = a.Cp[row];
     if (a.mode == 0) {
       for (int i = lane; i < n; i += 32) {
@@ -291,7 +298,7 @@ static int make_tables(const std::vector<int>& rows, const std::vector<long long
   std::vector<int> bits(n);
   long long tot = 0;
   for (int i = 0; i < n; ++i) {
-    bits[i] = std::max(5, ceil_log2(2 * std::max(1ll, sizes[i])));
+    bits[i] = std::max(5, ceil_log2(2 * std::max(1ll, sizes[i]) + (values ? 256 : 0)));
     off[i] = tot;
     tot += 1ll << bits[i];
   }
@@ -336,16 +343,20 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
     AIRG_TRY(scratch(&ovf_n, 1, s));
     AIRG_CUDA(cudaMemsetAsync(ovf_n, 0, sizeof(int), s));
     const int cbits[3] = {7, 10, 12}, cwarps[3] = {8, 8, 4};
+    AIRG_TRY(set_smem((const void*)spgemm_count_kernel, (size_t)8 * 4096 * sizeof(int)));
+    Fork fk;
+    AIRG_TRY(fk.begin(s));
     for (int c = 0; c < 3; ++c) {
       const int nr = cl.count[c];
       if (!nr) continue;
       const size_t shm = (size_t)cwarps[c] * (1 << cbits[c]) * sizeof(int);
-      AIRG_TRY(set_smem((const void*)spgemm_count_kernel, shm));
       CountArgs a{A.p, A.c, B.p, B.c, cl.list(c), nr, cbits[c], (1 << cbits[c]) * 3 / 4, cnt,
                   ovf_rows, ovf_n, nullptr, nullptr, nullptr};
-      spgemm_count_kernel<<<blocks_for(nr, cwarps[c], 148 * 32), cwarps[c] * 32, shm, s>>>(a);
+      spgemm_count_kernel<<<blocks_for(nr, cwarps[c], 148 * 32), cwarps[c] * 32, shm,
+                            fk.stream(c)>>>(a);
       AIRG_LAUNCH_CHECK();
     }
+    AIRG_TRY(fk.end(s));
     int novf = 0;
     AIRG_CUDA(cudaMemcpyAsync(&novf, ovf_n, sizeof(int), cudaMemcpyDeviceToHost, s));
     AIRG_CUDA(cudaStreamSynchronize(s));
@@ -388,16 +399,20 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
     Classes cl;
     AIRG_TRY(classify(m, rl, {32, 128, 512, 1024, 2048}, cl, s));
     const int cbits[5] = {6, 8, 10, 11, 12}, cwarps[5] = {8, 8, 8, 4, 2};
+    AIRG_TRY(set_smem((const void*)spgemm_numeric_kernel, 200 * 1024));
+    Fork fk;
+    AIRG_TRY(fk.begin(s));
     for (int c = 0; c < 5; ++c) {
       const int nr = cl.count[c];
       if (!nr) continue;
-      const size_t shm = (size_t)cwarps[c] * (1 << cbits[c]) * 12;
-      AIRG_TRY(set_smem((const void*)spgemm_numeric_kernel, shm));
+      const size_t shm = (size_t)cwarps[c] * ((1 << cbits[c]) * 12 + 1024);
       NumArgs a{A.p, A.c, A.v, B.p, B.c, B.v, cl.list(c), nr, cbits[c], Cp, ocol, oval, negate,
                 mode, tol, lump, cnt, anyd, nullptr, nullptr, nullptr, nullptr};
-      spgemm_numeric_kernel<<<blocks_for(nr, cwarps[c], 148 * 32), cwarps[c] * 32, shm, s>>>(a);
+      spgemm_numeric_kernel<<<blocks_for(nr, cwarps[c], 148 * 32), cwarps[c] * 32, shm,
+                              fk.stream(c)>>>(a);
       AIRG_LAUNCH_CHECK();
     }
+    AIRG_TRY(fk.end(s));
     const int nr = cl.count[5];
     if (nr) {
       std::vector<int> rows(nr);
