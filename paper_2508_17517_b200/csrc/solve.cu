@@ -62,15 +62,24 @@ __global__ void __launch_bounds__(256) spmv_vec_kernel(int nrows, const int* __r
     for (int k = b; k < e; ++k) s = add_rn(s, mul_rn(__ldg(val + k), mul_rn(xs, __ldg(x + __ldg(col + k)))));
   } else if (row < nrows) {
     const int b = __ldg(ptr + row), e = __ldg(ptr + row + 1);
-    int k = b + lane;
-    // two independent accumulators for MLP on long rows
-    double s2 = 0.0;
-    for (; k + VS < e; k += 2 * VS) {
-      s = fma(__ldg(val + k), xs * __ldg(x + __ldg(col + k)), s);
-      s2 = fma(__ldg(val + k + VS), xs * __ldg(x + __ldg(col + k + VS)), s2);
+    // rounds of 4 entries per lane: all column/value loads of a round are
+    // issued before the gathers, and all gathers before the FMAs, so every
+    // lane keeps ~8 independent requests in flight (the kernel is latency-,
+    // not issue-bound at these row lengths).
+    for (int k0 = b + lane; k0 < e; k0 += 4 * VS) {
+      int c[4];
+      double a[4], xv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = k0 + q * VS;
+        c[q] = k < e ? __ldg(col + k) : -1;
+        a[q] = k < e ? __ldg(val + k) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) xv[q] = c[q] >= 0 ? __ldg(x + c[q]) : 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) s = fma(a[q], xs * xv[q], s);
     }
-    if (k < e) s = fma(__ldg(val + k), xs * __ldg(x + __ldg(col + k)), s);
-    s += s2;
   }
   if (VS > 1) {
 #pragma unroll
@@ -110,13 +119,14 @@ __global__ void spmv_exact_kernel(int nrows, const int* __restrict__ ptr,
   }
 }
 
+// lanes per row: about 4-8 entries per lane (one or two unrolled rounds)
 static int pick_vs(long long nnz, int nrows) {
   double mean = nrows > 0 ? (double)nnz / nrows : 0.0;
-  if (mean <= 2.5) return 1;
-  if (mean <= 5) return 2;
-  if (mean <= 10) return 4;
-  if (mean <= 20) return 8;
-  if (mean <= 40) return 16;
+  if (mean <= 6) return 1;
+  if (mean <= 12) return 2;
+  if (mean <= 24) return 4;
+  if (mean <= 48) return 8;
+  if (mean <= 96) return 16;
   return 32;
 }
 
@@ -328,6 +338,149 @@ __global__ void __launch_bounds__(1024) newton_cta_kernel(
   }
 }
 
+// NaN-propagating max (np.max semantics)
+__device__ __forceinline__ double nanmax(double a, double b) {
+  return a != a ? a : (b != b ? b : fmax(a, b));
+}
+
+// Single-CTA Newton with u / w / x (and the matrix when it fits) in shared
+// memory.  Two barriers per root:
+//  * real root:  w = A u | barrier | x += (s/t) u, u -= w/t, local max | max barrier
+//    The "delta finite" test is taken from the previous max: with c = s/t,
+//    all_i finite(c*u_i) <=> finite(c*max|u|) (rounding is monotone), and the
+//    max propagates NaN like np.max.
+//  * pair:       w = A u (+ finite test) | barrier_or | z_i = (A w)_i, x, u
+//    updated by the owner of row i, local max | max barrier
+// The max reduction double-buffers its partials, so no third barrier.
+template <bool E>
+__global__ void __launch_bounds__(1024) newton_smem_kernel(
+    int n, const int* __restrict__ gptr, const int* __restrict__ gcol, const double* __restrict__ gval,
+    int mat_smem, const double* __restrict__ b, double* __restrict__ xout, int nunits,
+    const int* __restrict__ utype, const double* __restrict__ up1, const double* __restrict__ up2,
+    int identity_cols = 0) {
+  extern __shared__ double sm[];
+  __shared__ double red[2][32];
+  const int tid = threadIdx.x, nthr = blockDim.x, nw = nthr >> 5;
+  // identity_cols: CTA j applies q(A) to e_j and writes column j of Q (column-major)
+  const int jcol = identity_cols ? (int)blockIdx.x : -1;
+  if (identity_cols) xout += (size_t)jcol * n;
+  double* u = sm;
+  double* w = u + n;
+  double* x = w + n;
+  const int* ptr = gptr;
+  const int* col = gcol;
+  const double* val = gval;
+  if (mat_smem) {
+    const int nnz = gptr[n];
+    double* sval = x + n;
+    int* sptr = (int*)(sval + nnz);
+    int* scol = sptr + n + 1;
+    for (int i = tid; i < nnz; i += nthr) {
+      sval[i] = gval[i];
+      scol[i] = gcol[i];
+    }
+    for (int i = tid; i <= n; i += nthr) sptr[i] = gptr[i];
+    ptr = sptr;
+    col = scol;
+    val = sval;
+  }
+  double lmax = 0.0;
+  for (int i = tid; i < n; i += nthr) {
+    const double bi = identity_cols ? (i == jcol ? 1.0 : 0.0) : b[i];
+    u[i] = bi;
+    x[i] = 0.0;
+    lmax = nanmax(lmax, fabs(bi));
+  }
+  constexpr int VS = E ? 1 : 2;  // 512 row groups: coarse grids of <= 512 rows in one pass
+  const int g = tid / VS, gl = tid % VS, ng = nthr / VS;
+  // every lane of a group must call this (the shuffles name the whole warp);
+  // rows past n contribute an empty range
+  auto rowdot = [&](const double* v, int r) {
+    double s = 0.0;
+    const int kb = r < n ? ptr[r] : 0, ke = r < n ? ptr[r + 1] : 0;
+    if (E) {
+      for (int k = kb; k < ke; ++k) s = add_rn(s, mul_rn(val[k], v[col[k]]));
+    } else {
+      for (int k = kb + gl; k < ke; k += VS) s = fma(val[k], v[col[k]], s);
+#pragma unroll
+      for (int o = VS / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, VS);
+    }
+    return s;
+  };
+  auto block_max = [&](double v, int parity) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = nanmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((tid & 31) == 0) red[parity][tid >> 5] = v;
+    __syncthreads();
+    // every warp reduces the partials itself (no serial 32-step loop, no 2nd barrier)
+    double m = (tid & 31) < nw ? red[parity][tid & 31] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = nanmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    return m;
+  };
+  double nrm = block_max(lmax, 1);
+  double scale = 1.0;
+  const int rows_pad = ((n + ng - 1) / ng) * ng;  // whole groups iterate together (shuffles)
+  for (int k = 0; k < nunits; ++k) {
+    lmax = 0.0;
+    if (utype[k] == 0) {
+      const double t = up1[k];
+      const double sc = scale / t;
+      if (!isfinite(mul<E>(sc, nrm))) break;
+      for (int r = g; r < rows_pad; r += ng) {
+        const double s = rowdot(u, r);
+        if (gl == 0 && r < n) w[r] = s;
+      }
+      __syncthreads();
+      for (int i = tid; i < n; i += nthr) {
+        const double ui = u[i];
+        x[i] = E ? add_rn(x[i], mul_rn(sc, ui)) : x[i] + sc * ui;
+        const double un = E ? sub_rn(ui, __ddiv_rn(w[i], t)) : ui - w[i] / t;
+        u[i] = un;
+        lmax = nanmax(lmax, fabs(un));
+      }
+    } else {
+      const double two_a = up1[k], m2 = up2[k];
+      const double sc = scale / m2;
+      int bad = 0;
+      for (int r = g; r < rows_pad; r += ng) {
+        const double s = rowdot(u, r);
+        if (gl == 0 && r < n) {
+          w[r] = s;
+          const double d = E ? mul_rn(sc, sub_rn(mul_rn(two_a, u[r]), s)) : sc * (two_a * u[r] - s);
+          bad |= !isfinite(d);
+        }
+      }
+      if (__syncthreads_or(bad)) break;
+      for (int r = g; r < rows_pad; r += ng) {
+        const double z = rowdot(w, r);
+        if (gl == 0 && r < n) {
+          const double ui = u[r], wi = w[r];
+          if (E) {
+            x[r] = add_rn(x[r], mul_rn(sc, sub_rn(mul_rn(two_a, ui), wi)));
+            u[r] = add_rn(ui, __ddiv_rn(sub_rn(z, mul_rn(two_a, wi)), m2));
+          } else {
+            x[r] += sc * (two_a * ui - wi);
+            u[r] = ui + (z - two_a * wi) / m2;
+          }
+          lmax = nanmax(lmax, fabs(u[r]));
+        }
+      }
+    }
+    nrm = block_max(lmax, k & 1);
+    if (nrm == 0.0) break;
+    if (nrm > 1e150 || nrm < 1e-150) {
+      for (int i = tid; i < n; i += nthr) u[i] = E ? __ddiv_rn(u[i], nrm) : u[i] / nrm;
+      scale = E ? mul_rn(scale, nrm) : scale * nrm;
+      nrm = 1.0;  // max|u/nrm| == 1 exactly
+      __syncthreads();
+      if (!isfinite(scale) || scale == 0.0) break;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += nthr) xout[i] = x[i];
+}
+
 // Multi-CTA Newton for large coarse grids: host loop over roots with the
 // scale / stop state kept on the device.
 struct NewtonState {
@@ -468,6 +621,7 @@ struct Poly {
 };
 
 constexpr int kNewtonCtaMax = 16384;  // single-CTA Newton up to this many rows
+constexpr int kDenseCoarseMax = 2048;  // fast mode: dense Q = q(A) up to this many rows
 
 struct Work {
   double* buf = nullptr;
@@ -558,6 +712,28 @@ static int poly_apply_dev(const Poly& p, const Csr& A, const double* b, double* 
   }
   // Newton
   const int nunits = (int)p.utype.size();
+  const size_t vec_bytes = (size_t)3 * n * sizeof(double);
+  const size_t mat_bytes = (size_t)A.nnz * 12 + (size_t)(n + 1) * 4;
+  const size_t smem_cap = 200 * 1024;
+  if (vec_bytes <= smem_cap) {
+    const int mat_smem = vec_bytes + mat_bytes <= smem_cap ? 1 : 0;
+    const size_t shm = vec_bytes + (mat_smem ? mat_bytes : 0);
+    const int thr = 1024;
+    if (exact) {
+      AIRG_CUDA(cudaFuncSetAttribute(newton_smem_kernel<true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap));
+      newton_smem_kernel<true><<<1, thr, shm, s>>>(n, A.ptr, A.col, A.val, mat_smem, b, y, nunits,
+                                                   p.d_utype, p.d_p1, p.d_p2);
+    } else {
+      AIRG_CUDA(cudaFuncSetAttribute(newton_smem_kernel<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap));
+      newton_smem_kernel<false><<<1, thr, shm, s>>>(n, A.ptr, A.col, A.val, mat_smem, b, y, nunits,
+                                                    p.d_utype, p.d_p1, p.d_p2);
+    }
+    ++g_launches;
+    AIRG_LAUNCH_CHECK();
+    return AIRG_OK;
+  }
   if (n <= kNewtonCtaMax) {
     if (exact)
       newton_cta_kernel<true><<<1, 1024, 0, s>>>(n, A.ptr, A.col, A.val, b, y, t0, t1, t2, nunits,
@@ -659,7 +835,20 @@ struct LevelOps {
   double* t2 = nullptr;   // n_f (extra smooths)
 };
 
+struct GraphEntry {
+  int kind, level;
+  const void* a;
+  const void* b;
+  int fits;
+  bool exact;
+  cudaGraphExec_t exec;
+  long long nk;  // kernels per replay
+};
+
 struct airg_plan {
+  cudaStream_t cs = nullptr;  // plan stream: captures and replays
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  std::vector<GraphEntry> graphs;
   int nlevels = 0;
   std::vector<LevelOps> lv;
   Csr top;
@@ -678,6 +867,7 @@ struct airg_plan {
   long long launches = 0;
   bool ready_top = false, ready_coarse = false;
   bool exact = false;  // reference arithmetic order (parity mode)
+  double* coarseQ = nullptr;  // dense q(A_coarse) for the fast coarse solve
 };
 
 static int alloc_vec(double** p, long long n) {
@@ -777,13 +967,20 @@ int airg_plan_create(int nlevels, airg_plan** out) {
 
 int airg_plan_destroy(airg_plan* p) {
   if (!p) return AIRG_OK;
+  for (auto& g : p->graphs) cudaGraphExecDestroy(g.exec);
+  if (p->cs) {
+    cudaStreamSynchronize(p->cs);
+    cudaStreamDestroy(p->cs);
+    cudaEventDestroy(p->ev_in);
+    cudaEventDestroy(p->ev_out);
+  }
   for (auto& L : p->lv) {
     for (double* q : {L.rc, L.ec, L.rhs, L.ef, L.t0, L.t1, L.t2})
       if (q) dfree(q);
     free_poly(L.sm);
   }
   free_poly(p->coarse_poly);
-  for (double* q : {p->cw0, p->cw1, p->cw2, p->cw3, p->r, p->e, p->parts, p->norm_d})
+  for (double* q : {p->cw0, p->cw1, p->cw2, p->cw3, p->r, p->e, p->parts, p->norm_d, p->coarseQ})
     if (q) dfree(q);
   if (p->iflag) dfree(p->iflag);
   if (p->nst) dfree(p->nst);
@@ -868,6 +1065,54 @@ static int smooth_level(airg_plan* p, LevelOps& L, const double* rhs, double* ou
                         s, p->exact);
 }
 
+// y = Q r, Q column-major n x n (coalesced over rows)
+// block = 32 rows x 8 column slices; lanes read 32 consecutive rows (256 B)
+__global__ void __launch_bounds__(256) dense_gemv_kernel(int n, const double* __restrict__ Q,
+                                                         const double* __restrict__ r,
+                                                         double* __restrict__ y) {
+  __shared__ double part[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + lane;
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  if (i < n) {
+    int j = w;
+    for (; j + 24 < n; j += 32) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) s[q] = fma(__ldg(Q + (size_t)(j + 8 * q) * n + i), __ldg(r + j + 8 * q), s[q]);
+    }
+    for (; j < n; j += 8) s[0] = fma(__ldg(Q + (size_t)j * n + i), __ldg(r + j), s[0]);
+  }
+  part[w][lane] = (s[0] + s[1]) + (s[2] + s[3]);
+  __syncthreads();
+  if (w == 0 && i < n) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t += part[q][lane];
+    y[i] = t;
+  }
+}
+
+// Q = q(A_coarse) applied to every identity column, one CTA per column.
+static int build_dense_coarse(airg_plan* p, cudaStream_t s) {
+  const int n = p->coarse.nrows;
+  AIRG_CUDA(dmalloc(&p->coarseQ, (size_t)n * n * sizeof(double)));
+  const Poly& cp = p->coarse_poly;
+  const Csr& A = p->coarse;
+  const size_t vec_bytes = (size_t)3 * n * sizeof(double);
+  const size_t mat_bytes = (size_t)A.nnz * 12 + (size_t)(n + 1) * 4;
+  const size_t cap = 200 * 1024;
+  const int mat_smem = vec_bytes + mat_bytes <= cap ? 1 : 0;
+  const size_t shm = vec_bytes + (mat_smem ? mat_bytes : 0);
+  AIRG_CUDA(cudaFuncSetAttribute(newton_smem_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)cap));
+  newton_smem_kernel<false><<<n, 256, shm, s>>>(n, A.ptr, A.col, A.val, mat_smem, nullptr,
+                                                p->coarseQ, (int)cp.utype.size(), cp.d_utype,
+                                                cp.d_p1, cp.d_p2, 1);
+  ++g_launches;
+  AIRG_LAUNCH_CHECK();
+  return AIRG_OK;
+}
+
 // V-cycle from `level` with residual r (size n_level) -> e (size n_level).
 static int vcycle_rec(airg_plan* p, int level, const double* r, double* e, int fits,
                       cudaStream_t s) {
@@ -875,6 +1120,15 @@ static int vcycle_rec(airg_plan* p, int level, const double* r, double* e, int f
     if (!p->ready_coarse) {
       set_error("plan has no coarse solver");
       return AIRG_ERR_ARG;
+    }
+    if (!p->exact && p->coarse_poly.kind == 1 && p->coarse.nrows <= kDenseCoarseMax) {
+      // fast mode: y = Q r with Q = q(A_coarse) precomputed column by column
+      if (!p->coarseQ) AIRG_TRY(build_dense_coarse(p, s));
+      const int n = p->coarse.nrows;
+      dense_gemv_kernel<<<(n + 31) / 32, 256, 0, s>>>(n, p->coarseQ, r, e);
+      ++g_launches;
+      AIRG_LAUNCH_CHECK();
+      return AIRG_OK;
     }
     return poly_apply_dev(p->coarse_poly, p->coarse, r, e, p->cw0, p->cw1, p->cw2, p->cw3,
                           p->iflag, p->parts, p->nst, s, p->exact);
@@ -910,6 +1164,67 @@ static int vcycle_rec(airg_plan* p, int level, const double* r, double* e, int f
   return AIRG_OK;
 }
 
+// ---------------------------------------------------------------------------
+// CUDA-graph replay: a V-cycle is ~170 dependent launches; capturing it once
+// per (operation, vectors) removes the host launch gaps between them.
+// ---------------------------------------------------------------------------
+static bool graphs_enabled() {
+  static int v = -1;
+  if (v < 0) v = getenv("AIRG_NO_GRAPH") ? 0 : 1;
+  return v == 1;
+}
+
+static int plan_streams(airg_plan* p) {
+  if (!p->cs) {
+    AIRG_CUDA(cudaStreamCreateWithFlags(&p->cs, cudaStreamNonBlocking));
+    AIRG_CUDA(cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming));
+    AIRG_CUDA(cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming));
+  }
+  return AIRG_OK;
+}
+
+// things a capture must not do (synchronous allocation) are done up front
+static int prepare_capture(airg_plan* p, cudaStream_t s) {
+  if (!p->exact && p->ready_coarse && p->coarse_poly.kind == 1 &&
+      p->coarse.nrows <= kDenseCoarseMax && !p->coarseQ) {
+    AIRG_TRY(build_dense_coarse(p, s));
+    AIRG_CUDA(cudaStreamSynchronize(s));
+  }
+  return AIRG_OK;
+}
+
+template <class F>
+static int run_graph(airg_plan* p, int kind, int level, const void* a, const void* b, int fits,
+                     cudaStream_t cs, F&& issue) {
+  if (!graphs_enabled()) return issue(cs);
+  GraphEntry* ent = nullptr;
+  for (auto& g : p->graphs)
+    if (g.kind == kind && g.level == level && g.a == a && g.b == b && g.fits == fits &&
+        g.exact == p->exact)
+      ent = &g;
+  if (!ent) {
+    const long long l0 = g_launches;
+    AIRG_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+    const int st = issue(cs);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+    if (st != AIRG_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return st;
+    }
+    AIRG_CUDA(ce);
+    cudaGraphExec_t ex = nullptr;
+    AIRG_CUDA(cudaGraphInstantiate(&ex, graph, 0));
+    cudaGraphDestroy(graph);
+    p->graphs.push_back(GraphEntry{kind, level, a, b, fits, p->exact, ex, g_launches - l0});
+    ent = &p->graphs.back();
+    g_launches = l0;
+  }
+  AIRG_CUDA(cudaGraphLaunch(ent->exec, cs));
+  g_launches += ent->nk;
+  return AIRG_OK;
+}
+
 extern "C" {
 
 int airg_plan_vcycle(airg_plan* p, int level, const double* r, double* e, int f_smooth_its,
@@ -918,7 +1233,17 @@ int airg_plan_vcycle(airg_plan* p, int level, const double* r, double* e, int f_
     set_error("level %d out of range", level);
     return AIRG_ERR_ARG;
   }
-  return vcycle_rec(p, level, r, e, f_smooth_its < 1 ? 1 : f_smooth_its, (cudaStream_t)stream);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int fits = f_smooth_its < 1 ? 1 : f_smooth_its;
+  AIRG_TRY(plan_streams(p));
+  AIRG_TRY(prepare_capture(p, s));
+  AIRG_CUDA(cudaEventRecord(p->ev_in, s));
+  AIRG_CUDA(cudaStreamWaitEvent(p->cs, p->ev_in, 0));
+  AIRG_TRY(run_graph(p, 0, level, r, e, fits, p->cs,
+                     [&](cudaStream_t t) { return vcycle_rec(p, level, r, e, fits, t); }));
+  AIRG_CUDA(cudaEventRecord(p->ev_out, p->cs));
+  AIRG_CUDA(cudaStreamWaitEvent(s, p->ev_out, 0));
+  return AIRG_OK;
 }
 
 int64_t airg_plan_launches(airg_plan* p) { return p ? p->launches : 0; }
@@ -930,9 +1255,8 @@ int airg_plan_set_exact(airg_plan* p, int exact) {
 
 }  // extern "C"
 
-// r = b - A x, with deterministic norm into p->norm_h (synchronous)
-static int residual_norm(airg_plan* p, const double* b, const double* x, double* rnorm,
-                         cudaStream_t s) {
+// r = b - A x with the fixed-order norm reduction into p->norm_d (stream-ordered)
+static int residual_launch(airg_plan* p, const double* b, const double* x, cudaStream_t s) {
   const Csr& A = p->top;
   const int nb = p->exact ? (A.nrows + 255) / 256 : spmv_blocks(A);  // blocks of the launch below
   double* parts = p->parts;
@@ -945,23 +1269,50 @@ static int residual_norm(airg_plan* p, const double* b, const double* x, double*
   finish_norm_kernel<<<1, 1024, 0, s>>>(nb, parts, p->norm_d);
   ++g_launches;
   AIRG_LAUNCH_CHECK();
+  return AIRG_OK;
+}
+
+// r = b - A x, with deterministic norm into p->norm_h (synchronous)
+static int residual_norm(airg_plan* p, const double* b, const double* x, double* rnorm,
+                         cudaStream_t s) {
+  AIRG_TRY(residual_launch(p, b, x, s));
   AIRG_CUDA(cudaMemcpyAsync(p->norm_h, p->norm_d, sizeof(double), cudaMemcpyDeviceToHost, s));
   AIRG_CUDA(cudaStreamSynchronize(s));
   *rnorm = *p->norm_h;
   return AIRG_OK;
 }
 
+static int richardson_body(airg_plan* p, const double* b, double* x, double rtol, double atol,
+                           int max_iters, int f_smooth_its, double* history, int* iterations,
+                           int* converged, cudaStream_t s);
+
 extern "C" int airg_plan_richardson(airg_plan* p, const double* b, double* x, double rtol,
                                     double atol, int max_iters, int f_smooth_its,
                                     double* history, int* iterations, int* converged,
                                     void* stream) {
-  cudaStream_t s = (cudaStream_t)stream;
+  cudaStream_t caller = (cudaStream_t)stream;
   if (!p->ready_top) {
     set_error("plan has no top matrix");
     return AIRG_ERR_ARG;
   }
+  AIRG_TRY(plan_streams(p));
+  AIRG_TRY(prepare_capture(p, caller));
+  AIRG_CUDA(cudaEventRecord(p->ev_in, caller));
+  AIRG_CUDA(cudaStreamWaitEvent(p->cs, p->ev_in, 0));
+  cudaStream_t s = p->cs;
+  const int st = richardson_body(p, b, x, rtol, atol, max_iters, f_smooth_its, history, iterations,
+                                 converged, s);
+  cudaEventRecord(p->ev_out, s);
+  cudaStreamWaitEvent(caller, p->ev_out, 0);
+  return st;
+}
+
+static int richardson_body(airg_plan* p, const double* b, double* x, double rtol, double atol,
+                           int max_iters, int f_smooth_its, double* history, int* iterations,
+                           int* converged, cudaStream_t s) {
   const long long l0 = g_launches;
   const int n = p->top.nrows;
+  const int fits = f_smooth_its < 1 ? 1 : f_smooth_its;
   double bnorm = 0.0, rnorm = 0.0;
   {
     // ||b|| with the same fixed-order reduction
@@ -987,9 +1338,15 @@ extern "C" int airg_plan_richardson(airg_plan* p, const double* b, double* x, do
   bool conv = rnorm <= thr;
   int its = 0;
   while (!conv && its < max_iters) {
-    AIRG_TRY(vcycle_rec(p, 0, p->r, p->e, f_smooth_its < 1 ? 1 : f_smooth_its, s));
-    AIRG_TRY(launch_axpby(n, x, nullptr, 1.0, x, nullptr, 1.0, p->e, s, p->exact));
-    AIRG_TRY(residual_norm(p, b, x, &rnorm, s));
+    // x += V-cycle(r); r = b - A x; ||r|| partials -> one captured graph
+    AIRG_TRY(run_graph(p, 1, 0, b, x, fits, s, [&](cudaStream_t t) {
+      AIRG_TRY(vcycle_rec(p, 0, p->r, p->e, fits, t));
+      AIRG_TRY(launch_axpby(n, x, nullptr, 1.0, x, nullptr, 1.0, p->e, t, p->exact));
+      return residual_launch(p, b, x, t);
+    }));
+    AIRG_CUDA(cudaMemcpyAsync(p->norm_h, p->norm_d, sizeof(double), cudaMemcpyDeviceToHost, s));
+    AIRG_CUDA(cudaStreamSynchronize(s));
+    rnorm = *p->norm_h;
     ++its;
     history[its] = rnorm;
     *iterations = its;
