@@ -78,9 +78,20 @@ def check(status, what=''):
     raise AirgError(f'{what}: status {status}: {msg}')
 
 
+CALL_TIMES = {} if os.environ.get('AIRG_PROFILE_CALLS') else None
+
+
 def call(name, *args):
     lib = load()
-    st = getattr(lib, name)(*args)
+    if CALL_TIMES is None:
+        st = getattr(lib, name)(*args)
+    else:
+        import time
+        t0 = time.perf_counter()
+        st = getattr(lib, name)(*args)
+        rec = CALL_TIMES.setdefault(name, [0, 0.0])
+        rec[0] += 1
+        rec[1] += time.perf_counter() - t0
     check(st, name)
     return st
 

@@ -14,7 +14,7 @@
 
 namespace airg {
 
-constexpr int kArnoldiCta = 32768;
+constexpr int kArnoldiCta = 4096;
 
 __device__ double block_sum(double v, double* red) {
   v = warp_sum(v);

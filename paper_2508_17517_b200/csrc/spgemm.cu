@@ -257,19 +257,54 @@ __global__ void __launch_bounds__(128) poly_assemble_kernel(PolyArgs a) {
       __syncwarp();
     }
     for (int k = 2; k <= d; ++k) {
-      // nxt = mask(cur * A): walk present entries of cur in column (= position) order
-      for (int q = 0; q < m; ++q) {
-        if (!fcur[q]) continue;
-        const int col_q = a.Pc[pb + q];
-        const double lv = cur[q];
-        for (int jj = a.Ap[col_q] + lane; jj < a.Ap[col_q + 1]; jj += 32) {
-          const int p = map_find(keys, pv, a.bits, a.Ac[jj]);
-          if (p >= 0) {
-            nxt[p] = add_rn(nxt[p], mul_rn(lv, a.Av[jj]));
-            fnxt[p] = 1;
-          }
+      // nxt = mask(cur * A): walk present entries of cur in column (= position)
+      // order; the A-row bounds of 32 positions are fetched at once (one per
+      // lane) and the next present row's head is loaded before the current
+      // row is processed.
+      for (int base = 0; base < m; base += 32) {
+        const int q = base + lane;
+        const bool pres = q < m && fcur[q];
+        int rb = 0, re = 0;
+        double lv = 0.0;
+        if (pres) {
+          const int col_q = a.Pc[pb + q];
+          rb = a.Ap[col_q];
+          re = a.Ap[col_q + 1];
+          lv = cur[q];
         }
-        __syncwarp();
+        unsigned todo = __ballot_sync(0xffffffffu, pres);
+        int t = todo ? __ffs(todo) - 1 : 0;
+        int cb = __shfl_sync(0xffffffffu, rb, t), ce = __shfl_sync(0xffffffffu, re, t);
+        int hc = cb + lane < ce ? a.Ac[cb + lane] : -1;
+        double hv = cb + lane < ce ? a.Av[cb + lane] : 0.0;
+        while (todo) {
+          const double l = __shfl_sync(0xffffffffu, lv, t);
+          const int tb = cb, te = ce, c0 = hc;
+          const double v0 = hv;
+          todo &= todo - 1;
+          if (todo) {  // prefetch the head of the next present row
+            t = __ffs(todo) - 1;
+            cb = __shfl_sync(0xffffffffu, rb, t);
+            ce = __shfl_sync(0xffffffffu, re, t);
+            hc = cb + lane < ce ? a.Ac[cb + lane] : -1;
+            hv = cb + lane < ce ? a.Av[cb + lane] : 0.0;
+          }
+          if (c0 >= 0) {
+            const int p = map_find(keys, pv, a.bits, c0);
+            if (p >= 0) {
+              nxt[p] = add_rn(nxt[p], mul_rn(l, v0));
+              fnxt[p] = 1;
+            }
+          }
+          for (int jj = tb + 32 + lane; jj < te; jj += 32) {
+            const int p = map_find(keys, pv, a.bits, a.Ac[jj]);
+            if (p >= 0) {
+              nxt[p] = add_rn(nxt[p], mul_rn(l, a.Av[jj]));
+              fnxt[p] = 1;
+            }
+          }
+          __syncwarp();
+        }
       }
       const double ck = a.coef[k];
       for (int i = lane; i < m; i += 32) {
