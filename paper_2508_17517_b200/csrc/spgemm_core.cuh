@@ -201,22 +201,41 @@ __device__ __forceinline__ void walk_products(const int* __restrict__ Ap, const 
       be = Bp[k + 1];
     }
     const int cnt = min(32, ae - base);
+    // the first kPre*32 entries of the next B row live in registers one step ahead
+    constexpr int kPre = 1;
     int cb = __shfl_sync(kFull, bb, 0), ce = __shfl_sync(kFull, be, 0);
-    int pc = cb + lane < ce ? Bc[cb + lane] : -1;
-    double pv = (VALUES && cb + lane < ce) ? Bv[cb + lane] : 0.0;
+    int pc[kPre];
+    double pv[kPre];
+#pragma unroll
+    for (int q = 0; q < kPre; ++q) {
+      const int jj = cb + 32 * q + lane;
+      pc[q] = jj < ce ? Bc[jj] : -1;
+      pv[q] = (VALUES && jj < ce) ? Bv[jj] : 0.0;
+    }
     for (int t = 0; t < cnt; ++t) {
       const double a = VALUES ? __shfl_sync(kFull, av, t) : 0.0;
       const int tb = cb, te = ce;
-      const int c0 = pc;
-      const double v0 = pv;
-      if (t + 1 < cnt) {  // prefetch the head of the next B row
+      int c0[kPre];
+      double v0[kPre];
+#pragma unroll
+      for (int q = 0; q < kPre; ++q) {
+        c0[q] = pc[q];
+        v0[q] = pv[q];
+      }
+      if (t + 1 < cnt) {  // prefetch the next B row
         cb = __shfl_sync(kFull, bb, t + 1);
         ce = __shfl_sync(kFull, be, t + 1);
-        pc = cb + lane < ce ? Bc[cb + lane] : -1;
-        if (VALUES) pv = cb + lane < ce ? Bv[cb + lane] : 0.0;
+#pragma unroll
+        for (int q = 0; q < kPre; ++q) {
+          const int jj = cb + 32 * q + lane;
+          pc[q] = jj < ce ? Bc[jj] : -1;
+          if (VALUES) pv[q] = jj < ce ? Bv[jj] : 0.0;
+        }
       }
-      if (c0 >= 0) f(a, c0, v0);
-      for (int jb = tb + 32; jb < te; jb += 96) {
+#pragma unroll
+      for (int q = 0; q < kPre; ++q)
+        if (c0[q] >= 0) f(a, c0[q], v0[q]);
+      for (int jb = tb + 32 * kPre; jb < te; jb += 96) {
         int cc[3];
         double vv[3];
 #pragma unroll

@@ -235,6 +235,87 @@ __global__ void __launch_bounds__(256) spgemm_numeric_kernel(NumArgs a) {
   }
 }
 
+// Long output rows: one CTA per row, the row's key -> slot table and
+// accumulators in shared memory shared by all warps.  Each B row is consumed
+// by the whole CTA in one step (threads split its entries); steps are ordered
+// by __syncthreads, so every output entry still receives its k in ascending
+// order.  The next B row is prefetched into registers during the current
+// step.  Warp 0 compacts, sorts and writes the row.
+__global__ void __launch_bounds__(128) spgemm_numeric_block_kernel(NumArgs a) {
+  extern __shared__ double smd[];
+  __shared__ int mbb[32], mbe[32];
+  __shared__ double mav[32];
+  const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31;
+  const int bits = a.bits;
+  const int T = 1 << bits;
+  double* acc = smd;
+  int* keys = (int*)(acc + T);
+  int* cnt = keys + T;
+  for (long long t = blockIdx.x; t < a.nrows; t += gridDim.x) {
+    const int row = a.rows[t];
+    for (int i = tid; i < T; i += nthr) {
+      keys[i] = kEmpty;
+      acc[i] = 0.0;
+    }
+    AccOp op{keys, acc, bits};
+    const int ab = a.Ap[row], ae = a.Ap[row + 1];
+    for (int base = ab; base < ae; base += 32) {
+      __syncthreads();
+      if (tid < 32 && base + tid < ae) {
+        const int k = a.Ac[base + tid];
+        mav[tid] = a.Av[base + tid];
+        mbb[tid] = a.Bp[k];
+        mbe[tid] = a.Bp[k + 1];
+      }
+      __syncthreads();
+      const int cnt_k = min(32, ae - base);
+      int cb = mbb[0], ce = mbe[0];
+      int pc = cb + tid < ce ? a.Bc[cb + tid] : -1;
+      double pv = cb + tid < ce ? a.Bv[cb + tid] : 0.0;
+      for (int tt = 0; tt < cnt_k; ++tt) {
+        const double av = mav[tt];
+        const int tb = cb, te = ce, c0 = pc;
+        const double v0 = pv;
+        if (tt + 1 < cnt_k) {
+          cb = mbb[tt + 1];
+          ce = mbe[tt + 1];
+          pc = cb + tid < ce ? a.Bc[cb + tid] : -1;
+          pv = cb + tid < ce ? a.Bv[cb + tid] : 0.0;
+        }
+        if (c0 >= 0) op(av, c0, v0);
+        for (int jj = tb + nthr + tid; jj < te; jj += nthr) op(av, a.Bc[jj], a.Bv[jj]);
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+    if (tid < 32) {
+      const int n = compact_slots(keys, acc, T, lane);
+      if (n <= 64) {
+        int P = 1;
+        while (P < n) P <<= 1;
+        for (int i = n + lane; i < P; i += 32) keys[i] = 0x7fffffff;
+        __syncwarp();
+        warp_bitonic(keys, acc, P, lane);
+      } else {
+        warp_radix_sort(keys, acc, keys + n, acc + n, n, cnt, lane);
+      }
+      const int o = a.Cp[row];
+      if (a.mode == 0) {
+        for (int i = lane; i < n; i += 32) {
+          a.Cc[o + i] = keys[i];
+          const double v = acc[i];
+          a.Cv[o + i] = a.negate ? -v : v;
+        }
+      } else {
+        const int wr = drop_lump_row(keys, acc, n, row, a.tol, a.lump, a.Cc, a.Cv,
+                                     (long long)o + row, lane, a.any_drop);
+        if (lane == 0) a.out_cnt[row] = wr;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void compact_raw_kernel(int m, const int* __restrict__ rawp, const int* __restrict__ optr,
                                    const int* __restrict__ icol, const double* __restrict__ ival,
                                    int* __restrict__ ocol, double* __restrict__ oval) {
@@ -402,14 +483,20 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
     AIRG_TRY(set_smem((const void*)spgemm_numeric_kernel, 200 * 1024));
     Fork fk;
     AIRG_TRY(fk.begin(s));
+    AIRG_TRY(set_smem((const void*)spgemm_numeric_block_kernel, 200 * 1024));
     for (int c = 0; c < 5; ++c) {
       const int nr = cl.count[c];
       if (!nr) continue;
-      const size_t shm = (size_t)cwarps[c] * ((1 << cbits[c]) * 12 + 1024);
       NumArgs a{A.p, A.c, A.v, B.p, B.c, B.v, cl.list(c), nr, cbits[c], Cp, ocol, oval, negate,
                 mode, tol, lump, cnt, anyd, nullptr, nullptr, nullptr, nullptr};
-      spgemm_numeric_kernel<<<blocks_for(nr, cwarps[c], 148 * 32), cwarps[c] * 32, shm,
-                              fk.stream(c)>>>(a);
+      if (c >= 3) {  // long rows: one CTA of 4 warps per row, table shared by the CTA
+        const size_t shm = (size_t)(1 << cbits[c]) * 12 + 1024;
+        spgemm_numeric_block_kernel<<<std::min(nr, 148 * 16), 128, shm, fk.stream(c)>>>(a);
+      } else {
+        const size_t shm = (size_t)cwarps[c] * ((1 << cbits[c]) * 12 + 1024);
+        spgemm_numeric_kernel<<<blocks_for(nr, cwarps[c], 148 * 32), cwarps[c] * 32, shm,
+                                fk.stream(c)>>>(a);
+      }
       AIRG_LAUNCH_CHECK();
     }
     AIRG_TRY(fk.end(s));

@@ -14,6 +14,9 @@ for rep in range(3):
     H = G.setup(A, G.SetupConfig())
     torch.cuda.synchronize(); t1 = time.perf_counter()
     print('rep', rep, 'setup', t1 - t0, {k: round(v, 3) for k, v in H.setup_breakdown.items()})
+    ms = torch.cuda.memory_stats()
+    print('   torch allocator: device allocs', ms.get('num_device_alloc'), 'frees',
+          ms.get('num_device_free'), 'reserved GB', ms.get('reserved_bytes.all.current', 0) / 1e9)
 tot = sum(v[1] for v in L.CALL_TIMES.values())
 print('sum of call wall', tot)
 for k, v in sorted(L.CALL_TIMES.items(), key=lambda kv: -kv[1][1])[:20]:
