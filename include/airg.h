@@ -117,6 +117,8 @@ int airg_pcg64_fill(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint6
  * ref: polynomial.py:61-65 */
 int airg_random_unit(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
                      int64_t n, double* out, double* norm_h, void* stream);
+/* Pre-grow the library's stream-ordered scratch pool by `bytes` (kept mapped). */
+int airg_reserve(int64_t bytes, void* stream);
 /* Main diagonal (structurally missing entries are 0).  ref: sparse.py:360-367 */
 int airg_diagonal(int n, const int32_t* p, const int32_t* c, const double* v, double* d,
                   void* stream);

@@ -141,6 +141,7 @@ sig('airg_result_free', vp)
 sig('airg_pcg64_fill', u64, u64, u64, u64, i64, f64, f64, vp, vp)
 sig('airg_random_unit', u64, u64, u64, u64, i64, vp, vp, vp)
 sig('airg_diagonal', i32, vp, vp, vp, vp, vp)
+sig('airg_reserve', i64, vp)
 sig('airg_advection_2d', i32, i32, f64, f64, vp, vp, vp, vp)
 sig('airg_strength', i32, vp, vp, vp, i64, f64, pp, pp, vp)
 sig('airg_pmisr', i32, vp, vp, u64, u64, u64, u64, C.c_int, vp, C.POINTER(i32), vp)

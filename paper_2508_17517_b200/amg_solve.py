@@ -99,7 +99,9 @@ class Plan:
         L.call('airg_plan_set_coarse', self.h, Cm.nrows, L.ptr(Cm.row_offsets),
                L.ptr(Cm.col_indices), L.ptr(Cm.values), code, nc, L.hptr(c), nu, L.hptr(t),
                L.hptr(a1), L.hptr(a2), L.ptr(ds))
-        self.hier = H  # keeps every referenced device buffer alive
+        # The plan is owned by H (H._plan) and H owns every device buffer the
+        # plan points at; no back-reference, so dropping H frees both at once
+        # (a cycle here left whole hierarchies to the cyclic GC).
 
     def __del__(self):
         try:
