@@ -46,6 +46,16 @@ def parse():
     return ap.parse_args()
 
 
+def max_over_ranks(value, dist, device):
+    """Max of a per-rank time over all ranks (the step time of the job)."""
+    if dist is None:
+        return float(value)
+    import torch
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def dist_env():
     return (int(os.environ.get('RANK', 0)), int(os.environ.get('WORLD_SIZE', 1)),
             int(os.environ.get('LOCAL_RANK', 0)))
@@ -297,10 +307,7 @@ def ours_arm(args, rank, world, local):
         stop.record()
         barrier()
     ms = start.elapsed_time(stop) / args.steps
-    if dist is not None:
-        t = torch.tensor([ms], device='cuda')
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, dist, 'cuda')
     H, st = info['H'], info['st']
 
     # ---- roofline: one V-cycle (the solve's kernel chain), CUDA events ----
@@ -353,10 +360,7 @@ def ours_arm(args, rank, world, local):
     f1.record()
     barrier()
     e2e_ms = f0.elapsed_time(f1) / k_e2e
-    if dist is not None:
-        t = torch.tensor([e2e_ms], device='cuda')
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = max_over_ranks(e2e_ms, dist, 'cuda')
 
     launches, mine = count_launches(step)
 
