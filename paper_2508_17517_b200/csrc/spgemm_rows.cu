@@ -99,6 +99,53 @@ struct CountCheckOp {
   __device__ __forceinline__ void operator()(double, int c, double) { added += set_insert(keys, bits, c); }
 };
 
+// Long rows (product upper bound > 512): one CTA per row sharing one
+// shared-memory key set.  Counting has no ordering constraint, so warps take
+// different A entries concurrently (warp w: entries w, w+nw, ...).
+__global__ void __launch_bounds__(128) spgemm_count_block_kernel(CountArgs a) {
+  extern __shared__ int keys[];
+  __shared__ int total, ovf;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+  const int bits = a.bits, T = 1 << bits;
+  for (long long t = blockIdx.x; t < a.nrows; t += gridDim.x) {
+    const int row = a.rows[t];
+    for (int i = tid; i < T; i += blockDim.x) keys[i] = kEmpty;
+    if (tid == 0) {
+      total = 0;
+      ovf = 0;
+    }
+    __syncthreads();
+    const int ab = a.Ap[row], ae = a.Ap[row + 1];
+    for (int kk = ab + w; kk < ae; kk += nw) {
+      const int k = a.Ac[kk];
+      const int bb = a.Bp[k], be = a.Bp[k + 1];
+      int added = 0;
+      for (int jb = bb; jb < be; jb += 128) {
+        int cc[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int jj = jb + 32 * q + lane;
+          cc[q] = jj < be ? a.Bc[jj] : -1;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (cc[q] >= 0) added += set_insert(keys, bits, cc[q]);
+      }
+      added = warp_sum(added);
+      if (lane == 0 && added) {
+        if (atomicAdd(&total, added) + added > a.limit) ovf = 1;
+      }
+      if (__shfl_sync(kFull, lane == 0 ? *(volatile int*)&ovf : 0, 0)) break;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      if (ovf || total > a.limit) a.ovf_rows[atomicAdd(a.ovf_n, 1)] = row;
+      else a.cnt[row] = total;
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(256) spgemm_count_kernel(CountArgs a) {
   extern __shared__ int smem[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -433,8 +480,13 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
       const size_t shm = (size_t)cwarps[c] * (1 << cbits[c]) * sizeof(int);
       CountArgs a{A.p, A.c, B.p, B.c, cl.list(c), nr, cbits[c], (1 << cbits[c]) * 3 / 4, cnt,
                   ovf_rows, ovf_n, nullptr, nullptr, nullptr};
-      spgemm_count_kernel<<<blocks_for(nr, cwarps[c], 148 * 32), cwarps[c] * 32, shm,
-                            fk.stream(c)>>>(a);
+      if (c == 2) {  // long rows: CTA per row, one shared key set
+        spgemm_count_block_kernel<<<std::min(nr, 148 * 16), 128, (size_t)(1 << cbits[c]) * 4,
+                                    fk.stream(c)>>>(a);
+      } else {
+        spgemm_count_kernel<<<blocks_for(nr, cwarps[c], 148 * 32), cwarps[c] * 32, shm,
+                              fk.stream(c)>>>(a);
+      }
       AIRG_LAUNCH_CHECK();
     }
     AIRG_TRY(fk.end(s));
@@ -489,9 +541,10 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
       if (!nr) continue;
       NumArgs a{A.p, A.c, A.v, B.p, B.c, B.v, cl.list(c), nr, cbits[c], Cp, ocol, oval, negate,
                 mode, tol, lump, cnt, anyd, nullptr, nullptr, nullptr, nullptr};
-      if (c >= 3) {  // long rows: one CTA of 4 warps per row, table shared by the CTA
+      if (c >= 2) {  // long rows: one CTA (2-4 warps) per row, table shared by the CTA
         const size_t shm = (size_t)(1 << cbits[c]) * 12 + 1024;
-        spgemm_numeric_block_kernel<<<std::min(nr, 148 * 16), 128, shm, fk.stream(c)>>>(a);
+        spgemm_numeric_block_kernel<<<std::min(nr, 148 * 32), c == 2 ? 64 : 128, shm,
+                                      fk.stream(c)>>>(a);
       } else {
         const size_t shm = (size_t)cwarps[c] * ((1 << cbits[c]) * 12 + 1024);
         spgemm_numeric_kernel<<<blocks_for(nr, cwarps[c], 148 * 32), cwarps[c] * 32, shm,
