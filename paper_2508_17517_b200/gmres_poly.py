@@ -148,13 +148,29 @@ def roots_from_hessenberg(H, k, beta, order, added_root_tol=1e-4):
         raise ValueError('complex roots of a real matrix must come in conjugate pairs')
     pool = [(t,) for t in real] + [(t, np.conj(t)) for t in upper]
     pool.sort(key=lambda u: max(abs(t) for t in u), reverse=True)
-    seq = [pool.pop(0)]
-    placed = list(seq[0])
-    while pool:
-        score = [sum(math.log(max(abs(t - q), 1e-300)) for t in u for q in placed) for u in pool]
-        u = pool.pop(int(np.argmax(score)))
-        seq.append(u)
-        placed.extend(u)
+    # Leja order by summed log-distance to the placed roots; the score of each
+    # remaining unit is updated incrementally (O(m^2) numpy instead of the
+    # reference's O(m^3) Python loop; ties still go to the first unit).
+    first = np.array([u[0] for u in pool], dtype=np.complex128)
+    second = np.array([u[1] if len(u) > 1 else np.nan for u in pool], dtype=np.complex128)
+    is_pair = np.array([len(u) > 1 for u in pool])
+    alive = np.ones(len(pool), dtype=bool)
+    score = np.zeros(len(pool))
+
+    def place(i):
+        alive[i] = False
+        for q in pool[i]:
+            d = np.log(np.maximum(np.abs(first - q), 1e-300))
+            d2 = np.where(is_pair, np.log(np.maximum(np.abs(second - q), 1e-300)), 0.0)
+            score[:] += d + d2
+
+    seq = [pool[0]]
+    place(0)
+    while alive.any():
+        cand = np.flatnonzero(alive)
+        i = int(cand[np.argmax(score[cand])])
+        seq.append(pool[i])
+        place(i)
     out, seen = [], []
     for u in seq:
         reps = 1
@@ -165,7 +181,27 @@ def roots_from_hessenberg(H, k, beta, order, added_root_tol=1e-4):
             out.extend(u)
         seen.extend(u)
     return PolySolver('newton_roots', order, k - 1, roots=np.array(out, dtype=np.complex128),
-                      residual_history=_history(H, k, beta))
+                      residual_history=_history_givens(H, k, beta))
+
+
+def _history_givens(H, k, beta):
+    """GMRES residual norms for steps 1..k from one Givens QR sweep of the
+    Hessenberg block (diagnostic history of the Newton kind; O(k^2) instead
+    of k least-squares solves)."""
+    R = np.array(H[:k + 1, :k], dtype=np.float64, copy=True)
+    g = np.zeros(k + 1)
+    g[0] = beta
+    out = []
+    for j in range(k):
+        a, b = R[j, j], R[j + 1, j]
+        r = math.hypot(a, b)
+        c, s = (1.0, 0.0) if r == 0 else (a / r, b / r)
+        Rj, Rj1 = R[j, j:].copy(), R[j + 1, j:].copy()
+        R[j, j:] = c * Rj + s * Rj1
+        R[j + 1, j:] = -s * Rj + c * Rj1
+        g[j], g[j + 1] = c * g[j], -s * g[j]
+        out.append(float(abs(g[j + 1])))
+    return tuple(out)
 
 
 def hessenberg(A, m, b):
