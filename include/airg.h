@@ -171,7 +171,15 @@ int airg_spgemm_masked(int m, int k, int n, const int32_t* Ap, const int32_t* Ac
 /* sum_k c_k mask(A^k), mask = pattern(A) + diagonal, exact zeros pruned.
  * ref: polynomial.py:372-416 (arnoldi_coeff kind) */
 int airg_poly_assemble(int n, const int32_t* Ap, const int32_t* Ac, const double* Av, int ncoef,
-                       const double* coef_h, airg_csr_result** out, void* stream);
+                       const double* coef_h, const int32_t* Qp, const int32_t* Qc,
+                       airg_csr_result** out, void* stream);
+/* Neumann base I + (-D^-1 A) with exact zeros pruned (the mask for its
+ * powers is pattern(A) + diag: pass A as Q to airg_poly_assemble), and the
+ * final right scaling v *= ds[col].  ref: polynomial.py:396-415 */
+int airg_neumann_base(int n, const int32_t* p, const int32_t* c, const double* v,
+                      const double* diag_scale, airg_csr_result** out, void* stream);
+int airg_scale_columns(int64_t nnz, const int32_t* c, const double* diag_scale, double* v,
+                       void* stream);
 /* Row-relative drop (+ sequential lump onto the diagonal); changed_h = any
  * entry dropped.  ref: sparse.py:307-352 */
 int airg_drop_lump(int m, int ncols, const int32_t* p, const int32_t* c, const double* v,

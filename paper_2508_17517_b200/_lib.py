@@ -153,7 +153,9 @@ sig('airg_repair_split', i32, vp, vp, vp, C.POINTER(i32), vp)
 sig('airg_prolong_onepoint', i32, vp, vp, vp, vp, vp, vp, vp)
 sig('airg_spgemm', i32, i32, i32, vp, vp, vp, vp, vp, vp, C.c_int, pp, vp)
 sig('airg_spgemm_masked', i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, pp, vp)
-sig('airg_poly_assemble', i32, vp, vp, vp, C.c_int, vp, pp, vp)
+sig('airg_poly_assemble', i32, vp, vp, vp, C.c_int, vp, vp, vp, pp, vp)
+sig('airg_neumann_base', i32, vp, vp, vp, vp, pp, vp)
+sig('airg_scale_columns', i64, vp, vp, vp, vp)
 sig('airg_drop_lump', i32, i32, vp, vp, vp, f64, C.c_int, pp, C.POINTER(i32), vp)
 sig('airg_galerkin', i32, i32, vp, vp, vp, vp, vp, vp, vp, f64, C.c_int, pp, vp)
 sig('airg_extract', i32, vp, vp, vp, vp, vp, i32, pp, vp)

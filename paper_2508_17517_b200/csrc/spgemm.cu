@@ -504,21 +504,26 @@ int airg_spgemm_masked(int m, int k, int n, const int32_t* Ap, const int32_t* Ac
 }
 
 int airg_poly_assemble(int n, const int32_t* Ap, const int32_t* Ac, const double* Av, int ncoef,
-                       const double* coef_h, airg_csr_result** out, void* stream) {
+                       const double* coef_h, const int32_t* Qp, const int32_t* Qc,
+                       airg_csr_result** out, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   if (ncoef < 1) {
     set_error("need at least one coefficient");
     return AIRG_ERR_VALUE;
   }
+  if (!Qp) {  // the mask comes from the base matrix itself (arnoldi_coeff kind)
+    Qp = Ap;
+    Qc = Ac;
+  }
   int *cnt = nullptr, *Pp = nullptr, *Pc = nullptr;
   AIRG_TRY(scratch(&cnt, n + 1, s));
   AIRG_TRY(scratch(&Pp, n + 1, s));
   const int nb = blocks_for(n, 256);
-  if (n > 0) pattern_diag_kernel<<<nb, 256, 0, s>>>(n, Ap, Ac, nullptr, nullptr, cnt);
+  if (n > 0) pattern_diag_kernel<<<nb, 256, 0, s>>>(n, Qp, Qc, nullptr, nullptr, cnt);
   long long pnnz = 0;
   AIRG_TRY(scan_counts(cnt, Pp, n, &pnnz, s));
   AIRG_TRY(scratch(&Pc, pnnz, s));
-  if (n > 0) pattern_diag_kernel<<<nb, 256, 0, s>>>(n, Ap, Ac, Pp, Pc, nullptr);
+  if (n > 0) pattern_diag_kernel<<<nb, 256, 0, s>>>(n, Qp, Qc, Pp, Pc, nullptr);
   AIRG_LAUNCH_CHECK();
   int maxlen = 0;
   AIRG_TRY(max_row_len(n, Pp, &maxlen, s));

@@ -264,14 +264,25 @@ def assemble_fixed_sparsity(p, A):
                          'newton_roots')
     if A.nrows != A.ncols:
         raise ValueError('require a square matrix')
-    if p.kind != 'arnoldi_coeff':
-        raise ValueError('fixed-sparsity assembly of the neumann kind is not implemented on '
-                         'the device')
+    if p.kind not in ('arnoldi_coeff', 'neumann'):
+        raise ValueError(f'unknown polynomial kind {p.kind!r}')
     c = np.ascontiguousarray(p.coeffs, dtype=np.float64)
+    base = A
+    if p.kind == 'neumann':
+        # series in N = I - D^-1 A (zeros pruned), mask from A itself
+        rb = C.c_void_p()
+        L.call('airg_neumann_base', A.nrows, L.ptr(A.row_offsets), L.ptr(A.col_indices),
+               L.ptr(A.values), L.ptr(p.diag_scale), C.byref(rb), L.stream_handle())
+        base = take(rb)
     r = C.c_void_p()
-    L.call('airg_poly_assemble', A.nrows, L.ptr(A.row_offsets), L.ptr(A.col_indices),
-           L.ptr(A.values), len(c), L.hptr(c), C.byref(r), L.stream_handle())
-    return take(r)
+    L.call('airg_poly_assemble', A.nrows, L.ptr(base.row_offsets), L.ptr(base.col_indices),
+           L.ptr(base.values), len(c), L.hptr(c), L.ptr(A.row_offsets), L.ptr(A.col_indices),
+           C.byref(r), L.stream_handle())
+    out = take(r)
+    if p.kind == 'neumann':
+        L.call('airg_scale_columns', out.nnz, L.ptr(out.col_indices), L.ptr(p.diag_scale),
+               L.ptr(out.values), L.stream_handle())
+    return out
 
 
 def export_diagnostics(p):

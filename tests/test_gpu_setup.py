@@ -321,6 +321,38 @@ def test_gpu_setup_replayed_by_oracle(G, nx, ny, v, order):
         assert np.max(np.abs(c_own - c_dev)) <= 1e-10 * np.max(np.abs(c_own))
 
 
+def test_neumann_assembly_bitwise(G, hier, hier_hard):
+    for h in (hier, hier_hard):
+        for L in h.levels[:4]:
+            p = O.neumann_poly(L.A_ff, 3)
+            same(G.assemble_fixed_sparsity(dev_poly(p), dev_csr(L.A_ff)), O.assemble_poly(p, L.A_ff))
+
+
+@pytest.mark.parametrize('nx,v', [(48, PI4), (40, HARD)])
+def test_krylov_free_setup_bitwise_without_injection(G, nx, v):
+    """nAIR variant (Neumann smoothers + Neumann coarse solver, no truncation):
+    no Krylov dot products anywhere, so the GPU hierarchy must equal the
+    oracle's bit for bit with NO coefficient injection, and the exact-mode
+    solve must reproduce x bitwise."""
+    kw = dict(inverse_type='neumann', coarsest_inverse_type='neumann', coarsest_poly_order=20,
+              auto_truncate_tol=None, poly_order=3, matrix_free_polys=False)
+    A, b = G.build_advection_2d(G.AdvectionProblem(nx=nx, ny=nx, vx=v[0], vy=v[1]))
+    H = G.setup(A, G.SetupConfig(**kw), keep_level_matrices=True)
+    Ao = O.advection_2d(nx, nx, *v)
+    Ho = O.setup(Ao, O.Cfg(**kw), keep_level_matrices=True)
+    assert H.num_levels == len(Ho.levels)
+    for L, Lo in zip(H.levels, Ho.levels):
+        assert np.array_equal(L.split.labels_host(), Lo.labels)
+        for a, o in ((L.R, Lo.R), (L.P, Lo.P), (L.A_ff, Lo.A_ff), (L.A_fc, Lo.A_fc), (L.A, Lo.A),
+                     (L.f_smoother_assembled, Lo.assembled)):
+            same(a, o)
+    same(H.coarsest_A, Ho.coarsest_A)
+    x, st = G.richardson_solve(H, b, np.ones(A.nrows), G.SolveConfig(max_iters=60), exact=True)
+    xo, hist, conv, its = O.richardson(Ho, np.zeros(Ao.nrows), np.ones(Ao.nrows), max_iters=60)
+    assert st.iterations == its
+    assert x.cpu().numpy().tobytes() == xo.tobytes()
+
+
 def test_setup_errors(G):
     with pytest.raises(ValueError):
         G.setup(G.SparseMatrix.csr(2, 3, [0, 1, 2], [0, 1], [1.0, 1.0]), G.SetupConfig())
