@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(256) spgemm_numeric_kernel(NumArgs a) {
 // by __syncthreads, so every output entry still receives its k in ascending
 // order.  The next B row is prefetched into registers during the current
 // step.  Warp 0 compacts, sorts and writes the row.
-__global__ void __launch_bounds__(128) spgemm_numeric_block_kernel(NumArgs a) {
+__global__ void __launch_bounds__(256) spgemm_numeric_block_kernel(NumArgs a) {
   extern __shared__ double smd[];
   __shared__ int mbb[32], mbe[32];
   __shared__ double mav[32];
@@ -543,7 +543,10 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
                 mode, tol, lump, cnt, anyd, nullptr, nullptr, nullptr, nullptr};
       if (c >= 2) {  // long rows: one CTA (2-4 warps) per row, table shared by the CTA
         const size_t shm = (size_t)(1 << cbits[c]) * 12 + 1024;
-        spgemm_numeric_block_kernel<<<std::min(nr, 148 * 32), c == 2 ? 64 : 128, shm,
+        // threads per row (measured at 2048^2: 64/128/192/256 -> 254/191/178/173 ms)
+        static const int bt = getenv("AIRG_BLOCK_THREADS") ? atoi(getenv("AIRG_BLOCK_THREADS")) : 256;
+        static const int bt2 = getenv("AIRG_BLOCK_THREADS2") ? atoi(getenv("AIRG_BLOCK_THREADS2")) : 128;
+        spgemm_numeric_block_kernel<<<std::min(nr, 148 * 32), c == 2 ? bt2 : bt, shm,
                                       fk.stream(c)>>>(a);
       } else {
         const size_t shm = (size_t)cwarps[c] * ((1 << cbits[c]) * 12 + 1024);
