@@ -202,6 +202,53 @@ int airg_restriction(int n, int nc, const int32_t* zp, const int32_t* zc, const 
                      const int32_t* f_idx, const int32_t* c_idx, airg_csr_result** out,
                      void* stream);
 
+/* ---- row-strip (multi-GPU) variants --------------------------------------
+ * A rank owns global rows [row0, row0 + n); column ids are global or
+ * renumbered to the extended space [local | ghost].  Same per-row semantics
+ * as the serial entry points (hence bitwise-identical hierarchies). */
+/* rows [row_begin, row_end) of the 2-D stencil; ptr == NULL: nnz query */
+int airg_advection_2d_rows(int nx, int ny, double vx, double vy, int64_t row_begin, int64_t row_end,
+                           int32_t* ptr, int32_t* col, double* val, int64_t* nnz_h, void* stream);
+/* strong couplings of local rows (global column ids).  ref: splitting.py:86-104 */
+int airg_strength_rows(int n, int row0, const int32_t* ptr, const int32_t* col, const double* val,
+                       int64_t nnz, double theta, airg_csr_result** S_out, void* stream);
+/* union of two row-sorted patterns (closure S + S^T).  ref: splitting.py:106 */
+int airg_union_rows(int n, const int32_t* ap, const int32_t* ac, const int32_t* bp, const int32_t* bc,
+                    airg_csr_result** out, void* stream);
+/* Luby weights of local rows at their global stream positions.  ref: splitting.py:119-120 */
+int airg_luby_weights(int n, int64_t row0, const int32_t* cptr, uint64_t state_hi, uint64_t state_lo,
+                      uint64_t inc_hi, uint64_t inc_lo, double* w, void* stream);
+/* one half-round of PMISR on ext arrays (phase 0 select, 1 block).  ref: splitting.py:144-157 */
+int airg_luby_round(int n, const int32_t* cptr, const int32_t* ccol_ext, const double* w_ext,
+                    const int32_t* gid_ext, int8_t* st_ext, int mark, int phase, int32_t* remaining_h,
+                    void* stream);
+int airg_luby_finish(int n, const int8_t* st, int8_t* labels, void* stream);
+/* DDC pieces (ratios + local min/max/sum, histogram over host edges, convert).
+ * ref: splitting.py:162-203 */
+int airg_ddc_ratios(int nf, int row0, const int32_t* f_loc, const int32_t* ptr, const int32_t* col_ext,
+                    const double* val, const int8_t* labels_ext, double* ratio, int32_t* bad_h,
+                    double* minmaxsum_h, void* stream);
+int airg_ddc_hist(int nf, const double* ratio, const double* edges_h, int nedges, uint64_t* hist,
+                  void* stream);
+int airg_ddc_convert(int nf, const int32_t* f_loc, const double* ratio, double cut, int all,
+                     int8_t* labels, int32_t* converted_h, void* stream);
+/* elements [start, start+n) of the PCG64 stream (a + b*random()) */
+int airg_pcg64_fill_at(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                       int64_t start, int64_t n, double a, double b, double* out, void* stream);
+/* C = A B (mode 0, optional negate) or drop_and_lump(A B) (mode 1) with the
+ * diagonal of local output row i at column row0 + i. */
+int airg_spgemm_ex(int m, int k, int n, const int32_t* Ap, const int32_t* Ac, const double* Av,
+                   const int32_t* Bp, const int32_t* Bc, const double* Bv, int negate, int mode,
+                   double tol, int lump, int row0, airg_csr_result** out, void* stream);
+/* fixed-sparsity assembly of local rows [0, n) (global row row0 + i); rows
+ * of A beyond n are fetched ghost rows, rowmap[global col] -> row of A. */
+int airg_poly_assemble_ex(int n, int row0, const int32_t* Ap, const int32_t* Ac, const double* Av,
+                          const int32_t* rowmap, int ncoef, const double* coef_h,
+                          const int32_t* Qp, const int32_t* Qc, airg_csr_result** out,
+                          void* stream);
+/* out[i] = map[in[i]] (negative ids pass through) */
+int airg_gather_int(int64_t n, const int32_t* in, const int32_t* map, int32_t* out, void* stream);
+
 /* ---- Krylov (polynomial.py:68-110) --------------------------------------
  * MGS Arnoldi from start vector b (device), m = min(order+1, n) steps, one
  * reorthogonalisation sweep when ||w|| < 0.7 ||A v||, lucky breakdown at

@@ -162,6 +162,20 @@ sig('airg_extract', i32, vp, vp, vp, vp, vp, i32, pp, vp)
 sig('airg_label_colmap', i32, vp, C.c_int, vp, vp, vp)
 sig('airg_restriction', i32, i32, vp, vp, vp, vp, vp, pp, vp)
 sig('airg_arnoldi', i32, vp, vp, vp, vp, C.c_int, vp, C.POINTER(i32), C.POINTER(f64), vp)
+sig('airg_advection_2d_rows', i32, i32, f64, f64, i64, i64, vp, vp, vp, C.POINTER(i64), vp)
+sig('airg_strength_rows', i32, i32, vp, vp, vp, i64, f64, pp, vp)
+sig('airg_union_rows', i32, vp, vp, vp, vp, pp, vp)
+sig('airg_luby_weights', i32, i64, vp, u64, u64, u64, u64, vp, vp)
+sig('airg_luby_round', i32, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.POINTER(i32), vp)
+sig('airg_luby_finish', i32, vp, vp, vp)
+sig('airg_ddc_ratios', i32, i32, vp, vp, vp, vp, vp, vp, C.POINTER(i32), vp, vp)
+sig('airg_ddc_hist', i32, vp, vp, C.c_int, vp, vp)
+sig('airg_ddc_convert', i32, vp, vp, f64, C.c_int, vp, C.POINTER(i32), vp)
+sig('airg_gather_int', i64, vp, vp, vp, vp)
+sig('airg_pcg64_fill_at', u64, u64, u64, u64, i64, i64, f64, f64, vp, vp)
+sig('airg_spgemm_ex', i32, i32, i32, vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, f64, C.c_int,
+    C.c_int, pp, vp)
+sig('airg_poly_assemble_ex', i32, i32, vp, vp, vp, vp, C.c_int, vp, vp, vp, pp, vp)
 
 
 def pcg_params(seed):

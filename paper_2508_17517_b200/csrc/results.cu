@@ -65,24 +65,24 @@ int result_alloc_entries(airg_csr_result* r, long long nnz, bool values) {
   return AIRG_OK;
 }
 
-__global__ void pcg_fill_kernel(u128 s0, u128 inc, long long n, long long chunk, double a, double b,
+__global__ void pcg_fill_kernel(u128 s0, u128 inc, long long n, long long chunk, double a, double b, long long start,
                                 double* __restrict__ out) {
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   long long i0 = t * chunk;
   if (i0 >= n) return;
   long long i1 = i0 + chunk < n ? i0 + chunk : n;
-  u128 st = pcg_jump(s0, inc, (unsigned long long)i0);
+  u128 st = pcg_jump(s0, inc, (unsigned long long)(start + i0));
   for (long long i = i0; i < i1; ++i) {
     st = pcg_step(st, inc);  // numpy steps first, then outputs the new state
     out[i] = add_rn(a, mul_rn(b, pcg_out_double(st)));
   }
 }
 
-int pcg64_fill(u128 s0, u128 inc, long long n, double a, double b, double* out, cudaStream_t s) {
+int pcg64_fill(u128 s0, u128 inc, long long n, double a, double b, double* out, cudaStream_t s, long long start) {
   if (n <= 0) return AIRG_OK;
   const long long chunk = 64;
   const long long threads = (n + chunk - 1) / chunk;
-  pcg_fill_kernel<<<(int)((threads + 255) / 256), 256, 0, s>>>(s0, inc, n, chunk, a, b, out);
+  pcg_fill_kernel<<<(int)((threads + 255) / 256), 256, 0, s>>>(s0, inc, n, chunk, a, b, start, out);
   AIRG_LAUNCH_CHECK();
   return AIRG_OK;
 }

@@ -123,6 +123,7 @@ __host__ __device__ __forceinline__ double pcg_out_double(u128 s) {
 // Fill out[i] = a + b * random()_i for i in [0, n): numpy Generator.random()
 // (a=0, b=1) or uniform(-1, 1) (a=-1, b=2) bit for bit.  Each thread jumps
 // to its chunk then steps sequentially.
-int pcg64_fill(u128 s0, u128 inc, long long n, double a, double b, double* out, cudaStream_t s);
+int pcg64_fill(u128 s0, u128 inc, long long n, double a, double b, double* out, cudaStream_t s,
+               long long start = 0);
 
 }  // namespace airg

@@ -130,15 +130,16 @@ static int finish_raw(int m, int ncols, const int* rawp, int* cnt, int* rcol, do
 // pattern = A + diag (sorted), count / fill
 __global__ void pattern_diag_kernel(int n, const int* __restrict__ p, const int* __restrict__ c,
                                     const int* __restrict__ optr, int* __restrict__ ocol,
-                                    int* __restrict__ cnt) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int b = p[i], e = p[i + 1];
+                                    int* __restrict__ cnt, int row0 = 0) {
+  for (long long li = blockIdx.x * (long long)blockDim.x + threadIdx.x; li < n;
+       li += (long long)gridDim.x * blockDim.x) {
+    const int b = p[li], e = p[li + 1];
+    const int i = row0 + (int)li;  // global id of the diagonal
     bool has = false;
     for (int k = b; k < e; ++k) has |= c[k] == i;
-    if (cnt) cnt[i] = e - b + (has ? 0 : 1);
+    if (cnt) cnt[li] = e - b + (has ? 0 : 1);
     if (ocol) {
-      int o = optr[i];
+      int o = optr[li];
       bool done = has;
       for (int k = b; k < e; ++k) {
         if (!done && c[k] > i) {
@@ -175,6 +176,10 @@ struct PolyArgs {
   int masked;
   const int *Lp, *Lc;
   const double* Lv;
+  // row-strip operation: global id of local row 0 and global column -> row
+  // of Ap (local rows first, then fetched ghost rows); null = identity
+  int row0;
+  const int* rowmap;
 };
 
 __global__ void __launch_bounds__(128) poly_assemble_kernel(PolyArgs a) {
@@ -239,7 +244,7 @@ __global__ void __launch_bounds__(128) poly_assemble_kernel(PolyArgs a) {
     // term 0: c0 * I (diagonal is always in the pattern)
     const double c0 = a.coef[0];
     if (lane == 0) {
-      const int p = map_find(keys, pv, a.bits, row);
+      const int p = map_find(keys, pv, a.bits, a.row0 + row);
       acc[p] = add_rn(acc[p], c0);  // 0 + c0 (=c0; -0 -> +0 is pruned anyway)
       facc[p] = 1;
     }
@@ -268,8 +273,9 @@ __global__ void __launch_bounds__(128) poly_assemble_kernel(PolyArgs a) {
         double lv = 0.0;
         if (pres) {
           const int col_q = a.Pc[pb + q];
-          rb = a.Ap[col_q];
-          re = a.Ap[col_q + 1];
+          const int rq = a.rowmap ? a.rowmap[col_q] : col_q;
+          rb = a.Ap[rq];
+          re = a.Ap[rq + 1];
           lv = cur[q];
         }
         unsigned todo = __ballot_sync(0xffffffffu, pres);
@@ -503,10 +509,35 @@ int airg_spgemm_masked(int m, int k, int n, const int32_t* Ap, const int32_t* Ac
   return AIRG_OK;
 }
 
+static int poly_assemble_impl(int n, const int32_t* Ap, const int32_t* Ac, const double* Av,
+                              int ncoef, const double* coef_h, const int32_t* Qp,
+                              const int32_t* Qc, int row0, const int32_t* rowmap,
+                              airg_csr_result** out, cudaStream_t s);
+
 int airg_poly_assemble(int n, const int32_t* Ap, const int32_t* Ac, const double* Av, int ncoef,
                        const double* coef_h, const int32_t* Qp, const int32_t* Qc,
                        airg_csr_result** out, void* stream) {
-  cudaStream_t s = (cudaStream_t)stream;
+  return poly_assemble_impl(n, Ap, Ac, Av, ncoef, coef_h, Qp, Qc, 0, nullptr, out,
+                            (cudaStream_t)stream);
+}
+
+// Row-strip assembly: rows [0, n) of Ap are the local rows (global row
+// row0 + i), further rows are fetched ghost rows; column ids are global and
+// rowmap[global column] gives the row of Ap holding it.
+int airg_poly_assemble_ex(int n, int row0, const int32_t* Ap, const int32_t* Ac, const double* Av,
+                          const int32_t* rowmap, int ncoef, const double* coef_h,
+                          const int32_t* Qp, const int32_t* Qc, airg_csr_result** out,
+                          void* stream) {
+  return poly_assemble_impl(n, Ap, Ac, Av, ncoef, coef_h, Qp, Qc, row0, rowmap, out,
+                            (cudaStream_t)stream);
+}
+
+}  // extern "C"
+
+static int poly_assemble_impl(int n, const int32_t* Ap, const int32_t* Ac, const double* Av,
+                              int ncoef, const double* coef_h, const int32_t* Qp,
+                              const int32_t* Qc, int row0, const int32_t* rowmap,
+                              airg_csr_result** out, cudaStream_t s) {
   if (ncoef < 1) {
     set_error("need at least one coefficient");
     return AIRG_ERR_VALUE;
@@ -519,11 +550,11 @@ int airg_poly_assemble(int n, const int32_t* Ap, const int32_t* Ac, const double
   AIRG_TRY(scratch(&cnt, n + 1, s));
   AIRG_TRY(scratch(&Pp, n + 1, s));
   const int nb = blocks_for(n, 256);
-  if (n > 0) pattern_diag_kernel<<<nb, 256, 0, s>>>(n, Qp, Qc, nullptr, nullptr, cnt);
+  if (n > 0) pattern_diag_kernel<<<nb, 256, 0, s>>>(n, Qp, Qc, nullptr, nullptr, cnt, row0);
   long long pnnz = 0;
   AIRG_TRY(scan_counts(cnt, Pp, n, &pnnz, s));
   AIRG_TRY(scratch(&Pc, pnnz, s));
-  if (n > 0) pattern_diag_kernel<<<nb, 256, 0, s>>>(n, Qp, Qc, Pp, Pc, nullptr);
+  if (n > 0) pattern_diag_kernel<<<nb, 256, 0, s>>>(n, Qp, Qc, Pp, Pc, nullptr, row0);
   AIRG_LAUNCH_CHECK();
   int maxlen = 0;
   AIRG_TRY(max_row_len(n, Pp, &maxlen, s));
@@ -545,6 +576,8 @@ int airg_poly_assemble(int n, const int32_t* Ap, const int32_t* Ac, const double
   a.out_val = pv;
   a.out_keep = keep;
   a.out_cnt = cnt;
+  a.row0 = row0;
+  a.rowmap = rowmap;
   AIRG_TRY(run_poly_kernel(a, maxlen, s));
   airg_csr_result* r = new_result(n, n, s);
   long long nnz = 0;
@@ -556,6 +589,8 @@ int airg_poly_assemble(int n, const int32_t* Ap, const int32_t* Ac, const double
   *out = r;
   return AIRG_OK;
 }
+
+extern "C" {
 
 int airg_drop_lump(int m, int ncols, const int32_t* p, const int32_t* c, const double* v,
                    double tol, int lump, airg_csr_result** out, int32_t* changed_h, void* stream) {

@@ -224,6 +224,7 @@ struct NumArgs {
   double* gacc;
   const long long* goff;
   const int* gbits;
+  int row0;  // global id of local output row 0 (diagonal of the drop/lump epilogue)
 };
 
 __global__ void __launch_bounds__(256) spgemm_numeric_kernel(NumArgs a) {
@@ -274,8 +275,8 @@ __global__ void __launch_bounds__(256) spgemm_numeric_kernel(NumArgs a) {
         a.Cv[o + i] = a.negate ? -v : v;
       }
     } else {
-      const int wr = drop_lump_row(keys, acc, n, row, a.tol, a.lump, a.Cc, a.Cv, (long long)o + row,
-                                   lane, a.any_drop);
+      const int wr = drop_lump_row(keys, acc, n, a.row0 + row, a.tol, a.lump, a.Cc, a.Cv,
+                                   (long long)o + row, lane, a.any_drop);
       if (lane == 0) a.out_cnt[row] = wr;
     }
     __syncwarp();
@@ -354,7 +355,7 @@ __global__ void __launch_bounds__(256) spgemm_numeric_block_kernel(NumArgs a) {
           a.Cv[o + i] = a.negate ? -v : v;
         }
       } else {
-        const int wr = drop_lump_row(keys, acc, n, row, a.tol, a.lump, a.Cc, a.Cv,
+        const int wr = drop_lump_row(keys, acc, n, a.row0 + row, a.tol, a.lump, a.Cc, a.Cv,
                                      (long long)o + row, lane, a.any_drop);
         if (lane == 0) a.out_cnt[row] = wr;
       }
@@ -453,7 +454,7 @@ static int gather_ll(const long long* d, const std::vector<int>& rows, std::vect
 
 // C = A B (mode 0, optionally negated) or drop_and_lump(A B) (mode 1).
 static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double tol, int lump,
-                       airg_csr_result** out, cudaStream_t s) {
+                       airg_csr_result** out, cudaStream_t s, int row0 = 0) {
   const int m = A.nrows;
   long long *ub = nullptr, *rl = nullptr;
   int *cnt = nullptr, *Cp = nullptr;
@@ -540,7 +541,7 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
       const int nr = cl.count[c];
       if (!nr) continue;
       NumArgs a{A.p, A.c, A.v, B.p, B.c, B.v, cl.list(c), nr, cbits[c], Cp, ocol, oval, negate,
-                mode, tol, lump, cnt, anyd, nullptr, nullptr, nullptr, nullptr};
+                mode, tol, lump, cnt, anyd, nullptr, nullptr, nullptr, nullptr, row0};
       if (c >= 2) {  // long rows: one CTA (2-4 warps) per row, table shared by the CTA
         const size_t shm = (size_t)(1 << cbits[c]) * 12 + 1024;
         // threads per row (measured at 2048^2: 64/128/192/256 -> 254/191/178/173 ms)
@@ -565,7 +566,7 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
       GlobalTables g;
       AIRG_TRY(make_tables(rows, sizes, true, g, s));
       NumArgs a{A.p, A.c, A.v, B.p, B.c, B.v, g.rows, nr, 0, Cp, ocol, oval, negate, mode, tol, lump,
-                cnt, anyd, g.keys, g.acc, g.off, g.bits};
+                cnt, anyd, g.keys, g.acc, g.off, g.bits, row0};
       spgemm_numeric_kernel<<<blocks_for(nr, 4), 128, 0, s>>>(a);
       AIRG_LAUNCH_CHECK();
       AIRG_CUDA(cudaStreamSynchronize(s));
@@ -610,6 +611,16 @@ int airg_spgemm(int m, int k, int n, const int32_t* Ap, const int32_t* Ac, const
                 airg_csr_result** out, void* stream) {
   Mat A{m, k, Ap, Ac, Av}, B{k, n, Bp, Bc, Bv};
   return spgemm_rows(A, B, negate, 0, 0.0, 0, out, (cudaStream_t)stream);
+}
+
+// General product with the optional fused drop/lump epilogue and a global
+// row offset (row-strip operators).  mode 0: C = A B (negate); mode 1:
+// drop_and_lump(A B, tol, lump) with diagonal column = row0 + local row.
+int airg_spgemm_ex(int m, int k, int n, const int32_t* Ap, const int32_t* Ac, const double* Av,
+                   const int32_t* Bp, const int32_t* Bc, const double* Bv, int negate, int mode,
+                   double tol, int lump, int row0, airg_csr_result** out, void* stream) {
+  Mat A{m, k, Ap, Ac, Av}, B{k, n, Bp, Bc, Bv};
+  return spgemm_rows(A, B, negate, mode, tol, lump, out, (cudaStream_t)stream, row0);
 }
 
 int airg_galerkin(int n, int nc, const int32_t* Rp, const int32_t* Rc, const double* Rv,
