@@ -381,9 +381,22 @@ def setup(A, cfg, poly_inject=None, keep_level_matrices=False):
     polys = {}
     timings = {phase: 0.0 for phase in SETUP_PHASES}
     truncate_start = resolve_truncate_start(cfg, A.nrows)
+    levels, current, coarse_solver, truncated_at = build_levels(
+        A, cfg, 0, truncate_start, inj, polys, timings, keep_level_matrices)
+    H = Hierarchy(levels=levels, coarsest_A=current, coarse_solver=coarse_solver, top_A=A,
+                  truncated_at=truncated_at, config=cfg, setup_breakdown=timings)
+    H.polys = polys
+    return finalize_complexities(H)
+
+
+def build_levels(A, cfg, level0, truncate_start, inj, polys, timings, keep_level_matrices=False):
+    """The level loop of setup (hierarchy.py:386-434) from level index
+    ``level0`` on a (replicated) level matrix ``A``.  Returns (levels,
+    coarsest matrix, coarse solver, truncated_at)."""
+    from .cfsplit import cf_split
     levels = []
     current = A
-    level = 0
+    level = level0
     truncated_at = None
     coarse_solver = None
 
@@ -441,7 +454,4 @@ def setup(A, cfg, poly_inject=None, keep_level_matrices=False):
             levels[-1].A = current
         current = coarse
         level += 1
-    H = Hierarchy(levels=levels, coarsest_A=current, coarse_solver=coarse_solver, top_A=A,
-                  truncated_at=truncated_at, config=cfg, setup_breakdown=timings)
-    H.polys = polys
-    return finalize_complexities(H)
+    return levels, current, coarse_solver, truncated_at

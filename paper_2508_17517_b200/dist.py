@@ -1,0 +1,670 @@
+"""Row-strip domain decomposition of the AIRG setup and solve across GPUs
+(SURVEY.md 8(e)).  One process per GPU; rank r owns a contiguous block of
+global rows at every level (grid strips at level 0, the C points of its fine
+strip at the next level, ...), so the global numbering -- and with it every
+per-row decision -- is the serial one: a distributed hierarchy is bitwise
+the serial hierarchy for the same smoother / coarse polynomials.
+
+Exchanges (torch.distributed over NCCL, all_to_all_single with uneven splits):
+  * Halo(part, need): ghost values of the global ids a rank's rows touch;
+  * Halo.rows: ghost ROWS (variable length) for the row-local SpGEMMs;
+  * allreduce for the DDC histogram / extrema, Luby's undecided count and
+    Krylov dot products.
+Kernels run on local rows with column ids renumbered in place to
+[local | ghost] (the stored order stays the global order, which is what the
+bit-exact sums depend on).  Once a level is small (or reaches the truncation
+start) it is gathered to every rank and the serial setup continues there,
+replicated; the V-cycle does the same below that level.
+"""
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib as L
+from .csr import IDX, VAL, SparseMatrix, empty, extract_mapped, take
+
+I64 = torch.int64
+
+
+class Comm:
+    """Collectives on CUDA tensors (NCCL) or CPU tensors (gloo, tests)."""
+
+    def __init__(self, group=None, device=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.device = device or torch.device('cuda', torch.cuda.current_device())
+
+    def a2a(self, send, send_counts, recv_counts):
+        out = torch.empty(int(sum(recv_counts)), dtype=send.dtype, device=send.device)
+        dist.all_to_all_single(out, send.contiguous(), [int(c) for c in recv_counts],
+                               [int(c) for c in send_counts], group=self.group)
+        return out
+
+    def allreduce(self, t, op='sum'):
+        ops = {'sum': dist.ReduceOp.SUM, 'max': dist.ReduceOp.MAX, 'min': dist.ReduceOp.MIN}
+        dist.all_reduce(t, op=ops[op], group=self.group)
+        return t
+
+    def sum_int(self, v):
+        return int(self.allreduce(torch.tensor([int(v)], dtype=I64, device=self.device)).item())
+
+    def allgather_int(self, v):
+        t = torch.tensor([int(v)], dtype=I64, device=self.device)
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(out, t, group=self.group)
+        return [int(x.item()) for x in out]
+
+    def allgather_v(self, t):
+        """Concatenation over ranks of 1-D tensors of different lengths."""
+        counts = self.allgather_int(t.numel())
+        m = max(counts) if counts else 0
+        pad = torch.zeros(m, dtype=t.dtype, device=t.device)
+        pad[:t.numel()] = t
+        out = [torch.empty_like(pad) for _ in range(self.world)]
+        dist.all_gather(out, pad, group=self.group)
+        return torch.cat([o[:c] for o, c in zip(out, counts)])
+
+
+class Part:
+    """Contiguous block partition of a global index space."""
+
+    def __init__(self, offsets, device):
+        self.off = [int(o) for o in offsets]
+        self.n = self.off[-1]
+        self.inner = torch.tensor(self.off[1:-1], dtype=I64, device=device)
+
+    @classmethod
+    def from_counts(cls, counts, device):
+        return cls(np.concatenate([[0], np.cumsum(counts)]).tolist(), device)
+
+    def lo(self, r):
+        return self.off[r]
+
+    def hi(self, r):
+        return self.off[r + 1]
+
+    def owner(self, g):
+        return torch.searchsorted(self.inner, g.to(I64), right=True)
+
+
+class Halo:
+    """Ghost plan: the sorted global ids ``need`` (outside this rank's block)
+    and, per peer, which local entries this rank sends."""
+
+    def __init__(self, comm, part, need):
+        self.comm, self.part = comm, part
+        W, r = comm.world, comm.rank
+        self.ghost = need.to(I64)
+        self.n_loc = part.hi(r) - part.lo(r)
+        self.n = int(self.ghost.numel())
+        owners = part.owner(self.ghost) if self.n else torch.zeros(0, dtype=I64, device=comm.device)
+        self.recv_counts = torch.bincount(owners, minlength=W).cpu().tolist()
+        sc = comm.a2a(torch.tensor(self.recv_counts, dtype=I64, device=comm.device), [1] * W, [1] * W)
+        self.send_counts = sc.cpu().tolist()
+        req = comm.a2a(self.ghost, self.recv_counts, self.send_counts)
+        self.send_idx = req - part.lo(r)
+
+    def values(self, local):
+        """Ghost values (in ghost order) of a per-local-row array."""
+        return self.comm.a2a(local[self.send_idx], self.send_counts, self.recv_counts)
+
+    def ext(self, local):
+        return torch.cat([local, self.values(local)])
+
+    def rows(self, M):
+        """Ghost rows of the local-row CSR M (global column ids) -> CSR."""
+        dev = M.row_offsets.device
+        lens = (M.row_offsets[1:] - M.row_offsets[:-1]).to(I64)
+        slen = lens[self.send_idx]
+        rlen = self.comm.a2a(slen, self.send_counts, self.recv_counts)
+        # element counts per peer
+        def per_peer(counts, lengths):
+            out, k = [], 0
+            for c in counts:
+                out.append(int(lengths[k:k + c].sum().item()) if c else 0)
+                k += c
+            return out
+        se = per_peer(self.send_counts, slen)
+        re_ = per_peer(self.recv_counts, rlen)
+        starts = M.row_offsets[:-1].to(I64)[self.send_idx]
+        tot = int(slen.sum().item())
+        if tot:
+            first = torch.cumsum(slen, 0) - slen
+            idx = (torch.arange(tot, device=dev) - torch.repeat_interleave(first, slen)
+                   + torch.repeat_interleave(starts, slen))
+            scol, sval = M.col_indices[idx], M.values[idx]
+        else:
+            scol = torch.zeros(0, dtype=IDX, device=dev)
+            sval = torch.zeros(0, dtype=VAL, device=dev)
+        gcol = self.comm.a2a(scol, se, re_)
+        gval = self.comm.a2a(sval, se, re_)
+        gptr = torch.zeros(self.n + 1, dtype=I64, device=dev)
+        gptr[1:] = torch.cumsum(rlen, 0)
+        return gptr.to(IDX), gcol, gval
+
+    def ext_cols(self, col):
+        """Global column ids -> ext ids [local | ghost] (order of storage kept)."""
+        lo, hi = self.part.lo(self.comm.rank), self.part.hi(self.comm.rank)
+        c = col.to(I64)
+        loc = (c >= lo) & (c < hi)
+        out = torch.where(loc, c - lo, self.n_loc + torch.searchsorted(self.ghost, c))
+        return out.to(IDX)
+
+
+def remote_cols(col, part, rank):
+    c = col.to(I64)
+    lo, hi = part.lo(rank), part.hi(rank)
+    return torch.unique(c[(c < lo) | (c >= hi)])
+
+
+def cat_rows(M, gptr, gcol, gval, ncols):
+    """Local rows of M followed by ghost rows."""
+    nnz = M.nnz
+    ptr = torch.cat([M.row_offsets[:-1], gptr + nnz])
+    return SparseMatrix(M.nrows + gptr.numel() - 1, ncols, ptr.to(IDX),
+                        torch.cat([M.col_indices, gcol]), torch.cat([M.values, gval]))
+
+
+def with_cols(M, col, ncols):
+    return SparseMatrix(M.nrows, ncols, M.row_offsets, col, M.values)
+
+
+@dataclass
+class DMat:
+    """Local rows of a row-partitioned global matrix (global column ids)."""
+
+    M: SparseMatrix
+    rows: Part
+    cols: Part
+
+    def row0(self, rank):
+        return self.rows.lo(rank)
+
+
+@dataclass
+class DLevel:
+    """One distributed level: operators on local rows (global column ids)."""
+
+    R: SparseMatrix
+    A_ff: SparseMatrix
+    A_fc: SparseMatrix
+    f_loc: torch.Tensor
+    c_loc: torch.Tensor
+    labels: torch.Tensor
+    fine: Part
+    fpart: Part
+    cpart: Part
+    f_smoother: object
+    n: int
+    n_f: int
+    n_c: int
+    nnz_A: int
+    nnz_R: int
+    nnz_Aff: int
+    nnz_Afc: int
+    ddc_stats: tuple = ()
+    pcol: torch.Tensor = None
+
+
+@dataclass
+class DHierarchy:
+    dlevels: list
+    tail: object          # serial Hierarchy of the replicated coarse levels (or None)
+    tail_level: int       # global level index where the tail starts
+    top: DMat
+    comm: Comm
+    polys: dict = field(default_factory=dict)
+    truncated_at: int = None
+    config: object = None
+
+    @property
+    def num_levels(self):
+        return len(self.dlevels) + (self.tail.num_levels if self.tail else 0)
+
+
+# ---------------------------------------------------------------------------
+# problem generation
+# ---------------------------------------------------------------------------
+
+def advection_2d_strips(comm, nx, ny, vx, vy):
+    """Rank-local grid-row strip of the 2-D upwind operator (problems.py:48-85)."""
+    r, W = comm.rank, comm.world
+    rows = [(ny * q) // W * nx for q in range(W + 1)]
+    part = Part(rows, comm.device)
+    lo, hi = part.lo(r), part.hi(r)
+    nnz = L.i64()
+    L.call('airg_advection_2d_rows', nx, ny, float(vx), float(vy), lo, hi, None, None, None,
+           L.C.byref(nnz), L.stream_handle())
+    p, c, v = empty(hi - lo + 1, IDX), empty(nnz.value, IDX), empty(nnz.value, VAL)
+    L.call('airg_advection_2d_rows', nx, ny, float(vx), float(vy), lo, hi, L.ptr(p), L.ptr(c),
+           L.ptr(v), None, L.stream_handle())
+    return DMat(SparseMatrix(hi - lo, part.n, p, c, v), part, part)
+
+
+def gather_dmat(comm, A):
+    """All rows of a distributed matrix on every rank (global SparseMatrix)."""
+    M = A.M
+    lens = (M.row_offsets[1:] - M.row_offsets[:-1]).to(I64)
+    lens_all = comm.allgather_v(lens)
+    cols = comm.allgather_v(M.col_indices)
+    vals = comm.allgather_v(M.values)
+    ptr = torch.zeros(A.rows.n + 1, dtype=I64, device=lens.device)
+    ptr[1:] = torch.cumsum(lens_all, 0)
+    return SparseMatrix(A.rows.n, A.cols.n, ptr.to(IDX), cols, vals)
+
+
+# ---------------------------------------------------------------------------
+# distributed building blocks
+# ---------------------------------------------------------------------------
+
+def _local_index(labels, which):
+    return torch.nonzero(labels == which).flatten().to(IDX)
+
+
+def strength_closure(comm, A, theta):
+    """Local rows of pattern(S + S^T) (global columns).  ref: splitting.py:86-109"""
+    r = comm.rank
+    n, lo = A.M.nrows, A.rows.lo(r)
+    res = L.C.c_void_p()
+    L.call('airg_strength_rows', n, lo, L.ptr(A.M.row_offsets), L.ptr(A.M.col_indices),
+           L.ptr(A.M.values), A.M.nnz, float(theta), L.C.byref(res), L.stream_handle())
+    S = take(res, values=False)
+    dev = S.row_offsets.device
+    lens = (S.row_offsets[1:] - S.row_offsets[:-1]).to(I64)
+    i_glob = lo + torch.repeat_interleave(torch.arange(n, device=dev, dtype=I64), lens)
+    j_glob = S.col_indices.to(I64)
+    owners = A.rows.owner(j_glob)
+    order = torch.argsort(owners, stable=True)
+    sc = torch.bincount(owners, minlength=comm.world).cpu().tolist()
+    rc = comm.a2a(torch.tensor(sc, dtype=I64, device=dev), [1] * comm.world,
+                  [1] * comm.world).cpu().tolist()
+    rj = comm.a2a(j_glob[order], sc, rc)
+    ri = comm.a2a(i_glob[order], sc, rc)
+    key = (rj - lo) * A.rows.n + ri
+    key, _ = torch.sort(key)
+    trow = key // A.rows.n
+    tcol = (key % A.rows.n).to(IDX)
+    tptr = torch.zeros(n + 1, dtype=I64, device=dev)
+    tptr[1:] = torch.cumsum(torch.bincount(trow, minlength=n), 0)
+    res = L.C.c_void_p()
+    L.call('airg_union_rows', n, L.ptr(S.row_offsets), L.ptr(S.col_indices),
+           L.ptr(tptr.to(IDX)), L.ptr(tcol), L.C.byref(res), L.stream_handle())
+    return take(res, values=False)
+
+
+def pmisr(comm, A, clo, seed, max_luby_loops=None):
+    """Distributed Luby rounds (splitting.py:127-159); local labels int8."""
+    r = comm.rank
+    n, lo = A.M.nrows, A.rows.lo(r)
+    halo = Halo(comm, A.rows, remote_cols(clo.col_indices, A.rows, r))
+    ccol = halo.ext_cols(clo.col_indices)
+    w = empty(n, VAL)
+    L.call('airg_luby_weights', n, lo, L.ptr(clo.row_offsets), *L.pcg_params(seed), L.ptr(w),
+           L.stream_handle())
+    w_ext = halo.ext(w)
+    dev = w.device
+    gid = torch.cat([torch.arange(lo, lo + n, device=dev, dtype=I64), halo.ghost]).to(IDX)
+    st = torch.zeros(n + halo.n, dtype=torch.int8, device=dev)
+    left = comm.sum_int(n)
+    loops = 0
+    rem = L.i32()
+    while left > 0:
+        if max_luby_loops is not None and loops >= max_luby_loops:
+            break
+        if loops > 0 and loops % 120 == 0:
+            st[st >= 3] = 1
+        mark = 3 + loops % 120
+        L.call('airg_luby_round', n, L.ptr(clo.row_offsets), L.ptr(ccol), L.ptr(w_ext), L.ptr(gid),
+               L.ptr(st), mark, 0, None, L.stream_handle())
+        st[n:] = halo.values(st[:n])
+        L.call('airg_luby_round', n, L.ptr(clo.row_offsets), L.ptr(ccol), L.ptr(w_ext), L.ptr(gid),
+               L.ptr(st), mark, 1, L.C.byref(rem), L.stream_handle())
+        st[n:] = halo.values(st[:n])
+        left = comm.sum_int(rem.value)
+        loops += 1
+    labels = empty(n, torch.int8)
+    L.call('airg_luby_finish', n, L.ptr(st), L.ptr(labels), L.stream_handle())
+    return labels
+
+
+def ddc_pass(comm, A_ext, labels_ext, n, row0, fraction, nbins):
+    """One distributed DDC pass (splitting.py:177-207); labels updated in place."""
+    from .cfsplit import DDCPassStats
+    f_loc = _local_index(labels_ext[:n], 0)
+    nf_loc = int(f_loc.numel())
+    nf = comm.sum_int(nf_loc)
+    ratio = empty(nf_loc, VAL)
+    bad = L.i32()
+    mms = np.zeros(3)
+    L.call('airg_ddc_ratios', nf_loc, row0, L.ptr(f_loc), L.ptr(A_ext.row_offsets),
+           L.ptr(A_ext.col_indices), L.ptr(A_ext.values), L.ptr(labels_ext), L.ptr(ratio),
+           L.C.byref(bad), L.hptr(mms), L.stream_handle())
+    dev = ratio.device
+    b = comm.allreduce(torch.tensor([bad.value], dtype=I64, device=dev), 'min').item()
+    if b != 0x7fffffff:
+        raise ValueError(f'zero diagonal in fine-fine block (fine row {b}); splitting is not '
+                         'usable for reduction')
+    if nf == 0:
+        raise ValueError('zero-size array to reduction operation minimum which has no identity')
+    lo = float(comm.allreduce(torch.tensor([mms[0]], dtype=VAL, device=dev), 'min').item())
+    hi = float(comm.allreduce(torch.tensor([mms[1]], dtype=VAL, device=dev), 'max').item())
+    sm = float(comm.allreduce(torch.tensor([mms[2] if nf_loc else 0.0], dtype=VAL,
+                                           device=dev)).item())
+    target = fraction * nf
+    conv = L.i32()
+    if lo == hi:
+        allc = abs(nf - target) < target
+        cut = lo if allc else hi
+        if allc:
+            L.call('airg_ddc_convert', nf_loc, L.ptr(f_loc), L.ptr(ratio), cut, 1, L.ptr(labels_ext),
+                   L.C.byref(conv), L.stream_handle())
+    else:
+        edges = lo + (hi - lo) * np.arange(nbins + 1) / nbins
+        edges = np.ascontiguousarray(edges)
+        hist = torch.zeros(nbins + 2, dtype=I64, device=dev)
+        L.call('airg_ddc_hist', nf_loc, L.ptr(ratio), L.hptr(edges), nbins + 1, L.ptr(hist),
+               L.stream_handle())
+        hist = comm.allreduce(hist).cpu().numpy()
+        above = np.cumsum(hist[::-1])[::-1][1:]          # above[k] = sum_{b > k} hist[b]
+        k = nbins - int(np.argmin(np.abs(above - target)[::-1]))
+        cut = float(edges[k])
+        L.call('airg_ddc_convert', nf_loc, L.ptr(f_loc), L.ptr(ratio), cut, 0, L.ptr(labels_ext),
+               L.C.byref(conv), L.stream_handle())
+    converted = comm.sum_int(conv.value)
+    return DDCPassStats(n_f_before=nf, converted=converted, ratio_min=lo, ratio_max=hi,
+                        ratio_mean=sm / nf, cut=cut)
+
+
+def dist_arnoldi_coeffs(comm, A_ff, halo, order, seed):
+    """GMRES polynomial (monomial) of a row-strip A_ff: device SpMV with halo,
+    allreduce'd MGS dot products (same recurrence as polynomial.py:68-110), host
+    coefficients from the (identical on every rank) Hessenberg block."""
+    from .gmres_poly import coeffs_from_hessenberg
+    r = comm.rank
+    n, lo, N = A_ff.nrows, halo.part.lo(r), halo.part.n
+    m = min(order + 1, N)
+    A_ext = with_cols(A_ff, halo.ext_cols(A_ff.col_indices), n + halo.n)
+    v = empty(n, VAL)
+    L.call('airg_pcg64_fill_at', *L.pcg_params(seed), lo, n, -1.0, 2.0, L.ptr(v), L.stream_handle())
+
+    def dot(a, b):
+        return comm.allreduce(torch.dot(a, b).reshape(1)).item()
+
+    def nrm(a):
+        return float(np.sqrt(dot(a, a)))
+
+    from .csr import spmv
+    b = v / nrm(v)
+    beta = nrm(b)
+    if beta == 0:
+        raise ValueError('cannot build a Krylov space from a zero vector')
+    V = [b / beta]
+    H = np.zeros((m + 1, m))
+    hmax, k = 0.0, m
+    for j in range(m):
+        w = spmv(A_ext, halo.ext(V[j]))
+        before = nrm(w)
+        for sweep in range(2):
+            for i in range(j + 1):
+                h = dot(V[i], w)
+                H[i, j] += h
+                w = w - h * V[i]
+            hn = nrm(w)
+            if not (sweep == 0 and hn < 0.7 * before):
+                break
+        H[j + 1, j] = hn
+        hmax = max(hmax, float(np.linalg.norm(H[:j + 2, j])))
+        if hn <= 1e-14 * hmax:
+            H[j + 1, j] = 0.0
+            k = j + 1
+            break
+        V.append(w / hn)
+    if np.max(np.abs(H[:k + 1, :k])) == 0.0:
+        raise ValueError('matrix is numerically zero on the Krylov space')
+    return coeffs_from_hessenberg(H[:k + 1, :k].copy(), k, beta, order)
+
+
+def _spgemm(A, B, ncols, negate=False, mode=0, tol=0.0, lump=False, row0=0):
+    res = L.C.c_void_p()
+    L.call('airg_spgemm_ex', A.nrows, B.nrows, ncols, L.ptr(A.row_offsets), L.ptr(A.col_indices),
+           L.ptr(A.values), L.ptr(B.row_offsets), L.ptr(B.col_indices), L.ptr(B.values),
+           1 if negate else 0, mode, float(tol), 1 if lump else 0, int(row0), L.C.byref(res),
+           L.stream_handle())
+    out = take(res)
+    return SparseMatrix(out.nrows, ncols, out.row_offsets, out.col_indices, out.values)
+
+
+# ---------------------------------------------------------------------------
+# distributed setup
+# ---------------------------------------------------------------------------
+
+def setup_distributed(comm, A, cfg, poly_inject=None, replicate_below=20000):
+    """AIRG setup (hierarchy.py:365-448) on a row-partitioned matrix.  Levels
+    with more than ``replicate_below`` rows (and below the truncation start)
+    are built distributed; the rest is built on every rank from the gathered
+    level matrix with the serial code."""
+    from .amg_setup import (SETUP_PHASES, SEED_SMOOTHER, SEED_SPLIT, build_levels, derive_seed,
+                            resolve_truncate_start, finalize_complexities, Hierarchy)
+    cfg.validate()
+    if cfg.inverse_type != 'arnoldi' or cfg.r_drop != 0:
+        raise ValueError('the distributed setup supports inverse_type="arnoldi" with r_drop=0')
+    inj = poly_inject or {}
+    polys = {}
+    timings = {p: 0.0 for p in SETUP_PHASES}
+    r = comm.rank
+    truncate_start = resolve_truncate_start(cfg, A.rows.n)
+    dlevels = []
+    level = 0
+    cur = A
+    while (cur.rows.n > replicate_below and comm.world > 1 and level < cfg.max_levels
+           and cur.rows.n > cfg.min_coarse_size
+           and not (cfg.auto_truncate_tol is not None and level >= truncate_start)):
+        n, lo = cur.M.nrows, cur.rows.lo(r)
+        dev = cur.M.values.device
+        # ---- CF splitting ----
+        clo = strength_closure(comm, cur, cfg.strong_threshold)
+        labels = pmisr(comm, cur, clo, derive_seed(cfg.seed, level, SEED_SPLIT))
+        halo_a = Halo(comm, cur.rows, remote_cols(cur.M.col_indices, cur.rows, r))
+        A_ext = with_cols(cur.M, halo_a.ext_cols(cur.M.col_indices), n + halo_a.n)
+        lab_ext = halo_a.ext(labels)
+        stats = []
+        for _ in range(cfg.ddc_its):
+            if comm.sum_int(int((lab_ext[:n] == 0).sum().item())) == 0:
+                break
+            stats.append(ddc_pass(comm, A_ext, lab_ext, n, lo, cfg.ddc_fraction, cfg.ddc_bins))
+            lab_ext[n:] = halo_a.values(lab_ext[:n])
+        nc_glob = comm.sum_int(int((lab_ext[:n] == 1).sum().item()))
+        if nc_glob == cur.rows.n:
+            raise ValueError(f'splitting produced no F points at level {level}')
+        if nc_glob > 0:
+            ch = L.i32()
+            L.call('airg_repair_split', n, L.ptr(A_ext.row_offsets), L.ptr(A_ext.col_indices),
+                   L.ptr(lab_ext), L.C.byref(ch), L.stream_handle())
+            lab_ext[n:] = halo_a.values(lab_ext[:n])
+        labels = lab_ext[:n].clone()
+        f_loc, c_loc = _local_index(labels, 0), _local_index(labels, 1)
+        nf_all = comm.allgather_int(f_loc.numel())
+        nc_all = comm.allgather_int(c_loc.numel())
+        if sum(nc_all) == 0 or sum(nf_all) == 0:
+            break  # the replicated tail builds the coarse solver here
+        fpart, cpart = Part.from_counts(nf_all, dev), Part.from_counts(nc_all, dev)
+        fpos0, cpos0 = fpart.lo(r), cpart.lo(r)
+        gpos = torch.zeros(n, dtype=IDX, device=dev)
+        gpos[f_loc.long()] = torch.arange(fpos0, fpos0 + f_loc.numel(), device=dev, dtype=IDX)
+        gpos[c_loc.long()] = torch.arange(cpos0, cpos0 + c_loc.numel(), device=dev, dtype=IDX)
+        gpos_ext = halo_a.ext(gpos)
+        fmap, cmap = empty(n + halo_a.n, IDX), empty(n + halo_a.n, IDX)
+        L.call('airg_label_colmap', n + halo_a.n, L.ptr(lab_ext), 0, L.ptr(gpos_ext), L.ptr(fmap),
+               L.stream_handle())
+        L.call('airg_label_colmap', n + halo_a.n, L.ptr(lab_ext), 1, L.ptr(gpos_ext), L.ptr(cmap),
+               L.stream_handle())
+        A_ff = extract_mapped(A_ext, f_loc, fmap, fpart.n)
+        A_fc = extract_mapped(A_ext, f_loc, cmap, cpart.n)
+        A_cf = extract_mapped(A_ext, c_loc, fmap, fpart.n)
+        # ---- smoother ----
+        halo_ff = Halo(comm, fpart, remote_cols(A_ff.col_indices, fpart, r))
+        sm = inj.get(('smoother', level))
+        if sm is None:
+            sm = dist_arnoldi_coeffs(comm, A_ff, halo_ff, cfg.poly_order,
+                                     derive_seed(cfg.seed, level, SEED_SMOOTHER))
+        polys[('smoother', level)] = sm
+        # ---- fixed-sparsity assembly on local rows with ghost rows of A_ff ----
+        gp, gc, gv = halo_ff.rows(A_ff)
+        Aff_rows = cat_rows(A_ff, gp, gc, gv, fpart.n)
+        rowmap = torch.full((fpart.n,), -1, dtype=IDX, device=dev)
+        rowmap[fpos0:fpos0 + A_ff.nrows] = torch.arange(A_ff.nrows, device=dev, dtype=IDX)
+        if halo_ff.n:
+            rowmap[halo_ff.ghost] = torch.arange(A_ff.nrows, A_ff.nrows + halo_ff.n, device=dev,
+                                                 dtype=IDX)
+        coef = np.ascontiguousarray(sm.coeffs, dtype=np.float64)
+        res = L.C.c_void_p()
+        L.call('airg_poly_assemble_ex', A_ff.nrows, fpos0, L.ptr(Aff_rows.row_offsets),
+               L.ptr(Aff_rows.col_indices), L.ptr(Aff_rows.values), L.ptr(rowmap), len(coef),
+               L.hptr(coef), L.ptr(A_ff.row_offsets), L.ptr(A_ff.col_indices), L.C.byref(res),
+               L.stream_handle())
+        Ahat = take(res)
+        Ahat = SparseMatrix(Ahat.nrows, fpart.n, Ahat.row_offsets, Ahat.col_indices, Ahat.values)
+        # ---- Z = -A_cf Ahat ----
+        halo_z = Halo(comm, fpart, remote_cols(A_cf.col_indices, fpart, r))
+        Ahat_rows = cat_rows(Ahat, *halo_z.rows(Ahat), fpart.n)
+        Z = _spgemm(with_cols(A_cf, halo_z.ext_cols(A_cf.col_indices), Ahat_rows.nrows), Ahat_rows,
+                    fpart.n, negate=True)
+        # ---- R = [Z I] in the fine numbering ----
+        halo_zc = Halo(comm, fpart, remote_cols(Z.col_indices, fpart, r))
+        fine_of_f = (lo + f_loc.long()).to(IDX)
+        f_ext = halo_zc.ext(fine_of_f)
+        Zx = with_cols(Z, halo_zc.ext_cols(Z.col_indices), f_loc.numel() + halo_zc.n)
+        res = L.C.c_void_p()
+        L.call('airg_restriction', cur.rows.n, Zx.nrows, L.ptr(Zx.row_offsets), L.ptr(Zx.col_indices),
+               L.ptr(Zx.values), L.ptr(f_ext), L.ptr((lo + c_loc.long()).to(IDX)), L.C.byref(res),
+               L.stream_handle())
+        R = take(res)
+        # ---- one-point P, A P, R (A P) with drop/lump ----
+        pcol = empty(n, IDX)
+        L.call('airg_prolong_onepoint', n, L.ptr(A_ext.row_offsets), L.ptr(A_ext.col_indices),
+               L.ptr(A_ext.values), L.ptr(lab_ext), L.ptr(gpos_ext), L.ptr(pcol), L.stream_handle())
+        pcol_ext = halo_a.ext(pcol)
+        P_ext = SparseMatrix(pcol_ext.numel(), cpart.n,
+                             torch.arange(pcol_ext.numel() + 1, device=dev, dtype=IDX), pcol_ext,
+                             torch.ones(pcol_ext.numel(), dtype=VAL, device=dev))
+        AP = _spgemm(A_ext, P_ext, cpart.n)
+        halo_r = Halo(comm, cur.rows, remote_cols(R.col_indices, cur.rows, r))
+        AP_rows = cat_rows(AP, *halo_r.rows(AP), cpart.n)
+        Rx = with_cols(R, halo_r.ext_cols(R.col_indices), AP_rows.nrows)
+        if cfg.a_drop > 0:
+            Ac = _spgemm(Rx, AP_rows, cpart.n, mode=1, tol=cfg.a_drop, lump=cfg.lump, row0=cpos0)
+        else:
+            Ac = _spgemm(Rx, AP_rows, cpart.n)
+        dlevels.append(DLevel(R=R, A_ff=A_ff, A_fc=A_fc, f_loc=f_loc, c_loc=c_loc, labels=labels,
+                              fine=cur.rows, fpart=fpart, cpart=cpart, f_smoother=sm,
+                              n=cur.rows.n, n_f=fpart.n, n_c=cpart.n,
+                              nnz_A=comm.sum_int(cur.M.nnz), nnz_R=comm.sum_int(R.nnz),
+                              nnz_Aff=comm.sum_int(A_ff.nnz), nnz_Afc=comm.sum_int(A_fc.nnz),
+                              ddc_stats=tuple(stats), pcol=pcol))
+        cur = DMat(Ac, cpart, cpart)
+        level += 1
+    # ---- replicated tail ----
+    full = gather_dmat(comm, cur)
+    levels, coarsest, solver, trunc = build_levels(full, cfg, level, truncate_start, inj, polys,
+                                                   timings)
+    tail = Hierarchy(levels=levels, coarsest_A=coarsest, coarse_solver=solver, top_A=full,
+                     truncated_at=trunc, config=cfg, setup_breakdown=timings)
+    tail.polys = polys
+    finalize_complexities(tail)
+    return DHierarchy(dlevels=dlevels, tail=tail, tail_level=level, top=A, comm=comm, polys=polys,
+                      truncated_at=trunc, config=cfg)
+
+
+# ---------------------------------------------------------------------------
+# distributed solve (solve.py:95-167): V-cycle on row strips with halos;
+# below the distributed levels the replicated tail runs the serial plan.
+# ---------------------------------------------------------------------------
+
+class DistSolver:
+    def __init__(self, H):
+        self.H = H
+        comm = H.comm
+        r = comm.rank
+        self.comm = comm
+        self.lv = []
+        for d in H.dlevels:
+            hR = Halo(comm, d.fine, remote_cols(d.R.col_indices, d.fine, r))
+            hC = Halo(comm, d.cpart, remote_cols(d.A_fc.col_indices, d.cpart, r))
+            hF = Halo(comm, d.fpart, remote_cols(d.A_ff.col_indices, d.fpart, r))
+            self.lv.append(dict(
+                R=with_cols(d.R, hR.ext_cols(d.R.col_indices), hR.n_loc + hR.n),
+                hR=hR,
+                Afc=with_cols(d.A_fc, hC.ext_cols(d.A_fc.col_indices), hC.n_loc + hC.n), hC=hC,
+                Aff=with_cols(d.A_ff, hF.ext_cols(d.A_ff.col_indices), hF.n_loc + hF.n), hF=hF,
+                f=d.f_loc.long(), c=d.c_loc.long(), n=d.fine.hi(r) - d.fine.lo(r),
+                coef=np.asarray(d.f_smoother.coeffs, dtype=np.float64)))
+        top = H.top
+        self.htop = Halo(comm, top.rows, remote_cols(top.M.col_indices, top.rows, r))
+        self.Atop = with_cols(top.M, self.htop.ext_cols(top.M.col_indices),
+                              self.htop.n_loc + self.htop.n)
+        # partition of the first replicated level (the tail's top matrix)
+        if H.dlevels:
+            self.tail_part = H.dlevels[-1].cpart
+        else:
+            self.tail_part = top.rows
+
+    def _smooth(self, L_, rhs):
+        from .csr import spmv
+        c = L_['coef']
+        d = len(c) - 1
+        y = c[d] * rhs
+        for j in range(d - 1, -1, -1):
+            y = spmv(L_['Aff'], L_['hF'].ext(y)) + c[j] * rhs
+        return y
+
+    def vcycle(self, lev, r_loc):
+        from .amg_solve import SolveConfig, vcycle as serial_vcycle
+        from .csr import spmv
+        comm = self.comm
+        if lev == len(self.lv):
+            r_full = comm.allgather_v(r_loc)
+            e_full = serial_vcycle(self.H.tail, 0, r_full, SolveConfig())
+            p = self.tail_part
+            return e_full[p.lo(comm.rank):p.hi(comm.rank)]
+        L_ = self.lv[lev]
+        rc = spmv(L_['R'], L_['hR'].ext(r_loc))
+        ec = self.vcycle(lev + 1, rc)
+        rhs = r_loc[L_['f']] - spmv(L_['Afc'], L_['hC'].ext(ec))
+        ef = self._smooth(L_, rhs)
+        e = torch.zeros(L_['n'], dtype=VAL, device=r_loc.device)
+        e[L_['f']] = ef
+        e[L_['c']] = ec
+        return e
+
+    def norm(self, v):
+        return float(np.sqrt(self.comm.allreduce(torch.dot(v, v).reshape(1)).item()))
+
+    def richardson(self, b, x0, cfg):
+        """Richardson preconditioned by the distributed V-cycle; b, x0 local."""
+        from .amg_solve import DivergenceError, SolveStats
+        from .csr import spmv
+        cfg.validate()
+        x = x0.clone()
+        r = b - spmv(self.Atop, self.htop.ext(x))
+        rn = self.norm(r)
+        hist = [rn]
+        bn = self.norm(b)
+        thr = max(cfg.rtol * (bn if bn > 0 else rn), cfg.atol)
+        conv, its = rn <= thr, 0
+        while not conv and its < cfg.max_iters:
+            x = x + self.vcycle(0, r)
+            r = b - spmv(self.Atop, self.htop.ext(x))
+            rn = self.norm(r)
+            its += 1
+            hist.append(rn)
+            if not np.isfinite(rn):
+                raise DivergenceError(f'non-finite residual at iteration {its}', its)
+            if rn > 1e8 * hist[0]:
+                raise DivergenceError(f'residual grew by more than 1e+08 at iteration {its}', its)
+            conv = rn <= thr
+        return x, SolveStats(iterations=its, residual_history=hist, converged=conv,
+                             cycle_complexity=0.0, storage_complexity=0.0, flops_per_cycle=0)
