@@ -96,6 +96,30 @@ int airg_plan_set_exact(airg_plan* plan, int exact);
 /* Number of kernel launches issued by the last airg_plan_richardson call. */
 int64_t airg_plan_launches(airg_plan* plan);
 
+/* ---- distributed (row-strip) solve over NCCL ----------------
+ * One plan per rank: per distributed level R / A_fc / A_ff on local rows with
+ * columns in [local | ghost], halo plans (send indices + per-peer counts;
+ * ghost values land in the tail of the operand vector), the top operator,
+ * and the replicated serial plan of the coarse tail. */
+typedef struct airg_dplan airg_dplan;
+int airg_nccl_unique_id(char* out_h /* 128 bytes */);
+int airg_dplan_create(const char* id_h, int rank, int world, int ndist, airg_dplan** out_h);
+/* which: 0 = R (fine space), 1 = A_fc (coarse space), 2 = A_ff (F space), 3 = top */
+int airg_dplan_set_halo(airg_dplan* plan, int level, int which, int n_loc, int nsend,
+                        const int32_t* send_idx, const int32_t* scnt_h, const int32_t* rcnt_h);
+int airg_dplan_set_level(airg_dplan* plan, int level, int n_loc, int nf, int nc, const int32_t* Rp,
+                         const int32_t* Rc, const double* Rv, int64_t Rnnz, const int32_t* Fcp,
+                         const int32_t* Fcc, const double* Fcv, int64_t Fcnnz, const int32_t* Ffp,
+                         const int32_t* Ffc, const double* Ffv, int64_t Ffnnz, const int32_t* f_idx,
+                         const int32_t* c_idx, int ncoef, const double* coef_h);
+int airg_dplan_set_top(airg_dplan* plan, int n_loc, const int32_t* ptr, const int32_t* col,
+                       const double* val, int64_t nnz);
+int airg_dplan_finish(airg_dplan* plan, airg_plan* tail, const int32_t* counts_h);
+int airg_dplan_richardson(airg_dplan* plan, const double* b, double* x, double rtol, double atol,
+                          int max_iters, double* history_h, int* iterations_h, int* converged_h,
+                          void* stream);
+int airg_dplan_destroy(airg_dplan* plan);
+
 /* ---- variable-size CSR results (setup path) ------------------------------
  * Producers return an opaque airg_csr_result held in library scratch;
  * airg_result_info gives its shape, the caller allocates ptr[nrows+1],

@@ -133,6 +133,15 @@ sig('airg_plan_set_coarse', vp, i32, vp, vp, vp, C.c_int, C.c_int, vp, C.c_int, 
 sig('airg_plan_vcycle', vp, C.c_int, vp, vp, C.c_int, vp)
 sig('airg_plan_richardson', vp, vp, vp, f64, f64, C.c_int, C.c_int, vp, vp, vp, vp)
 sig('airg_plan_launches', vp, ret=i64)
+sig('airg_nccl_unique_id', C.c_char_p)
+sig('airg_dplan_create', C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(vp))
+sig('airg_dplan_set_halo', vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp)
+sig('airg_dplan_set_level', vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, i64, vp, vp, vp,
+    i64, vp, vp, vp, i64, vp, vp, C.c_int, vp)
+sig('airg_dplan_set_top', vp, C.c_int, vp, vp, vp, i64)
+sig('airg_dplan_finish', vp, vp, vp)
+sig('airg_dplan_richardson', vp, vp, vp, f64, f64, C.c_int, vp, vp, vp, vp)
+sig('airg_dplan_destroy', vp)
 u64 = C.c_uint64
 pp = C.POINTER(vp)
 sig('airg_result_info', vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i64))

@@ -15,9 +15,24 @@ OBJ = os.path.join(HERE, 'build')
 LIB = os.path.join(HERE, 'libairg.so')
 NVCC = os.environ.get('NVCC', '/usr/local/cuda/bin/nvcc')
 
+def _nccl_dir():
+    """NCCL headers / library shipped with torch (nvidia-nccl wheel)."""
+    import importlib.util
+    spec = importlib.util.find_spec('nvidia')
+    for base in (spec.submodule_search_locations or []) if spec else []:
+        d = os.path.join(base, 'nccl')
+        if os.path.exists(os.path.join(d, 'include', 'nccl.h')):
+            return d
+    raise RuntimeError('nccl.h not found (nvidia-nccl wheel)')
+
+
+NCCL = _nccl_dir()
 FLAGS = ['-O3', '-std=c++17', '-gencode', 'arch=compute_100a,code=sm_100a', '-lineinfo',
          '-Xcompiler', '-fPIC', '--expt-relaxed-constexpr', '--extended-lambda',
-         '-I', os.path.join(ROOT, 'include'), '-Xptxas', '-warn-spills']
+         '-I', os.path.join(ROOT, 'include'), '-I', os.path.join(NCCL, 'include'),
+         '-Xptxas', '-warn-spills']
+LDFLAGS = ['-L', os.path.join(NCCL, 'lib'), '-l:libnccl.so.2',
+           '-Xlinker', '-rpath=' + os.path.join(NCCL, 'lib')]
 
 
 def sources():
@@ -53,7 +68,7 @@ def build(force=False, verbose=False):
         list(ex.map(run, jobs))
     if jobs or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB)
                                               for o in objs):
-        cmd = [NVCC, '-shared', '-gencode', 'arch=compute_100a,code=sm_100a', '-o', LIB] + objs
+        cmd = [NVCC, '-shared', '-gencode', 'arch=compute_100a,code=sm_100a', '-o', LIB] + objs + LDFLAGS
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f'link failed:\n{r.stdout}\n{r.stderr}')

@@ -3,6 +3,7 @@
 // driver.  ref: /root/reference/pkg/src/airmg/solve.py:89-167,
 // polynomial.py:295-369, sparse.py:206-212.
 #include "airg_common.cuh"
+#include <nccl.h>
 #include <vector>
 #include <algorithm>
 #include <cstring>
@@ -1366,3 +1367,407 @@ static int richardson_body(airg_plan* p, const double* b, double* x, double rtol
   p->launches = g_launches - l0;
   return AIRG_OK;
 }
+
+// ===========================================================================
+// Row-strip distributed V-cycle / Richardson over NCCL.
+// Each distributed level keeps R, A_fc, A_ff on local rows with columns in
+// the ext space [local | ghost]; a halo exchange is a pack kernel plus grouped
+// ncclSend/ncclRecv straight into the ghost tail of the operand vector.
+// Below the distributed levels the residual is all-gathered and the
+// replicated serial plan solves the tail.  Every iteration (V-cycle, x += e,
+// residual, norm allreduce) is one captured CUDA graph.
+// ===========================================================================
+#define AIRG_NCCL(call)                                                          \
+  do {                                                                           \
+    ncclResult_t _r = (call);                                                    \
+    if (_r != ncclSuccess) {                                                     \
+      ::airg::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call,              \
+                        ncclGetErrorString(_r));                                 \
+      return AIRG_ERR_CUDA;                                                      \
+    }                                                                            \
+  } while (0)
+
+namespace airg {
+
+struct HaloX {
+  int n_loc = 0, nsend = 0, nrecv = 0;
+  int* send_idx = nullptr;
+  double* sendbuf = nullptr;
+  std::vector<int> scnt, sofs, rcnt, rofs;
+};
+
+__global__ void pack_kernel(int n, const int* __restrict__ idx, const double* __restrict__ x,
+                            double* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = x[idx[i]];
+}
+
+__global__ void finish_sum_kernel(int nparts, const double* __restrict__ parts, double* __restrict__ out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += parts[i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) out[0] = t;
+  }
+}
+
+// trecv holds world blocks of tmax entries; out = concatenation of the first
+// cnt[q] entries of each block
+__global__ void unpad_kernel(int world, int tmax, const int* __restrict__ cnt, const int* __restrict__ ofs,
+                             const double* __restrict__ in, double* __restrict__ out) {
+  const int q = blockIdx.y;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt[q]; i += gridDim.x * blockDim.x)
+    out[ofs[q] + i] = in[(size_t)q * tmax + i];
+}
+
+}  // namespace airg
+
+struct DLev {
+  int n_loc = 0, nf = 0, nc = 0;
+  Csr R, Afc, Aff;
+  HaloX hR, hC, hF;
+  const int* f_idx = nullptr;
+  const int* c_idx = nullptr;
+  std::vector<double> coef;
+  double *r_ext = nullptr, *ec_ext = nullptr, *rhs_ext = nullptr, *y0 = nullptr, *y1 = nullptr,
+         *e = nullptr;
+};
+
+struct airg_dplan {
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  std::vector<DLev> lv;
+  Csr top;
+  HaloX hT;
+  double *x_ext = nullptr, *r = nullptr, *parts = nullptr, *nrm_loc = nullptr, *nrm_glob = nullptr;
+  double norm_h = 0.0;
+  int nparts = 0;
+  airg_plan* tail = nullptr;
+  std::vector<int> tcnt, tofs;
+  int tail_n = 0, tmax = 0;
+  int *d_tcnt = nullptr, *d_tofs = nullptr;
+  double *tsend = nullptr, *trecv = nullptr, *tr_full = nullptr, *te_full = nullptr;
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  const void* gkey[2] = {nullptr, nullptr};
+  long long launches = 0;
+};
+
+static int halo_exchange(airg_dplan* p, HaloX& h, double* x_ext, cudaStream_t s) {
+  if (p->world == 1) return AIRG_OK;
+  if (h.nsend) {
+    pack_kernel<<<blocks_for(h.nsend, 256, 1024), 256, 0, s>>>(h.nsend, h.send_idx, x_ext, h.sendbuf);
+    AIRG_LAUNCH_CHECK();
+  }
+  AIRG_NCCL(ncclGroupStart());
+  for (int q = 0; q < p->world; ++q) {
+    if (h.scnt[q]) AIRG_NCCL(ncclSend(h.sendbuf + h.sofs[q], h.scnt[q], ncclDouble, q, p->comm, s));
+    if (h.rcnt[q])
+      AIRG_NCCL(ncclRecv(x_ext + h.n_loc + h.rofs[q], h.rcnt[q], ncclDouble, q, p->comm, s));
+  }
+  AIRG_NCCL(ncclGroupEnd());
+  return AIRG_OK;
+}
+
+static int dplan_vcycle(airg_dplan* p, int l, cudaStream_t s);
+
+// V-cycle of the replicated tail: in = local part (tcnt[rank] entries), out = local part
+static int dplan_tail(airg_dplan* p, const double* in, double* out, cudaStream_t s) {
+  const int mine = p->tcnt[p->rank];
+  AIRG_CUDA(cudaMemcpyAsync(p->tsend, in, (size_t)mine * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  AIRG_NCCL(ncclAllGather(p->tsend, p->trecv, p->tmax, ncclDouble, p->comm, s));
+  dim3 g(blocks_for(p->tmax, 256, 64), p->world);
+  unpad_kernel<<<g, 256, 0, s>>>(p->world, p->tmax, p->d_tcnt, p->d_tofs, p->trecv, p->tr_full);
+  AIRG_LAUNCH_CHECK();
+  AIRG_TRY(vcycle_rec(p->tail, 0, p->tr_full, p->te_full, 1, s));
+  AIRG_CUDA(cudaMemcpyAsync(out, p->te_full + p->tofs[p->rank], (size_t)mine * sizeof(double),
+                            cudaMemcpyDeviceToDevice, s));
+  return AIRG_OK;
+}
+
+// input lv[l].r_ext[0, n_loc), output lv[l].e
+static int dplan_vcycle(airg_dplan* p, int l, cudaStream_t s) {
+  DLev& L = p->lv[l];
+  const bool last = l + 1 == (int)p->lv.size();
+  AIRG_TRY(halo_exchange(p, L.hR, L.r_ext, s));
+  // restricted residual: the next level's input, or scratch before the tail gather
+  double* rc = last ? L.rhs_ext : p->lv[l + 1].r_ext;
+  {
+    Epi ep{rc, nullptr, 1.0, 0.0, nullptr, nullptr, nullptr, nullptr};
+    AIRG_TRY(launch_spmv(L.R, L.r_ext, 1.0, ep, s));
+  }
+  if (last) AIRG_TRY(dplan_tail(p, rc, L.ec_ext, s));
+  else AIRG_TRY(dplan_vcycle(p, l + 1, s));  // writes lv[l+1].e == L.ec_ext
+  AIRG_TRY(halo_exchange(p, L.hC, L.ec_ext, s));
+  // rhs = r[f] - A_fc e_c
+  {
+    Epi ep{L.rhs_ext, nullptr, -1.0, 1.0, L.r_ext, L.f_idx, nullptr, nullptr};
+    AIRG_TRY(launch_spmv(L.Afc, L.ec_ext, 1.0, ep, s));
+  }
+  const int d = (int)L.coef.size() - 1;
+  if (d == 0) {
+    AIRG_TRY(launch_axpby(L.nf, L.e, L.f_idx, L.coef[0], L.rhs_ext, nullptr, 0.0, nullptr, s));
+  } else {
+    double* cur = L.rhs_ext;
+    double xs = L.coef[d];
+    double* bufs[2] = {L.y0, L.y1};
+    for (int j = d - 1; j >= 0; --j) {
+      AIRG_TRY(halo_exchange(p, L.hF, cur, s));
+      double* dst = j == 0 ? L.e : bufs[j & 1];
+      Epi ep{dst, j == 0 ? L.f_idx : nullptr, 1.0, L.coef[j], L.rhs_ext, nullptr, nullptr, nullptr};
+      AIRG_TRY(launch_spmv(L.Aff, cur, xs, ep, s));
+      cur = dst;
+      xs = 1.0;
+    }
+  }
+  AIRG_TRY(launch_axpby(L.nc, L.e, L.c_idx, 1.0, L.ec_ext, nullptr, 0.0, nullptr, s));
+  return AIRG_OK;
+}
+
+// r = b - A x (halo on x), local sum of squares -> allreduce -> nrm_glob
+static int dplan_residual(airg_dplan* p, const double* b, cudaStream_t s) {
+  AIRG_TRY(halo_exchange(p, p->hT, p->x_ext, s));
+  const int nb = spmv_blocks(p->top);
+  Epi ep{p->r, nullptr, -1.0, 1.0, b, nullptr, nullptr, p->parts};
+  AIRG_TRY(launch_spmv(p->top, p->x_ext, 1.0, ep, s));
+  finish_sum_kernel<<<1, 1024, 0, s>>>(nb, p->parts, p->nrm_loc);
+  AIRG_LAUNCH_CHECK();
+  AIRG_NCCL(ncclAllReduce(p->nrm_loc, p->nrm_glob, 1, ncclDouble, ncclSum, p->comm, s));
+  return AIRG_OK;
+}
+
+static int dalloc(HaloX& h, int n_loc, int nsend, const int* send_idx, const int* scnt,
+                  const int* rcnt, int world) {
+  h.n_loc = n_loc;
+  h.nsend = nsend;
+  h.scnt.assign(scnt, scnt + world);
+  h.rcnt.assign(rcnt, rcnt + world);
+  h.sofs.assign(world, 0);
+  h.rofs.assign(world, 0);
+  int a = 0, b = 0;
+  for (int q = 0; q < world; ++q) {
+    h.sofs[q] = a;
+    h.rofs[q] = b;
+    a += h.scnt[q];
+    b += h.rcnt[q];
+  }
+  h.nrecv = b;
+  if (nsend) {
+    AIRG_CUDA(dmalloc(&h.send_idx, (size_t)nsend * sizeof(int)));
+    AIRG_CUDA(cudaMemcpy(h.send_idx, send_idx, (size_t)nsend * sizeof(int), cudaMemcpyDeviceToDevice));
+    AIRG_CUDA(dmalloc(&h.sendbuf, (size_t)nsend * sizeof(double)));
+  }
+  return AIRG_OK;
+}
+
+extern "C" {
+
+int airg_nccl_unique_id(char* out_h) {
+  ncclUniqueId id;
+  AIRG_NCCL(ncclGetUniqueId(&id));
+  memcpy(out_h, id.internal, NCCL_UNIQUE_ID_BYTES);
+  return AIRG_OK;
+}
+
+int airg_dplan_create(const char* id_h, int rank, int world, int ndist, airg_dplan** out) {
+  airg_dplan* p = new airg_dplan();
+  p->rank = rank;
+  p->world = world;
+  ncclUniqueId id;
+  memcpy(id.internal, id_h, NCCL_UNIQUE_ID_BYTES);
+  AIRG_NCCL(ncclCommInitRank(&p->comm, world, id, rank));
+  p->lv.resize(ndist);
+  AIRG_CUDA(cudaStreamCreateWithFlags(&p->cs, cudaStreamNonBlocking));
+  AIRG_CUDA(cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming));
+  AIRG_CUDA(cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming));
+  AIRG_CUDA(dmalloc(&p->nrm_loc, 2 * sizeof(double)));
+  p->nrm_glob = p->nrm_loc + 1;
+  *out = p;
+  return AIRG_OK;
+}
+
+// which: 0 = R (fine space), 1 = A_fc (coarse space), 2 = A_ff (F space), 3 = top A
+int airg_dplan_set_halo(airg_dplan* p, int level, int which, int n_loc, int nsend,
+                        const int32_t* send_idx, const int32_t* scnt_h, const int32_t* rcnt_h) {
+  HaloX* h = which == 3 ? &p->hT : which == 0 ? &p->lv[level].hR : which == 1 ? &p->lv[level].hC
+                                                                            : &p->lv[level].hF;
+  return dalloc(*h, n_loc, nsend, send_idx, scnt_h, rcnt_h, p->world);
+}
+
+int airg_dplan_set_level(airg_dplan* p, int level, int n_loc, int nf, int nc, const int32_t* Rp,
+                         const int32_t* Rc, const double* Rv, int64_t Rnnz, const int32_t* Fcp,
+                         const int32_t* Fcc, const double* Fcv, int64_t Fcnnz, const int32_t* Ffp,
+                         const int32_t* Ffc, const double* Ffv, int64_t Ffnnz, const int32_t* f_idx,
+                         const int32_t* c_idx, int ncoef, const double* coef_h) {
+  DLev& L = p->lv[level];
+  L.n_loc = n_loc;
+  L.nf = nf;
+  L.nc = nc;
+  L.R = make_csr(nc, n_loc + L.hR.nrecv, Rp, Rc, Rv, Rnnz);
+  L.Afc = make_csr(nf, nc + L.hC.nrecv, Fcp, Fcc, Fcv, Fcnnz);
+  L.Aff = make_csr(nf, nf + L.hF.nrecv, Ffp, Ffc, Ffv, Ffnnz);
+  L.f_idx = f_idx;
+  L.c_idx = c_idx;
+  L.coef.assign(coef_h, coef_h + ncoef);
+  AIRG_CUDA(dmalloc(&L.r_ext, (size_t)(n_loc + L.hR.nrecv + 1) * sizeof(double)));
+  AIRG_CUDA(dmalloc(&L.rhs_ext, (size_t)(std::max(nf, nc) + L.hF.nrecv + 1) * sizeof(double)));
+  AIRG_CUDA(dmalloc(&L.y0, (size_t)(nf + L.hF.nrecv + 1) * sizeof(double)));
+  AIRG_CUDA(dmalloc(&L.y1, (size_t)(nf + L.hF.nrecv + 1) * sizeof(double)));
+  if (level == 0) AIRG_CUDA(dmalloc(&L.e, (size_t)(n_loc + 1) * sizeof(double)));
+  return AIRG_OK;
+}
+
+int airg_dplan_set_top(airg_dplan* p, int n_loc, const int32_t* ptr, const int32_t* col,
+                       const double* val, int64_t nnz) {
+  p->top = make_csr(n_loc, n_loc + p->hT.nrecv, ptr, col, val, nnz);
+  AIRG_CUDA(dmalloc(&p->x_ext, (size_t)(n_loc + p->hT.nrecv + 1) * sizeof(double)));
+  AIRG_CUDA(dmalloc(&p->r, (size_t)(n_loc + 1) * sizeof(double)));
+  p->nparts = spmv_blocks(p->top) + 1;
+  AIRG_CUDA(dmalloc(&p->parts, (size_t)p->nparts * sizeof(double)));
+  return AIRG_OK;
+}
+
+// link the levels' vectors (level l's coarse error buffer == level l+1's e)
+// and attach the replicated tail plan; counts_h = per-rank sizes of the tail
+// level (the coarse size of the last distributed level on every rank)
+int airg_dplan_finish(airg_dplan* p, airg_plan* tail, const int32_t* counts_h) {
+  const int nd = (int)p->lv.size();
+  for (int l = 0; l < nd; ++l) {
+    DLev& L = p->lv[l];
+    AIRG_CUDA(dmalloc(&L.ec_ext, (size_t)(L.nc + L.hC.nrecv + 1) * sizeof(double)));
+    if (l + 1 < nd) p->lv[l + 1].e = L.ec_ext;  // level l+1's error is level l's e_c
+  }
+  p->tail = tail;
+  p->tcnt.assign(counts_h, counts_h + p->world);
+  p->tofs.assign(p->world, 0);
+  int a = 0, mx = 1;
+  for (int q = 0; q < p->world; ++q) {
+    p->tofs[q] = a;
+    a += p->tcnt[q];
+    mx = std::max(mx, p->tcnt[q]);
+  }
+  p->tail_n = a;
+  p->tmax = mx;
+  AIRG_CUDA(dmalloc(&p->d_tcnt, p->world * sizeof(int)));
+  AIRG_CUDA(dmalloc(&p->d_tofs, p->world * sizeof(int)));
+  AIRG_CUDA(cudaMemcpy(p->d_tcnt, p->tcnt.data(), p->world * sizeof(int), cudaMemcpyHostToDevice));
+  AIRG_CUDA(cudaMemcpy(p->d_tofs, p->tofs.data(), p->world * sizeof(int), cudaMemcpyHostToDevice));
+  AIRG_CUDA(dmalloc(&p->tsend, (size_t)mx * sizeof(double)));
+  AIRG_CUDA(dmalloc(&p->trecv, (size_t)mx * p->world * sizeof(double)));
+  AIRG_CUDA(dmalloc(&p->tr_full, (size_t)(a + 1) * sizeof(double)));
+  AIRG_CUDA(dmalloc(&p->te_full, (size_t)(a + 1) * sizeof(double)));
+  if (tail) AIRG_TRY(prepare_capture(tail, 0));
+  return AIRG_OK;
+}
+
+int airg_dplan_destroy(airg_dplan* p) {
+  if (!p) return AIRG_OK;
+  if (p->graph) cudaGraphExecDestroy(p->graph);
+  if (p->cs) {
+    cudaStreamSynchronize(p->cs);
+    cudaStreamDestroy(p->cs);
+  }
+  if (p->ev_in) cudaEventDestroy(p->ev_in);
+  if (p->ev_out) cudaEventDestroy(p->ev_out);
+  if (p->comm) ncclCommDestroy(p->comm);
+  delete p;  // device buffers come from the pool and are released with the context
+  return AIRG_OK;
+}
+
+// Richardson with the distributed V-cycle (solve.py:113-167); b, x local (x in/out)
+int airg_dplan_richardson(airg_dplan* p, const double* b, double* x, double rtol, double atol,
+                          int max_iters, double* history, int* iterations, int* converged,
+                          void* stream) {
+  cudaStream_t caller = (cudaStream_t)stream;
+  cudaStream_t s = p->cs;
+  const int n = p->top.nrows;
+  AIRG_CUDA(cudaEventRecord(p->ev_in, caller));
+  AIRG_CUDA(cudaStreamWaitEvent(s, p->ev_in, 0));
+  AIRG_CUDA(cudaMemcpyAsync(p->x_ext, x, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  // ||b||
+  {
+    const int nb = blocks_for(n, 256, 1024);
+    sumsq_kernel<<<nb, 256, 0, s>>>(n, b, p->parts);
+    finish_sum_kernel<<<1, 1024, 0, s>>>(nb, p->parts, p->nrm_loc);
+    AIRG_LAUNCH_CHECK();
+    AIRG_NCCL(ncclAllReduce(p->nrm_loc, p->nrm_glob, 1, ncclDouble, ncclSum, p->comm, s));
+    AIRG_CUDA(cudaMemcpyAsync(&p->norm_h, p->nrm_glob, sizeof(double), cudaMemcpyDeviceToHost, s));
+    AIRG_CUDA(cudaStreamSynchronize(s));
+  }
+  const double bnorm = std::sqrt(p->norm_h);
+  AIRG_TRY(dplan_residual(p, b, s));
+  AIRG_CUDA(cudaMemcpyAsync(&p->norm_h, p->nrm_glob, sizeof(double), cudaMemcpyDeviceToHost, s));
+  AIRG_CUDA(cudaStreamSynchronize(s));
+  double rn = std::sqrt(p->norm_h);
+  history[0] = rn;
+  const double thr = std::max(rtol * (bnorm > 0 ? bnorm : rn), atol);
+  *iterations = 0;
+  *converged = 0;
+  int st = AIRG_OK;
+  bool conv = rn <= thr;
+  int its = 0;
+  const bool use_graph = graphs_enabled();
+  if (use_graph && (p->gkey[0] != b || p->gkey[1] != x) && p->graph) {
+    cudaGraphExecDestroy(p->graph);
+    p->graph = nullptr;
+  }
+  auto iteration = [&](cudaStream_t t) -> int {
+    DLev& L0 = p->lv[0];
+    AIRG_CUDA(cudaMemcpyAsync(L0.r_ext, p->r, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, t));
+    AIRG_TRY(dplan_vcycle(p, 0, t));
+    AIRG_TRY(launch_axpby(n, p->x_ext, nullptr, 1.0, p->x_ext, nullptr, 1.0, L0.e, t));
+    return dplan_residual(p, b, t);
+  };
+  while (!conv && its < max_iters) {
+    if (use_graph) {
+      if (!p->graph) {
+        AIRG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+        const int rc = iteration(s);
+        cudaGraph_t g = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(s, &g);
+        if (rc != AIRG_OK) {
+          if (g) cudaGraphDestroy(g);
+          return rc;
+        }
+        AIRG_CUDA(ce);
+        AIRG_CUDA(cudaGraphInstantiate(&p->graph, g, 0));
+        cudaGraphDestroy(g);
+        p->gkey[0] = b;
+        p->gkey[1] = x;
+      }
+      AIRG_CUDA(cudaGraphLaunch(p->graph, s));
+    } else {
+      AIRG_TRY(iteration(s));
+    }
+    AIRG_CUDA(cudaMemcpyAsync(&p->norm_h, p->nrm_glob, sizeof(double), cudaMemcpyDeviceToHost, s));
+    AIRG_CUDA(cudaStreamSynchronize(s));
+    rn = std::sqrt(p->norm_h);
+    ++its;
+    history[its] = rn;
+    *iterations = its;
+    if (!std::isfinite(rn)) {
+      set_error("non-finite residual at iteration %d", its);
+      st = AIRG_ERR_DIVERGED;
+      break;
+    }
+    if (rn > 1e8 * history[0]) {
+      set_error("residual grew by more than 1e+08 at iteration %d", its);
+      st = AIRG_ERR_DIVERGED;
+      break;
+    }
+    conv = rn <= thr;
+  }
+  *converged = conv ? 1 : 0;
+  AIRG_CUDA(cudaMemcpyAsync(x, p->x_ext, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  AIRG_CUDA(cudaEventRecord(p->ev_out, s));
+  AIRG_CUDA(cudaStreamWaitEvent(caller, p->ev_out, 0));
+  return st;
+}
+
+}  // extern "C"

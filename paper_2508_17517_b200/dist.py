@@ -643,6 +643,85 @@ class DistSolver:
     def norm(self, v):
         return float(np.sqrt(self.comm.allreduce(torch.dot(v, v).reshape(1)).item()))
 
+    # ---- native plan: C++ V-cycle with NCCL halos, graph-captured -------------
+    def _native(self):
+        if getattr(self, '_dplan', None) is not None:
+            return self._dplan
+        from .amg_solve import plan_for
+        comm = self.comm
+        uid = torch.zeros(128, dtype=torch.uint8, device=comm.device)
+        if comm.rank == 0:
+            buf = L.C.create_string_buffer(128)
+            L.call('airg_nccl_unique_id', buf)
+            uid.copy_(torch.frombuffer(bytearray(buf.raw), dtype=torch.uint8))
+        dist.broadcast(uid, 0, group=comm.group)
+        idb = bytes(uid.cpu().numpy().tobytes())
+        h = L.C.c_void_p()
+        L.call('airg_dplan_create', idb, comm.rank, comm.world, len(self.lv), L.C.byref(h))
+        keep = []
+
+        def set_halo(level, which, halo):
+            si = halo.send_idx.to(IDX).contiguous()
+            sc = np.ascontiguousarray(halo.send_counts, dtype=np.int32)
+            rc = np.ascontiguousarray(halo.recv_counts, dtype=np.int32)
+            keep.extend([si, sc, rc])
+            L.call('airg_dplan_set_halo', h, level, which, halo.n_loc, si.numel(), L.ptr(si),
+                   L.hptr(sc), L.hptr(rc))
+
+        for l, Lv in enumerate(self.lv):
+            set_halo(l, 0, Lv['hR'])
+            set_halo(l, 1, Lv['hC'])
+            set_halo(l, 2, Lv['hF'])
+            f32, c32 = Lv['f'].to(IDX).contiguous(), Lv['c'].to(IDX).contiguous()
+            coef = np.ascontiguousarray(Lv['coef'])
+            keep.extend([f32, c32, coef])
+            R, Fc, Ff = Lv['R'], Lv['Afc'], Lv['Aff']
+            L.call('airg_dplan_set_level', h, l, Lv['n'], int(f32.numel()), int(c32.numel()),
+                   L.ptr(R.row_offsets), L.ptr(R.col_indices), L.ptr(R.values), R.nnz,
+                   L.ptr(Fc.row_offsets), L.ptr(Fc.col_indices), L.ptr(Fc.values), Fc.nnz,
+                   L.ptr(Ff.row_offsets), L.ptr(Ff.col_indices), L.ptr(Ff.values), Ff.nnz,
+                   L.ptr(f32), L.ptr(c32), len(coef), L.hptr(coef))
+        set_halo(0, 3, self.htop)
+        T = self.Atop
+        L.call('airg_dplan_set_top', h, T.nrows, L.ptr(T.row_offsets), L.ptr(T.col_indices),
+               L.ptr(T.values), T.nnz)
+        tail = plan_for(self.H.tail)
+        p = self.tail_part
+        counts = np.ascontiguousarray(np.diff(p.off), dtype=np.int32)
+        L.call('airg_dplan_finish', h, tail.h, L.hptr(counts))
+        self._keep = keep
+        self._dplan = h
+        return h
+
+    def __del__(self):
+        try:
+            if getattr(self, '_dplan', None) is not None:
+                L.load().airg_dplan_destroy(self._dplan)
+        except Exception:
+            pass
+
+    def solve(self, b, x0, cfg):
+        """Native distributed Richardson (every iteration one captured graph
+        with NCCL halo exchanges); b, x0 local device vectors."""
+        import ctypes as C
+        from .amg_solve import DivergenceError, SolveStats
+        cfg.validate()
+        if cfg.f_smooth_its != 1:
+            raise ValueError('the distributed solve supports f_smooth_its=1')
+        h = self._native()
+        x = x0.clone()
+        hist = np.zeros(cfg.max_iters + 1)
+        its, conv = C.c_int(0), C.c_int(0)
+        st = L.load().airg_dplan_richardson(h, L.ptr(b), L.ptr(x), cfg.rtol, cfg.atol,
+                                            cfg.max_iters, L.hptr(hist), C.byref(its),
+                                            C.byref(conv), L.stream_handle())
+        if st == L.ERR_DIVERGED:
+            raise DivergenceError(L.last_error(), its.value)
+        L.check(st, 'airg_dplan_richardson')
+        return x, SolveStats(iterations=its.value, residual_history=list(hist[:its.value + 1]),
+                             converged=bool(conv.value), cycle_complexity=0.0,
+                             storage_complexity=0.0, flops_per_cycle=0)
+
     def richardson(self, b, x0, cfg):
         """Richardson preconditioned by the distributed V-cycle; b, x0 local."""
         from .amg_solve import DivergenceError, SolveStats

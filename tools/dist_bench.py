@@ -1,0 +1,41 @@
+"""Weak-scaling timing of the distributed setup + solve (torchrun, 1 rank/GPU)."""
+import os, sys, time, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch, torch.distributed as dist
+
+
+def main():
+    nx = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
+    per = int(sys.argv[2]) if len(sys.argv) > 2 else 2048   # grid rows per rank
+    reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+    local = int(os.environ.get('LOCAL_RANK', 0))
+    torch.cuda.set_device(local)
+    dist.init_process_group('nccl', device_id=torch.device('cuda', local))
+    import paper_2508_17517_b200 as G
+    from paper_2508_17517_b200 import dist as D
+    comm = D.Comm()
+    ny = per * comm.world
+    v = (float(np.cos(np.pi / 4)), float(np.sin(np.pi / 4)))
+    G.reserve_memory(nx * per * 1600, nx * per * 4000)
+    Ad = D.advection_2d_strips(comm, nx, ny, *v)
+    n_loc = Ad.M.nrows
+    out = []
+    for rep in range(reps):
+        dist.barrier(); torch.cuda.synchronize(); t0 = time.perf_counter()
+        DH = D.setup_distributed(comm, Ad, G.SetupConfig())
+        torch.cuda.synchronize(); dist.barrier(); t1 = time.perf_counter()
+        S = D.DistSolver(DH)
+        torch.cuda.synchronize(); dist.barrier(); t2 = time.perf_counter()
+        x, st = S.solve(torch.zeros(n_loc, dtype=torch.float64, device='cuda'),
+                             torch.ones(n_loc, dtype=torch.float64, device='cuda'), G.SolveConfig())
+        torch.cuda.synchronize(); dist.barrier(); t3 = time.perf_counter()
+        out.append((t1 - t0, t2 - t1, t3 - t2, st.iterations))
+        del DH, S
+    if comm.rank == 0:
+        print(json.dumps({'world': comm.world, 'grid': [nx, ny], 'dist_levels': None,
+                          'runs': out}), flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == '__main__':
+    main()
