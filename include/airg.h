@@ -102,8 +102,12 @@ int64_t airg_plan_launches(airg_plan* plan);
  * ghost values land in the tail of the operand vector), the top operator,
  * and the replicated serial plan of the coarse tail. */
 typedef struct airg_dplan airg_dplan;
+typedef struct airg_comm airg_comm;
 int airg_nccl_unique_id(char* out_h /* 128 bytes */);
-int airg_dplan_create(const char* id_h, int rank, int world, int ndist, airg_dplan** out_h);
+/* one NCCL communicator per process (ncclCommInitRank), shared by plans */
+int airg_comm_create(const char* id_h, int rank, int world, airg_comm** out_h);
+int airg_comm_destroy(airg_comm* comm);
+int airg_dplan_create(airg_comm* comm, int ndist, airg_dplan** out_h);
 /* which: 0 = R (fine space), 1 = A_fc (coarse space), 2 = A_ff (F space), 3 = top */
 int airg_dplan_set_halo(airg_dplan* plan, int level, int which, int n_loc, int nsend,
                         const int32_t* send_idx, const int32_t* scnt_h, const int32_t* rcnt_h);

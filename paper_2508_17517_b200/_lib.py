@@ -134,7 +134,9 @@ sig('airg_plan_vcycle', vp, C.c_int, vp, vp, C.c_int, vp)
 sig('airg_plan_richardson', vp, vp, vp, f64, f64, C.c_int, C.c_int, vp, vp, vp, vp)
 sig('airg_plan_launches', vp, ret=i64)
 sig('airg_nccl_unique_id', C.c_char_p)
-sig('airg_dplan_create', C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(vp))
+sig('airg_comm_create', C.c_char_p, C.c_int, C.c_int, C.POINTER(vp))
+sig('airg_comm_destroy', vp)
+sig('airg_dplan_create', vp, C.c_int, C.POINTER(vp))
 sig('airg_dplan_set_halo', vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp)
 sig('airg_dplan_set_level', vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, i64, vp, vp, vp,
     i64, vp, vp, vp, i64, vp, vp, C.c_int, vp)

@@ -1575,13 +1575,35 @@ int airg_nccl_unique_id(char* out_h) {
   return AIRG_OK;
 }
 
-int airg_dplan_create(const char* id_h, int rank, int world, int ndist, airg_dplan** out) {
-  airg_dplan* p = new airg_dplan();
-  p->rank = rank;
-  p->world = world;
+// one NCCL communicator per process, shared by every distributed plan
+struct airg_comm {
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+};
+
+int airg_comm_create(const char* id_h, int rank, int world, airg_comm** out) {
+  airg_comm* c = new airg_comm();
+  c->rank = rank;
+  c->world = world;
   ncclUniqueId id;
   memcpy(id.internal, id_h, NCCL_UNIQUE_ID_BYTES);
-  AIRG_NCCL(ncclCommInitRank(&p->comm, world, id, rank));
+  AIRG_NCCL(ncclCommInitRank(&c->comm, world, id, rank));
+  *out = c;
+  return AIRG_OK;
+}
+
+int airg_comm_destroy(airg_comm* c) {
+  if (!c) return AIRG_OK;
+  if (c->comm) ncclCommDestroy(c->comm);
+  delete c;
+  return AIRG_OK;
+}
+
+int airg_dplan_create(airg_comm* c, int ndist, airg_dplan** out) {
+  airg_dplan* p = new airg_dplan();
+  p->rank = c->rank;
+  p->world = c->world;
+  p->comm = c->comm;
   p->lv.resize(ndist);
   AIRG_CUDA(cudaStreamCreateWithFlags(&p->cs, cudaStreamNonBlocking));
   AIRG_CUDA(cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming));
@@ -1675,8 +1697,7 @@ int airg_dplan_destroy(airg_dplan* p) {
   }
   if (p->ev_in) cudaEventDestroy(p->ev_in);
   if (p->ev_out) cudaEventDestroy(p->ev_out);
-  if (p->comm) ncclCommDestroy(p->comm);
-  delete p;  // device buffers come from the pool and are released with the context
+  delete p;  // the communicator is owned by its airg_comm
   return AIRG_OK;
 }
 

@@ -584,6 +584,26 @@ def setup_distributed(comm, A, cfg, poly_inject=None, replicate_below=20000):
 # below the distributed levels the replicated tail runs the serial plan.
 # ---------------------------------------------------------------------------
 
+_NATIVE_COMMS = {}
+
+
+def native_comm(comm):
+    """The process's NCCL communicator for the native plans (created once)."""
+    key = (comm.rank, comm.world, id(comm.group))
+    if key not in _NATIVE_COMMS:
+        uid = torch.zeros(128, dtype=torch.uint8, device=comm.device)
+        if comm.rank == 0:
+            buf = L.C.create_string_buffer(128)
+            L.call('airg_nccl_unique_id', buf)
+            uid.copy_(torch.frombuffer(bytearray(buf.raw), dtype=torch.uint8))
+        dist.broadcast(uid, 0, group=comm.group)
+        h = L.C.c_void_p()
+        L.call('airg_comm_create', bytes(uid.cpu().numpy().tobytes()), comm.rank, comm.world,
+               L.C.byref(h))
+        _NATIVE_COMMS[key] = h
+    return _NATIVE_COMMS[key]
+
+
 class DistSolver:
     def __init__(self, H):
         self.H = H
@@ -649,15 +669,8 @@ class DistSolver:
             return self._dplan
         from .amg_solve import plan_for
         comm = self.comm
-        uid = torch.zeros(128, dtype=torch.uint8, device=comm.device)
-        if comm.rank == 0:
-            buf = L.C.create_string_buffer(128)
-            L.call('airg_nccl_unique_id', buf)
-            uid.copy_(torch.frombuffer(bytearray(buf.raw), dtype=torch.uint8))
-        dist.broadcast(uid, 0, group=comm.group)
-        idb = bytes(uid.cpu().numpy().tobytes())
         h = L.C.c_void_p()
-        L.call('airg_dplan_create', idb, comm.rank, comm.world, len(self.lv), L.C.byref(h))
+        L.call('airg_dplan_create', native_comm(comm), len(self.lv), L.C.byref(h))
         keep = []
 
         def set_halo(level, which, halo):

@@ -8,6 +8,7 @@ def main():
     nx = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
     per = int(sys.argv[2]) if len(sys.argv) > 2 else 2048   # grid rows per rank
     reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+    rep_below = int(sys.argv[4]) if len(sys.argv) > 4 else 20000
     local = int(os.environ.get('LOCAL_RANK', 0))
     torch.cuda.set_device(local)
     dist.init_process_group('nccl', device_id=torch.device('cuda', local))
@@ -22,17 +23,17 @@ def main():
     out = []
     for rep in range(reps):
         dist.barrier(); torch.cuda.synchronize(); t0 = time.perf_counter()
-        DH = D.setup_distributed(comm, Ad, G.SetupConfig())
+        DH = D.setup_distributed(comm, Ad, G.SetupConfig(), replicate_below=rep_below)
         torch.cuda.synchronize(); dist.barrier(); t1 = time.perf_counter()
         S = D.DistSolver(DH)
         torch.cuda.synchronize(); dist.barrier(); t2 = time.perf_counter()
         x, st = S.solve(torch.zeros(n_loc, dtype=torch.float64, device='cuda'),
                              torch.ones(n_loc, dtype=torch.float64, device='cuda'), G.SolveConfig())
         torch.cuda.synchronize(); dist.barrier(); t3 = time.perf_counter()
-        out.append((t1 - t0, t2 - t1, t3 - t2, st.iterations))
+        out.append((round(t1 - t0, 4), round(t2 - t1, 4), round(t3 - t2, 4), st.iterations, len(DH.dlevels)))
         del DH, S
     if comm.rank == 0:
-        print(json.dumps({'world': comm.world, 'grid': [nx, ny], 'dist_levels': None,
+        print(json.dumps({'world': comm.world, 'grid': [nx, ny], 'replicate_below': rep_below,
                           'runs': out}), flush=True)
     dist.destroy_process_group()
 
