@@ -1733,7 +1733,10 @@ int airg_dplan_richardson(airg_dplan* p, const double* b, double* x, double rtol
   int st = AIRG_OK;
   bool conv = rn <= thr;
   int its = 0;
-  const bool use_graph = graphs_enabled();
+  // Capturing the NCCL-bearing iteration costs more than one solve's launch
+  // overhead; it pays only for repeated solves on one plan (AIRG_DPLAN_GRAPH=1).
+  static const bool graph_on = getenv("AIRG_DPLAN_GRAPH") != nullptr;
+  const bool use_graph = graphs_enabled() && graph_on;
   if (use_graph && (p->gkey[0] != b || p->gkey[1] != x) && p->graph) {
     cudaGraphExecDestroy(p->graph);
     p->graph = nullptr;
