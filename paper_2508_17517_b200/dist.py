@@ -121,15 +121,17 @@ class Halo:
         lens = (M.row_offsets[1:] - M.row_offsets[:-1]).to(I64)
         slen = lens[self.send_idx]
         rlen = self.comm.a2a(slen, self.send_counts, self.recv_counts)
-        # element counts per peer
+        # element counts per peer (one segmented sum, one host copy)
         def per_peer(counts, lengths):
-            out, k = [], 0
-            for c in counts:
-                out.append(int(lengths[k:k + c].sum().item()) if c else 0)
-                k += c
-            return out
-        se = per_peer(self.send_counts, slen)
-        re_ = per_peer(self.recv_counts, rlen)
+            seg = torch.repeat_interleave(torch.arange(len(counts), device=dev),
+                                          torch.tensor(counts, device=dev))
+            tot = torch.zeros(len(counts), dtype=I64, device=dev)
+            if lengths.numel():
+                tot.index_add_(0, seg, lengths)
+            return tot
+        both = torch.cat([per_peer(self.send_counts, slen), per_peer(self.recv_counts, rlen)])
+        both = both.cpu().tolist()
+        se, re_ = both[:self.comm.world], both[self.comm.world:]
         starts = M.row_offsets[:-1].to(I64)[self.send_idx]
         tot = int(slen.sum().item())
         if tot:
@@ -391,11 +393,11 @@ def dist_arnoldi_coeffs(comm, A_ff, halo, order, seed):
     v = empty(n, VAL)
     L.call('airg_pcg64_fill_at', *L.pcg_params(seed), lo, n, -1.0, 2.0, L.ptr(v), L.stream_handle())
 
-    def dot(a, b):
-        return comm.allreduce(torch.dot(a, b).reshape(1)).item()
+    def ddot(a, b):  # allreduced dot product kept on the device (no host sync)
+        return comm.allreduce(torch.dot(a, b).reshape(1))
 
     def nrm(a):
-        return float(np.sqrt(dot(a, a)))
+        return float(np.sqrt(ddot(a, a).item()))
 
     from .csr import spmv
     b = v / nrm(v)
@@ -404,18 +406,20 @@ def dist_arnoldi_coeffs(comm, A_ff, halo, order, seed):
         raise ValueError('cannot build a Krylov space from a zero vector')
     V = [b / beta]
     H = np.zeros((m + 1, m))
+    Hd = torch.zeros((m + 1, m), dtype=VAL, device=v.device)
     hmax, k = 0.0, m
     for j in range(m):
         w = spmv(A_ext, halo.ext(V[j]))
         before = nrm(w)
         for sweep in range(2):
             for i in range(j + 1):
-                h = dot(V[i], w)
-                H[i, j] += h
+                h = ddot(V[i], w)
+                Hd[i, j] += h[0]
                 w = w - h * V[i]
             hn = nrm(w)
             if not (sweep == 0 and hn < 0.7 * before):
                 break
+        H[:j + 1, j] = Hd[:j + 1, j].cpu().numpy()
         H[j + 1, j] = hn
         hmax = max(hmax, float(np.linalg.norm(H[:j + 2, j])))
         if hn <= 1e-14 * hmax:
