@@ -9,10 +9,12 @@ configs[1]: 2D upwind advection, 2048 x 2048 (4.19M DOFs), theta = pi/4,
 default AIRG config (order-6 GMRES polynomial smoothers, order-100 Newton
 coarse solver, automatic truncation).
 
-value = DOFs / (setup s + solve s) summed over ranks (each rank owns one
-2048^2 problem -- weak scaling; the domain-decomposed single problem is not
-implemented yet).  Inputs are resident in HBM before the
-timed region; every level operator of the hierarchy (> 1 GB) exceeds L2.
+value = DOFs / (setup s + solve s).  At N>1 the job is ONE global problem of
+2048 x (2048 N) grid points split into N row strips of 2048^2 (weak scaling):
+distributed setup + native distributed Richardson with NCCL halo exchanges
+(paper_2508_17517_b200/dist.py), step time = max over ranks.  Inputs are
+resident in HBM before the timed region; every level operator of the
+hierarchy (> 1 GB per GPU) exceeds L2.
 """
 
 import argparse
@@ -251,11 +253,168 @@ def count_launches(step):
     return n, mine
 
 
+def hbm_peak():
+    try:
+        peaks = json.load(open(os.path.join(ROOT, 'MEASURED_PEAKS.json')))
+        return float(peaks['hbm_gbs']), 'MEASURED_PEAKS.json hbm_gbs'
+    except Exception:
+        return 6650.0, 'fallback (B200_PROFILING.md)'
+
+
+class SerialWorkload:
+    """N=1: the whole 2048^2 problem on one GPU (BASELINE.json configs[1])."""
+
+    def __init__(self, args):
+        import torch
+        import paper_2508_17517_b200 as G
+        self.G, self.args = G, args
+        nx = args.nx
+        self.n = self.n_total = nx * nx
+        self.cfg = G.SetupConfig(poly_order=args.order)
+        self.scfg = G.SolveConfig()
+        self.A, self.b = G.build_advection_2d(G.AdvectionProblem(nx=nx, ny=nx, vx=PI4[0], vy=PI4[1]))
+        self.x0 = torch.ones(self.n, dtype=torch.float64, device='cuda')
+        self.workload = (f'AIRG pi/4 advection {nx}x{nx}, order {args.order}, default SetupConfig '
+                         '(BASELINE.json configs[1])')
+        self.parallelism = 'single GPU'
+
+    def setup(self):
+        return self.G.setup(self.A, self.cfg)
+
+    def solve(self, H):
+        return self.G.richardson_solve(H, self.b, self.x0, self.scfg)
+
+    def roofline(self, H):
+        """One V-cycle (the solve's kernel chain) timed with CUDA events."""
+        import torch
+        from paper_2508_17517_b200 import _lib as L
+        from paper_2508_17517_b200.amg_solve import count_cycle_bytes, plan_for
+        plan = plan_for(H)
+        r = torch.randn(self.n, dtype=torch.float64, device='cuda')
+        e = torch.empty_like(r)
+        for _ in range(3):
+            L.call('airg_plan_vcycle', plan.h, 0, L.ptr(r), L.ptr(e), 1, L.stream_handle())
+        nv = 20
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(nv):
+            L.call('airg_plan_vcycle', plan.h, 0, L.ptr(r), L.ptr(e), 1, L.stream_handle())
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / nv
+        vbytes = count_cycle_bytes(H, include_top=False)
+        return ms, vbytes, ('one V-cycle (R/A_fc/A_ff SpMV chains + Newton coarse solve); '
+                            f'algorithmic bytes {vbytes} (count_cycle_bytes)')
+
+    def e2e(self):
+        """Step through the public API from pinned host buffers."""
+        import torch
+        G, n, A = self.G, self.n, self.A
+        Ap, Ac, Av = (t.cpu().pin_memory() for t in (A.row_offsets, A.col_indices, A.values))
+        bh = torch.zeros(n, dtype=torch.float64).pin_memory()
+        xh = torch.ones(n, dtype=torch.float64).pin_memory()
+        xout = torch.empty(n, dtype=torch.float64).pin_memory()
+        h2d = Ap.numel() * 4 + Ac.numel() * 4 + Av.numel() * 8 + 16 * n
+
+        def step():
+            Ad = G.SparseMatrix(n, n, Ap.to('cuda', non_blocking=True),
+                                Ac.to('cuda', non_blocking=True), Av.to('cuda', non_blocking=True))
+            H = G.setup(Ad, self.cfg)
+            x, _ = G.richardson_solve(H, bh.to('cuda', non_blocking=True),
+                                      xh.to('cuda', non_blocking=True), self.scfg)
+            xout.copy_(x, non_blocking=True)
+        return step, h2d, 8 * n
+
+    def extra(self, H, st):
+        return {'levels': H.num_levels, 'truncated_at': H.truncated_at,
+                'cycle_complexity': H.cycle_complexity,
+                'setup_breakdown_s': {k: round(v, 4) for k, v in H.setup_breakdown.items()}}
+
+
+class DistWorkload:
+    """N>1: ONE global problem of nx x (nx*N) grid points, row strips of
+    nx x nx per GPU; setup_distributed + native distributed
+    Richardson with NCCL halo exchanges over NVLink."""
+
+    def __init__(self, args, world):
+        import torch
+        import paper_2508_17517_b200 as G
+        from paper_2508_17517_b200 import dist as D
+        self.G, self.D, self.args = G, D, args
+        self.comm = D.Comm()
+        nx = args.nx
+        self.cfg = G.SetupConfig(poly_order=args.order)
+        self.scfg = G.SolveConfig()
+        self.Ad = D.advection_2d_strips(self.comm, nx, nx * world, *PI4)
+        self.n = self.Ad.M.nrows
+        self.n_total = self.Ad.rows.n
+        self.b = torch.zeros(self.n, dtype=torch.float64, device='cuda')
+        self.x0 = torch.ones(self.n, dtype=torch.float64, device='cuda')
+        self.workload = (f'AIRG pi/4 advection {nx}x{nx * world} global grid ({world} row strips '
+                         f'of {nx}x{nx}), order {args.order}, default SetupConfig')
+        self.parallelism = (f'row-strip domain decomposition over {world} GPUs, NCCL halo '
+                            'exchanges; replicated coarse tail')
+
+    def setup(self):
+        return self.D.setup_distributed(self.comm, self.Ad, self.cfg)
+
+    def solve(self, DH):
+        S = self.D.DistSolver(DH)
+        x, st = S.solve(self.b, self.x0, self.scfg)
+        self.S = S
+        return x, st
+
+    def roofline(self, DH):
+        """Per-iteration time of the native distributed Richardson (V-cycle +
+        residual, halo exchanges included), CUDA events on this rank."""
+        import torch
+        S = self.S
+        S.solve(self.b, self.x0, self.scfg)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        reps = 5
+        for _ in range(reps):
+            _, st = S.solve(self.b, self.x0, self.scfg)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps / max(st.iterations, 1)
+        by = self.D.dist_cycle_bytes(S, include_top=True)
+        return ms, by, ('one distributed Richardson iteration per rank (V-cycle over local strips '
+                        '+ replicated tail + top residual, NCCL halos inside); algorithmic bytes '
+                        f'{by} per rank (dist_cycle_bytes)')
+
+    def e2e(self):
+        import torch
+        G, D, M = self.G, self.D, self.Ad.M
+        Ap, Ac, Av = (t.cpu().pin_memory() for t in (M.row_offsets, M.col_indices, M.values))
+        n = self.n
+        bh = torch.zeros(n, dtype=torch.float64).pin_memory()
+        xh = torch.ones(n, dtype=torch.float64).pin_memory()
+        xout = torch.empty(n, dtype=torch.float64).pin_memory()
+        h2d = Ap.numel() * 4 + Ac.numel() * 4 + Av.numel() * 8 + 16 * n
+
+        def step():
+            Mh = G.SparseMatrix(n, M.ncols, Ap.to('cuda', non_blocking=True),
+                                Ac.to('cuda', non_blocking=True), Av.to('cuda', non_blocking=True))
+            Ad = D.DMat(Mh, self.Ad.rows, self.Ad.cols)
+            DH = D.setup_distributed(self.comm, Ad, self.cfg)
+            x, _ = D.DistSolver(DH).solve(bh.to('cuda', non_blocking=True),
+                                          xh.to('cuda', non_blocking=True), self.scfg)
+            xout.copy_(x, non_blocking=True)
+        return step, h2d, 8 * n
+
+    def extra(self, DH, st):
+        return {'levels': DH.num_levels, 'distributed_levels': len(DH.dlevels),
+                'truncated_at': DH.truncated_at,
+                'setup_breakdown_s': {k: round(v, 4) for k, v in DH.setup_breakdown.items()
+                                      if '.' not in k and '@' not in k}}
+
+
 def ours_arm(args, rank, world, local):
     import torch
     import paper_2508_17517_b200 as G
-    from paper_2508_17517_b200.amg_solve import count_cycle_bytes, plan_for
-    from paper_2508_17517_b200 import _lib as L
 
     torch.cuda.set_device(local)
     dist = None
@@ -268,23 +427,19 @@ def ours_arm(args, rank, world, local):
             dist.barrier()
         torch.cuda.synchronize()
 
-    nx = args.nx
-    n = nx * nx
-    cfg = G.SetupConfig(poly_order=args.order)
-    scfg = G.SolveConfig()
-    A, b = G.build_advection_2d(G.AdvectionProblem(nx=nx, ny=nx, vx=PI4[0], vy=PI4[1]))
-    x0 = torch.ones(n, dtype=torch.float64, device='cuda')
-    # grow both device pools once before warm-up (scaled to the problem; 2048^2
-    # peaks at ~4 GB library scratch and ~9 GB of torch-owned hierarchy)
+    W = DistWorkload(args, world) if world > 1 else SerialWorkload(args)
+    n = W.n
+    # grow both device pools once before warm-up (scaled to the per-GPU problem;
+    # 2048^2 peaks at ~4 GB library scratch and ~9 GB of torch-owned hierarchy)
     G.reserve_memory(library_bytes=n * 1600, torch_bytes=n * 4000)
     info = {}
 
     def step():
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record()
-        H = G.setup(A, cfg)
+        H = W.setup()
         ev[1].record()
-        x, st = G.richardson_solve(H, b, x0, scfg)
+        x, st = W.solve(H)
         ev[2].record()
         info['H'], info['st'], info['ev'] = H, st, ev
         return H
@@ -310,46 +465,13 @@ def ours_arm(args, rank, world, local):
     ms = max_over_ranks(ms, dist, 'cuda')
     H, st = info['H'], info['st']
 
-    # ---- roofline: one V-cycle (the solve's kernel chain), CUDA events ----
-    plan = plan_for(H)
-    r = torch.randn(n, dtype=torch.float64, device='cuda')
-    e = torch.empty_like(r)
-    for _ in range(3):
-        L.call('airg_plan_vcycle', plan.h, 0, L.ptr(r), L.ptr(e), 1, L.stream_handle())
-    nv = 20
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record()
-    for _ in range(nv):
-        L.call('airg_plan_vcycle', plan.h, 0, L.ptr(r), L.ptr(e), 1, L.stream_handle())
-    e1.record()
-    torch.cuda.synchronize()
-    vms = e0.elapsed_time(e1) / nv
-    vbytes = count_cycle_bytes(H, include_top=False)
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, 'MEASURED_PEAKS.json')))
-    except Exception:
-        pass
-    peak = float(peaks.get('hbm_gbs', 6650.0))
+    # ---- roofline of the solve's kernel chain ----
+    vms, vbytes, what = W.roofline(H)
+    peak, peak_src = hbm_peak()
     achieved = vbytes / (vms * 1e-3) / 1e9
 
     # ---- e2e through the public API with pinned host buffers ----
-    Ap, Ac, Av = (t.cpu().pin_memory() for t in (A.row_offsets, A.col_indices, A.values))
-    bh = torch.zeros(n, dtype=torch.float64).pin_memory()
-    xh = torch.ones(n, dtype=torch.float64).pin_memory()
-    xout = torch.empty(n, dtype=torch.float64).pin_memory()
-    h2d = (Ap.numel() * 4 + Ac.numel() * 4 + Av.numel() * 8 + 16 * n)
-    d2h = 8 * n
-
-    def e2e_step():
-        Ad = G.SparseMatrix(n, n, Ap.to('cuda', non_blocking=True), Ac.to('cuda', non_blocking=True),
-                            Av.to('cuda', non_blocking=True))
-        Hh = G.setup(Ad, cfg)
-        x, _ = G.richardson_solve(Hh, bh.to('cuda', non_blocking=True),
-                                  xh.to('cuda', non_blocking=True), scfg)
-        xout.copy_(x, non_blocking=True)
-
+    e2e_step, h2d, d2h = W.e2e()
     e2e_step()
     k_e2e = max(1, min(args.steps, 3))
     barrier()
@@ -369,33 +491,28 @@ def ours_arm(args, rank, world, local):
         a, bs, its = cpu_run(args.cpu_nx, args.order)
         ncpu, blas = cpu_cores_note()
         cpu = {'value': args.cpu_nx ** 2 / (a + bs), 'unit': 'DOF/s', 'cores': 1, 'kind': 'port',
-               'sample': f'one setup + timed second solve at {args.cpu_nx}^2 (of the {nx}^2 '
+               'sample': f'one setup + timed second solve at {args.cpu_nx}^2 (of the {args.nx}^2 '
                          f'workload) with oracle/airg_oracle.py (numpy/scipy restatement of airmg; '
                          f'scipy sparse kernels single-threaded; BLAS {blas}; {ncpu} host cpus); '
                          f'setup {a:.2f} s, solve {bs:.3f} s, {its} its'}
 
     if rank == 0:
         line = {
-            'metric': METRIC, 'value': world * n / (ms * 1e-3), 'unit': 'DOF/s', 'n_gpus': world,
+            'metric': METRIC, 'value': W.n_total / (ms * 1e-3), 'unit': 'DOF/s', 'n_gpus': world,
             'steps': args.steps, 'warmup': args.warmup, 'ms_per_step': ms,
             'higher_is_better': True, 'scaling': 'weak', 'vs_baseline': None, 'dtype': 'f64',
             'data': 'synthetic (2D upwind advection stencil generated on device, b=0, x0=1)',
-            'config': {'workload': f'AIRG pi/4 advection {nx}x{nx} per GPU, order {args.order}, '
-                                   'default SetupConfig (BASELINE.json configs[1])',
-                       'dofs_per_gpu': n, 'rtol': 1e-10,
-                       'parallelism': f'{world} independent per-rank problems (weak scaling)',
-                       'l2': 'hierarchy operators (>1 GB) exceed the 126 MB L2'},
+            'config': {'workload': W.workload, 'dofs_total': W.n_total, 'dofs_per_gpu': n,
+                       'rtol': 1e-10, 'parallelism': W.parallelism,
+                       'l2': 'hierarchy operators (>1 GB per GPU) exceed the 126 MB L2'},
             'setup_s': float(np.mean(setup_ms)) / 1e3, 'solve_s': float(np.mean(solve_ms)) / 1e3,
-            'iterations': st.iterations, 'levels': H.num_levels,
-            'truncated_at': H.truncated_at, 'cycle_complexity': H.cycle_complexity,
-            'setup_breakdown_s': {k: round(v, 4) for k, v in H.setup_breakdown.items()},
+            'iterations': st.iterations,
+            **W.extra(H, st),
             'vcycle_ms': vms,
             'roofline': {'bound': 'hbm', 'achieved': achieved, 'peak': peak, 'unit': 'GB/s',
-                         'frac': achieved / peak, 'traffic': None,
-                         'kernel': 'one V-cycle (R/A_fc/A_ff SpMV chains + Newton coarse solve); '
-                                   f'algorithmic bytes {vbytes} (count_cycle_bytes)',
-                         'peak_source': 'MEASURED_PEAKS.json hbm_gbs' if peaks else 'fallback'},
-            'e2e': {'value': world * n / (e2e_ms * 1e-3), 'unit': 'DOF/s',
+                         'frac': achieved / peak, 'traffic': None, 'kernel': what,
+                         'peak_source': peak_src},
+            'e2e': {'value': W.n_total / (e2e_ms * 1e-3), 'unit': 'DOF/s',
                     'h2d_bytes_per_step': int(h2d), 'd2h_bytes_per_step': int(d2h),
                     'ms_per_step': e2e_ms},
             'gpu_launches': int(mine * args.steps),

@@ -222,6 +222,7 @@ class DHierarchy:
     polys: dict = field(default_factory=dict)
     truncated_at: int = None
     config: object = None
+    setup_breakdown: dict = None
 
     @property
     def num_levels(self):
@@ -446,11 +447,40 @@ def _spgemm(A, B, ncols, negate=False, mode=0, tol=0.0, lump=False, row0=0):
 # distributed setup
 # ---------------------------------------------------------------------------
 
-def setup_distributed(comm, A, cfg, poly_inject=None, replicate_below=20000):
+class _Ticker:
+    """Phase timer for the distributed setup: each call charges the time
+    since the previous call (device synchronised) to the named phase."""
+
+    def __init__(self, sink):
+        import os
+        import time
+        self.sink, self.clock = sink, time.perf_counter
+        self.per_level = bool(os.environ.get('AIRG_DIST_LEVEL_TIMES'))
+        self.level = 0
+        torch.cuda.synchronize()
+        self.t = self.clock()
+
+    def __call__(self, phase):
+        torch.cuda.synchronize()
+        t = self.clock()
+        if phase is not None:
+            self.sink[phase] = self.sink.get(phase, 0.0) + t - self.t
+            if self.per_level:
+                key = f'{phase}@{self.level}'
+                self.sink[key] = self.sink.get(key, 0.0) + t - self.t
+        self.t = t
+
+    def note(self, key, value):
+        if self.per_level:
+            self.sink[f'{key}@{self.level}'] = value
+
+
+def setup_distributed(comm, A, cfg, poly_inject=None, replicate_below=20000, force=False):
     """AIRG setup (hierarchy.py:365-448) on a row-partitioned matrix.  Levels
     with more than ``replicate_below`` rows (and below the truncation start)
     are built distributed; the rest is built on every rank from the gathered
-    level matrix with the serial code."""
+    level matrix with the serial code.  ``force`` runs the distributed levels
+    even on a single rank (overhead measurements)."""
     from .amg_setup import (SETUP_PHASES, SEED_SMOOTHER, SEED_SPLIT, build_levels, derive_seed,
                             resolve_truncate_start, finalize_complexities, Hierarchy)
     cfg.validate()
@@ -461,10 +491,11 @@ def setup_distributed(comm, A, cfg, poly_inject=None, replicate_below=20000):
     timings = {p: 0.0 for p in SETUP_PHASES}
     r = comm.rank
     truncate_start = resolve_truncate_start(cfg, A.rows.n)
+    tick = _Ticker(timings)
     dlevels = []
     level = 0
     cur = A
-    while (cur.rows.n > replicate_below and comm.world > 1 and level < cfg.max_levels
+    while (cur.rows.n > replicate_below and (comm.world > 1 or force) and level < cfg.max_levels
            and cur.rows.n > cfg.min_coarse_size
            and not (cfg.auto_truncate_tol is not None and level >= truncate_start)):
         n, lo = cur.M.nrows, cur.rows.lo(r)
@@ -482,6 +513,7 @@ def setup_distributed(comm, A, cfg, poly_inject=None, replicate_below=20000):
             stats.append(ddc_pass(comm, A_ext, lab_ext, n, lo, cfg.ddc_fraction, cfg.ddc_bins))
             lab_ext[n:] = halo_a.values(lab_ext[:n])
         nc_glob = comm.sum_int(int((lab_ext[:n] == 1).sum().item()))
+        tick('cf_split')
         if nc_glob == cur.rows.n:
             raise ValueError(f'splitting produced no F points at level {level}')
         if nc_glob > 0:
@@ -509,6 +541,7 @@ def setup_distributed(comm, A, cfg, poly_inject=None, replicate_below=20000):
         A_ff = extract_mapped(A_ext, f_loc, fmap, fpart.n)
         A_fc = extract_mapped(A_ext, f_loc, cmap, cpart.n)
         A_cf = extract_mapped(A_ext, c_loc, fmap, fpart.n)
+        tick('extract')
         # ---- smoother ----
         halo_ff = Halo(comm, fpart, remote_cols(A_ff.col_indices, fpart, r))
         sm = inj.get(('smoother', level))
@@ -532,11 +565,15 @@ def setup_distributed(comm, A, cfg, poly_inject=None, replicate_below=20000):
                L.stream_handle())
         Ahat = take(res)
         Ahat = SparseMatrix(Ahat.nrows, fpart.n, Ahat.row_offsets, Ahat.col_indices, Ahat.values)
+        tick('polynomial')
         # ---- Z = -A_cf Ahat ----
         halo_z = Halo(comm, fpart, remote_cols(A_cf.col_indices, fpart, r))
+        tick('spgemm_R.halo')
         Ahat_rows = cat_rows(Ahat, *halo_z.rows(Ahat), fpart.n)
+        tick('spgemm_R.rows')
         Z = _spgemm(with_cols(A_cf, halo_z.ext_cols(A_cf.col_indices), Ahat_rows.nrows), Ahat_rows,
                     fpart.n, negate=True)
+        tick('spgemm_R.Z')
         # ---- R = [Z I] in the fine numbering ----
         halo_zc = Halo(comm, fpart, remote_cols(Z.col_indices, fpart, r))
         fine_of_f = (lo + f_loc.long()).to(IDX)
@@ -547,6 +584,7 @@ def setup_distributed(comm, A, cfg, poly_inject=None, replicate_below=20000):
                L.ptr(Zx.values), L.ptr(f_ext), L.ptr((lo + c_loc.long()).to(IDX)), L.C.byref(res),
                L.stream_handle())
         R = take(res)
+        tick('spgemm_R')
         # ---- one-point P, A P, R (A P) with drop/lump ----
         pcol = empty(n, IDX)
         L.call('airg_prolong_onepoint', n, L.ptr(A_ext.row_offsets), L.ptr(A_ext.col_indices),
@@ -556,31 +594,43 @@ def setup_distributed(comm, A, cfg, poly_inject=None, replicate_below=20000):
                              torch.arange(pcol_ext.numel() + 1, device=dev, dtype=IDX), pcol_ext,
                              torch.ones(pcol_ext.numel(), dtype=VAL, device=dev))
         AP = _spgemm(A_ext, P_ext, cpart.n)
+        tick('prolongator')
         halo_r = Halo(comm, cur.rows, remote_cols(R.col_indices, cur.rows, r))
+        tick('spgemm_coarse.halo')
         AP_rows = cat_rows(AP, *halo_r.rows(AP), cpart.n)
+        tick('spgemm_coarse.rows')
         Rx = with_cols(R, halo_r.ext_cols(R.col_indices), AP_rows.nrows)
         if cfg.a_drop > 0:
             Ac = _spgemm(Rx, AP_rows, cpart.n, mode=1, tol=cfg.a_drop, lump=cfg.lump, row0=cpos0)
         else:
             Ac = _spgemm(Rx, AP_rows, cpart.n)
+        tick('spgemm_coarse.RAP')
+        tick.note('nnz_R', R.nnz)
+        tick.note('nnz_AP', AP_rows.nnz)
+        tick.note('nnz_Ac', Ac.nnz)
+        tick.note('n', n)
         dlevels.append(DLevel(R=R, A_ff=A_ff, A_fc=A_fc, f_loc=f_loc, c_loc=c_loc, labels=labels,
                               fine=cur.rows, fpart=fpart, cpart=cpart, f_smoother=sm,
                               n=cur.rows.n, n_f=fpart.n, n_c=cpart.n,
                               nnz_A=comm.sum_int(cur.M.nnz), nnz_R=comm.sum_int(R.nnz),
                               nnz_Aff=comm.sum_int(A_ff.nnz), nnz_Afc=comm.sum_int(A_fc.nnz),
                               ddc_stats=tuple(stats), pcol=pcol))
+        tick('spgemm_coarse')
         cur = DMat(Ac, cpart, cpart)
         level += 1
+        tick.level = level
     # ---- replicated tail ----
     full = gather_dmat(comm, cur)
+    tick('gather_tail')
     levels, coarsest, solver, trunc = build_levels(full, cfg, level, truncate_start, inj, polys,
                                                    timings)
     tail = Hierarchy(levels=levels, coarsest_A=coarsest, coarse_solver=solver, top_A=full,
                      truncated_at=trunc, config=cfg, setup_breakdown=timings)
     tail.polys = polys
     finalize_complexities(tail)
+    tick(None)
     return DHierarchy(dlevels=dlevels, tail=tail, tail_level=level, top=A, comm=comm, polys=polys,
-                      truncated_at=trunc, config=cfg)
+                      truncated_at=trunc, config=cfg, setup_breakdown=timings)
 
 
 # ---------------------------------------------------------------------------
@@ -764,3 +814,24 @@ class DistSolver:
             conv = rn <= thr
         return x, SolveStats(iterations=its, residual_history=hist, converged=conv,
                              cycle_complexity=0.0, storage_complexity=0.0, flops_per_cycle=0)
+
+
+def dist_cycle_bytes(S, include_top=True):
+    """Algorithmic HBM bytes one rank moves per distributed Richardson
+    iteration (same accounting as amg_solve.count_cycle_bytes): its local rows
+    of every distributed level, the whole replicated tail, and the top
+    residual on its strip.  Halo payloads are not HBM traffic of the
+    kernels' operands and are left out."""
+    from .amg_solve import _spmat_bytes, count_cycle_bytes
+    tot = 0
+    for Lv in S.lv:
+        nf, nc, n = int(Lv['f'].numel()), int(Lv['c'].numel()), Lv['n']
+        d = len(Lv['coef']) - 1
+        tot += _spmat_bytes(Lv['R']) + 8 * n + 8 * nc
+        tot += _spmat_bytes(Lv['Afc']) + 8 * nc + 16 * nf
+        tot += 16 * nf + d * (_spmat_bytes(Lv['Aff']) + 24 * nf)
+        tot += 16 * n
+    tot += count_cycle_bytes(S.H.tail, include_top=False)
+    if include_top:
+        tot += _spmat_bytes(S.Atop) + 40 * S.Atop.nrows
+    return int(tot)
