@@ -180,6 +180,9 @@ struct PolyArgs {
   // of Ap (local rows first, then fetched ghost rows); null = identity
   int row0;
   const int* rowmap;
+  // rows handled by this launch (one length class); null = all n rows
+  const int* rows;
+  int nrows;
 };
 
 __global__ void __launch_bounds__(128) poly_assemble_kernel(PolyArgs a) {
@@ -198,8 +201,8 @@ __global__ void __launch_bounds__(128) poly_assemble_kernel(PolyArgs a) {
   unsigned char* fcur = (unsigned char*)(pv + T);
   unsigned char* fnxt = fcur + cap;
   unsigned char* facc = fnxt + cap;
-  for (long long r = (long long)blockIdx.x * nw + w; r < a.n; r += (long long)gridDim.x * nw) {
-    const int row = (int)r;
+  for (long long r = (long long)blockIdx.x * nw + w; r < a.nrows; r += (long long)gridDim.x * nw) {
+    const int row = a.rows ? a.rows[r] : (int)r;
     const int pb = a.Pp[row], pe = a.Pp[row + 1], m = pe - pb;
     if (m > cap) continue;  // handled by the global pass (flag via out_cnt = -1)
     for (int i = lane; i < T; i += 32) keys[i] = kEmpty;
@@ -375,25 +378,55 @@ static int max_row_len(int m, const int* p, int* out, cudaStream_t s) {
   return AIRG_OK;
 }
 
+// Rows are classified by pattern length (caps 32, 64, ..., next pow2 >= the
+// longest row) and each class runs with its own shared-memory footprint
+// (43 B x cap per warp), so a few long rows no longer cut the occupancy of
+// every row of the level.
 static int run_poly_kernel(PolyArgs& a, int maxlen, cudaStream_t s) {
-  int cap = 32;
-  while (cap < maxlen) cap <<= 1;
-  a.cap = cap;
-  a.bits = ceil_log2(2ll * cap);
-  const size_t T = (size_t)1 << a.bits;
-  const size_t per = (T * 8 + (size_t)cap * 27 + 15) & ~(size_t)15;
-  int warps = 4;
-  while (warps > 1 && per * warps > (size_t)smem_limit()) warps >>= 1;
-  if (per > (size_t)smem_limit()) {
+  int capmax = 32;
+  while (capmax < maxlen) capmax <<= 1;
+  auto per_warp = [](int cap) {
+    const size_t T = (size_t)1 << ceil_log2(2ll * cap);
+    return (T * 8 + (size_t)cap * 27 + 15) & ~(size_t)15;
+  };
+  if (per_warp(capmax) > (size_t)smem_limit()) {
     set_error("pattern row of %d entries exceeds the shared-memory assembly kernel", maxlen);
     return AIRG_ERR_VALUE;
   }
-  const size_t shm = per * warps;
-  if (shm > 48 * 1024)
+  static bool attr = false;
+  if (!attr) {
     AIRG_CUDA(cudaFuncSetAttribute(poly_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)shm));
-  poly_assemble_kernel<<<blocks_for(a.n, warps, 148 * 32), warps * 32, shm, s>>>(a);
+                                   smem_limit()));
+    attr = true;
+  }
+  std::vector<long long> th;
+  for (long long c = 32; c < capmax; c <<= 1) th.push_back(c);
+  long long* len = nullptr;
+  AIRG_TRY(scratch(&len, a.n > 0 ? a.n : 1, s));
+  if (a.n > 0) rowlen_kernel<<<blocks_for(a.n, 256), 256, 0, s>>>(a.n, a.Pp, len);
   AIRG_LAUNCH_CHECK();
+  Classes cl;
+  AIRG_TRY(classify(a.n, len, th, cl, s));
+  Fork fk;
+  AIRG_TRY(fk.begin(s));
+  for (int c = 0; c < (int)cl.count.size(); ++c) {
+    const int nr = cl.count[c];
+    if (!nr) continue;
+    PolyArgs b = a;
+    b.cap = 32 << c;
+    b.bits = ceil_log2(2ll * b.cap);
+    b.rows = cl.list(c);
+    b.nrows = nr;
+    const size_t per = per_warp(b.cap);
+    int warps = 4;
+    while (warps > 1 && per * warps > (size_t)smem_limit()) warps >>= 1;
+    poly_assemble_kernel<<<blocks_for(nr, warps, 148 * 32), warps * 32, per * warps,
+                           fk.stream(c)>>>(b);
+    AIRG_LAUNCH_CHECK();
+  }
+  AIRG_TRY(fk.end(s));
+  release(len, s);
+  release(cl.lists, s);
   return AIRG_OK;
 }
 

@@ -13,6 +13,7 @@
 // before the current one is processed.
 #pragma once
 #include "setup_common.cuh"
+#include <vector>
 
 namespace airg {
 
@@ -296,7 +297,7 @@ __device__ __forceinline__ int compact_slots(int* keys, V* pay, int T, int lane)
 // keep = diagonal | |v| >= tol*max|v|; dropped values summed sequentially in
 // column order onto the diagonal (inserted when absent and the sum != 0).
 // Writes kept entries to out_col/out_val[o...]; returns the written count.
-__device__ static int drop_lump_row(const int* col, const double* val, int n, int row, double tol, int lump,
+__device__ static int drop_lump_row(const int* col, double* val, int n, int row, double tol, int lump,
                              int* __restrict__ out_col, double* __restrict__ out_val, long long o,
                              int lane, int* any_drop) {
   double mx = 0.0;
@@ -308,20 +309,27 @@ __device__ static int drop_lump_row(const int* col, const double* val, int n, in
   mx = warp_max(mx);
   dpos = __reduce_max_sync(kFull, dpos);
   const double thr = mul_rn(tol, mx);
-  double lumped = 0.0;
+  // dropped values, in column order, are packed into val[n ..) (callers'
+  // tables hold >= 2n slots) and summed one by one by lane 0: the serial
+  // chain is one add per dropped entry with its loads pipelined
+  double* dropped = val + n;
   int ndrop = 0;
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    const double x = i < n ? val[i] : 0.0;
+    const bool d = i < n && i != dpos && !(fabs(x) >= thr);
+    const unsigned bal = __ballot_sync(kFull, d);
+    if (d) dropped[ndrop + __popc(bal & ((1u << lane) - 1u))] = x;
+    ndrop += __popc(bal);
+  }
+  __syncwarp();
+  double lumped = 0.0;
   if (lane == 0) {
-    for (int i = 0; i < n; ++i) {
-      const double x = val[i];
-      if (i != dpos && !(fabs(x) >= thr)) {
-        lumped = add_rn(lumped, x);
-        ++ndrop;
-      }
-    }
+#pragma unroll 8
+    for (int i = 0; i < ndrop; ++i) lumped = add_rn(lumped, dropped[i]);
     if (ndrop && any_drop) atomicOr(any_drop, 1);
   }
   lumped = __shfl_sync(kFull, lumped, 0);
-  ndrop = __shfl_sync(kFull, ndrop, 0);
   const bool insert = lump && ndrop > 0 && dpos < 0 && lumped != 0.0;
   int written = 0, before = 0;
   for (int base = 0; base < n; base += 32) {
@@ -353,6 +361,63 @@ __device__ static int drop_lump_row(const int* col, const double* val, int n, in
     ++written;
   }
   return written;
+}
+
+// ---- row classification by size (shared by the SpGEMM and assembly kernels) ----
+static __global__ void rowlen_kernel(int m, const int* __restrict__ ptr, long long* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = ptr[i + 1] - ptr[i];
+}
+
+constexpr int kMaxCls = 8;
+
+// block-aggregated append of row ids to per-class lists (lists[c*m + ...])
+static __global__ void classify_kernel(int m, const long long* __restrict__ size, const long long* __restrict__ th,
+                                int ncls, int* __restrict__ lists, int* __restrict__ counts) {
+  __shared__ int scnt[kMaxCls], sbase[kMaxCls];
+  if (threadIdx.x < ncls) scnt[threadIdx.x] = 0;
+  __syncthreads();
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  int c = 0, slot = 0;
+  if (i < m) {
+    const long long v = size[i];
+    while (c < ncls - 1 && v > th[c]) ++c;
+    slot = atomicAdd(scnt + c, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < ncls) sbase[threadIdx.x] = atomicAdd(counts + threadIdx.x, scnt[threadIdx.x]);
+  __syncthreads();
+  if (i < m) lists[(long long)c * m + sbase[c] + slot] = (int)i;
+}
+
+struct Classes {
+  std::vector<int> count;
+  int* lists = nullptr;
+  int m = 0;
+  const int* list(int c) const { return lists + (long long)c * m; }
+};
+
+static int classify(int m, const long long* size, const std::vector<long long>& th, Classes& out,
+                    cudaStream_t s) {
+  const int ncls = (int)th.size() + 1;
+  long long* dth = nullptr;
+  int* cnt = nullptr;
+  AIRG_TRY(scratch(&out.lists, (size_t)ncls * (m > 0 ? m : 1), s));
+  AIRG_TRY(scratch(&dth, th.size() + 1, s));
+  AIRG_TRY(scratch(&cnt, ncls, s));
+  if (!th.empty())
+    AIRG_CUDA(cudaMemcpyAsync(dth, th.data(), th.size() * sizeof(long long), cudaMemcpyHostToDevice, s));
+  AIRG_CUDA(cudaMemsetAsync(cnt, 0, ncls * sizeof(int), s));
+  if (m > 0) classify_kernel<<<(m + 255) / 256, 256, 0, s>>>(m, size, dth, ncls, out.lists, cnt);
+  AIRG_LAUNCH_CHECK();
+  out.count.assign(ncls, 0);
+  AIRG_CUDA(cudaMemcpyAsync(out.count.data(), cnt, ncls * sizeof(int), cudaMemcpyDeviceToHost, s));
+  AIRG_CUDA(cudaStreamSynchronize(s));
+  out.m = m;
+  release(dth, s);
+  release(cnt, s);
+  return AIRG_OK;
 }
 
 }  // namespace airg

@@ -21,62 +21,6 @@ __global__ void product_ub_kernel(int m, const int* __restrict__ Ap, const int* 
   }
 }
 
-__global__ void rowlen_kernel(int m, const int* __restrict__ ptr, long long* __restrict__ out) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
-       i += (long long)gridDim.x * blockDim.x)
-    out[i] = ptr[i + 1] - ptr[i];
-}
-
-constexpr int kMaxCls = 8;
-
-// block-aggregated append of row ids to per-class lists (lists[c*m + ...])
-__global__ void classify_kernel(int m, const long long* __restrict__ size, const long long* __restrict__ th,
-                                int ncls, int* __restrict__ lists, int* __restrict__ counts) {
-  __shared__ int scnt[kMaxCls], sbase[kMaxCls];
-  if (threadIdx.x < ncls) scnt[threadIdx.x] = 0;
-  __syncthreads();
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  int c = 0, slot = 0;
-  if (i < m) {
-    const long long v = size[i];
-    while (c < ncls - 1 && v > th[c]) ++c;
-    slot = atomicAdd(scnt + c, 1);
-  }
-  __syncthreads();
-  if (threadIdx.x < ncls) sbase[threadIdx.x] = atomicAdd(counts + threadIdx.x, scnt[threadIdx.x]);
-  __syncthreads();
-  if (i < m) lists[(long long)c * m + sbase[c] + slot] = (int)i;
-}
-
-struct Classes {
-  std::vector<int> count;
-  int* lists = nullptr;
-  int m = 0;
-  const int* list(int c) const { return lists + (long long)c * m; }
-};
-
-static int classify(int m, const long long* size, const std::vector<long long>& th, Classes& out,
-                    cudaStream_t s) {
-  const int ncls = (int)th.size() + 1;
-  long long* dth = nullptr;
-  int* cnt = nullptr;
-  AIRG_TRY(scratch(&out.lists, (size_t)ncls * (m > 0 ? m : 1), s));
-  AIRG_TRY(scratch(&dth, th.size() + 1, s));
-  AIRG_TRY(scratch(&cnt, ncls, s));
-  if (!th.empty())
-    AIRG_CUDA(cudaMemcpyAsync(dth, th.data(), th.size() * sizeof(long long), cudaMemcpyHostToDevice, s));
-  AIRG_CUDA(cudaMemsetAsync(cnt, 0, ncls * sizeof(int), s));
-  if (m > 0) classify_kernel<<<(m + 255) / 256, 256, 0, s>>>(m, size, dth, ncls, out.lists, cnt);
-  AIRG_LAUNCH_CHECK();
-  out.count.assign(ncls, 0);
-  AIRG_CUDA(cudaMemcpyAsync(out.count.data(), cnt, ncls * sizeof(int), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
-  out.m = m;
-  release(dth, s);
-  release(cnt, s);
-  return AIRG_OK;
-}
-
 // ---- pass 1: structural count -------------------------------------------------
 struct CountArgs {
   const int *Ap, *Ac, *Bp, *Bc;
@@ -101,7 +45,7 @@ struct CountCheckOp {
 
 // Long rows (product upper bound > 512): one CTA per row sharing one
 // shared-memory key set.  Counting has no ordering constraint, so warps take
-// different A entries concurrently (warp w: entries w, w+nw, ...).
+// different chunks of A entries concurrently.
 __global__ void __launch_bounds__(128) spgemm_count_block_kernel(CountArgs a) {
   extern __shared__ int keys[];
   __shared__ int total, ovf;
@@ -116,20 +60,39 @@ __global__ void __launch_bounds__(128) spgemm_count_block_kernel(CountArgs a) {
     }
     __syncthreads();
     const int ab = a.Ap[row], ae = a.Ap[row + 1];
-    for (int kk = ab + w; kk < ae; kk += nw) {
-      const int k = a.Ac[kk];
-      const int bb = a.Bp[k], be = a.Bp[k + 1];
+    // warp w takes chunks of 32 A entries (w, w + nw, ...): the B-row bounds of
+    // a chunk are loaded lane-parallel, the next B row's first 32 columns are
+    // prefetched while the current row is inserted
+    for (int base = ab + 32 * w; base < ae; base += 32 * nw) {
+      int bb = 0, be = 0;
+      if (base + lane < ae) {
+        const int k = a.Ac[base + lane];
+        bb = a.Bp[k];
+        be = a.Bp[k + 1];
+      }
+      const int cnt = min(32, ae - base);
+      int cb = __shfl_sync(kFull, bb, 0), ce = __shfl_sync(kFull, be, 0);
+      int pc = cb + lane < ce ? a.Bc[cb + lane] : -1;
       int added = 0;
-      for (int jb = bb; jb < be; jb += 128) {
-        int cc[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int jj = jb + 32 * q + lane;
-          cc[q] = jj < be ? a.Bc[jj] : -1;
+      for (int tt = 0; tt < cnt; ++tt) {
+        const int tb = cb, te = ce, c0 = pc;
+        if (tt + 1 < cnt) {
+          cb = __shfl_sync(kFull, bb, tt + 1);
+          ce = __shfl_sync(kFull, be, tt + 1);
+          pc = cb + lane < ce ? a.Bc[cb + lane] : -1;
         }
+        if (c0 >= 0) added += set_insert(keys, bits, c0);
+        for (int jb = tb + 32; jb < te; jb += 96) {
+          int cc[3];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (cc[q] >= 0) added += set_insert(keys, bits, cc[q]);
+          for (int q = 0; q < 3; ++q) {
+            const int jj = jb + 32 * q + lane;
+            cc[q] = jj < te ? a.Bc[jj] : -1;
+          }
+#pragma unroll
+          for (int q = 0; q < 3; ++q)
+            if (cc[q] >= 0) added += set_insert(keys, bits, cc[q]);
+        }
       }
       added = warp_sum(added);
       if (lane == 0 && added) {
@@ -288,24 +251,24 @@ __global__ void __launch_bounds__(256) spgemm_numeric_kernel(NumArgs a) {
 // by the whole CTA in one step (threads split its entries); steps are ordered
 // by __syncthreads, so every output entry still receives its k in ascending
 // order.  The next B row is prefetched into registers during the current
-// step.  Warp 0 compacts, sorts and writes the row.
-__global__ void __launch_bounds__(256) spgemm_numeric_block_kernel(NumArgs a) {
+// step.  Warp 0 compacts, sorts and writes the row (a block-wide CUB sort
+// was tried: 112 registers/thread cut occupancy to 25% and doubled the time).
+template <int NT, int BITS>
+__global__ void __launch_bounds__(NT) spgemm_numeric_block_kernel(NumArgs a) {
+  constexpr int T = 1 << BITS;
   extern __shared__ double smd[];
   __shared__ int mbb[32], mbe[32];
   __shared__ double mav[32];
-  const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31;
-  const int bits = a.bits;
-  const int T = 1 << bits;
+  const int tid = threadIdx.x, lane = tid & 31;
   double* acc = smd;
   int* keys = (int*)(acc + T);
-  int* cnt = keys + T;
   for (long long t = blockIdx.x; t < a.nrows; t += gridDim.x) {
     const int row = a.rows[t];
-    for (int i = tid; i < T; i += nthr) {
+    for (int i = tid; i < T; i += NT) {
       keys[i] = kEmpty;
       acc[i] = 0.0;
     }
-    AccOp op{keys, acc, bits};
+    AccOp op{keys, acc, BITS};
     const int ab = a.Ap[row], ae = a.Ap[row + 1];
     for (int base = ab; base < ae; base += 32) {
       __syncthreads();
@@ -331,12 +294,12 @@ __global__ void __launch_bounds__(256) spgemm_numeric_block_kernel(NumArgs a) {
           pv = cb + tid < ce ? a.Bv[cb + tid] : 0.0;
         }
         if (c0 >= 0) op(av, c0, v0);
-        for (int jj = tb + nthr + tid; jj < te; jj += nthr) op(av, a.Bc[jj], a.Bv[jj]);
+        for (int jj = tb + NT + tid; jj < te; jj += NT) op(av, a.Bc[jj], a.Bv[jj]);
         __syncthreads();
       }
     }
     __syncthreads();
-    if (tid < 32) {
+    if (tid < 32) {  // warp 0 compacts, sorts and writes the row
       const int n = compact_slots(keys, acc, T, lane);
       if (n <= 64) {
         int P = 1;
@@ -345,7 +308,7 @@ __global__ void __launch_bounds__(256) spgemm_numeric_block_kernel(NumArgs a) {
         __syncwarp();
         warp_bitonic(keys, acc, P, lane);
       } else {
-        warp_radix_sort(keys, acc, keys + n, acc + n, n, cnt, lane);
+        warp_radix_sort(keys, acc, keys + n, acc + n, n, keys + T, lane);
       }
       const int o = a.Cp[row];
       if (a.mode == 0) {
@@ -536,19 +499,23 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
     AIRG_TRY(set_smem((const void*)spgemm_numeric_kernel, 200 * 1024));
     Fork fk;
     AIRG_TRY(fk.begin(s));
-    AIRG_TRY(set_smem((const void*)spgemm_numeric_block_kernel, 200 * 1024));
+    AIRG_TRY(set_smem((const void*)spgemm_numeric_block_kernel<128, 10>, 200 * 1024));
+    AIRG_TRY(set_smem((const void*)spgemm_numeric_block_kernel<256, 11>, 200 * 1024));
+    AIRG_TRY(set_smem((const void*)spgemm_numeric_block_kernel<256, 12>, 200 * 1024));
     for (int c = 0; c < 5; ++c) {
       const int nr = cl.count[c];
       if (!nr) continue;
       NumArgs a{A.p, A.c, A.v, B.p, B.c, B.v, cl.list(c), nr, cbits[c], Cp, ocol, oval, negate,
                 mode, tol, lump, cnt, anyd, nullptr, nullptr, nullptr, nullptr, row0};
-      if (c >= 2) {  // long rows: one CTA (2-4 warps) per row, table shared by the CTA
+      if (c >= 2) {  // long rows: one CTA per row, table shared by the CTA
         const size_t shm = (size_t)(1 << cbits[c]) * 12 + 1024;
-        // threads per row (measured at 2048^2: 64/128/192/256 -> 254/191/178/173 ms)
-        static const int bt = getenv("AIRG_BLOCK_THREADS") ? atoi(getenv("AIRG_BLOCK_THREADS")) : 256;
-        static const int bt2 = getenv("AIRG_BLOCK_THREADS2") ? atoi(getenv("AIRG_BLOCK_THREADS2")) : 128;
-        spgemm_numeric_block_kernel<<<std::min(nr, 148 * 32), c == 2 ? bt2 : bt, shm,
-                                      fk.stream(c)>>>(a);
+        const int grid = std::min(nr, 148 * 32);
+        if (c == 2)
+          spgemm_numeric_block_kernel<128, 10><<<grid, 128, shm, fk.stream(c)>>>(a);
+        else if (c == 3)
+          spgemm_numeric_block_kernel<256, 11><<<grid, 256, shm, fk.stream(c)>>>(a);
+        else
+          spgemm_numeric_block_kernel<256, 12><<<grid, 256, shm, fk.stream(c)>>>(a);
       } else {
         const size_t shm = (size_t)cwarps[c] * ((1 << cbits[c]) * 12 + 1024);
         spgemm_numeric_kernel<<<blocks_for(nr, cwarps[c], 148 * 32), cwarps[c] * 32, shm,
