@@ -39,6 +39,22 @@ struct Epi {
   double* partial;  // optional: per-block sum of squares of value
 };
 
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// spin on one peer's message count; traps (fails the context) after ~20 s
+// instead of hanging the device
+__device__ __forceinline__ void wait_count(const unsigned long long* flag, unsigned long long want) {
+  const long long t0 = clock64();
+  while (ld_acquire_sys(flag) < want) {
+    __nanosleep(64);
+    if (clock64() - t0 > 40000000000ll) __trap();
+  }
+}
+
 template <bool E>
 __device__ __forceinline__ double madd(double a, double b, double c) {
   return E ? add_rn(c, mul_rn(a, b)) : fma(a, b, c);
@@ -1369,13 +1385,23 @@ static int richardson_body(airg_plan* p, const double* b, double* x, double rtol
 }
 
 // ===========================================================================
-// Row-strip distributed V-cycle / Richardson over NCCL.
+// Row-strip distributed V-cycle / Richardson.
 // Each distributed level keeps R, A_fc, A_ff on local rows with columns in
-// the ext space [local | ghost]; a halo exchange is a pack kernel plus grouped
-// ncclSend/ncclRecv straight into the ghost tail of the operand vector.
-// Below the distributed levels the residual is all-gathered and the
-// replicated serial plan solves the tail.  Every iteration (V-cycle, x += e,
-// residual, norm allreduce) is one captured CUDA graph.
+// the ext space [local | ghost].  Ghost values travel over NVLink by direct
+// peer stores: every vector that receives ghosts lives in one cudaMalloc
+// arena per rank, shared with the other ranks through CUDA IPC; a put kernel
+// gathers the send entries and stores them straight into the peers' ghost
+// tails, then publishes a per-(sender, receiver) message count with a
+// system-scope release; the consumer's wait kernel acquires it.  Flags flow
+// both ways between every pair that shares a halo (also when one direction
+// carries no data), which is what makes reusing the ghost tails safe: a
+// sender can only overwrite a tail after the receiver's flag for a later
+// exchange, which the receiver issues after consuming the tail.  The norm
+// allreduce and the replicated-tail gather use the same put/flag scheme, so
+// an iteration contains no NCCL call and is one captured CUDA graph.
+// NCCL (pack + grouped send/recv) remains as the transport when IPC is not
+// available (AIRG_DPLAN_NCCL=1 forces it); it also carries the one-time
+// exchange of IPC handles at plan build.
 // ===========================================================================
 #define AIRG_NCCL(call)                                                          \
   do {                                                                           \
@@ -1389,12 +1415,99 @@ static int richardson_body(airg_plan* p, const double* b, double* x, double rtol
 
 namespace airg {
 
+constexpr int kMaxPeers = 8;
+
 struct HaloX {
   int n_loc = 0, nsend = 0, nrecv = 0;
   int* send_idx = nullptr;
-  double* sendbuf = nullptr;
+  double* sendbuf = nullptr;  // NCCL transport
   std::vector<int> scnt, sofs, rcnt, rofs;
 };
+
+// one put: entries [sofs[j], sofs[j+1]) of the gathered send list go to dst[j]
+// (idx == nullptr: entry i is x[i - sofs[j]]); rflag[j] (null = local copy)
+// receives the new message count for peer[j]
+struct PutDesc {
+  int nsend = 0;
+  const int* idx = nullptr;
+  int npeer = 0;
+  int sofs[kMaxPeers + 2] = {};
+  double* dst[kMaxPeers + 1] = {};
+  unsigned long long* rflag[kMaxPeers + 1] = {};
+  int peer[kMaxPeers + 1] = {};
+};
+
+struct WaitDesc {
+  int npeer = 0;
+  int peer[kMaxPeers] = {};
+};
+
+struct NormDesc {
+  int npeer = 0, me = 0, world = 1;
+  int peer[kMaxPeers] = {};
+  double* slots[kMaxPeers] = {};             // peer's slot array (2 x world)
+  unsigned long long* rflag[kMaxPeers] = {};
+};
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// gathers and stores the send entries into the peers' ghost tails, then (last
+// CTA) publishes the new message counts and raises the expected counts of the
+// messages this exchange receives (the consumer kernel waits on those)
+__global__ void put_kernel(PutDesc d, const double* __restrict__ x, unsigned long long* sent,
+                           unsigned long long* expect, unsigned int* ticket) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d.nsend; i += gridDim.x * blockDim.x) {
+    int q = 0;
+    while (i >= d.sofs[q + 1]) ++q;
+    d.dst[q][i - d.sofs[q]] = d.idx ? x[d.idx[i]] : x[i - d.sofs[q]];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();  // cumulative over the CTA's stores ordered by the barrier
+    const unsigned t = atomicAdd(ticket, 1u);
+    if (t == gridDim.x - 1) {  // last CTA: every CTA's stores are fenced
+      *ticket = 0u;
+      __threadfence_system();
+      for (int j = 0; j < d.npeer; ++j)
+        if (d.rflag[j]) {
+          st_release_sys(d.rflag[j], ++sent[d.peer[j]]);
+          ++expect[d.peer[j]];
+        }
+    }
+  }
+}
+
+// wait for the listed peers' messages (counts raised by the matching put)
+__global__ void wait_kernel(WaitDesc w, const unsigned long long* flags, const unsigned long long* expect) {
+  const int t = threadIdx.x;
+  if (t < w.npeer) wait_count(flags + w.peer[t], expect[w.peer[t]]);
+}
+
+// norm allreduce, step 1: my partial sum into every peer's slot (parity of the
+// local call count keeps consecutive reductions apart)
+__global__ void norm_put_kernel(NormDesc d, const double* loc, const unsigned long long* ncount,
+                                unsigned long long* sent, unsigned long long* expect) {
+  const int par = (int)(*ncount & 1ull);
+  const double v = *loc;
+  for (int j = 0; j < d.npeer; ++j) d.slots[j][par * d.world + d.me] = v;
+  __threadfence_system();
+  for (int j = 0; j < d.npeer; ++j) {
+    st_release_sys(d.rflag[j], ++sent[d.peer[j]]);
+    ++expect[d.peer[j]];
+  }
+}
+
+// step 2 (after the wait): rank-ordered sum of the partials -> out
+__global__ void norm_sum_kernel(int me, int world, const double* loc, const double* slots,
+                                unsigned long long* ncount, double* out) {
+  const int par = (int)(*ncount & 1ull);
+  double s = 0.0;
+  for (int q = 0; q < world; ++q) s += q == me ? *loc : slots[par * world + q];
+  *out = s;
+  *ncount += 1ull;
+}
 
 __global__ void pack_kernel(int n, const int* __restrict__ idx, const double* __restrict__ x,
                             double* __restrict__ out) {
@@ -1427,6 +1540,12 @@ __global__ void unpad_kernel(int world, int tmax, const int* __restrict__ cnt, c
 
 }  // namespace airg
 
+// P2P halo of one target vector
+struct P2PHalo {
+  PutDesc put;
+  WaitDesc wait;
+};
+
 struct DLev {
   int n_loc = 0, nf = 0, nc = 0;
   Csr R, Afc, Aff;
@@ -1436,22 +1555,35 @@ struct DLev {
   std::vector<double> coef;
   double *r_ext = nullptr, *ec_ext = nullptr, *rhs_ext = nullptr, *y0 = nullptr, *y1 = nullptr,
          *e = nullptr;
+  bool own_e = false;
+  P2PHalo pR, pC, pF[3];  // pF: targets rhs_ext, y0, y1
 };
 
 struct airg_dplan {
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
+  bool p2p = false;
   std::vector<DLev> lv;
   Csr top;
   HaloX hT;
+  P2PHalo pT, pTail;
+  NormDesc nd;
+  WaitDesc nwait;
   double *x_ext = nullptr, *r = nullptr, *parts = nullptr, *nrm_loc = nullptr, *nrm_glob = nullptr;
   double norm_h = 0.0;
-  int nparts = 0;
+  int nparts = 0, n_top = 0;
   airg_plan* tail = nullptr;
   std::vector<int> tcnt, tofs;
   int tail_n = 0, tmax = 0;
   int *d_tcnt = nullptr, *d_tofs = nullptr;
   double *tsend = nullptr, *trecv = nullptr, *tr_full = nullptr, *te_full = nullptr;
+  // P2P transport state
+  double* arena = nullptr;
+  std::vector<double*> peer_base;
+  double* nslots = nullptr;
+  unsigned long long *flags = nullptr, *sent = nullptr, *recvd = nullptr, *ncount = nullptr;
+  unsigned int* ticket = nullptr;
+  std::vector<void*> owned;  // dmalloc'd buffers freed at destroy
   cudaStream_t cs = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   cudaGraphExec_t graph = nullptr;
@@ -1459,8 +1591,45 @@ struct airg_dplan {
   long long launches = 0;
 };
 
-static int halo_exchange(airg_dplan* p, HaloX& h, double* x_ext, cudaStream_t s) {
+template <typename T>
+static int dalloc_owned(airg_dplan* p, T** ptr, size_t count) {
+  AIRG_CUDA(dmalloc(ptr, (count ? count : 1) * sizeof(T)));
+  p->owned.push_back((void*)*ptr);
+  return AIRG_OK;
+}
+
+// put half of a P2P exchange (the consumer waits: wait_into / wait_kernel)
+static int wait_now(airg_dplan* p, const WaitDesc& w, cudaStream_t s);
+
+static int halo_put(airg_dplan* p, const P2PHalo& h, const double* x, cudaStream_t s) {
+  const PutDesc& d = h.put;
+  if (d.npeer == 0) return AIRG_OK;
+  // measured: spreading the gather over CTAs beats one CTA (dependent
+  // idx -> x -> remote-store chains); at most 16 CTAs
+  put_kernel<<<std::max(1, blocks_for(d.nsend, 256, 16)), 256, 0, s>>>(d, x, p->sent, p->recvd,
+                                                                      p->ticket);
+  AIRG_LAUNCH_CHECK();
+  ++p->launches;
+  return AIRG_OK;
+}
+
+
+static int wait_now(airg_dplan* p, const WaitDesc& w, cudaStream_t s) {
+  if (!w.npeer) return AIRG_OK;
+  wait_kernel<<<1, 32, 0, s>>>(w, p->flags, p->recvd);
+  AIRG_LAUNCH_CHECK();
+  ++p->launches;
+  return AIRG_OK;
+}
+
+// P2P: put + wait kernel (a wait folded into the consuming SpMV made every CTA
+// poll at system scope and doubled the SpMV time); NCCL: pack + send/recv
+static int halo_exchange(airg_dplan* p, HaloX& h, const P2PHalo* ph, double* x_ext, cudaStream_t s) {
   if (p->world == 1) return AIRG_OK;
+  if (p->p2p) {
+    AIRG_TRY(halo_put(p, *ph, x_ext, s));
+    return wait_now(p, ph->wait, s);
+  }
   if (h.nsend) {
     pack_kernel<<<blocks_for(h.nsend, 256, 1024), 256, 0, s>>>(h.nsend, h.send_idx, x_ext, h.sendbuf);
     AIRG_LAUNCH_CHECK();
@@ -1475,16 +1644,40 @@ static int halo_exchange(airg_dplan* p, HaloX& h, double* x_ext, cudaStream_t s)
   return AIRG_OK;
 }
 
+// nrm_loc -> nrm_glob (sum over ranks)
+static int norm_allreduce(airg_dplan* p, cudaStream_t s) {
+  if (p->world == 1) {
+    AIRG_CUDA(cudaMemcpyAsync(p->nrm_glob, p->nrm_loc, sizeof(double), cudaMemcpyDeviceToDevice, s));
+    return AIRG_OK;
+  }
+  if (!p->p2p) {
+    AIRG_NCCL(ncclAllReduce(p->nrm_loc, p->nrm_glob, 1, ncclDouble, ncclSum, p->comm, s));
+    return AIRG_OK;
+  }
+  norm_put_kernel<<<1, 1, 0, s>>>(p->nd, p->nrm_loc, p->ncount, p->sent, p->recvd);
+  AIRG_LAUNCH_CHECK();
+  AIRG_TRY(wait_now(p, p->nwait, s));
+  norm_sum_kernel<<<1, 1, 0, s>>>(p->rank, p->world, p->nrm_loc, p->nslots, p->ncount, p->nrm_glob);
+  AIRG_LAUNCH_CHECK();
+  p->launches += 2;
+  return AIRG_OK;
+}
+
 static int dplan_vcycle(airg_dplan* p, int l, cudaStream_t s);
 
 // V-cycle of the replicated tail: in = local part (tcnt[rank] entries), out = local part
 static int dplan_tail(airg_dplan* p, const double* in, double* out, cudaStream_t s) {
   const int mine = p->tcnt[p->rank];
-  AIRG_CUDA(cudaMemcpyAsync(p->tsend, in, (size_t)mine * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  AIRG_NCCL(ncclAllGather(p->tsend, p->trecv, p->tmax, ncclDouble, p->comm, s));
-  dim3 g(blocks_for(p->tmax, 256, 64), p->world);
-  unpad_kernel<<<g, 256, 0, s>>>(p->world, p->tmax, p->d_tcnt, p->d_tofs, p->trecv, p->tr_full);
-  AIRG_LAUNCH_CHECK();
+  if (p->p2p) {
+    AIRG_TRY(halo_put(p, p->pTail, in, s));
+    AIRG_TRY(wait_now(p, p->pTail.wait, s));
+  } else {
+    AIRG_CUDA(cudaMemcpyAsync(p->tsend, in, (size_t)mine * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    AIRG_NCCL(ncclAllGather(p->tsend, p->trecv, p->tmax, ncclDouble, p->comm, s));
+    dim3 g(blocks_for(p->tmax, 256, 64), p->world);
+    unpad_kernel<<<g, 256, 0, s>>>(p->world, p->tmax, p->d_tcnt, p->d_tofs, p->trecv, p->tr_full);
+    AIRG_LAUNCH_CHECK();
+  }
   AIRG_TRY(vcycle_rec(p->tail, 0, p->tr_full, p->te_full, 1, s));
   AIRG_CUDA(cudaMemcpyAsync(out, p->te_full + p->tofs[p->rank], (size_t)mine * sizeof(double),
                             cudaMemcpyDeviceToDevice, s));
@@ -1495,7 +1688,7 @@ static int dplan_tail(airg_dplan* p, const double* in, double* out, cudaStream_t
 static int dplan_vcycle(airg_dplan* p, int l, cudaStream_t s) {
   DLev& L = p->lv[l];
   const bool last = l + 1 == (int)p->lv.size();
-  AIRG_TRY(halo_exchange(p, L.hR, L.r_ext, s));
+  AIRG_TRY(halo_exchange(p, L.hR, &L.pR, L.r_ext, s));
   // restricted residual: the next level's input, or scratch before the tail gather
   double* rc = last ? L.rhs_ext : p->lv[l + 1].r_ext;
   {
@@ -1504,7 +1697,7 @@ static int dplan_vcycle(airg_dplan* p, int l, cudaStream_t s) {
   }
   if (last) AIRG_TRY(dplan_tail(p, rc, L.ec_ext, s));
   else AIRG_TRY(dplan_vcycle(p, l + 1, s));  // writes lv[l+1].e == L.ec_ext
-  AIRG_TRY(halo_exchange(p, L.hC, L.ec_ext, s));
+  AIRG_TRY(halo_exchange(p, L.hC, &L.pC, L.ec_ext, s));
   // rhs = r[f] - A_fc e_c
   {
     Epi ep{L.rhs_ext, nullptr, -1.0, 1.0, L.r_ext, L.f_idx, nullptr, nullptr};
@@ -1518,7 +1711,8 @@ static int dplan_vcycle(airg_dplan* p, int l, cudaStream_t s) {
     double xs = L.coef[d];
     double* bufs[2] = {L.y0, L.y1};
     for (int j = d - 1; j >= 0; --j) {
-      AIRG_TRY(halo_exchange(p, L.hF, cur, s));
+      const P2PHalo* ph = cur == L.rhs_ext ? &L.pF[0] : cur == L.y0 ? &L.pF[1] : &L.pF[2];
+      AIRG_TRY(halo_exchange(p, L.hF, ph, cur, s));
       double* dst = j == 0 ? L.e : bufs[j & 1];
       Epi ep{dst, j == 0 ? L.f_idx : nullptr, 1.0, L.coef[j], L.rhs_ext, nullptr, nullptr, nullptr};
       AIRG_TRY(launch_spmv(L.Aff, cur, xs, ep, s));
@@ -1532,24 +1726,23 @@ static int dplan_vcycle(airg_dplan* p, int l, cudaStream_t s) {
 
 // r = b - A x (halo on x), local sum of squares -> allreduce -> nrm_glob
 static int dplan_residual(airg_dplan* p, const double* b, cudaStream_t s) {
-  AIRG_TRY(halo_exchange(p, p->hT, p->x_ext, s));
+  AIRG_TRY(halo_exchange(p, p->hT, &p->pT, p->x_ext, s));
   const int nb = spmv_blocks(p->top);
   Epi ep{p->r, nullptr, -1.0, 1.0, b, nullptr, nullptr, p->parts};
   AIRG_TRY(launch_spmv(p->top, p->x_ext, 1.0, ep, s));
   finish_sum_kernel<<<1, 1024, 0, s>>>(nb, p->parts, p->nrm_loc);
   AIRG_LAUNCH_CHECK();
-  AIRG_NCCL(ncclAllReduce(p->nrm_loc, p->nrm_glob, 1, ncclDouble, ncclSum, p->comm, s));
-  return AIRG_OK;
+  return norm_allreduce(p, s);
 }
 
-static int dalloc(HaloX& h, int n_loc, int nsend, const int* send_idx, const int* scnt,
-                  const int* rcnt, int world) {
+static int dalloc(airg_dplan* p, HaloX& h, int n_loc, int nsend, const int* send_idx,
+                  const int* scnt, const int* rcnt, int world) {
   h.n_loc = n_loc;
   h.nsend = nsend;
   h.scnt.assign(scnt, scnt + world);
   h.rcnt.assign(rcnt, rcnt + world);
-  h.sofs.assign(world, 0);
-  h.rofs.assign(world, 0);
+  h.sofs.assign(world + 1, 0);
+  h.rofs.assign(world + 1, 0);
   int a = 0, b = 0;
   for (int q = 0; q < world; ++q) {
     h.sofs[q] = a;
@@ -1557,12 +1750,206 @@ static int dalloc(HaloX& h, int n_loc, int nsend, const int* send_idx, const int
     a += h.scnt[q];
     b += h.rcnt[q];
   }
+  h.sofs[world] = a;
+  h.rofs[world] = b;
   h.nrecv = b;
   if (nsend) {
-    AIRG_CUDA(dmalloc(&h.send_idx, (size_t)nsend * sizeof(int)));
+    AIRG_TRY(dalloc_owned(p, &h.send_idx, (size_t)nsend));
     AIRG_CUDA(cudaMemcpy(h.send_idx, send_idx, (size_t)nsend * sizeof(int), cudaMemcpyDeviceToDevice));
-    AIRG_CUDA(dmalloc(&h.sendbuf, (size_t)nsend * sizeof(double)));
+    AIRG_TRY(dalloc_owned(p, &h.sendbuf, (size_t)nsend));
   }
+  return AIRG_OK;
+}
+
+// ---- P2P set-up --------------------------------------------------------------
+// Every rank lays its ghost-receiving vectors out in one arena and publishes a
+// directory of int64 entries (same layout on every rank):
+//   per level: offsets of r_ext, ec_ext, rhs_ext, y0, y1; then for hR, hC, hF:
+//              n_loc, rofs[0..W-1]
+//   top: offset of x_ext, hT.n_loc, hT.rofs[0..W-1]
+//   offsets of tr_full, norm slots, flags
+enum { kDirLev = 5 };
+
+static size_t dir_len(int nd, int W) { return (size_t)nd * (kDirLev + 3 * (1 + W)) + (2 + W) + 3; }
+
+static int p2p_peers(const HaloX& h, int me, int W, std::vector<int>& out) {
+  out.clear();
+  for (int q = 0; q < W; ++q)
+    if (q != me && (h.scnt[q] > 0 || h.rcnt[q] > 0)) out.push_back(q);
+  if ((int)out.size() > kMaxPeers) {
+    set_error("halo spans %d peers (max %d)", (int)out.size(), kMaxPeers);
+    return AIRG_ERR_VALUE;
+  }
+  return AIRG_OK;
+}
+
+// put/wait descriptors of halo h into the peers' vector at directory slot
+// vec_slot; n_loc/rofs of that halo at dir slot hslot
+static int build_p2p_halo(airg_dplan* p, const HaloX& h, const std::vector<long long>& dir, size_t dl,
+                          size_t vec_slot, size_t hslot, P2PHalo& out) {
+  const int me = p->rank, W = p->world;
+  std::vector<int> peers;
+  AIRG_TRY(p2p_peers(h, me, W, peers));
+  PutDesc d{};
+  d.nsend = h.nsend;
+  d.idx = h.send_idx;
+  d.npeer = (int)peers.size();
+  for (int j = 0; j < d.npeer; ++j) {
+    const int q = peers[j];
+    const long long* D = dir.data() + (size_t)q * dl;
+    d.peer[j] = q;
+    d.sofs[j] = h.sofs[q];
+    d.dst[j] = p->peer_base[q] + D[vec_slot] + D[hslot] + D[hslot + 1 + me];
+    d.rflag[j] = (unsigned long long*)(p->peer_base[q] + D[dl - 1]) + me;
+  }
+  d.sofs[d.npeer] = h.nsend;
+  // entries for peers that receive nothing form empty segments in rank order
+  for (int j = d.npeer - 1; j >= 0; --j)
+    if (h.scnt[d.peer[j]] == 0) d.sofs[j] = d.sofs[j + 1];
+  out.put = d;
+  out.wait.npeer = d.npeer;
+  for (int j = 0; j < d.npeer; ++j) out.wait.peer[j] = peers[j];
+  return AIRG_OK;
+}
+
+static int p2p_setup(airg_dplan* p) {
+  const int W = p->world, me = p->rank, nd = (int)p->lv.size();
+  auto up = [](size_t n) { return (n + 31) & ~(size_t)31; };
+  std::vector<long long> mine(dir_len(nd, W), 0);
+  size_t off = 0;
+  size_t k = 0;
+  std::vector<size_t> lev_off(nd * kDirLev);
+  for (int l = 0; l < nd; ++l) {
+    DLev& L = p->lv[l];
+    const size_t sz[kDirLev] = {(size_t)L.n_loc + L.hR.nrecv + 1, (size_t)L.nc + L.hC.nrecv + 1,
+                                (size_t)std::max(L.nf, L.nc) + L.hF.nrecv + 1,
+                                (size_t)L.nf + L.hF.nrecv + 1, (size_t)L.nf + L.hF.nrecv + 1};
+    for (int v = 0; v < kDirLev; ++v) {
+      lev_off[l * kDirLev + v] = off;
+      mine[k++] = (long long)off;
+      off += up(sz[v]);
+    }
+    for (const HaloX* h : {&L.hR, &L.hC, &L.hF}) {
+      mine[k++] = h->n_loc;
+      for (int q = 0; q < W; ++q) mine[k++] = h->rofs[q];
+    }
+  }
+  const size_t x_off = off;
+  mine[k++] = (long long)off;
+  off += up((size_t)p->n_top + p->hT.nrecv + 1);
+  mine[k++] = p->hT.n_loc;
+  for (int q = 0; q < W; ++q) mine[k++] = p->hT.rofs[q];
+  const size_t tr_off = off;
+  mine[k++] = (long long)off;
+  off += up((size_t)p->tail_n + 1);
+  const size_t ns_off = off;
+  mine[k++] = (long long)off;
+  off += up((size_t)2 * W);
+  const size_t fl_off = off;
+  mine[k++] = (long long)off;
+  off += up((size_t)W);
+  AIRG_CUDA(cudaMalloc((void**)&p->arena, off * sizeof(double)));
+  AIRG_CUDA(cudaMemset(p->arena, 0, off * sizeof(double)));
+  for (int l = 0; l < nd; ++l) {
+    DLev& L = p->lv[l];
+    double** vs[kDirLev] = {&L.r_ext, &L.ec_ext, &L.rhs_ext, &L.y0, &L.y1};
+    for (int v = 0; v < kDirLev; ++v) *vs[v] = p->arena + lev_off[l * kDirLev + v];
+    if (l > 0) L.e = p->lv[l - 1].ec_ext;  // level l's error is level l-1's e_c
+  }
+  p->x_ext = p->arena + x_off;
+  p->tr_full = p->arena + tr_off;
+  p->nslots = p->arena + ns_off;
+  p->flags = (unsigned long long*)(p->arena + fl_off);
+  // exchange directories + IPC handles (one NCCL all-gather at build time)
+  const size_t dl = dir_len(nd, W);
+  const size_t rec = dl + 8;  // + 64 bytes of cudaIpcMemHandle_t
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+  std::vector<long long> hrec(rec);
+  std::copy(mine.begin(), mine.end(), hrec.begin());
+  cudaIpcMemHandle_t hdl;
+  AIRG_CUDA(cudaIpcGetMemHandle(&hdl, p->arena));
+  memcpy(hrec.data() + dl, &hdl, 64);
+  long long *dsend = nullptr, *drecv = nullptr;
+  AIRG_CUDA(cudaMalloc((void**)&dsend, rec * sizeof(long long)));
+  AIRG_CUDA(cudaMalloc((void**)&drecv, rec * W * sizeof(long long)));
+  AIRG_CUDA(cudaMemcpy(dsend, hrec.data(), rec * sizeof(long long), cudaMemcpyHostToDevice));
+  AIRG_NCCL(ncclAllGather(dsend, drecv, rec * 2, ncclFloat, p->comm, p->cs));  // 8-byte words as 2 floats
+  AIRG_CUDA(cudaStreamSynchronize(p->cs));
+  std::vector<long long> all(rec * W);
+  AIRG_CUDA(cudaMemcpy(all.data(), drecv, rec * W * sizeof(long long), cudaMemcpyDeviceToHost));
+  cudaFree(dsend);
+  cudaFree(drecv);
+  std::vector<long long> dir(dl * W);
+  p->peer_base.assign(W, nullptr);
+  for (int q = 0; q < W; ++q) {
+    std::copy(all.begin() + q * rec, all.begin() + q * rec + dl, dir.begin() + q * dl);
+    if (q == me) {
+      p->peer_base[q] = p->arena;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, all.data() + q * rec + dl, 64);
+    void* base = nullptr;
+    AIRG_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    p->peer_base[q] = (double*)base;
+  }
+  // descriptors
+  const size_t per_lev = kDirLev + 3 * (1 + W);
+  for (int l = 0; l < nd; ++l) {
+    DLev& L = p->lv[l];
+    const size_t b = (size_t)l * per_lev;
+    const size_t hR = b + kDirLev, hC = hR + 1 + W, hF = hC + 1 + W;
+    AIRG_TRY(build_p2p_halo(p, L.hR, dir, dl, b + 0, hR, L.pR));
+    AIRG_TRY(build_p2p_halo(p, L.hC, dir, dl, b + 1, hC, L.pC));
+    for (int v = 0; v < 3; ++v) AIRG_TRY(build_p2p_halo(p, L.hF, dir, dl, b + 2 + v, hF, L.pF[v]));
+  }
+  const size_t tb = (size_t)nd * per_lev;
+  AIRG_TRY(build_p2p_halo(p, p->hT, dir, dl, tb, tb + 1, p->pT));
+  // tail gather: my part to every rank's tr_full (self included, no flag)
+  {
+    PutDesc d{};
+    const int n = p->tcnt[me];
+    d.idx = nullptr;
+    int j = 0;
+    for (int q = 0; q < W; ++q) {
+      const long long* D = dir.data() + (size_t)q * dl;
+      d.peer[j] = q;
+      d.sofs[j] = j * n;
+      d.dst[j] = p->peer_base[q] + D[dl - 3] + p->tofs[me];
+      d.rflag[j] = q == me ? nullptr : (unsigned long long*)(p->peer_base[q] + D[dl - 1]) + me;
+      ++j;
+    }
+    d.npeer = j;
+    d.sofs[j] = j * n;
+    d.nsend = j * n;
+    p->pTail.put = d;
+    WaitDesc w{};
+    for (int q = 0; q < W; ++q)
+      if (q != me) w.peer[w.npeer++] = q;
+    p->pTail.wait = w;
+    // norm slots
+    NormDesc nd_{};
+    nd_.me = me;
+    nd_.world = W;
+    for (int q = 0; q < W; ++q) {
+      if (q == me) continue;
+      const long long* D = dir.data() + (size_t)q * dl;
+      nd_.peer[nd_.npeer] = q;
+      nd_.slots[nd_.npeer] = p->peer_base[q] + D[dl - 2];
+      nd_.rflag[nd_.npeer] = (unsigned long long*)(p->peer_base[q] + D[dl - 1]) + me;
+      ++nd_.npeer;
+    }
+    p->nd = nd_;
+    p->nwait = w;
+  }
+  unsigned long long* ctr = nullptr;
+  AIRG_TRY(dalloc_owned(p, &ctr, (size_t)3 * W + 2));
+  AIRG_CUDA(cudaMemset(ctr, 0, ((size_t)3 * W + 2) * sizeof(unsigned long long)));
+  p->sent = ctr;
+  p->recvd = ctr + W;
+  p->ncount = ctr + 2 * W;
+  p->ticket = (unsigned int*)(ctr + 2 * W + 1);
+  AIRG_CUDA(cudaDeviceSynchronize());
   return AIRG_OK;
 }
 
@@ -1600,6 +1987,10 @@ int airg_comm_destroy(airg_comm* c) {
 }
 
 int airg_dplan_create(airg_comm* c, int ndist, airg_dplan** out) {
+  if (c->world > kMaxPeers + 1) {
+    set_error("at most %d ranks", kMaxPeers + 1);
+    return AIRG_ERR_VALUE;
+  }
   airg_dplan* p = new airg_dplan();
   p->rank = c->rank;
   p->world = c->world;
@@ -1608,7 +1999,7 @@ int airg_dplan_create(airg_comm* c, int ndist, airg_dplan** out) {
   AIRG_CUDA(cudaStreamCreateWithFlags(&p->cs, cudaStreamNonBlocking));
   AIRG_CUDA(cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming));
   AIRG_CUDA(cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming));
-  AIRG_CUDA(dmalloc(&p->nrm_loc, 2 * sizeof(double)));
+  AIRG_TRY(dalloc_owned(p, &p->nrm_loc, 2));
   p->nrm_glob = p->nrm_loc + 1;
   *out = p;
   return AIRG_OK;
@@ -1619,7 +2010,7 @@ int airg_dplan_set_halo(airg_dplan* p, int level, int which, int n_loc, int nsen
                         const int32_t* send_idx, const int32_t* scnt_h, const int32_t* rcnt_h) {
   HaloX* h = which == 3 ? &p->hT : which == 0 ? &p->lv[level].hR : which == 1 ? &p->lv[level].hC
                                                                             : &p->lv[level].hF;
-  return dalloc(*h, n_loc, nsend, send_idx, scnt_h, rcnt_h, p->world);
+  return dalloc(p, *h, n_loc, nsend, send_idx, scnt_h, rcnt_h, p->world);
 }
 
 int airg_dplan_set_level(airg_dplan* p, int level, int n_loc, int nf, int nc, const int32_t* Rp,
@@ -1637,34 +2028,28 @@ int airg_dplan_set_level(airg_dplan* p, int level, int n_loc, int nf, int nc, co
   L.f_idx = f_idx;
   L.c_idx = c_idx;
   L.coef.assign(coef_h, coef_h + ncoef);
-  AIRG_CUDA(dmalloc(&L.r_ext, (size_t)(n_loc + L.hR.nrecv + 1) * sizeof(double)));
-  AIRG_CUDA(dmalloc(&L.rhs_ext, (size_t)(std::max(nf, nc) + L.hF.nrecv + 1) * sizeof(double)));
-  AIRG_CUDA(dmalloc(&L.y0, (size_t)(nf + L.hF.nrecv + 1) * sizeof(double)));
-  AIRG_CUDA(dmalloc(&L.y1, (size_t)(nf + L.hF.nrecv + 1) * sizeof(double)));
-  if (level == 0) AIRG_CUDA(dmalloc(&L.e, (size_t)(n_loc + 1) * sizeof(double)));
+  if (level == 0) {
+    AIRG_TRY(dalloc_owned(p, &L.e, (size_t)n_loc + 1));
+    L.own_e = true;
+  }
   return AIRG_OK;
 }
 
 int airg_dplan_set_top(airg_dplan* p, int n_loc, const int32_t* ptr, const int32_t* col,
                        const double* val, int64_t nnz) {
+  p->n_top = n_loc;
   p->top = make_csr(n_loc, n_loc + p->hT.nrecv, ptr, col, val, nnz);
-  AIRG_CUDA(dmalloc(&p->x_ext, (size_t)(n_loc + p->hT.nrecv + 1) * sizeof(double)));
-  AIRG_CUDA(dmalloc(&p->r, (size_t)(n_loc + 1) * sizeof(double)));
+  AIRG_TRY(dalloc_owned(p, &p->r, (size_t)n_loc + 1));
   p->nparts = spmv_blocks(p->top) + 1;
-  AIRG_CUDA(dmalloc(&p->parts, (size_t)p->nparts * sizeof(double)));
+  AIRG_TRY(dalloc_owned(p, &p->parts, (size_t)p->nparts));
   return AIRG_OK;
 }
 
-// link the levels' vectors (level l's coarse error buffer == level l+1's e)
-// and attach the replicated tail plan; counts_h = per-rank sizes of the tail
-// level (the coarse size of the last distributed level on every rank)
+// allocate and link the levels' vectors (level l's coarse error buffer ==
+// level l+1's e) and attach the replicated tail plan; counts_h = per-rank
+// sizes of the tail level (the coarse size of the last distributed level)
 int airg_dplan_finish(airg_dplan* p, airg_plan* tail, const int32_t* counts_h) {
   const int nd = (int)p->lv.size();
-  for (int l = 0; l < nd; ++l) {
-    DLev& L = p->lv[l];
-    AIRG_CUDA(dmalloc(&L.ec_ext, (size_t)(L.nc + L.hC.nrecv + 1) * sizeof(double)));
-    if (l + 1 < nd) p->lv[l + 1].e = L.ec_ext;  // level l+1's error is level l's e_c
-  }
   p->tail = tail;
   p->tcnt.assign(counts_h, counts_h + p->world);
   p->tofs.assign(p->world, 0);
@@ -1676,25 +2061,44 @@ int airg_dplan_finish(airg_dplan* p, airg_plan* tail, const int32_t* counts_h) {
   }
   p->tail_n = a;
   p->tmax = mx;
-  AIRG_CUDA(dmalloc(&p->d_tcnt, p->world * sizeof(int)));
-  AIRG_CUDA(dmalloc(&p->d_tofs, p->world * sizeof(int)));
-  AIRG_CUDA(cudaMemcpy(p->d_tcnt, p->tcnt.data(), p->world * sizeof(int), cudaMemcpyHostToDevice));
-  AIRG_CUDA(cudaMemcpy(p->d_tofs, p->tofs.data(), p->world * sizeof(int), cudaMemcpyHostToDevice));
-  AIRG_CUDA(dmalloc(&p->tsend, (size_t)mx * sizeof(double)));
-  AIRG_CUDA(dmalloc(&p->trecv, (size_t)mx * p->world * sizeof(double)));
-  AIRG_CUDA(dmalloc(&p->tr_full, (size_t)(a + 1) * sizeof(double)));
-  AIRG_CUDA(dmalloc(&p->te_full, (size_t)(a + 1) * sizeof(double)));
+  static const bool force_nccl = getenv("AIRG_DPLAN_NCCL") != nullptr;
+  p->p2p = p->world > 1 && !force_nccl;
+  if (p->p2p) {
+    const int rc = p2p_setup(p);
+    if (rc != AIRG_OK) return rc;
+  } else {
+    for (int l = 0; l < nd; ++l) {
+      DLev& L = p->lv[l];
+      AIRG_TRY(dalloc_owned(p, &L.r_ext, (size_t)L.n_loc + L.hR.nrecv + 1));
+      AIRG_TRY(dalloc_owned(p, &L.rhs_ext, (size_t)std::max(L.nf, L.nc) + L.hF.nrecv + 1));
+      AIRG_TRY(dalloc_owned(p, &L.y0, (size_t)L.nf + L.hF.nrecv + 1));
+      AIRG_TRY(dalloc_owned(p, &L.y1, (size_t)L.nf + L.hF.nrecv + 1));
+      AIRG_TRY(dalloc_owned(p, &L.ec_ext, (size_t)L.nc + L.hC.nrecv + 1));
+      if (l > 0) L.e = p->lv[l - 1].ec_ext;
+    }
+    AIRG_TRY(dalloc_owned(p, &p->x_ext, (size_t)p->n_top + p->hT.nrecv + 1));
+    AIRG_TRY(dalloc_owned(p, &p->tr_full, (size_t)a + 1));
+    AIRG_TRY(dalloc_owned(p, &p->d_tcnt, (size_t)p->world));
+    AIRG_TRY(dalloc_owned(p, &p->d_tofs, (size_t)p->world));
+    AIRG_CUDA(cudaMemcpy(p->d_tcnt, p->tcnt.data(), p->world * sizeof(int), cudaMemcpyHostToDevice));
+    AIRG_CUDA(cudaMemcpy(p->d_tofs, p->tofs.data(), p->world * sizeof(int), cudaMemcpyHostToDevice));
+    AIRG_TRY(dalloc_owned(p, &p->tsend, (size_t)mx));
+    AIRG_TRY(dalloc_owned(p, &p->trecv, (size_t)mx * p->world));
+  }
+  AIRG_TRY(dalloc_owned(p, &p->te_full, (size_t)a + 1));
   if (tail) AIRG_TRY(prepare_capture(tail, 0));
   return AIRG_OK;
 }
 
 int airg_dplan_destroy(airg_dplan* p) {
   if (!p) return AIRG_OK;
+  if (p->cs) cudaStreamSynchronize(p->cs);
   if (p->graph) cudaGraphExecDestroy(p->graph);
-  if (p->cs) {
-    cudaStreamSynchronize(p->cs);
-    cudaStreamDestroy(p->cs);
-  }
+  for (int q = 0; q < (int)p->peer_base.size(); ++q)
+    if (q != p->rank && p->peer_base[q]) cudaIpcCloseMemHandle(p->peer_base[q]);
+  if (p->arena) cudaFree(p->arena);
+  for (void* b : p->owned) dfree(b);
+  if (p->cs) cudaStreamDestroy(p->cs);
   if (p->ev_in) cudaEventDestroy(p->ev_in);
   if (p->ev_out) cudaEventDestroy(p->ev_out);
   delete p;  // the communicator is owned by its airg_comm
@@ -1717,7 +2121,7 @@ int airg_dplan_richardson(airg_dplan* p, const double* b, double* x, double rtol
     sumsq_kernel<<<nb, 256, 0, s>>>(n, b, p->parts);
     finish_sum_kernel<<<1, 1024, 0, s>>>(nb, p->parts, p->nrm_loc);
     AIRG_LAUNCH_CHECK();
-    AIRG_NCCL(ncclAllReduce(p->nrm_loc, p->nrm_glob, 1, ncclDouble, ncclSum, p->comm, s));
+    AIRG_TRY(norm_allreduce(p, s));
     AIRG_CUDA(cudaMemcpyAsync(&p->norm_h, p->nrm_glob, sizeof(double), cudaMemcpyDeviceToHost, s));
     AIRG_CUDA(cudaStreamSynchronize(s));
   }
@@ -1733,10 +2137,11 @@ int airg_dplan_richardson(airg_dplan* p, const double* b, double* x, double rtol
   int st = AIRG_OK;
   bool conv = rn <= thr;
   int its = 0;
-  // Capturing the NCCL-bearing iteration costs more than one solve's launch
-  // overhead; it pays only for repeated solves on one plan (AIRG_DPLAN_GRAPH=1).
+  // With the P2P transport an iteration is kernels only and is captured once
+  // per (b, x); capturing the NCCL-bearing iteration costs more than one
+  // solve's launch overhead (opt-in: AIRG_DPLAN_GRAPH=1).
   static const bool graph_on = getenv("AIRG_DPLAN_GRAPH") != nullptr;
-  const bool use_graph = graphs_enabled() && graph_on;
+  const bool use_graph = graphs_enabled() && (p->p2p || graph_on);
   if (use_graph && (p->gkey[0] != b || p->gkey[1] != x) && p->graph) {
     cudaGraphExecDestroy(p->graph);
     p->graph = nullptr;
