@@ -341,6 +341,130 @@ __global__ void __launch_bounds__(128) poly_assemble_kernel(PolyArgs a) {
   }
 }
 
+// Long pattern rows (cap >= 256): one CTA per row.  Same recurrence and
+// summation order as poly_assemble_kernel: within a power the present
+// positions q are consumed in ascending order, all threads splitting the A
+// row of col_q (distinct columns -> distinct positions), a barrier between
+// consecutive q.  The present positions of a power and their A-row bounds are
+// staged in shared memory first, so a step issues no dependent global loads.
+// Shared memory per CTA: keys/pos T ints each, cur/nxt/acc cap doubles,
+// list/rb/re cap ints, flags 3 cap bytes.
+__global__ void __launch_bounds__(256) poly_assemble_block_kernel(PolyArgs a) {
+  extern __shared__ unsigned char smraw[];
+  __shared__ int s_np, s_cnt;
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int T = 1 << a.bits;
+  const int cap = a.cap;
+  double* cur = (double*)smraw;
+  double* nxt = cur + cap;
+  double* acc = nxt + cap;
+  int* keys = (int*)(acc + cap);
+  int* pv = keys + T;
+  int* list = pv + T;
+  int* rbs = list + cap;
+  int* res = rbs + cap;
+  unsigned char* fcur = (unsigned char*)(res + cap);
+  unsigned char* fnxt = fcur + cap;
+  unsigned char* facc = fnxt + cap;
+  for (long long r = blockIdx.x; r < a.nrows; r += gridDim.x) {
+    const int row = a.rows ? a.rows[r] : (int)r;
+    const int pb = a.Pp[row], pe = a.Pp[row + 1], m = pe - pb;
+    for (int i = tid; i < T; i += NT) keys[i] = kEmpty;
+    __syncthreads();
+    for (int i = tid; i < m; i += NT) {
+      map_insert(keys, pv, a.bits, a.Pc[pb + i], i);
+      cur[i] = 0.0;
+      nxt[i] = 0.0;
+      acc[i] = 0.0;
+      fcur[i] = 0;
+      fnxt[i] = 0;
+      facc[i] = 0;
+    }
+    __syncthreads();
+    const int d = a.ncoef - 1;
+    if (tid == 0) {  // term 0: c0 * I (the diagonal is always in the pattern)
+      const int p = map_find(keys, pv, a.bits, a.row0 + row);
+      acc[p] = add_rn(acc[p], a.coef[0]);
+      facc[p] = 1;
+    }
+    __syncthreads();
+    if (d >= 1) {
+      const double c1 = a.coef[1];
+      for (int kk = a.Ap[row] + tid; kk < a.Ap[row + 1]; kk += NT) {
+        const int p = map_find(keys, pv, a.bits, a.Ac[kk]);
+        const double v = a.Av[kk];
+        acc[p] = add_rn(acc[p], mul_rn(c1, v));
+        facc[p] = 1;
+        cur[p] = v;
+        fcur[p] = 1;
+      }
+      __syncthreads();
+    }
+    for (int k = 2; k <= d; ++k) {
+      // present positions in ascending order + their A-row bounds
+      if (tid < 32) {
+        int np = 0;
+        for (int base = 0; base < m; base += 32) {
+          const int q = base + tid;
+          const bool pres = q < m && fcur[q];
+          const unsigned bal = __ballot_sync(0xffffffffu, pres);
+          if (pres) list[np + __popc(bal & ((1u << tid) - 1u))] = q;
+          np += __popc(bal);
+        }
+        if (tid == 0) s_np = np;
+      }
+      __syncthreads();
+      const int np = s_np;
+      for (int t = tid; t < np; t += NT) {
+        const int q = list[t];
+        const int col_q = a.Pc[pb + q];
+        const int rq = a.rowmap ? a.rowmap[col_q] : col_q;
+        rbs[t] = a.Ap[rq];
+        res[t] = a.Ap[rq + 1];
+      }
+      __syncthreads();
+      for (int t = 0; t < np; ++t) {
+        const double l = cur[list[t]];
+        const int rb = rbs[t], re = res[t];
+        for (int jj = rb + tid; jj < re; jj += NT) {
+          const int p = map_find(keys, pv, a.bits, a.Ac[jj]);
+          if (p >= 0) {
+            nxt[p] = add_rn(nxt[p], mul_rn(l, a.Av[jj]));
+            fnxt[p] = 1;
+          }
+        }
+        __syncthreads();
+      }
+      const double ck = a.coef[k];
+      for (int i = tid; i < m; i += NT) {
+        if (fnxt[i]) {
+          acc[i] = add_rn(acc[i], mul_rn(ck, nxt[i]));
+          facc[i] = 1;
+        }
+        cur[i] = nxt[i];
+        fcur[i] = fnxt[i];
+        nxt[i] = 0.0;
+        fnxt[i] = 0;
+      }
+      __syncthreads();
+    }
+    if (tid == 0) s_cnt = 0;
+    __syncthreads();
+    int c = 0;
+    for (int i = tid; i < m; i += NT) {
+      const bool keep = d == 0 ? (bool)facc[i] : (facc[i] && acc[i] != 0.0);
+      a.out_val[pb + i] = acc[i];
+      a.out_keep[pb + i] = keep;
+      c += keep;
+    }
+    c = warp_sum(c);
+    if ((tid & 31) == 0 && c) atomicAdd(&s_cnt, c);
+    __syncthreads();
+    if (tid == 0) a.out_cnt[row] = s_cnt;
+    __syncthreads();
+  }
+}
+
 __global__ void compact_keep_kernel(int m, const int* __restrict__ pp, const int* __restrict__ pc,
                                     const double* __restrict__ pv, const unsigned char* __restrict__ keep,
                                     const int* __restrict__ optr, int* __restrict__ oc,
@@ -382,6 +506,8 @@ static int max_row_len(int m, const int* p, int* out, cudaStream_t s) {
 // longest row) and each class runs with its own shared-memory footprint
 // (43 B x cap per warp), so a few long rows no longer cut the occupancy of
 // every row of the level.
+static const int kPolyBlockCap = getenv("AIRG_POLY_BLOCK_CAP") ? atoi(getenv("AIRG_POLY_BLOCK_CAP")) : 256;
+
 static int run_poly_kernel(PolyArgs& a, int maxlen, cudaStream_t s) {
   int capmax = 32;
   while (capmax < maxlen) capmax <<= 1;
@@ -397,6 +523,8 @@ static int run_poly_kernel(PolyArgs& a, int maxlen, cudaStream_t s) {
   if (!attr) {
     AIRG_CUDA(cudaFuncSetAttribute(poly_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    smem_limit()));
+    AIRG_CUDA(cudaFuncSetAttribute(poly_assemble_block_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem_limit()));
     attr = true;
   }
   std::vector<long long> th;
@@ -417,11 +545,18 @@ static int run_poly_kernel(PolyArgs& a, int maxlen, cudaStream_t s) {
     b.bits = ceil_log2(2ll * b.cap);
     b.rows = cl.list(c);
     b.nrows = nr;
-    const size_t per = per_warp(b.cap);
-    int warps = 4;
-    while (warps > 1 && per * warps > (size_t)smem_limit()) warps >>= 1;
-    poly_assemble_kernel<<<blocks_for(nr, warps, 148 * 32), warps * 32, per * warps,
-                           fk.stream(c)>>>(b);
+    if (b.cap >= kPolyBlockCap && !b.masked) {  // long rows: CTA per row
+      const size_t T = (size_t)1 << b.bits;
+      const size_t shm = T * 8 + (size_t)b.cap * (24 + 12 + 3);
+      poly_assemble_block_kernel<<<std::min(nr, 148 * 16), b.cap >= 512 ? 256 : 128, shm,
+                                   fk.stream(c)>>>(b);
+    } else {
+      const size_t per = per_warp(b.cap);
+      int warps = 4;
+      while (warps > 1 && per * warps > (size_t)smem_limit()) warps >>= 1;
+      poly_assemble_kernel<<<blocks_for(nr, warps, 148 * 32), warps * 32, per * warps,
+                             fk.stream(c)>>>(b);
+    }
     AIRG_LAUNCH_CHECK();
   }
   AIRG_TRY(fk.end(s));
