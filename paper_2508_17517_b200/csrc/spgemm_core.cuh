@@ -29,9 +29,13 @@ __device__ __forceinline__ int set_insert(int* keys, int bits, int key) {
   const unsigned mask = (1u << bits) - 1u;
   unsigned h = hash_of(key, bits);
   for (unsigned probe = 0; probe <= mask; ++probe) {
-    const int prev = atomicCAS(keys + h, kEmpty, key);
-    if (prev == kEmpty) return 1;
-    if (prev == key) return 0;
+    const int cur = keys[h];  // most products hit a present key: read before CAS
+    if (cur == key) return 0;
+    if (cur == kEmpty) {
+      const int prev = atomicCAS(keys + h, kEmpty, key);
+      if (prev == kEmpty) return 1;
+      if (prev == key) return 0;
+    }
     h = (h + 1u) & mask;
   }
   return 1 << 20;
