@@ -1559,6 +1559,21 @@ struct DLev {
   P2PHalo pR, pC, pF[3];  // pF: targets rhs_ext, y0, y1
 };
 
+// one NCCL communicator per process, shared by every distributed plan, plus
+// the process's IPC arena for the P2P transport: grow-only, laid out by the
+// most recent plan (owner); peers' mappings are re-opened only when their
+// arena generation changes
+struct airg_comm {
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  double* arena = nullptr;
+  size_t cap = 0;  // doubles
+  int gen = 0;
+  std::vector<double*> peer_base;
+  std::vector<int> peer_gen;
+  long long owner = -1, next_id = 0;
+};
+
 struct airg_dplan {
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
@@ -1577,7 +1592,10 @@ struct airg_dplan {
   int tail_n = 0, tmax = 0;
   int *d_tcnt = nullptr, *d_tofs = nullptr;
   double *tsend = nullptr, *trecv = nullptr, *tr_full = nullptr, *te_full = nullptr;
-  // P2P transport state
+  // P2P transport state (arena owned by the communicator)
+  airg_comm* cm = nullptr;
+  long long id = 0;
+  int arena_gen = -1;
   double* arena = nullptr;
   std::vector<double*> peer_base;
   double* nslots = nullptr;
@@ -1848,8 +1866,22 @@ static int p2p_setup(airg_dplan* p) {
   const size_t fl_off = off;
   mine[k++] = (long long)off;
   off += up((size_t)W);
-  AIRG_CUDA(cudaMalloc((void**)&p->arena, off * sizeof(double)));
+  airg_comm* cm = p->cm;
+  if (off > cm->cap) {  // grow (peers re-open on the generation change)
+    AIRG_CUDA(cudaDeviceSynchronize());
+    if (cm->arena) AIRG_CUDA(cudaFree(cm->arena));
+    cm->arena = nullptr;
+    cm->cap = off + off / 4;
+    AIRG_CUDA(cudaMalloc((void**)&cm->arena, cm->cap * sizeof(double)));
+    ++cm->gen;
+  }
+  p->arena = cm->arena;
+  p->arena_gen = cm->gen;
+  cm->owner = p->id;
+  // the message counts restart at zero for this layout; the peers cannot
+  // write into it before the directory exchange below
   AIRG_CUDA(cudaMemset(p->arena, 0, off * sizeof(double)));
+  AIRG_CUDA(cudaDeviceSynchronize());
   for (int l = 0; l < nd; ++l) {
     DLev& L = p->lv[l];
     double** vs[kDirLev] = {&L.r_ext, &L.ec_ext, &L.rhs_ext, &L.y0, &L.y1};
@@ -1862,13 +1894,14 @@ static int p2p_setup(airg_dplan* p) {
   p->flags = (unsigned long long*)(p->arena + fl_off);
   // exchange directories + IPC handles (one NCCL all-gather at build time)
   const size_t dl = dir_len(nd, W);
-  const size_t rec = dl + 8;  // + 64 bytes of cudaIpcMemHandle_t
+  const size_t rec = dl + 9;  // + 64 bytes of cudaIpcMemHandle_t + arena generation
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
   std::vector<long long> hrec(rec);
   std::copy(mine.begin(), mine.end(), hrec.begin());
   cudaIpcMemHandle_t hdl;
   AIRG_CUDA(cudaIpcGetMemHandle(&hdl, p->arena));
   memcpy(hrec.data() + dl, &hdl, 64);
+  hrec[dl + 8] = cm->gen;
   long long *dsend = nullptr, *drecv = nullptr;
   AIRG_CUDA(cudaMalloc((void**)&dsend, rec * sizeof(long long)));
   AIRG_CUDA(cudaMalloc((void**)&drecv, rec * W * sizeof(long long)));
@@ -1880,19 +1913,28 @@ static int p2p_setup(airg_dplan* p) {
   cudaFree(dsend);
   cudaFree(drecv);
   std::vector<long long> dir(dl * W);
-  p->peer_base.assign(W, nullptr);
+  if ((int)cm->peer_base.size() != W) {
+    cm->peer_base.assign(W, nullptr);
+    cm->peer_gen.assign(W, -1);
+  }
   for (int q = 0; q < W; ++q) {
     std::copy(all.begin() + q * rec, all.begin() + q * rec + dl, dir.begin() + q * dl);
     if (q == me) {
-      p->peer_base[q] = p->arena;
+      cm->peer_base[q] = p->arena;
+      cm->peer_gen[q] = cm->gen;
       continue;
     }
+    const int g = (int)all[q * rec + dl + 8];
+    if (cm->peer_gen[q] == g && cm->peer_base[q]) continue;
+    if (cm->peer_base[q]) cudaIpcCloseMemHandle(cm->peer_base[q]);
     cudaIpcMemHandle_t h;
     memcpy(&h, all.data() + q * rec + dl, 64);
     void* base = nullptr;
     AIRG_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
-    p->peer_base[q] = (double*)base;
+    cm->peer_base[q] = (double*)base;
+    cm->peer_gen[q] = g;
   }
+  p->peer_base = cm->peer_base;
   // descriptors
   const size_t per_lev = kDirLev + 3 * (1 + W);
   for (int l = 0; l < nd; ++l) {
@@ -1942,13 +1984,15 @@ static int p2p_setup(airg_dplan* p) {
     p->nd = nd_;
     p->nwait = w;
   }
-  unsigned long long* ctr = nullptr;
-  AIRG_TRY(dalloc_owned(p, &ctr, (size_t)3 * W + 2));
-  AIRG_CUDA(cudaMemset(ctr, 0, ((size_t)3 * W + 2) * sizeof(unsigned long long)));
-  p->sent = ctr;
-  p->recvd = ctr + W;
-  p->ncount = ctr + 2 * W;
-  p->ticket = (unsigned int*)(ctr + 2 * W + 1);
+  if (!p->sent) {
+    unsigned long long* ctr = nullptr;
+    AIRG_TRY(dalloc_owned(p, &ctr, (size_t)3 * W + 2));
+    p->sent = ctr;
+    p->recvd = ctr + W;
+    p->ncount = ctr + 2 * W;
+    p->ticket = (unsigned int*)(ctr + 2 * W + 1);
+  }
+  AIRG_CUDA(cudaMemset(p->sent, 0, ((size_t)3 * W + 2) * sizeof(unsigned long long)));
   AIRG_CUDA(cudaDeviceSynchronize());
   return AIRG_OK;
 }
@@ -1962,11 +2006,6 @@ int airg_nccl_unique_id(char* out_h) {
   return AIRG_OK;
 }
 
-// one NCCL communicator per process, shared by every distributed plan
-struct airg_comm {
-  ncclComm_t comm = nullptr;
-  int rank = 0, world = 1;
-};
 
 int airg_comm_create(const char* id_h, int rank, int world, airg_comm** out) {
   airg_comm* c = new airg_comm();
@@ -1981,6 +2020,10 @@ int airg_comm_create(const char* id_h, int rank, int world, airg_comm** out) {
 
 int airg_comm_destroy(airg_comm* c) {
   if (!c) return AIRG_OK;
+  cudaDeviceSynchronize();
+  for (int q = 0; q < (int)c->peer_base.size(); ++q)
+    if (q != c->rank && c->peer_base[q]) cudaIpcCloseMemHandle(c->peer_base[q]);
+  if (c->arena) cudaFree(c->arena);
   if (c->comm) ncclCommDestroy(c->comm);
   delete c;
   return AIRG_OK;
@@ -1995,6 +2038,8 @@ int airg_dplan_create(airg_comm* c, int ndist, airg_dplan** out) {
   p->rank = c->rank;
   p->world = c->world;
   p->comm = c->comm;
+  p->cm = c;
+  p->id = c->next_id++;
   p->lv.resize(ndist);
   AIRG_CUDA(cudaStreamCreateWithFlags(&p->cs, cudaStreamNonBlocking));
   AIRG_CUDA(cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming));
@@ -2094,10 +2139,7 @@ int airg_dplan_destroy(airg_dplan* p) {
   if (!p) return AIRG_OK;
   if (p->cs) cudaStreamSynchronize(p->cs);
   if (p->graph) cudaGraphExecDestroy(p->graph);
-  for (int q = 0; q < (int)p->peer_base.size(); ++q)
-    if (q != p->rank && p->peer_base[q]) cudaIpcCloseMemHandle(p->peer_base[q]);
-  if (p->arena) cudaFree(p->arena);
-  for (void* b : p->owned) dfree(b);
+  for (void* b : p->owned) dfree(b);  // the arena and the peer mappings belong to the communicator
   if (p->cs) cudaStreamDestroy(p->cs);
   if (p->ev_in) cudaEventDestroy(p->ev_in);
   if (p->ev_out) cudaEventDestroy(p->ev_out);
@@ -2112,6 +2154,16 @@ int airg_dplan_richardson(airg_dplan* p, const double* b, double* x, double rtol
   cudaStream_t caller = (cudaStream_t)stream;
   cudaStream_t s = p->cs;
   const int n = p->top.nrows;
+  if (p->p2p && p->cm->owner != p->id) {
+    // a newer plan laid the shared arena out since: lay this plan out again
+    // (collective: every rank uses its plans in the same order)
+    double* old = p->arena;
+    AIRG_TRY(p2p_setup(p));
+    if (p->arena != old && p->graph) {
+      cudaGraphExecDestroy(p->graph);
+      p->graph = nullptr;
+    }
+  }
   AIRG_CUDA(cudaEventRecord(p->ev_in, caller));
   AIRG_CUDA(cudaStreamWaitEvent(s, p->ev_in, 0));
   AIRG_CUDA(cudaMemcpyAsync(p->x_ext, x, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, s));

@@ -210,6 +210,8 @@ class DLevel:
     nnz_Afc: int
     ddc_stats: tuple = ()
     pcol: torch.Tensor = None
+    halo_R: object = None   # ghost plan of R's columns (fine space), reused by the solve
+    halo_F: object = None   # ghost plan of A_ff's columns (F space)
 
 
 @dataclass
@@ -614,7 +616,7 @@ def setup_distributed(comm, A, cfg, poly_inject=None, replicate_below=20000, for
                               n=cur.rows.n, n_f=fpart.n, n_c=cpart.n,
                               nnz_A=comm.sum_int(cur.M.nnz), nnz_R=comm.sum_int(R.nnz),
                               nnz_Aff=comm.sum_int(A_ff.nnz), nnz_Afc=comm.sum_int(A_fc.nnz),
-                              ddc_stats=tuple(stats), pcol=pcol))
+                              ddc_stats=tuple(stats), pcol=pcol, halo_R=halo_r, halo_F=halo_ff))
         tick('spgemm_coarse')
         cur = DMat(Ac, cpart, cpart)
         level += 1
@@ -666,9 +668,10 @@ class DistSolver:
         self.comm = comm
         self.lv = []
         for d in H.dlevels:
-            hR = Halo(comm, d.fine, remote_cols(d.R.col_indices, d.fine, r))
+            # the R and A_ff ghost plans of the setup are the solve's
+            hR = d.halo_R or Halo(comm, d.fine, remote_cols(d.R.col_indices, d.fine, r))
             hC = Halo(comm, d.cpart, remote_cols(d.A_fc.col_indices, d.cpart, r))
-            hF = Halo(comm, d.fpart, remote_cols(d.A_ff.col_indices, d.fpart, r))
+            hF = d.halo_F or Halo(comm, d.fpart, remote_cols(d.A_ff.col_indices, d.fpart, r))
             self.lv.append(dict(
                 R=with_cols(d.R, hR.ext_cols(d.R.col_indices), hR.n_loc + hR.n),
                 hR=hR,
