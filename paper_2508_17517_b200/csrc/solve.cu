@@ -55,6 +55,42 @@ __device__ __forceinline__ void wait_count(const unsigned long long* flag, unsig
   }
 }
 
+// Programmatic dependent launch: a kernel launched with the programmatic
+// serialization attribute starts while its predecessor drains; it waits here
+// (until the predecessor grid completed and its writes are visible) before
+// touching any input, then lets its own successor be scheduled.  Both are
+// no-ops for a normal launch.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+
+static bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) v = getenv("AIRG_PDL") && atoi(getenv("AIRG_PDL")) == 0 ? 0 : 1;
+  return v == 1;
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*k)(KArgs...), int grid, int block, cudaStream_t s,
+                              Args&&... args) {
+  if (!pdl_enabled()) {
+    k<<<grid, block, 0, s>>>(std::forward<Args>(args)...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 template <bool E>
 __device__ __forceinline__ double madd(double a, double b, double c) {
   return E ? add_rn(c, mul_rn(a, b)) : fma(a, b, c);
@@ -70,6 +106,7 @@ __global__ void __launch_bounds__(256) spmv_vec_kernel(int nrows, const int* __r
                                                        const double* __restrict__ val,
                                                        const double* __restrict__ x, double xs,
                                                        Epi ep) {
+  pdl_enter();
   const int lane = threadIdx.x & (VS - 1);
   const long long row = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / VS;
   double s = 0.0;
@@ -172,8 +209,11 @@ static int launch_spmv(const Csr& A, const double* x, double xs, const Epi& ep, 
   }
   const long long groups = (long long)A.nrows * A.vs;
   const int blocks = (int)((groups + threads - 1) / threads);
-#define AIRG_SPMV_CASE(V) \
-  case V: spmv_vec_kernel<V, false><<<blocks, threads, 0, s>>>(A.nrows, A.ptr, A.col, A.val, x, xs, ep); break;
+#define AIRG_SPMV_CASE(V)                                                                  \
+  case V:                                                                                \
+    AIRG_CUDA(launch_pdl(spmv_vec_kernel<V, false>, blocks, threads, s, A.nrows, A.ptr, A.col, \
+                         A.val, x, xs, ep));                                             \
+    break;
   switch (A.vs) {
     AIRG_SPMV_CASE(1)
     AIRG_SPMV_CASE(2)
@@ -198,6 +238,7 @@ template <bool E>
 __global__ void axpby_kernel(long long n, double* __restrict__ out, const int* __restrict__ omap,
                              double a, const double* __restrict__ x, const int* __restrict__ xmap,
                              double b, const double* __restrict__ y) {
+  pdl_enter();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     double r = mul<E>(a, x[xmap ? xmap[i] : i]);
@@ -211,7 +252,7 @@ static int launch_axpby(long long n, double* out, const int* omap, double a, con
                         bool exact = false) {
   if (n == 0) return AIRG_OK;
   if (exact) axpby_kernel<true><<<blocks_for(n, 256), 256, 0, s>>>(n, out, omap, a, x, xmap, b, y);
-  else axpby_kernel<false><<<blocks_for(n, 256), 256, 0, s>>>(n, out, omap, a, x, xmap, b, y);
+  else AIRG_CUDA(launch_pdl(axpby_kernel<false>, blocks_for(n, 256), 256, s, n, out, omap, a, x, xmap, b, y));
   ++g_launches;
   AIRG_LAUNCH_CHECK();
   return AIRG_OK;
