@@ -304,8 +304,16 @@ class SerialWorkload:
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / nv
         vbytes = count_cycle_bytes(H, include_top=False)
+        self.traffic = None
+        try:  # ncu DRAM bytes of one V-cycle of this configuration (profiles/)
+            t = json.load(open(os.path.join(ROOT, 'profiles', 'r01_vcycle_traffic.json')))
+            if int(t['algorithmic_bytes']) == int(vbytes):
+                self.traffic = int(t['dram_total_bytes'])
+        except Exception:
+            pass
         return ms, vbytes, ('one V-cycle (R/A_fc/A_ff SpMV chains + Newton coarse solve); '
-                            f'algorithmic bytes {vbytes} (count_cycle_bytes)')
+                            f'algorithmic bytes {vbytes} (count_cycle_bytes); traffic = ncu '
+                            'dram__bytes_read+write of the same V-cycle (profiles/r01_vcycle_traffic.json)')
 
     def e2e(self):
         """Step through the public API from pinned host buffers."""
@@ -510,7 +518,7 @@ def ours_arm(args, rank, world, local):
             **W.extra(H, st),
             'vcycle_ms': vms,
             'roofline': {'bound': 'hbm', 'achieved': achieved, 'peak': peak, 'unit': 'GB/s',
-                         'frac': achieved / peak, 'traffic': None, 'kernel': what,
+                         'frac': achieved / peak, 'traffic': getattr(W, 'traffic', None), 'kernel': what,
                          'peak_source': peak_src},
             'e2e': {'value': W.n_total / (e2e_ms * 1e-3), 'unit': 'DOF/s',
                     'h2d_bytes_per_step': int(h2d), 'd2h_bytes_per_step': int(d2h),
