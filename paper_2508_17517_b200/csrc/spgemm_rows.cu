@@ -494,28 +494,55 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
   if (m > 0) rowlen_kernel<<<blocks_for(m, 256), 256, 0, s>>>(m, Cp, rl);
   {
     Classes cl;
-    AIRG_TRY(classify(m, rl, {32, 128, 512, 1024, 2048}, cl, s));
-    const int cbits[5] = {6, 8, 10, 11, 12}, cwarps[5] = {8, 8, 8, 4, 2};
+    // output-length classes: <= 32 / 128 warp per row; <= 512 ... 8192 CTA per
+    // row with a shared table of 2 x class slots (bits 10 .. 14; the 8192 class
+    // takes 197 KB, one CTA per SM); longer rows use global tables
+    AIRG_TRY(classify(m, rl, {32, 128, 512, 1024, 2048, 4096, 8192}, cl, s));
+    const int cbits[7] = {6, 8, 10, 11, 12, 13, 14}, cwarps[2] = {8, 8};
+    constexpr int kGlobalClass = 7;
     AIRG_TRY(set_smem((const void*)spgemm_numeric_kernel, 200 * 1024));
     Fork fk;
     AIRG_TRY(fk.begin(s));
-    AIRG_TRY(set_smem((const void*)spgemm_numeric_block_kernel<128, 10>, 200 * 1024));
-    AIRG_TRY(set_smem((const void*)spgemm_numeric_block_kernel<256, 11>, 200 * 1024));
-    AIRG_TRY(set_smem((const void*)spgemm_numeric_block_kernel<256, 12>, 200 * 1024));
-    for (int c = 0; c < 5; ++c) {
+    static bool attr = false;
+    if (!attr) {
+      const int lim = 200 * 1024;  // >= the 8192-class table (193 KB)
+#define AIRG_F3(B) (const void*)spgemm_numeric_block_kernel<64, B>, \
+    (const void*)spgemm_numeric_block_kernel<128, B>, (const void*)spgemm_numeric_block_kernel<256, B>
+      for (const void* f : {AIRG_F3(10), AIRG_F3(11), AIRG_F3(12), AIRG_F3(13), AIRG_F3(14)})
+#undef AIRG_F3
+        AIRG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+      attr = true;
+    }
+    for (int c = 0; c < kGlobalClass; ++c) {
       const int nr = cl.count[c];
       if (!nr) continue;
       NumArgs a{A.p, A.c, A.v, B.p, B.c, B.v, cl.list(c), nr, cbits[c], Cp, ocol, oval, negate,
                 mode, tol, lump, cnt, anyd, nullptr, nullptr, nullptr, nullptr, row0};
-      if (c >= 2) {  // long rows: one CTA per row, table shared by the CTA
+      if (c >= 2) {
+        // one CTA per row, table shared by the CTA.  Threads per row measured
+        // at 2048^2 (level-5 Galerkin, tools/nt_sweep.sh): the steps carry one
+        // B row (~70-200 entries), so 128 threads beat 256 (38 vs 49 ms) for
+        // the 512..1024 class; the long classes keep 256.
         const size_t shm = (size_t)(1 << cbits[c]) * 12 + 1024;
         const int grid = std::min(nr, 148 * 32);
-        if (c == 2)
-          spgemm_numeric_block_kernel<128, 10><<<grid, 128, shm, fk.stream(c)>>>(a);
-        else if (c == 3)
-          spgemm_numeric_block_kernel<256, 11><<<grid, 256, shm, fk.stream(c)>>>(a);
-        else
-          spgemm_numeric_block_kernel<256, 12><<<grid, 256, shm, fk.stream(c)>>>(a);
+        static int nts[7] = {0, 0, 128, 128, 256, 256, 256};
+        static bool parsed = false;
+        if (!parsed) {  // AIRG_NT="t2,t3,t4,t5,t6" overrides (measurement only)
+          if (const char* e = getenv("AIRG_NT"))
+            sscanf(e, "%d,%d,%d,%d,%d", &nts[2], &nts[3], &nts[4], &nts[5], &nts[6]);
+          parsed = true;
+        }
+        const int nt = nts[c];
+#define AIRG_NUMBLK(T, B) spgemm_numeric_block_kernel<T, B><<<grid, T, shm, fk.stream(c)>>>(a)
+#define AIRG_NUMBLK3(B) \
+  if (nt == 64) AIRG_NUMBLK(64, B); else if (nt == 128) AIRG_NUMBLK(128, B); else AIRG_NUMBLK(256, B)
+        if (c == 2) { AIRG_NUMBLK3(10); }
+        else if (c == 3) { AIRG_NUMBLK3(11); }
+        else if (c == 4) { AIRG_NUMBLK3(12); }
+        else if (c == 5) { AIRG_NUMBLK3(13); }
+        else { AIRG_NUMBLK3(14); }
+#undef AIRG_NUMBLK3
+#undef AIRG_NUMBLK
       } else {
         const size_t shm = (size_t)cwarps[c] * ((1 << cbits[c]) * 12 + 1024);
         spgemm_numeric_kernel<<<blocks_for(nr, cwarps[c], 148 * 32), cwarps[c] * 32, shm,
@@ -524,10 +551,11 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
       AIRG_LAUNCH_CHECK();
     }
     AIRG_TRY(fk.end(s));
-    const int nr = cl.count[5];
+    const int nr = cl.count[kGlobalClass];
     if (nr) {
       std::vector<int> rows(nr);
-      AIRG_CUDA(cudaMemcpyAsync(rows.data(), cl.list(5), nr * sizeof(int), cudaMemcpyDeviceToHost, s));
+      AIRG_CUDA(cudaMemcpyAsync(rows.data(), cl.list(kGlobalClass), nr * sizeof(int),
+                                cudaMemcpyDeviceToHost, s));
       std::vector<long long> sizes;
       AIRG_TRY(gather_ll(rl, rows, sizes, s, m));
       GlobalTables g;
