@@ -59,11 +59,14 @@ __global__ void __launch_bounds__(128) spgemm_count_block_kernel(CountArgs a) {
       ovf = 0;
     }
     __syncthreads();
-    const int ab = a.Ap[row], ae = a.Ap[row + 1];
-    // warp w takes chunks of 32 A entries (w, w + nw, ...): the B-row bounds of
-    // a chunk are loaded lane-parallel, the next B row's first 32 columns are
-    // prefetched while the current row is inserted
-    for (int base = ab + 32 * w; base < ae; base += 32 * nw) {
+    const int ab0 = a.Ap[row], ae0 = a.Ap[row + 1];
+    // warp w takes a contiguous quarter of the A row (balanced), walked in
+    // chunks of 32 entries: the B-row bounds of a chunk are loaded
+    // lane-parallel, the next B row's first 32 columns are prefetched while the
+    // current row is inserted
+    const int len = ae0 - ab0;
+    const int ab = ab0 + (int)((long long)len * w / nw), ae = ab0 + (int)((long long)len * (w + 1) / nw);
+    for (int base = ab; base < ae; base += 32) {
       int bb = 0, be = 0;
       if (base + lane < ae) {
         const int k = a.Ac[base + lane];
