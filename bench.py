@@ -414,10 +414,15 @@ class DistWorkload:
         return step, h2d, 8 * n
 
     def extra(self, DH, st):
+        brk = {}
+        for k, v in DH.setup_breakdown.items():  # sub-phases ("spgemm_coarse.RAP") into their phase
+            if '@' in k:
+                continue
+            key = k.split('.')[0]
+            brk[key] = brk.get(key, 0.0) + v
         return {'levels': DH.num_levels, 'distributed_levels': len(DH.dlevels),
                 'truncated_at': DH.truncated_at,
-                'setup_breakdown_s': {k: round(v, 4) for k, v in DH.setup_breakdown.items()
-                                      if '.' not in k and '@' not in k}}
+                'setup_breakdown_s': {k: round(v, 4) for k, v in brk.items()}}
 
 
 def ours_arm(args, rank, world, local):

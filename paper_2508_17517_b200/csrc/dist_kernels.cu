@@ -374,8 +374,10 @@ int airg_luby_round(int n, const int32_t* cptr, const int32_t* ccol_ext, const d
     luby_block_ext_kernel<<<nb, 256, 0, s>>>(n, cptr, ccol_ext, (signed char*)st_ext, (signed char)mark,
                                              rem);
   AIRG_LAUNCH_CHECK();
-  AIRG_CUDA(cudaMemcpyAsync(remaining_h, rem, sizeof(int), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
+  if (remaining_h) {  // null: no convergence check this round (no host sync)
+    AIRG_CUDA(cudaMemcpyAsync(remaining_h, rem, sizeof(int), cudaMemcpyDeviceToHost, s));
+    AIRG_CUDA(cudaStreamSynchronize(s));
+  }
   release(rem, s);
   return AIRG_OK;
 }

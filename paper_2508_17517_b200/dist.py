@@ -317,19 +317,24 @@ def pmisr(comm, A, clo, seed, max_luby_loops=None):
     left = comm.sum_int(n)
     loops = 0
     rem = L.i32()
+    # the global undecided count is checked every `every` rounds (a round after
+    # convergence changes nothing: no undecided vertex is left to select)
+    every = 1 if max_luby_loops is not None else 3
     while left > 0:
         if max_luby_loops is not None and loops >= max_luby_loops:
             break
         if loops > 0 and loops % 120 == 0:
             st[st >= 3] = 1
         mark = 3 + loops % 120
+        check = (loops + 1) % every == 0
         L.call('airg_luby_round', n, L.ptr(clo.row_offsets), L.ptr(ccol), L.ptr(w_ext), L.ptr(gid),
                L.ptr(st), mark, 0, None, L.stream_handle())
         st[n:] = halo.values(st[:n])
         L.call('airg_luby_round', n, L.ptr(clo.row_offsets), L.ptr(ccol), L.ptr(w_ext), L.ptr(gid),
-               L.ptr(st), mark, 1, L.C.byref(rem), L.stream_handle())
+               L.ptr(st), mark, 1, L.C.byref(rem) if check else None, L.stream_handle())
         st[n:] = halo.values(st[:n])
-        left = comm.sum_int(rem.value)
+        if check:
+            left = comm.sum_int(rem.value)
         loops += 1
     labels = empty(n, torch.int8)
     L.call('airg_luby_finish', n, L.ptr(st), L.ptr(labels), L.stream_handle())
@@ -386,9 +391,15 @@ def ddc_pass(comm, A_ext, labels_ext, n, row0, fraction, nbins):
 
 def dist_arnoldi_coeffs(comm, A_ff, halo, order, seed):
     """GMRES polynomial (monomial) of a row-strip A_ff: device SpMV with halo,
-    allreduce'd MGS dot products (same recurrence as polynomial.py:68-110), host
-    coefficients from the (identical on every rank) Hessenberg block."""
+    Gram-Schmidt with the reference's selective reorthogonalisation and
+    lucky-breakdown rules (polynomial.py:68-110), host coefficients from the
+    (identical on every rank) Hessenberg block.  The projections of a sweep
+    are formed at once (classical Gram-Schmidt: V^T w, one allreduce of j+1
+    numbers) instead of one allreduce per basis vector; the coefficients then
+    differ from the modified Gram-Schmidt ones by rounding only, like the
+    serial GPU's (whose dot products round differently from the reference)."""
     from .gmres_poly import coeffs_from_hessenberg
+    from .csr import spmv
     r = comm.rank
     n, lo, N = A_ff.nrows, halo.part.lo(r), halo.part.n
     m = min(order + 1, N)
@@ -396,40 +407,37 @@ def dist_arnoldi_coeffs(comm, A_ff, halo, order, seed):
     v = empty(n, VAL)
     L.call('airg_pcg64_fill_at', *L.pcg_params(seed), lo, n, -1.0, 2.0, L.ptr(v), L.stream_handle())
 
-    def ddot(a, b):  # allreduced dot product kept on the device (no host sync)
-        return comm.allreduce(torch.dot(a, b).reshape(1))
+    def allred(t):  # one allreduce, one host read
+        return comm.allreduce(t).cpu().numpy()
 
-    def nrm(a):
-        return float(np.sqrt(ddot(a, a).item()))
-
-    from .csr import spmv
-    b = v / nrm(v)
-    beta = nrm(b)
+    b = v / float(np.sqrt(allred(torch.dot(v, v).reshape(1))[0]))
+    beta = float(np.sqrt(allred(torch.dot(b, b).reshape(1))[0]))
     if beta == 0:
         raise ValueError('cannot build a Krylov space from a zero vector')
-    V = [b / beta]
+    V = torch.empty((m + 1, n), dtype=VAL, device=v.device)
+    V[0] = b / beta
     H = np.zeros((m + 1, m))
-    Hd = torch.zeros((m + 1, m), dtype=VAL, device=v.device)
     hmax, k = 0.0, m
     for j in range(m):
         w = spmv(A_ext, halo.ext(V[j]))
-        before = nrm(w)
-        for sweep in range(2):
-            for i in range(j + 1):
-                h = ddot(V[i], w)
-                Hd[i, j] += h[0]
-                w = w - h * V[i]
-            hn = nrm(w)
-            if not (sweep == 0 and hn < 0.7 * before):
-                break
-        H[:j + 1, j] = Hd[:j + 1, j].cpu().numpy()
+        Vj = V[:j + 1]
+        g = allred(torch.cat([torch.mv(Vj, w), torch.dot(w, w).reshape(1)]))
+        before, h = float(np.sqrt(g[-1])), g[:-1].copy()
+        w = w - torch.mv(Vj.t(), torch.from_numpy(h).to(w.device))
+        hn = float(np.sqrt(allred(torch.dot(w, w).reshape(1))[0]))
+        if hn < 0.7 * before:  # second sweep
+            h2 = allred(torch.mv(Vj, w))
+            w = w - torch.mv(Vj.t(), torch.from_numpy(h2).to(w.device))
+            h += h2
+            hn = float(np.sqrt(allred(torch.dot(w, w).reshape(1))[0]))
+        H[:j + 1, j] = h
         H[j + 1, j] = hn
         hmax = max(hmax, float(np.linalg.norm(H[:j + 2, j])))
         if hn <= 1e-14 * hmax:
             H[j + 1, j] = 0.0
             k = j + 1
             break
-        V.append(w / hn)
+        V[j + 1] = w / hn
     if np.max(np.abs(H[:k + 1, :k])) == 0.0:
         raise ValueError('matrix is numerically zero on the Krylov space')
     return coeffs_from_hessenberg(H[:k + 1, :k].copy(), k, beta, order)
