@@ -218,6 +218,12 @@ int airg_drop_lump(int m, int ncols, const int32_t* p, const int32_t* c, const d
 int airg_galerkin(int n, int nc, const int32_t* Rp, const int32_t* Rc, const double* Rv,
                   const int32_t* Ap, const int32_t* Ac, const double* Av, const int32_t* pcol,
                   double a_drop, int lump, airg_csr_result** out, void* stream);
+/* A P for the one-point prolongator P[j, pcol[j]] = 1 (A: m x k, pcol[k],
+ * result m x nc): columns mapped and merged, values summed in A's column
+ * order, cancellation zeros kept.  ref: hierarchy.py:281-286 (A @ P),
+ * sparse.py:222-240 */
+int airg_ap_onepoint(int m, int k, int nc, const int32_t* Ap, const int32_t* Ac, const double* Av,
+                     const int32_t* pcol, airg_csr_result** out, void* stream);
 /* A[rows, cols] with colmap[old col] = new col or -1.  ref: sparse.py:278-304 */
 int airg_extract(int nr_sel, const int32_t* rows, const int32_t* p, const int32_t* c,
                  const double* v, const int32_t* colmap, int ncols_sel, airg_csr_result** out,

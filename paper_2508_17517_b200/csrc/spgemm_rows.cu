@@ -598,6 +598,151 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
   return AIRG_OK;
 }
 
+// ---- A P for a one-point P --------------------------------------------------
+// P[k, pcol[k]] = 1 (hierarchy.py:250-278), so row i of A P is A's row i with
+// its columns mapped through pcol and equal columns merged.  scipy csr_matmat
+// semantics with the reference's structural zeros (sparse.py:222-240): the
+// unique mapped columns ascending, value = 0 + a_1*1 + a_2*1 + ... in the
+// order of A's columns (cancellations stay as +0.0).  One warp per row, the
+// row staged in shared memory; the first occurrence of a column owns the
+// output entry, its rank among the unique columns is its position.  Rows are
+// written raw at A's offsets and compacted after the scan.
+constexpr int kApCap = 1024, kApWarps = 4;
+
+__global__ void __launch_bounds__(32 * kApWarps) ap_onepoint_kernel(
+    int n, const int* __restrict__ Ap, const int* __restrict__ Ac, const double* __restrict__ Av,
+    const int* __restrict__ pcol, int* __restrict__ rcol, double* __restrict__ rval, int* __restrict__ cnt) {
+  extern __shared__ unsigned char apsm[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int* cs = (int*)apsm + (size_t)w * kApCap;
+  double* as = (double*)(apsm + (size_t)kApWarps * kApCap * 4) + (size_t)w * kApCap;
+  unsigned char* fs = apsm + (size_t)kApWarps * kApCap * 12 + (size_t)w * kApCap;
+  for (long long r = (long long)blockIdx.x * kApWarps + w; r < n; r += (long long)gridDim.x * kApWarps) {
+    const int row = (int)r;
+    const int b = Ap[row], L = Ap[row + 1] - b;
+    for (int j = lane; j < L; j += 32) {
+      cs[j] = pcol[Ac[b + j]];
+      as[j] = Av[b + j];
+    }
+    __syncwarp();
+    int U = 0;
+    for (int j0 = 0; j0 < L; j0 += 32) {
+      const int j = j0 + lane;
+      bool first = false;
+      if (j < L) {
+        const int c = cs[j];
+        first = true;
+        for (int jj = 0; jj < j; ++jj)
+          if (cs[jj] == c) {
+            first = false;
+            break;
+          }
+        fs[j] = first ? 1 : 0;
+      }
+      U += __popc(__ballot_sync(kFull, first));
+    }
+    __syncwarp();
+    for (int j = lane; j < L; j += 32) {
+      if (!fs[j]) continue;
+      const int c = cs[j];
+      int rank = 0;
+      double s = 0.0;
+      for (int jj = 0; jj < L; ++jj) {
+        const int cj = cs[jj];
+        rank += (fs[jj] && cj < c) ? 1 : 0;
+        if (jj >= j && cj == c) s = add_rn(s, mul_rn(as[jj], 1.0));
+      }
+      rcol[b + rank] = c;
+      rval[b + rank] = s;
+    }
+    if (lane == 0) cnt[row] = U;
+    __syncwarp();
+  }
+}
+
+__global__ void ap_compact_kernel(int n, const int* __restrict__ Ap, const int* __restrict__ Cp,
+                                  const int* __restrict__ rcol, const double* __restrict__ rval,
+                                  int* __restrict__ oc, double* __restrict__ ov) {
+  const int lane = threadIdx.x & 31;
+  for (long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; r < n;
+       r += ((long long)gridDim.x * blockDim.x) >> 5) {
+    const int b = Ap[r], o = Cp[r], u = Cp[r + 1] - o;
+    for (int j = lane; j < u; j += 32) {
+      oc[o + j] = rcol[b + j];
+      ov[o + j] = rval[b + j];
+    }
+  }
+}
+
+__global__ void ap_maxlen_kernel(int n, const int* __restrict__ p, int* __restrict__ mx) {
+  int v = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    v = max(v, p[i + 1] - p[i]);
+  v = __reduce_max_sync(kFull, v);
+  if ((threadIdx.x & 31) == 0) atomicMax(mx, v);
+}
+
+static int ap_onepoint(const Mat& A, int nc, const int* pcol, airg_csr_result** out, cudaStream_t s) {
+  const int n = A.nrows;
+  int* info = nullptr;  // [max row length, nnz(A)]
+  AIRG_TRY(scratch(&info, 2, s));
+  AIRG_CUDA(cudaMemsetAsync(info, 0, sizeof(int), s));
+  if (n > 0) ap_maxlen_kernel<<<blocks_for(n, 256, 148 * 8), 256, 0, s>>>(n, A.p, info);
+  AIRG_LAUNCH_CHECK();
+  AIRG_CUDA(cudaMemcpyAsync(info + 1, A.p + n, sizeof(int), cudaMemcpyDeviceToDevice, s));
+  int hinfo[2];
+  AIRG_CUDA(cudaMemcpyAsync(hinfo, info, sizeof hinfo, cudaMemcpyDeviceToHost, s));
+  AIRG_CUDA(cudaStreamSynchronize(s));
+  release(info, s);
+  // the per-row merge is O(L x unique columns): for long rows (a row beyond the
+  // staging buffer, or > 300 entries on average, measured at the dense 2048^2
+  // levels) the general hash product is faster
+  if (hinfo[0] > kApCap || (long long)hinfo[1] > 300ll * n) {
+    int* Pp = nullptr;
+    double* Pv = nullptr;
+    AIRG_TRY(scratch(&Pp, A.ncols + 1, s));
+    AIRG_TRY(scratch(&Pv, A.ncols > 0 ? A.ncols : 1, s));
+    iota_kernel<<<blocks_for(A.ncols + 1, 256), 256, 0, s>>>(A.ncols, Pp);
+    ones_kernel<<<blocks_for(A.ncols, 256), 256, 0, s>>>(A.ncols, Pv);
+    AIRG_LAUNCH_CHECK();
+    Mat P{A.ncols, nc, Pp, pcol, Pv};
+    AIRG_TRY(spgemm_rows(A, P, 0, 0, 0.0, 0, out, s));
+    release(Pp, s);
+    release(Pv, s);
+    return AIRG_OK;
+  }
+  const long long annz = hinfo[1];
+  int *rcol = nullptr, *cnt = nullptr;
+  double* rval = nullptr;
+  AIRG_TRY(scratch(&rcol, annz > 0 ? annz : 1, s));
+  AIRG_TRY(scratch(&rval, annz > 0 ? annz : 1, s));
+  AIRG_TRY(scratch(&cnt, n + 1, s));
+  const size_t shm = (size_t)kApWarps * kApCap * 13;
+  static bool attr = false;
+  if (!attr) {
+    AIRG_CUDA(cudaFuncSetAttribute(ap_onepoint_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    attr = true;
+  }
+  if (n > 0)
+    ap_onepoint_kernel<<<blocks_for(n, kApWarps, 148 * 16), 32 * kApWarps, shm, s>>>(
+        n, A.p, A.c, A.v, pcol, rcol, rval, cnt);
+  AIRG_LAUNCH_CHECK();
+  airg_csr_result* r = new_result(n, nc, s);
+  long long nnz = 0;
+  AIRG_TRY(scan_counts(cnt, r->ptr, n, &nnz, s));
+  AIRG_TRY(result_alloc_entries(r, nnz, true));
+  if (n > 0)
+    ap_compact_kernel<<<blocks_for((long long)n * 32, 256), 256, 0, s>>>(n, A.p, r->ptr, rcol, rval,
+                                                                        r->col, r->val);
+  AIRG_LAUNCH_CHECK();
+  release(rcol, s);
+  release(rval, s);
+  release(cnt, s);
+  *out = r;
+  return AIRG_OK;
+}
+
 }  // namespace airg
 
 using namespace airg;
@@ -625,22 +770,21 @@ int airg_galerkin(int n, int nc, const int32_t* Rp, const int32_t* Rc, const dou
                   const int32_t* Ap, const int32_t* Ac, const double* Av, const int32_t* pcol,
                   double a_drop, int lump, airg_csr_result** out, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  int* Pp = nullptr;
-  double* Pv = nullptr;
-  AIRG_TRY(scratch(&Pp, n + 1, s));
-  AIRG_TRY(scratch(&Pv, n, s));
-  iota_kernel<<<blocks_for(n + 1, 256), 256, 0, s>>>(n, Pp);
-  ones_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, Pv);
-  AIRG_LAUNCH_CHECK();
-  Mat A{n, n, Ap, Ac, Av}, P{n, nc, Pp, pcol, Pv};
+  Mat A{n, n, Ap, Ac, Av};
   airg_csr_result* AP = nullptr;
-  AIRG_TRY(spgemm_rows(A, P, 0, 0, 0.0, 0, &AP, s));
+  AIRG_TRY(ap_onepoint(A, nc, pcol, &AP, s));
   Mat R{nc, n, Rp, Rc, Rv}, APm{n, nc, AP->ptr, AP->col, AP->val};
   AIRG_TRY(spgemm_rows(R, APm, 0, a_drop == 0.0 ? 0 : 1, a_drop, lump, out, s));
   airg_result_free(AP);
-  release(Pp, s);
-  release(Pv, s);
   return AIRG_OK;
+}
+
+// A P for a one-point prolongator given by pcol (rows of A on a strip with
+// ext columns: pcol has one entry per ext column); ref hierarchy.py:281-286
+int airg_ap_onepoint(int m, int k, int nc, const int32_t* Ap, const int32_t* Ac, const double* Av,
+                     const int32_t* pcol, airg_csr_result** out, void* stream) {
+  Mat A{m, k, Ap, Ac, Av};
+  return ap_onepoint(A, nc, pcol, out, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -600,10 +600,12 @@ def setup_distributed(comm, A, cfg, poly_inject=None, replicate_below=20000, for
         L.call('airg_prolong_onepoint', n, L.ptr(A_ext.row_offsets), L.ptr(A_ext.col_indices),
                L.ptr(A_ext.values), L.ptr(lab_ext), L.ptr(gpos_ext), L.ptr(pcol), L.stream_handle())
         pcol_ext = halo_a.ext(pcol)
-        P_ext = SparseMatrix(pcol_ext.numel(), cpart.n,
-                             torch.arange(pcol_ext.numel() + 1, device=dev, dtype=IDX), pcol_ext,
-                             torch.ones(pcol_ext.numel(), dtype=VAL, device=dev))
-        AP = _spgemm(A_ext, P_ext, cpart.n)
+        res = L.C.c_void_p()
+        L.call('airg_ap_onepoint', A_ext.nrows, A_ext.ncols, cpart.n, L.ptr(A_ext.row_offsets),
+               L.ptr(A_ext.col_indices), L.ptr(A_ext.values), L.ptr(pcol_ext), L.C.byref(res),
+               L.stream_handle())
+        AP = take(res)
+        AP = SparseMatrix(AP.nrows, cpart.n, AP.row_offsets, AP.col_indices, AP.values)
         tick('prolongator')
         halo_r = Halo(comm, cur.rows, remote_cols(R.col_indices, cur.rows, r))
         tick('spgemm_coarse.halo')
