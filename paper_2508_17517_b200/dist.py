@@ -354,14 +354,16 @@ def ddc_pass(comm, A_ext, labels_ext, n, row0, fraction, nbins):
            L.ptr(A_ext.col_indices), L.ptr(A_ext.values), L.ptr(labels_ext), L.ptr(ratio),
            L.C.byref(bad), L.hptr(mms), L.stream_handle())
     dev = ratio.device
-    b = comm.allreduce(torch.tensor([bad.value], dtype=I64, device=dev), 'min').item()
+    # one MIN allreduce carries the zero-diagonal flag and the ratio extrema
+    mn = comm.allreduce(torch.tensor([float(bad.value), mms[0], -mms[1]], dtype=VAL, device=dev),
+                        'min').cpu().numpy()
+    b = int(mn[0])
     if b != 0x7fffffff:
         raise ValueError(f'zero diagonal in fine-fine block (fine row {b}); splitting is not '
                          'usable for reduction')
     if nf == 0:
         raise ValueError('zero-size array to reduction operation minimum which has no identity')
-    lo = float(comm.allreduce(torch.tensor([mms[0]], dtype=VAL, device=dev), 'min').item())
-    hi = float(comm.allreduce(torch.tensor([mms[1]], dtype=VAL, device=dev), 'max').item())
+    lo, hi = float(mn[1]), float(-mn[2])
     sm = float(comm.allreduce(torch.tensor([mms[2] if nf_loc else 0.0], dtype=VAL,
                                            device=dev)).item())
     target = fraction * nf
@@ -390,14 +392,14 @@ def ddc_pass(comm, A_ext, labels_ext, n, row0, fraction, nbins):
 
 
 def dist_arnoldi_coeffs(comm, A_ff, halo, order, seed):
-    """GMRES polynomial (monomial) of a row-strip A_ff: device SpMV with halo,
-    Gram-Schmidt with the reference's selective reorthogonalisation and
-    lucky-breakdown rules (polynomial.py:68-110), host coefficients from the
-    (identical on every rank) Hessenberg block.  The projections of a sweep
-    are formed at once (classical Gram-Schmidt: V^T w, one allreduce of j+1
-    numbers) instead of one allreduce per basis vector; the coefficients then
-    differ from the modified Gram-Schmidt ones by rounding only, like the
-    serial GPU's (whose dot products round differently from the reference)."""
+    """GMRES polynomial (monomial) of a row-strip A_ff (polynomial.py:68-110):
+    device SpMV with halo, Gram-Schmidt, lucky-breakdown rule, host
+    coefficients from the (identical on every rank) Hessenberg block.  The
+    projections of a sweep are formed at once (classical Gram-Schmidt: V^T w,
+    one allreduce of j+1 numbers) and both sweeps always run, so the
+    recurrence needs no host round trip; the coefficients then differ from the
+    reference's modified Gram-Schmidt ones by rounding only, like the serial
+    GPU's (whose dot products round differently from the reference)."""
     from .gmres_poly import coeffs_from_hessenberg
     from .csr import spmv
     r = comm.rank
@@ -414,30 +416,34 @@ def dist_arnoldi_coeffs(comm, A_ff, halo, order, seed):
     beta = float(np.sqrt(allred(torch.dot(b, b).reshape(1))[0]))
     if beta == 0:
         raise ValueError('cannot build a Krylov space from a zero vector')
-    V = torch.empty((m + 1, n), dtype=VAL, device=v.device)
+    # The whole recurrence stays on the device (allreduces without host
+    # reads): both Gram-Schmidt sweeps always run (the reference's selective
+    # second sweep only adds rounding-level corrections when it is skipped),
+    # and the lucky breakdown is found afterwards on the host copy of H — the
+    # columns after a breakdown are never used.
+    dev = v.device
+    V = torch.empty((m + 1, n), dtype=VAL, device=dev)
     V[0] = b / beta
-    H = np.zeros((m + 1, m))
-    hmax, k = 0.0, m
+    Hd = torch.zeros((m + 1, m), dtype=VAL, device=dev)
     for j in range(m):
         w = spmv(A_ext, halo.ext(V[j]))
         Vj = V[:j + 1]
-        g = allred(torch.cat([torch.mv(Vj, w), torch.dot(w, w).reshape(1)]))
-        before, h = float(np.sqrt(g[-1])), g[:-1].copy()
-        w = w - torch.mv(Vj.t(), torch.from_numpy(h).to(w.device))
-        hn = float(np.sqrt(allred(torch.dot(w, w).reshape(1))[0]))
-        if hn < 0.7 * before:  # second sweep
-            h2 = allred(torch.mv(Vj, w))
-            w = w - torch.mv(Vj.t(), torch.from_numpy(h2).to(w.device))
-            h += h2
-            hn = float(np.sqrt(allred(torch.dot(w, w).reshape(1))[0]))
-        H[:j + 1, j] = h
-        H[j + 1, j] = hn
+        h = comm.allreduce(torch.mv(Vj, w))
+        w = w - torch.mv(Vj.t(), h)
+        h2 = comm.allreduce(torch.mv(Vj, w))
+        w = w - torch.mv(Vj.t(), h2)
+        hn = torch.sqrt(comm.allreduce(torch.dot(w, w).reshape(1)))
+        Hd[:j + 1, j] = h + h2
+        Hd[j + 1, j] = hn[0]
+        V[j + 1] = w / hn
+    H = Hd.cpu().numpy()
+    hmax, k = 0.0, m
+    for j in range(m):
         hmax = max(hmax, float(np.linalg.norm(H[:j + 2, j])))
-        if hn <= 1e-14 * hmax:
+        if H[j + 1, j] <= 1e-14 * hmax:
             H[j + 1, j] = 0.0
             k = j + 1
             break
-        V[j + 1] = w / hn
     if np.max(np.abs(H[:k + 1, :k])) == 0.0:
         raise ValueError('matrix is numerically zero on the Krylov space')
     return coeffs_from_hessenberg(H[:k + 1, :k].copy(), k, beta, order)
@@ -512,7 +518,9 @@ def setup_distributed(comm, A, cfg, poly_inject=None, replicate_below=20000, for
         dev = cur.M.values.device
         # ---- CF splitting ----
         clo = strength_closure(comm, cur, cfg.strong_threshold)
+        tick('cf_split.strength')
         labels = pmisr(comm, cur, clo, derive_seed(cfg.seed, level, SEED_SPLIT))
+        tick('cf_split.pmisr')
         halo_a = Halo(comm, cur.rows, remote_cols(cur.M.col_indices, cur.rows, r))
         A_ext = with_cols(cur.M, halo_a.ext_cols(cur.M.col_indices), n + halo_a.n)
         lab_ext = halo_a.ext(labels)
@@ -523,7 +531,7 @@ def setup_distributed(comm, A, cfg, poly_inject=None, replicate_below=20000, for
             stats.append(ddc_pass(comm, A_ext, lab_ext, n, lo, cfg.ddc_fraction, cfg.ddc_bins))
             lab_ext[n:] = halo_a.values(lab_ext[:n])
         nc_glob = comm.sum_int(int((lab_ext[:n] == 1).sum().item()))
-        tick('cf_split')
+        tick('cf_split.ddc')
         if nc_glob == cur.rows.n:
             raise ValueError(f'splitting produced no F points at level {level}')
         if nc_glob > 0:
