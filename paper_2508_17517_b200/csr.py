@@ -282,3 +282,38 @@ def random_unit_vector(n, seed):
     out = empty(n, VAL)
     L.call('airg_random_unit', *L.pcg_params(seed), int(n), L.ptr(out), None, L.stream_handle())
     return out
+
+
+def write_matrix_market(A, path):
+    """Matrix Market coordinate real general, values with 17 significant
+    digits (exact float64 round trip).  ref: sparse.py:370-381"""
+    p, c, v = A.to_host()
+    rows = np.repeat(np.arange(A.nrows), np.diff(p)) + 1
+    with open(path, 'w') as fh:
+        fh.write('%%MatrixMarket matrix coordinate real general\n')
+        fh.write(f'{A.nrows} {A.ncols} {len(v)}\n')
+        fh.writelines(f'{i} {j} {x:.16e}\n' for i, j, x in zip(rows, c + 1, v))
+
+
+def read_matrix_market(path):
+    """Read a Matrix Market coordinate real general file into a device CSR
+    (duplicates summed, sorted columns).  ref: sparse.py:384-410"""
+    with open(path) as fh:
+        banner = fh.readline().split()
+        if (len(banner) != 5 or banner[0] != '%%MatrixMarket'
+                or [t.lower() for t in banner[1:]] != ['matrix', 'coordinate', 'real', 'general']):
+            raise ValueError('expected a "matrix coordinate real general" file')
+        line = fh.readline()
+        while line.startswith('%'):
+            line = fh.readline()
+        dims = line.split()
+        if len(dims) != 3:
+            raise ValueError('malformed size line')
+        nrows, ncols, nnz = (int(t) for t in dims)
+        body = np.loadtxt(fh, comments='%', ndmin=2) if nnz else np.zeros((0, 3))
+    if body.size == 0:
+        body = body.reshape(0, 3)
+    if body.shape[0] != nnz or (nnz and body.shape[1] != 3):
+        raise ValueError('entry count does not match the size line')
+    return SparseMatrix.from_coo(nrows, ncols, body[:, 0].astype(np.int64) - 1,
+                                 body[:, 1].astype(np.int64) - 1, body[:, 2])
