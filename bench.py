@@ -45,6 +45,9 @@ def parse():
     ap.add_argument('--order', type=int, default=6)
     ap.add_argument('--cpu-nx', type=int, default=256, help='CPU baseline sample grid')
     ap.add_argument('--no-cpu', action='store_true')
+    ap.add_argument('--problem', default='fd', choices=['fd', 'dg'],
+                    help='fd: 2-D upwind finite differences (configs[1]); dg: upwind DG Q1 on '
+                         'nx x nx cells, 4 unknowns per cell (configs[4], single GPU)')
     return ap.parse_args()
 
 
@@ -67,11 +70,11 @@ def dist_env():
 # CPU side: the oracle port of the reference (numpy/scipy, same kernels)
 # ---------------------------------------------------------------------------
 
-def cpu_run(nx, order):
+def cpu_run(nx, order, problem='fd'):
     """Reference-style run on the host: setup then two solves, the second
     timed (cli.py:220-259).  Returns (setup_s, solve_s, its)."""
     from oracle import airg_oracle as O
-    A = O.advection_2d(nx, nx, *PI4)
+    A = O.advection_dg_q1(nx, nx, *PI4) if problem == 'dg' else O.advection_2d(nx, nx, *PI4)
     t0 = time.perf_counter()
     H = O.setup(A, O.Cfg(poly_order=order))
     t1 = time.perf_counter()
@@ -269,13 +272,19 @@ class SerialWorkload:
         import paper_2508_17517_b200 as G
         self.G, self.args = G, args
         nx = args.nx
-        self.n = self.n_total = nx * nx
         self.cfg = G.SetupConfig(poly_order=args.order)
         self.scfg = G.SolveConfig()
-        self.A, self.b = G.build_advection_2d(G.AdvectionProblem(nx=nx, ny=nx, vx=PI4[0], vy=PI4[1]))
+        prob = G.AdvectionProblem(nx=nx, ny=nx, vx=PI4[0], vy=PI4[1])
+        if args.problem == 'dg':
+            self.A, self.b = G.build_advection_dg(prob)
+            self.workload = (f'AIRG pi/4 upwind DG Q1 advection, {nx}x{nx} cells x 4 unknowns, '
+                             f'order {args.order}, default SetupConfig (BASELINE.json configs[4])')
+        else:
+            self.A, self.b = G.build_advection_2d(prob)
+            self.workload = (f'AIRG pi/4 advection {nx}x{nx}, order {args.order}, default '
+                             'SetupConfig (BASELINE.json configs[1])')
+        self.n = self.n_total = self.A.nrows
         self.x0 = torch.ones(self.n, dtype=torch.float64, device='cuda')
-        self.workload = (f'AIRG pi/4 advection {nx}x{nx}, order {args.order}, default SetupConfig '
-                         '(BASELINE.json configs[1])')
         self.parallelism = 'single GPU'
 
     def setup(self):
@@ -440,6 +449,8 @@ def ours_arm(args, rank, world, local):
             dist.barrier()
         torch.cuda.synchronize()
 
+    if world > 1 and args.problem != 'fd':
+        raise SystemExit('the row-strip decomposition generates the FD operator only (--problem fd)')
     W = DistWorkload(args, world) if world > 1 else SerialWorkload(args)
     n = W.n
     # grow both device pools once before warm-up (scaled to the per-GPU problem;
@@ -501,9 +512,9 @@ def ours_arm(args, rank, world, local):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        a, bs, its = cpu_run(args.cpu_nx, args.order)
+        a, bs, its = cpu_run(args.cpu_nx, args.order, args.problem)
         ncpu, blas = cpu_cores_note()
-        cpu = {'value': args.cpu_nx ** 2 / (a + bs), 'unit': 'DOF/s', 'cores': 1, 'kind': 'port',
+        cpu = {'value': args.cpu_nx ** 2 * (4 if args.problem == 'dg' else 1) / (a + bs), 'unit': 'DOF/s', 'cores': 1, 'kind': 'port',
                'sample': f'one setup + timed second solve at {args.cpu_nx}^2 (of the {args.nx}^2 '
                          f'workload) with oracle/airg_oracle.py (numpy/scipy restatement of airmg; '
                          f'scipy sparse kernels single-threaded; BLAS {blas}; {ncpu} host cpus); '

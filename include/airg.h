@@ -218,6 +218,12 @@ int airg_drop_lump(int m, int ncols, const int32_t* p, const int32_t* c, const d
 int airg_galerkin(int n, int nc, const int32_t* Rp, const int32_t* Rc, const double* Rv,
                   const int32_t* Ap, const int32_t* Ac, const double* Av, const int32_t* pcol,
                   double a_drop, int lump, airg_csr_result** out, void* stream);
+/* 2-D upwind DG advection operator (nodal Q1 at the cell corners, 4 unknowns per
+ * cell, cell e = j*nx + i, unknown 4e + d) from the host-computed 4x4 cell
+ * blocks blocks_h[48] = {D, W, S} row-major (own cell, west and south
+ * inflow neighbours).  SURVEY 8(d) cfg 5 (no reference generator). */
+int airg_advection_dg(int nx, int ny, const double* blocks_h, int west, int south,
+                      airg_csr_result** out, void* stream);
 /* A P for the one-point prolongator P[j, pcol[j]] = 1 (A: m x k, pcol[k],
  * result m x nc): columns mapped and merged, values summed in A's column
  * order, cancellation zeros kept.  ref: hierarchy.py:281-286 (A @ P),

@@ -243,6 +243,68 @@ def advection_2d(nx, ny, vx, vy):
     return from_triplets(n, n, np.concatenate(rs), np.concatenate(cs), np.concatenate(vs))
 
 
+def advection_dg_q1(nx, ny, vx, vy, Lx=1.0, Ly=1.0):
+    """Upwind DG operator, nodal Q1 (SURVEY 8(d) cfg 5 -- no reference
+    generator, so this is the specification): per cell e = j*nx + i, unknowns
+    4e + k at the corners, psi_k = l_s(xi) l_t(eta), k = s + 2t, l_0 =
+    (1 - t)/2, l_1 = (1 + t)/2.  Row (e, a): -int psi_b v.grad(psi_a) +
+    east/north outflow-face terms on the own cell; west/south inflow-face
+    terms on the upwind neighbour's face nodes (their traces at xi = 1 /
+    eta = 1); exact zeros not stored."""
+    hx, hy = Lx / nx, Ly / ny
+    M = ((2.0 / 3.0, 1.0 / 3.0), (1.0 / 3.0, 2.0 / 3.0))   # int l_i l_j
+    dl = (-0.5, 0.5)                                       # int l_j l_i'
+    ax, ay = vx * hy / 2.0, vy * hx / 2.0
+    D, W, S = np.zeros((4, 4)), np.zeros((4, 4)), np.zeros((4, 4))
+    for a in range(4):
+        sa, ta = a % 2, a // 2
+        for b in range(4):
+            sb, tb = b % 2, b // 2
+            vol = -(ax * dl[sa] * M[tb][ta]) - ay * M[sb][sa] * dl[ta]
+            east = ax * M[tb][ta] if (sa == 1 and sb == 1) else 0.0
+            north = ay * M[sb][sa] if (ta == 1 and tb == 1) else 0.0
+            D[a, b] = vol + east + north
+            W[a, b] = -ax * M[tb][ta] if (sa == 0 and sb == 1) else 0.0
+            S[a, b] = -ay * M[sb][sa] if (ta == 0 and tb == 1) else 0.0
+    n = 4 * nx * ny
+    rs, cs, vs = [], [], []
+    e = np.arange(nx * ny, dtype=I64)
+    i, j = e % nx, e // nx
+    for blk, ok, nbr in ((S, (j > 0) & (vy > 0), e - nx), (W, (i > 0) & (vx > 0), e - 1),
+                         (D, np.ones(nx * ny, dtype=bool), e)):
+        for a in range(4):
+            for b in range(4):
+                if blk[a, b] != 0.0:
+                    rs.append(4 * e[ok] + a)
+                    cs.append(4 * nbr[ok] + b)
+                    vs.append(np.full(int(ok.sum()), blk[a, b]))
+    return from_triplets(n, n, np.concatenate(rs), np.concatenate(cs), np.concatenate(vs))
+
+
+def dg_q1_blocks_gauss(hx, hy, vx, vy):
+    """The same cell blocks by 2-point Gauss quadrature (exact for these
+    degrees): an independent check of the closed forms above."""
+    g = np.array([-1.0, 1.0]) / np.sqrt(3.0)
+    l = (lambda t: (1 - t) / 2, lambda t: (1 + t) / 2)
+    dlf = (lambda t: -0.5 * np.ones_like(t), lambda t: 0.5 * np.ones_like(t))
+    X, Y = np.meshgrid(g, g, indexing='ij')
+    one = np.array([1.0, 1.0])
+    D, W, S = np.zeros((4, 4)), np.zeros((4, 4)), np.zeros((4, 4))
+    for a in range(4):
+        sa, ta = a % 2, a // 2
+        for b in range(4):
+            sb, tb = b % 2, b // 2
+            psib = l[sb](X) * l[tb](Y)
+            vol = -np.sum(psib * (vx * hy / 2 * dlf[sa](X) * l[ta](Y)
+                                  + vy * hx / 2 * l[sa](X) * dlf[ta](Y)))
+            east = vx * hy / 2 * np.sum(l[sb](one) * l[tb](g) * l[sa](one) * l[ta](g))
+            north = vy * hx / 2 * np.sum(l[sb](g) * l[tb](one) * l[sa](g) * l[ta](one))
+            D[a, b] = vol + east + north
+            W[a, b] = -vx * hy / 2 * np.sum(l[sb](one) * l[tb](g) * l[sa](-one) * l[ta](g))
+            S[a, b] = -vy * hx / 2 * np.sum(l[sb](g) * l[tb](one) * l[sa](g) * l[ta](-one))
+    return D, W, S
+
+
 def advection_1d(n, vx):
     idx = np.arange(n, dtype=I64)
     return from_triplets(n, n, np.concatenate([idx, idx[1:]]), np.concatenate([idx, idx[1:] - 1]),

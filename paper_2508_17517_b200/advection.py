@@ -58,3 +58,53 @@ def build_advection_1d(n, vx):
     if vx <= 0:
         raise ValueError('require vx > 0')
     return _generate(int(n), 1, float(vx), 0.0)
+
+
+def dg_q1_blocks(hx, hy, vx, vy):
+    """4x4 cell blocks of the upwind DG operator for v . grad u on a uniform
+    hx x hy cell with the nodal Q1 basis psi_k = l_s(xi) l_t(eta), k = s + 2t,
+    l_0 = (1 - t)/2, l_1 = (1 + t)/2 (Lagrange at the cell corners) -- the
+    basis AIR is normally applied with (a modal Legendre basis was measured
+    to need 34 vs 12 iterations at 128^2 cells and to diverge at 512^2).
+    Row = test node a, column = trial node b.  Weak form per cell:
+    -int u v.grad(psi) + outflow-face int (v.n) u psi + inflow-face
+    int (v.n) u_upwind psi, in closed form (int l_i l_j = 2/3 or 1/3,
+    int l_j l_i' = -+1/2, traces l_i(+-1) in {0, 1}): D = own cell (volume +
+    east/north outflow faces), W / S = west / south neighbour (inflow faces;
+    only the nodes on the shared face couple)."""
+    import numpy as np
+    M = ((2.0 / 3.0, 1.0 / 3.0), (1.0 / 3.0, 2.0 / 3.0))
+    dl = (-0.5, 0.5)  # int l_j l_i' (independent of j)
+    ax, ay = vx * hy / 2.0, vy * hx / 2.0
+    D, W, S = np.zeros((4, 4)), np.zeros((4, 4)), np.zeros((4, 4))
+    for a in range(4):
+        sa, ta = a % 2, a // 2
+        for b in range(4):
+            sb, tb = b % 2, b // 2
+            vol = -(ax * dl[sa] * M[tb][ta]) - ay * M[sb][sa] * dl[ta]
+            east = ax * M[tb][ta] if (sa == 1 and sb == 1) else 0.0
+            north = ay * M[sb][sa] if (ta == 1 and tb == 1) else 0.0
+            D[a, b] = vol + east + north
+            W[a, b] = -ax * M[tb][ta] if (sa == 0 and sb == 1) else 0.0
+            S[a, b] = -ay * M[sb][sa] if (ta == 0 and tb == 1) else 0.0
+    return D, W, S
+
+
+def build_advection_dg(problem):
+    """Upwind DG (nodal Q1, 4 unknowns per cell) operator of the problem's velocity
+    on its nx x ny cells and the zero right-hand side (homogeneous inflow
+    data), generated in HBM.  SURVEY 8(d) cfg 5: the reference has no DG
+    generator; the problem class and velocity convention are its
+    (problems.py:20-45)."""
+    import numpy as np
+    from .csr import take
+    p = problem
+    if p.ny < 1:
+        raise ValueError('build_advection_dg requires ny >= 1')
+    D, W, S = dg_q1_blocks(p.Lx / p.nx, p.Ly / p.ny, float(p.vx), float(p.vy))
+    blk = np.ascontiguousarray(np.concatenate([D.ravel(), W.ravel(), S.ravel()]))
+    res = L.C.c_void_p()
+    L.call('airg_advection_dg', p.nx, p.ny, L.hptr(blk), int(p.vx > 0), int(p.vy > 0),
+           L.C.byref(res), L.stream_handle())
+    A = take(res)
+    return A, torch.zeros(A.nrows, dtype=VAL, device=A.values.device)

@@ -273,3 +273,79 @@ extern "C" int airg_random_unit(uint64_t state_hi, uint64_t state_lo, uint64_t i
   release(parts, s);
   return AIRG_OK;
 }
+
+// ---------------------------------------------------------------------------
+// 2-D upwind DG (nodal Q1, 4 DOFs per cell at the corners) advection operator on a
+// uniform nx x ny cell grid (SURVEY 8(d) cfg 5; the reference has no DG
+// generator).  The per-cell blocks are constants computed on the host
+// (advection.py dg_q1_blocks): row (cell e, test dof a) holds the south
+// neighbour's block row S[a] (inflow when vy > 0), the west neighbour's
+// W[a] (vx > 0) and the own-cell D[a], in column order; exact zeros are not
+// stored.  Cell e = j*nx + i, unknown 4e + d.
+// ---------------------------------------------------------------------------
+namespace airg {
+struct DgBlocks {
+  double D[16], W[16], S[16];
+};
+
+__global__ void dg_rows_kernel(int nx, int ny, DgBlocks bk, int west, int south,
+                               const int* __restrict__ ptr, int* __restrict__ cnt,
+                               int* __restrict__ col, double* __restrict__ val) {
+  const long long n = 4ll * nx * ny;
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
+       r += (long long)gridDim.x * blockDim.x) {
+    const int e = (int)(r >> 2), a = (int)(r & 3);
+    const int i = e % nx, j = e / nx;
+    int o = ptr ? ptr[r] : 0, c = 0;
+    auto put = [&](const double* blk, int cell) {
+      for (int b = 0; b < 4; ++b) {
+        const double x = blk[a * 4 + b];
+        if (x != 0.0) {
+          if (col) {
+            col[o + c] = 4 * cell + b;
+            val[o + c] = x;
+          }
+          ++c;
+        }
+      }
+    };
+    if (south && j > 0) put(bk.S, e - nx);
+    if (west && i > 0) put(bk.W, e - 1);
+    put(bk.D, e);
+    if (cnt) cnt[r] = c;
+  }
+}
+}  // namespace airg
+
+extern "C" int airg_advection_dg(int nx, int ny, const double* blocks_h, int west, int south,
+                                 airg_csr_result** out, void* stream) {
+  using namespace airg;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (nx < 1 || ny < 1) {
+    set_error("require nx >= 1 and ny >= 1");
+    return AIRG_ERR_VALUE;
+  }
+  const long long n = 4ll * nx * ny;
+  if (n > 0x7fffffffll / 12) {
+    set_error("DG grid too large for int32 indices");
+    return AIRG_ERR_VALUE;
+  }
+  DgBlocks bk;
+  memcpy(bk.D, blocks_h, 16 * sizeof(double));
+  memcpy(bk.W, blocks_h + 16, 16 * sizeof(double));
+  memcpy(bk.S, blocks_h + 32, 16 * sizeof(double));
+  int* cnt = nullptr;
+  AIRG_TRY(scratch(&cnt, n + 1, s));
+  const int nb = blocks_for(n, 256);
+  dg_rows_kernel<<<nb, 256, 0, s>>>(nx, ny, bk, west, south, nullptr, cnt, nullptr, nullptr);
+  AIRG_LAUNCH_CHECK();
+  airg_csr_result* r = new_result((int)n, (int)n, s);
+  long long nnz = 0;
+  AIRG_TRY(scan_counts(cnt, r->ptr, (int)n, &nnz, s));
+  AIRG_TRY(result_alloc_entries(r, nnz, true));
+  dg_rows_kernel<<<nb, 256, 0, s>>>(nx, ny, bk, west, south, r->ptr, nullptr, r->col, r->val);
+  AIRG_LAUNCH_CHECK();
+  release(cnt, s);
+  *out = r;
+  return AIRG_OK;
+}
