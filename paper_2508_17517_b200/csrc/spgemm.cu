@@ -548,8 +548,10 @@ static int run_poly_kernel(PolyArgs& a, int maxlen, cudaStream_t s) {
     if (b.cap >= kPolyBlockCap && !b.masked) {  // long rows: CTA per row
       const size_t T = (size_t)1 << b.bits;
       const size_t shm = T * 8 + (size_t)b.cap * (24 + 12 + 3);
-      poly_assemble_block_kernel<<<std::min(nr, 148 * 16), b.cap >= 512 ? 256 : 128, shm,
-                                   fk.stream(c)>>>(b);
+      static const int nt128 = getenv("AIRG_POLY_NT128") ? atoi(getenv("AIRG_POLY_NT128")) : 64;
+      static const int nt256 = getenv("AIRG_POLY_NT256") ? atoi(getenv("AIRG_POLY_NT256")) : 128;
+      const int nt = b.cap >= 512 ? 256 : b.cap >= 256 ? nt256 : nt128;
+      poly_assemble_block_kernel<<<std::min(nr, 148 * 16), nt, shm, fk.stream(c)>>>(b);
     } else {
       const size_t per = per_warp(b.cap);
       int warps = 4;
