@@ -53,10 +53,19 @@ class Comm:
         return int(self.allreduce(torch.tensor([int(v)], dtype=I64, device=self.device)).item())
 
     def allgather_int(self, v):
-        t = torch.tensor([int(v)], dtype=I64, device=self.device)
-        out = [torch.empty_like(t) for _ in range(self.world)]
-        dist.all_gather(out, t, group=self.group)
-        return [int(x.item()) for x in out]
+        """Per-rank integers (one or a list per rank) -> list over ranks;
+        one host read."""
+        many = isinstance(v, (list, tuple))
+        t = torch.tensor(list(v) if many else [int(v)], dtype=I64, device=self.device)
+        out = torch.empty(self.world * t.numel(), dtype=I64, device=self.device)
+        dist.all_gather_into_tensor(out, t, group=self.group)
+        h = out.view(self.world, t.numel()).cpu().tolist()
+        return h if many else [x[0] for x in h]
+
+    def sum_ints(self, vals):
+        """Elementwise sum over ranks of a list of integers; one host read."""
+        t = torch.tensor([int(x) for x in vals], dtype=I64, device=self.device)
+        return self.allreduce(t).cpu().tolist()
 
     def allgather_v(self, t):
         """Concatenation over ranks of 1-D tensors of different lengths."""
@@ -526,11 +535,11 @@ def setup_distributed(comm, A, cfg, poly_inject=None, replicate_below=20000, for
         lab_ext = halo_a.ext(labels)
         stats = []
         for _ in range(cfg.ddc_its):
-            if comm.sum_int(int((lab_ext[:n] == 0).sum().item())) == 0:
+            if int(comm.allreduce((lab_ext[:n] == 0).sum().reshape(1).to(I64)).item()) == 0:
                 break
             stats.append(ddc_pass(comm, A_ext, lab_ext, n, lo, cfg.ddc_fraction, cfg.ddc_bins))
             lab_ext[n:] = halo_a.values(lab_ext[:n])
-        nc_glob = comm.sum_int(int((lab_ext[:n] == 1).sum().item()))
+        nc_glob = int(comm.allreduce((lab_ext[:n] == 1).sum().reshape(1).to(I64)).item())
         tick('cf_split.ddc')
         if nc_glob == cur.rows.n:
             raise ValueError(f'splitting produced no F points at level {level}')
@@ -541,8 +550,9 @@ def setup_distributed(comm, A, cfg, poly_inject=None, replicate_below=20000, for
             lab_ext[n:] = halo_a.values(lab_ext[:n])
         labels = lab_ext[:n].clone()
         f_loc, c_loc = _local_index(labels, 0), _local_index(labels, 1)
-        nf_all = comm.allgather_int(f_loc.numel())
-        nc_all = comm.allgather_int(c_loc.numel())
+        fc_all = comm.allgather_int([f_loc.numel(), c_loc.numel()])
+        nf_all = [x[0] for x in fc_all]
+        nc_all = [x[1] for x in fc_all]
         if sum(nc_all) == 0 or sum(nf_all) == 0:
             break  # the replicated tail builds the coarse solver here
         fpart, cpart = Part.from_counts(nf_all, dev), Part.from_counts(nc_all, dev)
@@ -629,11 +639,11 @@ def setup_distributed(comm, A, cfg, poly_inject=None, replicate_below=20000, for
         tick.note('nnz_AP', AP_rows.nnz)
         tick.note('nnz_Ac', Ac.nnz)
         tick.note('n', n)
+        nnz_A, nnz_R, nnz_Aff, nnz_Afc = comm.sum_ints([cur.M.nnz, R.nnz, A_ff.nnz, A_fc.nnz])
         dlevels.append(DLevel(R=R, A_ff=A_ff, A_fc=A_fc, f_loc=f_loc, c_loc=c_loc, labels=labels,
                               fine=cur.rows, fpart=fpart, cpart=cpart, f_smoother=sm,
                               n=cur.rows.n, n_f=fpart.n, n_c=cpart.n,
-                              nnz_A=comm.sum_int(cur.M.nnz), nnz_R=comm.sum_int(R.nnz),
-                              nnz_Aff=comm.sum_int(A_ff.nnz), nnz_Afc=comm.sum_int(A_fc.nnz),
+                              nnz_A=nnz_A, nnz_R=nnz_R, nnz_Aff=nnz_Aff, nnz_Afc=nnz_Afc,
                               ddc_stats=tuple(stats), pcol=pcol, halo_R=halo_r, halo_F=halo_ff))
         tick('spgemm_coarse')
         cur = DMat(Ac, cpart, cpart)
