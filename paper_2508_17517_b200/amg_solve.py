@@ -224,9 +224,13 @@ def count_cycle_bytes(H, include_top=True):
         tot += _spmat_bytes(lv.A_fc) + 8 * nc + 16 * nf
         if lv.f_smoother_assembled is not None:
             tot += 16 * nf + _spmat_bytes(lv.f_smoother_assembled)
+            tot += 16 * lv.n                      # scatter e[f] = e_f, e[c] = e_c
         else:
             tot += 16 * nf + d * (_spmat_bytes(lv.A_ff) + 24 * nf)
-        tot += 16 * lv.n
+            if p.kind == 'arnoldi_coeff' and d > 0:
+                tot += 16 * nc                    # e[f] written by the last Horner step
+            else:
+                tot += 16 * lv.n
     Cm, p = H.coarsest_A, H.coarse_solver
     if p.kind == 'newton_roots':
         i = 0

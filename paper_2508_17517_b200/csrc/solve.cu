@@ -723,25 +723,32 @@ static int newton_multi(const Poly& p, const Csr& A, const double* b, double* y,
 // y = q(A) b using scratch t0..t3 (each n doubles).  ymap: optional scatter
 // of the result (y[ymap[i]] = ...).  Only the Horner path supports ymap; the
 // caller handles others.
+// ymap (coefficient polynomials only): the result lands at y[ymap[i]] (the
+// V-cycle scatters e[f] = e_f through it instead of a separate kernel)
 static int poly_apply_dev(const Poly& p, const Csr& A, const double* b, double* y, double* t0,
                           double* t1, double* t2, double* t3, int* iflag, double* parts,
-                          NewtonState* nst, cudaStream_t s, bool exact) {
+                          NewtonState* nst, cudaStream_t s, bool exact,
+                          const int* ymap = nullptr) {
   const int n = A.nrows;
   if (n == 0) return AIRG_OK;
+  if (ymap && p.kind != 0) {
+    set_error("an output map needs a coefficient polynomial");
+    return AIRG_ERR_ARG;
+  }
   if (p.kind == 0) {
     const int d = (int)p.coef.size() - 1;
     if (d < 0) {
       set_error("empty coefficient polynomial");
       return AIRG_ERR_ARG;
     }
-    if (d == 0) return launch_axpby(n, y, nullptr, p.coef[0], b, nullptr, 0.0, nullptr, s, exact);
+    if (d == 0) return launch_axpby(n, y, ymap, p.coef[0], b, nullptr, 0.0, nullptr, s, exact);
     // y_1 = A (c_d b) + c_{d-1} b ; y_{j} = A y_{j-1} + c_j b
     const double* cur = b;
     double xs = p.coef[d];
     double* bufs[2] = {t0, t1};
     for (int j = d - 1; j >= 0; --j) {
       double* dst = (j == 0) ? y : bufs[j & 1];
-      Epi ep{dst, nullptr, 1.0, p.coef[j], b, nullptr, nullptr, nullptr};
+      Epi ep{dst, j == 0 ? ymap : nullptr, 1.0, p.coef[j], b, nullptr, nullptr, nullptr};
       AIRG_TRY(launch_spmv(A, cur, xs, ep, s, exact));
       cur = dst;
       xs = 1.0;
@@ -1202,6 +1209,13 @@ static int vcycle_rec(airg_plan* p, int level, const double* r, double* e, int f
   {
     Epi ep{L.rhs, nullptr, -1.0, 1.0, r, L.f_idx, nullptr, nullptr};
     AIRG_TRY(launch_spmv(L.Afc, L.ec, 1.0, ep, s, p->exact));
+  }
+  if (fits == 1 && !L.has_asm && L.sm.kind == 0) {
+    // e[f] = q(A_ff) rhs written straight through f_idx by the last Horner step
+    AIRG_TRY(poly_apply_dev(L.sm, L.Aff, L.rhs, e, L.t0, L.t1, L.t2, L.t2, p->iflag, p->parts,
+                            p->nst, s, p->exact, L.f_idx));
+    AIRG_TRY(launch_axpby(L.n_c, e, L.c_idx, 1.0, L.ec, nullptr, 0.0, nullptr, s, p->exact));
+    return AIRG_OK;
   }
   AIRG_TRY(smooth_level(p, L, L.rhs, L.ef, s));
   for (int it = 1; it < fits; ++it) {
