@@ -183,8 +183,11 @@ def hierarchy_summary(H):
 
 
 class _Timer:
-    """Per-phase wall-clock accumulation (hierarchy.py:184-197); the device
-    is synchronised at both ends so the phase owns its kernels."""
+    """Per-phase time accumulation (hierarchy.py:184-197).  CUDA events are
+    recorded on the setup stream at both ends of the phase (in stream order,
+    so the phase owns its kernels and any device idle time inside it); the
+    elapsed times are summed by _flush_timings once at the end of the level
+    loop, instead of synchronising the device twice per phase."""
 
     def __init__(self, sink, phase):
         self.sink = sink
@@ -192,16 +195,28 @@ class _Timer:
 
     def __enter__(self):
         import torch
-        torch.cuda.synchronize()
-        self.t0 = time.perf_counter()
+        if self.sink is not None:
+            self.e0 = torch.cuda.Event(enable_timing=True)
+            self.e0.record()
         return self
 
     def __exit__(self, *exc):
         import torch
-        torch.cuda.synchronize()
         if self.sink is not None:
-            self.sink[self.phase] = self.sink.get(self.phase, 0.0) + time.perf_counter() - self.t0
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record()
+            self.sink.setdefault('_pending', []).append((self.phase, self.e0, e1))
         return False
+
+
+def _flush_timings(sink):
+    """Sum the recorded phase events into seconds (one synchronisation)."""
+    pend = sink.pop('_pending', None) if sink is not None else None
+    if not pend:
+        return
+    pend[-1][2].synchronize()
+    for phase, e0, e1 in pend:
+        sink[phase] = sink.get(phase, 0.0) + e0.elapsed_time(e1) / 1e3
 
 
 def resolve_truncate_start(cfg, n_top):
@@ -454,4 +469,5 @@ def build_levels(A, cfg, level0, truncate_start, inj, polys, timings, keep_level
             levels[-1].A = current
         current = coarse
         level += 1
+    _flush_timings(timings)
     return levels, current, coarse_solver, truncated_at
