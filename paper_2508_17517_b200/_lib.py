@@ -111,8 +111,12 @@ def hptr(a):
 
 
 def stream_handle():
+    """Raw cudaStream_t of torch's current stream on the current device.
+    (torch.cuda.current_stream() costs ~16 us per call in device-index
+    bookkeeping; the setup makes thousands of library calls.)"""
     import torch
-    return vp(torch.cuda.current_stream().cuda_stream)
+    C_ = torch._C
+    return vp(C_._cuda_getCurrentRawStream(C_._cuda_getDevice()))
 
 
 # ---- signatures (mirror include/airg.h) ---------------------------------
