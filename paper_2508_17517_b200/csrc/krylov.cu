@@ -6,8 +6,7 @@
 // recurrence inside ONE CTA: V lives in global memory (L2-resident), every
 // dot product is a block reduction, no host round trips.  Large operators
 // use a device-resident multi-kernel path: SpMV, fixed-order dot partials,
-// axpy; the reorthogonalisation / breakdown decisions are taken on the host
-// from 2 scalars per step.
+// axpy, with the reorthogonalisation / breakdown decisions taken on the device.
 #include "setup_common.cuh"
 #include <vector>
 #include <cmath>
@@ -109,8 +108,21 @@ __global__ void __launch_bounds__(1024) arnoldi_cta_kernel(int n, const int* __r
 }
 
 // ---- multi-kernel path ----------------------------------------------------
+// The modified Gram-Schmidt recurrence of the single-CTA kernel, spread over
+// the GPU (SpMV, fixed-order dot partials + finish, axpy).  The selective
+// second sweep and the lucky-breakdown test are decided on the device by a
+// one-thread control kernel; later kernels read the decisions through a
+// Gate and exit early, so a whole Arnoldi is enqueued without a host round
+// trip (the host reads beta once and H, k at the end).
+struct Gate {
+  const int* stop;  // skip when *stop != 0 (breakdown reached)
+  const int* need;  // skip when need && *need == 0 (no second sweep)
+  __device__ __forceinline__ bool off() const { return (stop && *stop) || (need && !*need); }
+};
+
 __global__ void dot_partial_kernel(long long n, const double* __restrict__ x, const double* __restrict__ y,
-                                   double* __restrict__ parts) {
+                                   double* __restrict__ parts, Gate g) {
+  if (g.off()) return;
   __shared__ double red[33];
   double s = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -121,7 +133,9 @@ __global__ void dot_partial_kernel(long long n, const double* __restrict__ x, co
 }
 
 // out = sum(parts) (+ optional accumulate into *acc), fixed order
-__global__ void dot_finish_kernel(int np, const double* __restrict__ parts, double* out, double* acc) {
+__global__ void dot_finish_kernel(int np, const double* __restrict__ parts, double* out, double* acc,
+                                  Gate g) {
+  if (g.off()) return;
   __shared__ double red[33];
   double s = 0.0;
   for (int i = threadIdx.x; i < np; i += blockDim.x) s += parts[i];
@@ -133,22 +147,28 @@ __global__ void dot_finish_kernel(int np, const double* __restrict__ parts, doub
 }
 
 __global__ void axpy_dev_kernel(long long n, const double* __restrict__ hptr, const double* __restrict__ x,
-                                double* __restrict__ y) {
+                                double* __restrict__ y, Gate g) {
+  if (g.off()) return;
   const double h = *hptr;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     y[i] -= h * x[i];
 }
 
-__global__ void scale_div_kernel(long long n, const double* __restrict__ x, double d, double* __restrict__ y) {
+// y = x / d (d by value, or *dptr when given)
+__global__ void scale_div_kernel(long long n, const double* __restrict__ x, double d, const double* dptr,
+                                 double* __restrict__ y, Gate g) {
+  if (g.off()) return;
+  const double dd = dptr ? *dptr : d;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
-    y[i] = x[i] / d;
+    y[i] = x[i] / dd;
 }
 
 __global__ void spmv_rows_kernel(int n, const int* __restrict__ p, const int* __restrict__ c,
                                  const double* __restrict__ v, const double* __restrict__ x,
-                                 double* __restrict__ y) {
+                                 double* __restrict__ y, Gate g) {
+  if (g.off()) return;
   // warp per row (rows of coarse operators are long)
   const int lane = threadIdx.x & 31;
   for (long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; r < n;
@@ -160,15 +180,39 @@ __global__ void spmv_rows_kernel(int n, const int* __restrict__ p, const int* __
   }
 }
 
+// dsc: [0] scratch, [1] projection h, [2] ||w||^2 before, [3] ||w||^2 after, [4] hmax, [5] hn
+// ctl: [0] stopped, [1] second sweep, [2] k
+__global__ void arnoldi_ctl_kernel(int phase, int j, int m, double* Hd, double* dsc, int* ctl) {
+  if (ctl[0]) return;
+  const double hn = sqrt(dsc[3]);
+  if (phase == 0) {  // after sweep 0: reorthogonalise iff ||w|| dropped below 0.7 of before
+    ctl[1] = hn < 0.7 * sqrt(dsc[2]) ? 1 : 0;
+    return;
+  }
+  Hd[(size_t)(j + 1) * m + j] = hn;
+  double cn = 0.0;
+  for (int q = 0; q <= j + 1; ++q) {
+    const double h = Hd[(size_t)q * m + j];
+    cn = __dadd_rn(cn, __dmul_rn(h, h));
+  }
+  dsc[4] = fmax(dsc[4], sqrt(cn));
+  if (hn <= 1e-14 * dsc[4]) {  // lucky breakdown
+    Hd[(size_t)(j + 1) * m + j] = 0.0;
+    ctl[2] = j + 1;
+    ctl[0] = 1;
+  }
+  dsc[5] = hn;
+}
+
 struct DotCtx {
   double* parts;
   int np;
 };
 
 static int dev_dot(long long n, const double* x, const double* y, double* out, double* acc,
-                   const DotCtx& d, cudaStream_t s) {
-  dot_partial_kernel<<<d.np, 256, 0, s>>>(n, x, y, d.parts);
-  dot_finish_kernel<<<1, 256, 0, s>>>(d.np, d.parts, out, acc);
+                   const DotCtx& d, Gate g, cudaStream_t s) {
+  dot_partial_kernel<<<d.np, 256, 0, s>>>(n, x, y, d.parts, g);
+  dot_finish_kernel<<<1, 256, 0, s>>>(d.np, d.parts, out, acc, g);
   AIRG_LAUNCH_CHECK();
   return AIRG_OK;
 }
@@ -176,22 +220,26 @@ static int dev_dot(long long n, const double* x, const double* y, double* out, d
 static int arnoldi_multi(int n, const int* p, const int* c, const double* v, const double* b, int m,
                          double* H_h, int* k_h, double* beta_h, cudaStream_t s) {
   double *V = nullptr, *w = nullptr, *sc = nullptr, *Hd = nullptr;
+  int* ctl = nullptr;
   const int np = blocks_for(n, 256, 148 * 4);
   AIRG_TRY(scratch(&V, (size_t)(m + 1) * n, s));
   AIRG_TRY(scratch(&w, n, s));
   AIRG_TRY(scratch(&sc, np + 8, s));
   AIRG_TRY(scratch(&Hd, (size_t)(m + 1) * m, s));
+  AIRG_TRY(scratch(&ctl, 4, s));
   AIRG_CUDA(cudaMemsetAsync(Hd, 0, (size_t)(m + 1) * m * sizeof(double), s));
+  AIRG_CUDA(cudaMemsetAsync(sc, 0, 8 * sizeof(double), s));
+  const int ctl0[4] = {0, 0, m, 0};
+  AIRG_CUDA(cudaMemcpyAsync(ctl, ctl0, sizeof ctl0, cudaMemcpyHostToDevice, s));
   DotCtx d{sc + 8, np};
-  double* scal = sc;  // [0] scratch scalar
-  auto host_scalar = [&](double* dptr, double* out) -> int {
-    AIRG_CUDA(cudaMemcpyAsync(out, dptr, sizeof(double), cudaMemcpyDeviceToHost, s));
-    AIRG_CUDA(cudaStreamSynchronize(s));
-    return AIRG_OK;
-  };
+  double* dsc = sc;
+  const Gate always{nullptr, nullptr};
+  const Gate live{ctl, nullptr};        // until the breakdown
+  const Gate second{ctl, ctl + 1};      // second sweep only
   double bb = 0;
-  AIRG_TRY(dev_dot(n, b, b, scal, nullptr, d, s));
-  AIRG_TRY(host_scalar(scal, &bb));
+  AIRG_TRY(dev_dot(n, b, b, dsc, nullptr, d, always, s));
+  AIRG_CUDA(cudaMemcpyAsync(&bb, dsc, sizeof(double), cudaMemcpyDeviceToHost, s));
+  AIRG_CUDA(cudaStreamSynchronize(s));
   const double beta = std::sqrt(bb);
   *beta_h = beta;
   if (beta == 0.0) {
@@ -199,53 +247,35 @@ static int arnoldi_multi(int n, const int* p, const int* c, const double* v, con
     return AIRG_ERR_VALUE;
   }
   const int nb = blocks_for(n, 256);
-  scale_div_kernel<<<nb, 256, 0, s>>>(n, b, beta, V);
-  double hmax = 0.0;
-  int k = m;
-  std::vector<double> Hh((size_t)(m + 1) * m, 0.0);
+  scale_div_kernel<<<nb, 256, 0, s>>>(n, b, beta, nullptr, V, always);
   for (int j = 0; j < m; ++j) {
     const double* Vj = V + (size_t)j * n;
-    spmv_rows_kernel<<<blocks_for((long long)n * 32, 256), 256, 0, s>>>(n, p, c, v, Vj, w);
+    spmv_rows_kernel<<<blocks_for((long long)n * 32, 256), 256, 0, s>>>(n, p, c, v, Vj, w, live);
     AIRG_LAUNCH_CHECK();
-    double before2 = 0, hn2 = 0;
-    AIRG_TRY(dev_dot(n, w, w, scal, nullptr, d, s));
-    AIRG_TRY(host_scalar(scal, &before2));
-    const double before = std::sqrt(before2);
-    double hn = 0.0;
+    AIRG_TRY(dev_dot(n, w, w, dsc + 2, nullptr, d, live, s));
     for (int sweep = 0; sweep < 2; ++sweep) {
+      const Gate g = sweep == 0 ? live : second;
       for (int q = 0; q <= j; ++q) {
         const double* Vq = V + (size_t)q * n;
-        AIRG_TRY(dev_dot(n, Vq, w, scal + 1, Hd + q * m + j, d, s));
-        axpy_dev_kernel<<<nb, 256, 0, s>>>(n, scal + 1, Vq, w);
+        AIRG_TRY(dev_dot(n, Vq, w, dsc + 1, Hd + q * m + j, d, g, s));
+        axpy_dev_kernel<<<nb, 256, 0, s>>>(n, dsc + 1, Vq, w, g);
       }
-      AIRG_TRY(dev_dot(n, w, w, scal, nullptr, d, s));
-      AIRG_TRY(host_scalar(scal, &hn2));
-      hn = std::sqrt(hn2);
-      if (!(sweep == 0 && hn < 0.7 * before)) break;
+      AIRG_TRY(dev_dot(n, w, w, dsc + 3, nullptr, d, g, s));
+      arnoldi_ctl_kernel<<<1, 1, 0, s>>>(sweep, j, m, Hd, dsc, ctl);
     }
-    AIRG_CUDA(cudaMemcpyAsync(Hh.data(), Hd, Hh.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
-    AIRG_CUDA(cudaStreamSynchronize(s));
-    Hh[(size_t)(j + 1) * m + j] = hn;
-    double cn = 0.0;
-    for (int q = 0; q <= j + 1; ++q) cn += Hh[(size_t)q * m + j] * Hh[(size_t)q * m + j];
-    hmax = std::max(hmax, std::sqrt(cn));
-    AIRG_CUDA(cudaMemcpyAsync(Hd + (size_t)(j + 1) * m + j, &Hh[(size_t)(j + 1) * m + j], sizeof(double),
-                              cudaMemcpyHostToDevice, s));
-    if (hn <= 1e-14 * hmax) {
-      Hh[(size_t)(j + 1) * m + j] = 0.0;
-      k = j + 1;
-      break;
-    }
-    scale_div_kernel<<<nb, 256, 0, s>>>(n, w, hn, V + (size_t)(j + 1) * n);
+    scale_div_kernel<<<nb, 256, 0, s>>>(n, w, 0.0, dsc + 5, V + (size_t)(j + 1) * n, live);
     AIRG_LAUNCH_CHECK();
   }
+  int ctlh[4];
+  AIRG_CUDA(cudaMemcpyAsync(H_h, Hd, (size_t)(m + 1) * m * sizeof(double), cudaMemcpyDeviceToHost, s));
+  AIRG_CUDA(cudaMemcpyAsync(ctlh, ctl, sizeof ctlh, cudaMemcpyDeviceToHost, s));
   AIRG_CUDA(cudaStreamSynchronize(s));
-  for (size_t i = 0; i < Hh.size(); ++i) H_h[i] = Hh[i];
-  *k_h = k;
+  *k_h = ctlh[2];
   release(V, s);
   release(w, s);
   release(sc, s);
   release(Hd, s);
+  release(ctl, s);
   return AIRG_OK;
 }
 
