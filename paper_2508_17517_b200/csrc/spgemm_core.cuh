@@ -402,8 +402,9 @@ struct Classes {
   const int* list(int c) const { return lists + (long long)c * m; }
 };
 
+// extra_dev/extra_h: one more device int read back with the same synchronisation
 static int classify(int m, const long long* size, const std::vector<long long>& th, Classes& out,
-                    cudaStream_t s) {
+                    cudaStream_t s, const int* extra_dev = nullptr, int* extra_h = nullptr) {
   const int ncls = (int)th.size() + 1;
   long long* dth = nullptr;
   int* cnt = nullptr;
@@ -417,6 +418,7 @@ static int classify(int m, const long long* size, const std::vector<long long>& 
   AIRG_LAUNCH_CHECK();
   out.count.assign(ncls, 0);
   AIRG_CUDA(cudaMemcpyAsync(out.count.data(), cnt, ncls * sizeof(int), cudaMemcpyDeviceToHost, s));
+  if (extra_dev) AIRG_CUDA(cudaMemcpyAsync(extra_h, extra_dev, sizeof(int), cudaMemcpyDeviceToHost, s));
   AIRG_CUDA(cudaStreamSynchronize(s));
   out.m = m;
   release(dth, s);

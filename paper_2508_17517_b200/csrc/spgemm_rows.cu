@@ -478,9 +478,18 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
     release(ovf_n, s);
     release(cl.lists, s);
   }
-  long long nnz = 0;
-  AIRG_TRY(scan_counts(cnt, Cp, m, &nnz, s));
   // ---- pass 2 ----
+  // the scan total (output nnz) is read back with the class counts: one sync
+  AIRG_TRY(scan_counts(cnt, Cp, m, nullptr, s));
+  AIRG_TRY(scratch(&rl, m, s));
+  if (m > 0) rowlen_kernel<<<blocks_for(m, 256), 256, 0, s>>>(m, Cp, rl);
+  Classes cl;
+  // output-length classes: <= 32 / 128 warp per row; <= 512 ... 8192 CTA per
+  // row with a shared table of 2 x class slots (bits 10 .. 14; the 8192 class
+  // takes 197 KB, one CTA per SM); longer rows use global tables
+  int nnz32 = 0;
+  AIRG_TRY(classify(m, rl, {32, 128, 512, 1024, 2048, 4096, 8192}, cl, s, Cp + m, &nnz32));
+  const long long nnz = nnz32;
   airg_csr_result* r = new airg_csr_result();
   r->nrows = m;
   r->ncols = B.ncols;
@@ -493,14 +502,7 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
   AIRG_TRY(scratch(&oval, cap, s));
   AIRG_TRY(scratch(&anyd, 1, s));
   AIRG_CUDA(cudaMemsetAsync(anyd, 0, sizeof(int), s));
-  AIRG_TRY(scratch(&rl, m, s));
-  if (m > 0) rowlen_kernel<<<blocks_for(m, 256), 256, 0, s>>>(m, Cp, rl);
   {
-    Classes cl;
-    // output-length classes: <= 32 / 128 warp per row; <= 512 ... 8192 CTA per
-    // row with a shared table of 2 x class slots (bits 10 .. 14; the 8192 class
-    // takes 197 KB, one CTA per SM); longer rows use global tables
-    AIRG_TRY(classify(m, rl, {32, 128, 512, 1024, 2048, 4096, 8192}, cl, s));
     const int cbits[7] = {6, 8, 10, 11, 12, 13, 14}, cwarps[2] = {8, 8};
     constexpr int kGlobalClass = 7;
     AIRG_TRY(set_smem((const void*)spgemm_numeric_kernel, 200 * 1024));
