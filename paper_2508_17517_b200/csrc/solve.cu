@@ -45,14 +45,23 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   return v;
 }
 
-// spin on one peer's message count; traps (fails the context) after ~20 s
-// instead of hanging the device
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// spin on one peer's message count (relaxed polls, one acquire fence once it
+// is reached: an acquire per poll would keep invalidating the SM's L1 under
+// the CTAs sharing it); traps (fails the context) after ~20 s instead of
+// hanging the device
 __device__ __forceinline__ void wait_count(const unsigned long long* flag, unsigned long long want) {
   const long long t0 = clock64();
-  while (ld_acquire_sys(flag) < want) {
+  while (ld_relaxed_sys(flag) < want) {
     __nanosleep(64);
     if (clock64() - t0 > 40000000000ll) __trap();
   }
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
 
 // Programmatic dependent launch: a kernel launched with the programmatic
@@ -1695,8 +1704,10 @@ static int wait_now(airg_dplan* p, const WaitDesc& w, cudaStream_t s) {
   return AIRG_OK;
 }
 
-// P2P: put + wait kernel (a wait folded into the consuming SpMV made every CTA
-// poll at system scope and doubled the SpMV time); NCCL: pack + send/recv
+// P2P: put kernel + one-CTA wait kernel.  Waiting inside the consuming SpMV
+// was measured slower both with every CTA polling (2x SpMV time) and with only
+// the CTAs that read ghost columns polling (solve 30 vs 21 ms at N = 2: the
+// peer wait lands inside the large kernels).  NCCL: pack + send/recv
 static int halo_exchange(airg_dplan* p, HaloX& h, const P2PHalo* ph, double* x_ext, cudaStream_t s) {
   if (p->world == 1) return AIRG_OK;
   if (p->p2p) {
