@@ -97,14 +97,15 @@ def cpu_cores_note():
 def reference_arm(args, rank, world):
     if rank != 0:
         return 0
+    problem = getattr(args, 'problem', 'fd')
     setup_s, solve_s, its = [], [], 0
     for i in range(args.warmup + args.steps):
-        a, b, its = cpu_run(args.cpu_nx, args.order)
+        a, b, its = cpu_run(args.cpu_nx, args.order, problem)
         if i >= args.warmup:
             setup_s.append(a)
             solve_s.append(b)
     t = float(np.mean(setup_s) + np.mean(solve_s))
-    n = args.cpu_nx * args.cpu_nx
+    n = args.cpu_nx * args.cpu_nx * (4 if problem == 'dg' else 1)
     ncpu, blas = cpu_cores_note()
     v = n / t
     line = {
@@ -112,7 +113,9 @@ def reference_arm(args, rank, world):
         'n_gpus': world, 'steps': args.steps, 'warmup': args.warmup, 'ms_per_step': t * 1e3,
         'higher_is_better': True, 'scaling': 'weak', 'vs_baseline': None, 'dtype': 'f64',
         'data': 'synthetic (2D upwind advection stencil, b=0, x0=1)',
-        'config': {'workload': f'AIRG pi/4 advection {args.nx}x{args.nx} order {args.order}',
+        'config': {'workload': (f'AIRG pi/4 upwind DG Q1 advection {args.nx}x{args.nx} cells'
+                                if problem == 'dg' else
+                                f'AIRG pi/4 advection {args.nx}x{args.nx}') + f' order {args.order}',
                    'sample': f'{args.cpu_nx}x{args.cpu_nx}', 'rtol': 1e-10},
         'setup_s': float(np.mean(setup_s)), 'solve_s': float(np.mean(solve_s)), 'iterations': its,
         'cpu_baseline': {'value': v, 'unit': 'DOF/s', 'cores': 1, 'kind': 'port',

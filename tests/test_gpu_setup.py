@@ -362,3 +362,36 @@ def test_setup_errors(G):
     H = G.setup(A, G.SetupConfig(poly_order=2))
     x, st = G.richardson_solve(H, np.zeros(64), np.ones(64), G.SolveConfig())
     assert st.converged and st.iterations <= 2
+
+
+@pytest.mark.parametrize('seed', [0, 1, 2])
+def test_ap_onepoint_structural_zeros(G, seed):
+    """A P for a one-point P (the warp-per-row column merge): structure =
+    structural product, values summed in A's column order, exact
+    cancellations kept as +0.0 -- bitwise the oracle's spgemm(A, P)."""
+    import ctypes as C
+    import torch
+    from paper_2508_17517_b200 import _lib as L
+    from paper_2508_17517_b200.csr import take
+    rng = np.random.default_rng(seed)
+    n, nc = 300, 40
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        k = int(rng.integers(1, 40))
+        cs = np.unique(rng.integers(0, n, size=k))
+        vs = rng.choice([1.0, -1.0, 0.5, -0.5, 1e-300, 3.0], size=len(cs))
+        rows += [i] * len(cs)
+        cols += cs.tolist()
+        vals += vs.tolist()
+    A = O.from_triplets(n, n, np.array(rows), np.array(cols), np.array(vals))
+    pcol = rng.integers(0, nc, size=n)
+    P = O.from_triplets(n, nc, np.arange(n), pcol, np.ones(n))
+    ref = O.spgemm(A, P)
+    Ad = dev_csr(A)
+    pd = torch.tensor(pcol, dtype=torch.int32, device='cuda')
+    res = C.c_void_p()
+    L.call('airg_ap_onepoint', n, n, nc, L.ptr(Ad.row_offsets), L.ptr(Ad.col_indices),
+           L.ptr(Ad.values), L.ptr(pd), C.byref(res), L.stream_handle())
+    same(take(res), ref)
+    assert np.any(ref.val == 0.0)          # the case exercises cancellations
+    assert not np.any(np.signbit(ref.val[ref.val == 0.0]))
