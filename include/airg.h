@@ -40,6 +40,15 @@ int airg_sm_count(void);
  * vector CSR with FMA (solve path).  ref: sparse.py:206-212 */
 int airg_spmv(int nrows, const int32_t* ptr, const int32_t* col, const double* val,
               const double* x, double* y, int exact, void* stream);
+/* ELL storage for the fixed-nnz/row structured stencils: width slots per row,
+ * column-major (slot k of row i at k*nrows + i), padding (value 0, column =
+ * row) after a row's entries.  airg_csr_to_ell fails (status 3) when a row is
+ * longer than width.  airg_spmv_ell: y = A x; exact = 1 gives the CSR exact
+ * (scipy csr_matvec) result bitwise.  ref: sparse.py:206-212 */
+int airg_csr_to_ell(int nrows, const int32_t* ptr, const int32_t* col, const double* val, int width,
+                    int32_t* ell_col, double* ell_val, void* stream);
+int airg_spmv_ell(int nrows, int width, const int32_t* ell_col, const double* ell_val, const double* x,
+                  double* y, int exact, void* stream);
 
 /* Euclidean norm of x (deterministic fixed-order reduction) into out_h. */
 int airg_norm2(int n, const double* x, double* out_h, void* stream);

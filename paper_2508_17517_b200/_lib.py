@@ -124,6 +124,8 @@ sig('airg_version')
 sig('airg_last_error', C.c_char_p, C.c_int)
 sig('airg_sm_count')
 sig('airg_spmv', i32, vp, vp, vp, vp, vp, C.c_int, vp)
+sig('airg_csr_to_ell', i32, vp, vp, vp, C.c_int, vp, vp, vp)
+sig('airg_spmv_ell', i32, C.c_int, vp, vp, vp, vp, C.c_int, vp)
 sig('airg_norm2', i32, vp, vp, vp)
 sig('airg_poly_apply', C.c_int, i32, vp, vp, vp, C.c_int, vp, C.c_int, vp, vp, vp, vp, vp, vp,
     C.c_int, vp)

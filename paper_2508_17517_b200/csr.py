@@ -162,6 +162,41 @@ def spmv(A, x, exact=False):
     return y
 
 
+@dataclass(frozen=True, eq=False)
+class EllMatrix:
+    """Fixed-width (ELL) copy of a CSR matrix for the structured stencils:
+    ``cols`` / ``vals`` hold ``width`` slots per row, column-major."""
+
+    nrows: int
+    ncols: int
+    width: int
+    cols: torch.Tensor
+    vals: torch.Tensor
+
+
+def to_ell(A, width=None):
+    """CSR -> ELL (width = longest row unless given)."""
+    lens = A.row_offsets[1:] - A.row_offsets[:-1]
+    w = int(lens.max().item()) if width is None and A.nrows else int(width or 0)
+    cols = empty(max(A.nrows * w, 1), IDX)
+    vals = empty(max(A.nrows * w, 1), VAL)
+    L.call('airg_csr_to_ell', A.nrows, L.ptr(A.row_offsets), L.ptr(A.col_indices), L.ptr(A.values),
+           w, L.ptr(cols), L.ptr(vals), L.stream_handle())
+    return EllMatrix(A.nrows, A.ncols, w, cols, vals)
+
+
+def spmv_ell(E, x, exact=False):
+    """y = A x on the ELL copy; ``exact=True`` is bitwise ``spmv(A, x, exact=True)``."""
+    x = to_dev(x, VAL)
+    if x.dim() != 1 or x.numel() != E.ncols:
+        raise ValueError(f'vector of length {x.numel()} incompatible with '
+                         f'{E.nrows}x{E.ncols} matrix')
+    y = empty(E.nrows, VAL)
+    L.call('airg_spmv_ell', E.nrows, E.width, L.ptr(E.cols), L.ptr(E.vals), L.ptr(x), L.ptr(y),
+           1 if exact else 0, L.stream_handle())
+    return y
+
+
 def norm2(x):
     out = np.zeros(1)
     L.call('airg_norm2', x.numel(), L.ptr(x), L.hptr(out), L.stream_handle())

@@ -949,6 +949,40 @@ static int alloc_vec(double** p, long long n) {
   return AIRG_OK;
 }
 
+// ---- ELL (fixed width, column-major slots k*n + i) for the fixed-nnz/row
+// structured stencils.  Padding slots (value 0, column = row) follow a row's
+// real entries, so the exact mode adds only +-0 after the reference's sums:
+// bitwise the CSR exact result.
+__global__ void csr_to_ell_kernel(int n, int width, const int* __restrict__ ptr, const int* __restrict__ col,
+                                  const double* __restrict__ val, int* __restrict__ ecol,
+                                  double* __restrict__ eval, int* __restrict__ overflow) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int b = ptr[i], len = ptr[i + 1] - b;
+    if (len > width) atomicExch(overflow, 1);
+    for (int k = 0; k < width; ++k) {
+      const bool real = k < len;
+      ecol[(size_t)k * n + i] = real ? col[b + k] : i;
+      eval[(size_t)k * n + i] = real ? val[b + k] : 0.0;
+    }
+  }
+}
+
+template <bool E>
+__global__ void __launch_bounds__(256) spmv_ell_kernel(int n, int width, const int* __restrict__ ecol,
+                                                       const double* __restrict__ eval,
+                                                       const double* __restrict__ x, double* __restrict__ y) {
+  pdl_enter();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < width; ++k) {
+      const double a = __ldg(eval + (size_t)k * n + i);
+      const double xv = __ldg(x + __ldg(ecol + (size_t)k * n + i));
+      s = E ? add_rn(s, mul_rn(a, xv)) : fma(a, xv, s);
+    }
+    y[i] = s;
+  }
+}
+
 extern "C" {
 
 int airg_version(void) { return 1; }
@@ -982,6 +1016,43 @@ int airg_spmv(int nrows, const int32_t* ptr, const int32_t* col, const double* v
   Csr A = make_csr(nrows, 0, ptr, col, val, read_nnz(ptr, nrows));
   Epi ep{y, nullptr, 1.0, 0.0, nullptr, nullptr, nullptr, nullptr};
   return launch_spmv(A, x, 1.0, ep, s);
+}
+
+int airg_csr_to_ell(int nrows, const int32_t* ptr, const int32_t* col, const double* val, int width,
+                    int32_t* ell_col, double* ell_val, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (nrows < 0 || width < 0) {
+    set_error("negative size");
+    return AIRG_ERR_ARG;
+  }
+  if (nrows == 0 || width == 0) return AIRG_OK;
+  int* ovf = nullptr;
+  AIRG_TRY(scratch(&ovf, 1, s));
+  AIRG_CUDA(cudaMemsetAsync(ovf, 0, sizeof(int), s));
+  csr_to_ell_kernel<<<blocks_for(nrows, 256), 256, 0, s>>>(nrows, width, ptr, col, val, ell_col, ell_val, ovf);
+  AIRG_LAUNCH_CHECK();
+  int h = 0;
+  AIRG_CUDA(cudaMemcpyAsync(&h, ovf, sizeof(int), cudaMemcpyDeviceToHost, s));
+  AIRG_CUDA(cudaStreamSynchronize(s));
+  release(ovf, s);
+  if (h) {
+    set_error("a row is longer than the ELL width %d", width);
+    return AIRG_ERR_VALUE;
+  }
+  return AIRG_OK;
+}
+
+int airg_spmv_ell(int nrows, int width, const int32_t* ell_col, const double* ell_val, const double* x,
+                  double* y, int exact, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (nrows < 0 || width < 0) {
+    set_error("negative size");
+    return AIRG_ERR_ARG;
+  }
+  if (nrows == 0) return AIRG_OK;
+  if (exact) AIRG_CUDA(launch_pdl(spmv_ell_kernel<true>, blocks_for(nrows, 256), 256, s, nrows, width, ell_col, ell_val, x, y));
+  else AIRG_CUDA(launch_pdl(spmv_ell_kernel<false>, blocks_for(nrows, 256), 256, s, nrows, width, ell_col, ell_val, x, y));
+  return AIRG_OK;
 }
 
 int airg_norm2(int n, const double* x, double* out_h, void* stream) {

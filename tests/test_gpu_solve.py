@@ -52,6 +52,26 @@ def test_spmv_empty_and_ragged(G):
         G.spmv(dev_csr(A), np.ones(3))
 
 
+def test_ell_spmv_matches_csr(G, hier64):
+    """ELL copy of the structured stencil (and of ragged level operators):
+    exact mode bitwise == scipy csr_matvec, fast mode within rounding."""
+    from paper_2508_17517_b200.csr import spmv_ell, to_ell
+    rng = np.random.default_rng(3)
+    A, _ = G.build_advection_2d(G.AdvectionProblem(nx=97, ny=61, vx=PI4[0], vy=PI4[1]))
+    E = to_ell(A)
+    assert E.width == 3
+    x = rng.standard_normal(A.ncols)
+    want = O.spmv(O.advection_2d(97, 61, *PI4), x)
+    assert spmv_ell(E, x, exact=True).cpu().numpy().tobytes() == want.tobytes()
+    assert np.allclose(spmv_ell(E, x).cpu().numpy(), want, rtol=1e-14, atol=1e-14)
+    for M in (hier64.levels[2].R, hier64.levels[3].A_ff, hier64.coarsest_A):
+        x = rng.standard_normal(M.ncols)
+        got = spmv_ell(to_ell(dev_csr(M)), x, exact=True).cpu().numpy()
+        assert got.tobytes() == O.spmv(M, x).tobytes()
+    with pytest.raises(ValueError):
+        to_ell(dev_csr(hier64.levels[2].R), width=1)
+
+
 def test_poly_apply_kinds_match_oracle(G, hier64):
     rng = np.random.default_rng(1)
     L = hier64.levels[2]
