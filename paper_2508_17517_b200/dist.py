@@ -473,27 +473,40 @@ def _spgemm(A, B, ncols, negate=False, mode=0, tol=0.0, lump=False, row0=0):
 # ---------------------------------------------------------------------------
 
 class _Ticker:
-    """Phase timer for the distributed setup: each call charges the time
-    since the previous call (device synchronised) to the named phase."""
+    """Phase timer for the distributed setup: each call charges the stream
+    time since the previous call to the named phase.  CUDA events in stream
+    order (the interval includes any device idle time waiting for the host);
+    the elapsed times are summed once, at tick(None), instead of
+    synchronising the device at every phase boundary."""
 
     def __init__(self, sink):
         import os
-        import time
-        self.sink, self.clock = sink, time.perf_counter
+        self.sink = sink
         self.per_level = bool(os.environ.get('AIRG_DIST_LEVEL_TIMES'))
         self.level = 0
-        torch.cuda.synchronize()
-        self.t = self.clock()
+        self.pending = []
+        self.prev = torch.cuda.Event(enable_timing=True)
+        self.prev.record()
 
     def __call__(self, phase):
-        torch.cuda.synchronize()
-        t = self.clock()
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
         if phase is not None:
-            self.sink[phase] = self.sink.get(phase, 0.0) + t - self.t
+            self.pending.append((phase, self.level, self.prev, e))
+        self.prev = e
+        if phase is None:
+            self.flush()
+
+    def flush(self):
+        if self.pending:
+            self.pending[-1][3].synchronize()
+        for phase, level, e0, e1 in self.pending:
+            dt = e0.elapsed_time(e1) / 1e3
+            self.sink[phase] = self.sink.get(phase, 0.0) + dt
             if self.per_level:
-                key = f'{phase}@{self.level}'
-                self.sink[key] = self.sink.get(key, 0.0) + t - self.t
-        self.t = t
+                key = f'{phase}@{level}'
+                self.sink[key] = self.sink.get(key, 0.0) + dt
+        self.pending = []
 
     def note(self, key, value):
         if self.per_level:
