@@ -1,3 +1,4 @@
+"""cProfile (host side) of one setup + solve at nx^2."""
 import sys, cProfile, pstats, time
 sys.path.insert(0, '.')
 import numpy as np, torch

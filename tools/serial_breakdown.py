@@ -1,3 +1,4 @@
+"""Serial 2048^2 setup wall time and per-phase breakdown (3 runs, last reported)."""
 import sys, os, json, time
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch
