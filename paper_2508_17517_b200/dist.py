@@ -244,10 +244,16 @@ class DHierarchy:
 # problem generation
 # ---------------------------------------------------------------------------
 
-def advection_2d_strips(comm, nx, ny, vx, vy):
-    """Rank-local grid-row strip of the 2-D upwind operator (problems.py:48-85)."""
+def advection_2d_strips(comm, nx, ny, vx, vy, weights=None):
+    """Rank-local grid-row strip of the 2-D upwind operator (problems.py:48-85).
+    ``weights`` (per rank) sets relative strip heights; the global numbering,
+    and with it every level operator, does not depend on them."""
     r, W = comm.rank, comm.world
-    rows = [(ny * q) // W * nx for q in range(W + 1)]
+    if weights is None:
+        rows = [(ny * q) // W * nx for q in range(W + 1)]
+    else:
+        c = np.concatenate([[0.0], np.cumsum(np.asarray(weights, dtype=np.float64))])
+        rows = [int(round(ny * c[q] / c[-1])) * nx for q in range(W + 1)]
     part = Part(rows, comm.device)
     lo, hi = part.lo(r), part.hi(r)
     nnz = L.i64()

@@ -85,7 +85,7 @@ def test_distributed_path_on_one_rank_is_the_serial_hierarchy(single_rank):
 def test_two_gpu_strips_match_serial():
     cmd = [sys.executable, '-m', 'torch.distributed.run', '--nnodes=1', '--nproc-per-node', '2',
            '--master-addr', '127.0.0.1', '--master-port', str(_free_port()),
-           os.path.join(ROOT, 'tools', 'dist_check.py'), '192', '1500']
+           os.path.join(ROOT, 'tools', 'dist_check.py'), '192', '1500', 'weighted']
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=420)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert 'DIST OK world=2' in r.stdout + r.stderr

@@ -3,7 +3,7 @@ the row-strip distributed setup equals the serial GPU setup bit for bit when
 the distributed run's polynomials are injected, and the distributed solve
 matches the serial solve's history within 1e-10 of ||r0||.
 
-    torchrun --nproc-per-node 2 tools/dist_check.py [nx] [replicate_below]
+    torchrun --nproc-per-node 2 tools/dist_check.py [nx] [replicate_below] [weighted]
 """
 import os
 import sys
@@ -25,7 +25,10 @@ def main():
     comm = D.Comm()
     v = (float(np.cos(np.pi / 4)), float(np.sin(np.pi / 4)))
     cfg = G.SetupConfig(poly_order=4)
-    Ad = D.advection_2d_strips(comm, nx, nx, *v)
+    w = None
+    if len(sys.argv) > 3 and sys.argv[3] == 'weighted':   # uneven strips
+        w = [1.3] + [1.0 + 0.1 * q for q in range(1, comm.world)]
+    Ad = D.advection_2d_strips(comm, nx, nx, *v, weights=w)
     DH = D.setup_distributed(comm, Ad, cfg, replicate_below=rep)
     A, b = G.build_advection_2d(G.AdvectionProblem(nx=nx, ny=nx, vx=v[0], vy=v[1]))
     # the generated strips are the global matrix's rows
