@@ -700,7 +700,8 @@ static int ap_onepoint(const Mat& A, int nc, const int* pcol, airg_csr_result** 
   // the per-row merge is O(L x unique columns): for long rows (a row beyond the
   // staging buffer, or > 300 entries on average, measured at the dense 2048^2
   // levels) the general hash product is faster
-  if (hinfo[0] > kApCap || (long long)hinfo[1] > 300ll * n) {
+  static const long long avg_cap = getenv("AIRG_AP_AVG") ? atoll(getenv("AIRG_AP_AVG")) : 300;
+  if (hinfo[0] > kApCap || (long long)hinfo[1] > avg_cap * n) {
     int* Pp = nullptr;
     double* Pv = nullptr;
     AIRG_TRY(scratch(&Pp, A.ncols + 1, s));
