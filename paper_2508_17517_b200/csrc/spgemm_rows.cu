@@ -605,57 +605,53 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
 // its columns mapped through pcol and equal columns merged.  scipy csr_matmat
 // semantics with the reference's structural zeros (sparse.py:222-240): the
 // unique mapped columns ascending, value = 0 + a_1*1 + a_2*1 + ... in the
-// order of A's columns (cancellations stay as +0.0).  One warp per row, the
-// row staged in shared memory; the first occurrence of a column owns the
-// output entry, its rank among the unique columns is its position.  Rows are
-// written raw at A's offsets and compacted after the scan.
-constexpr int kApCap = 1024, kApWarps = 4;
+// order of A's columns (cancellations stay as +0.0).  Rows are written raw at
+// A's offsets and compacted after the scan.
+constexpr int kApCap = 1024;
 
-__global__ void __launch_bounds__(32 * kApWarps) ap_onepoint_kernel(
-    int n, const int* __restrict__ Ap, const int* __restrict__ Ac, const double* __restrict__ Av,
-    const int* __restrict__ pcol, int* __restrict__ rcol, double* __restrict__ rval, int* __restrict__ cnt) {
+// One warp per row: stage the mapped columns and values of A's row, stable
+// LSD radix sort them by column (equal columns keep A's column order), then
+// each run of equal columns is summed by the lane holding its head, in A's
+// column order -- the sum the first-occurrence merge formed, now in
+// O(L log span) instead of O(L x unique).  CAP entries of staging per warp.
+template <int CAP, int NW>
+__global__ void __launch_bounds__(32 * NW) ap_onepoint_kernel(
+    int nr, const int* __restrict__ rows, const int* __restrict__ Ap, const int* __restrict__ Ac,
+    const double* __restrict__ Av, const int* __restrict__ pcol, int* __restrict__ rcol,
+    double* __restrict__ rval, int* __restrict__ cnt) {
   extern __shared__ unsigned char apsm[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int* cs = (int*)apsm + (size_t)w * kApCap;
-  double* as = (double*)(apsm + (size_t)kApWarps * kApCap * 4) + (size_t)w * kApCap;
-  unsigned char* fs = apsm + (size_t)kApWarps * kApCap * 12 + (size_t)w * kApCap;
-  for (long long r = (long long)blockIdx.x * kApWarps + w; r < n; r += (long long)gridDim.x * kApWarps) {
-    const int row = (int)r;
+  unsigned char* base = apsm + (size_t)w * (CAP * 24 + 1024);
+  double* as = (double*)base;
+  double* v2 = as + CAP;
+  int* cs = (int*)(v2 + CAP);
+  int* k2 = cs + CAP;
+  int* hist = k2 + CAP;
+  const unsigned lt = (1u << lane) - 1u;
+  for (long long r = (long long)blockIdx.x * NW + w; r < nr; r += (long long)gridDim.x * NW) {
+    const int row = rows[r];
     const int b = Ap[row], L = Ap[row + 1] - b;
     for (int j = lane; j < L; j += 32) {
       cs[j] = pcol[Ac[b + j]];
       as[j] = Av[b + j];
     }
     __syncwarp();
+    if (L > 1) warp_radix_sort(cs, as, k2, v2, L, hist, lane);
+    __syncwarp();
     int U = 0;
     for (int j0 = 0; j0 < L; j0 += 32) {
       const int j = j0 + lane;
-      bool first = false;
-      if (j < L) {
+      const bool head = j < L && (j == 0 || cs[j] != cs[j - 1]);
+      const unsigned bal = __ballot_sync(kFull, head);
+      if (head) {
         const int c = cs[j];
-        first = true;
-        for (int jj = 0; jj < j; ++jj)
-          if (cs[jj] == c) {
-            first = false;
-            break;
-          }
-        fs[j] = first ? 1 : 0;
+        double sum = 0.0;
+        for (int jj = j; jj < L && cs[jj] == c; ++jj) sum = add_rn(sum, mul_rn(as[jj], 1.0));
+        const int rank = U + __popc(bal & lt);
+        rcol[b + rank] = c;
+        rval[b + rank] = sum;
       }
-      U += __popc(__ballot_sync(kFull, first));
-    }
-    __syncwarp();
-    for (int j = lane; j < L; j += 32) {
-      if (!fs[j]) continue;
-      const int c = cs[j];
-      int rank = 0;
-      double s = 0.0;
-      for (int jj = 0; jj < L; ++jj) {
-        const int cj = cs[jj];
-        rank += (fs[jj] && cj < c) ? 1 : 0;
-        if (jj >= j && cj == c) s = add_rn(s, mul_rn(as[jj], 1.0));
-      }
-      rcol[b + rank] = c;
-      rval[b + rank] = s;
+      U += __popc(bal);
     }
     if (lane == 0) cnt[row] = U;
     __syncwarp();
@@ -676,32 +672,24 @@ __global__ void ap_compact_kernel(int n, const int* __restrict__ Ap, const int* 
   }
 }
 
-__global__ void ap_maxlen_kernel(int n, const int* __restrict__ p, int* __restrict__ mx) {
-  int v = 0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    v = max(v, p[i + 1] - p[i]);
-  v = __reduce_max_sync(kFull, v);
-  if ((threadIdx.x & 31) == 0) atomicMax(mx, v);
-}
-
 static int ap_onepoint(const Mat& A, int nc, const int* pcol, airg_csr_result** out, cudaStream_t s) {
   const int n = A.nrows;
-  int* info = nullptr;  // [max row length, nnz(A)]
-  AIRG_TRY(scratch(&info, 2, s));
-  AIRG_CUDA(cudaMemsetAsync(info, 0, sizeof(int), s));
-  if (n > 0) ap_maxlen_kernel<<<blocks_for(n, 256, 148 * 8), 256, 0, s>>>(n, A.p, info);
+  // row classes by length (<= 256, <= 1024, longer); nnz(A) read back in the
+  // same sync
+  long long* len = nullptr;
+  AIRG_TRY(scratch(&len, n > 0 ? n : 1, s));
+  if (n > 0) rowlen_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, A.p, len);
   AIRG_LAUNCH_CHECK();
-  AIRG_CUDA(cudaMemcpyAsync(info + 1, A.p + n, sizeof(int), cudaMemcpyDeviceToDevice, s));
-  int hinfo[2];
-  AIRG_CUDA(cudaMemcpyAsync(hinfo, info, sizeof hinfo, cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
-  release(info, s);
-  // the per-row merge is O(L x unique columns): for long rows (a row beyond the
-  // staging buffer, or > 300 entries on average, measured at the dense 2048^2
-  // levels) the general hash product is faster
-  static const long long avg_cap = getenv("AIRG_AP_AVG") ? atoll(getenv("AIRG_AP_AVG")) : 300;
-  if (hinfo[0] > kApCap || (long long)hinfo[1] > avg_cap * n) {
+  Classes cl;
+  int annz32 = 0;
+  AIRG_TRY(classify(n, len, {256, kApCap}, cl, s, A.p + n, &annz32));
+  release(len, s);
+  // rows beyond the staging buffer, or (measurement knob AIRG_AP_AVG) a mean
+  // row length above the cutoff, go to the general hash product
+  static const long long avg_cap = getenv("AIRG_AP_AVG") ? atoll(getenv("AIRG_AP_AVG")) : (1ll << 40);
+  const long long annz = annz32;
+  if (cl.count[2] > 0 || annz > avg_cap * n) {
+    release(cl.lists, s);
     int* Pp = nullptr;
     double* Pv = nullptr;
     AIRG_TRY(scratch(&Pp, A.ncols + 1, s));
@@ -715,22 +703,34 @@ static int ap_onepoint(const Mat& A, int nc, const int* pcol, airg_csr_result** 
     release(Pv, s);
     return AIRG_OK;
   }
-  const long long annz = hinfo[1];
   int *rcol = nullptr, *cnt = nullptr;
   double* rval = nullptr;
   AIRG_TRY(scratch(&rcol, annz > 0 ? annz : 1, s));
   AIRG_TRY(scratch(&rval, annz > 0 ? annz : 1, s));
   AIRG_TRY(scratch(&cnt, n + 1, s));
-  const size_t shm = (size_t)kApWarps * kApCap * 13;
+  constexpr int kW0 = 8, kW1 = 2;
+  const size_t shm0 = (size_t)kW0 * (256 * 24 + 1024), shm1 = (size_t)kW1 * (kApCap * 24 + 1024);
   static bool attr = false;
   if (!attr) {
-    AIRG_CUDA(cudaFuncSetAttribute(ap_onepoint_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    AIRG_CUDA(cudaFuncSetAttribute(ap_onepoint_kernel<256, kW0>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm0));
+    AIRG_CUDA(cudaFuncSetAttribute(ap_onepoint_kernel<kApCap, kW1>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm1));
     attr = true;
   }
-  if (n > 0)
-    ap_onepoint_kernel<<<blocks_for(n, kApWarps, 148 * 16), 32 * kApWarps, shm, s>>>(
-        n, A.p, A.c, A.v, pcol, rcol, rval, cnt);
+  Fork fk;
+  AIRG_TRY(fk.begin(s));
+  if (cl.count[0])
+    ap_onepoint_kernel<256, kW0><<<blocks_for(cl.count[0], kW0, 148 * 4), 32 * kW0, shm0, fk.stream(0)>>>(
+        cl.count[0], cl.list(0), A.p, A.c, A.v, pcol, rcol, rval, cnt);
   AIRG_LAUNCH_CHECK();
+  if (cl.count[1])
+    ap_onepoint_kernel<kApCap, kW1><<<blocks_for(cl.count[1], kW1, 148 * 4), 32 * kW1, shm1,
+                                      fk.stream(1)>>>(cl.count[1], cl.list(1), A.p, A.c, A.v, pcol,
+                                                      rcol, rval, cnt);
+  AIRG_LAUNCH_CHECK();
+  AIRG_TRY(fk.end(s));
+  release(cl.lists, s);
   airg_csr_result* r = new_result(n, nc, s);
   long long nnz = 0;
   AIRG_TRY(scan_counts(cnt, r->ptr, n, &nnz, s));
