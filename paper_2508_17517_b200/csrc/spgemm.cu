@@ -570,25 +570,37 @@ static int run_poly_kernel(PolyArgs& a, int maxlen, cudaStream_t s) {
 // ----------------------------------------------------------------------------
 // extract / restriction assembly
 // ----------------------------------------------------------------------------
+// VS lanes per selected row (coalesced walk of the row, ballot compaction of
+// the kept entries in column order); one group per row, no grid stride so
+// every lane of a warp reaches the ballots
+template <int VS>
 __global__ void extract_kernel(int nr, const int* __restrict__ rows, const int* __restrict__ p,
                                const int* __restrict__ c, const double* __restrict__ v,
                                const int* __restrict__ colmap, const int* __restrict__ optr,
                                int* __restrict__ oc, double* __restrict__ ov, int* __restrict__ cnt) {
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nr;
-       t += (long long)gridDim.x * blockDim.x) {
+  const long long t = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / VS;
+  const int lane = threadIdx.x & 31, g = lane & (VS - 1), sh = lane - g;
+  const unsigned gmask = (VS == 32 ? 0xffffffffu : ((1u << VS) - 1u)) << sh;
+  int b = 0, e = 0, o = 0;
+  if (t < nr) {
     const int i = rows[t];
-    int o = optr ? optr[t] : 0, n = 0;
-    for (int k = p[i]; k < p[i + 1]; ++k) {
-      const int m = colmap[c[k]];
-      if (m < 0) continue;
-      if (oc) {
-        oc[o + n] = m;
-        ov[o + n] = v[k];
-      }
-      ++n;
-    }
-    if (cnt) cnt[t] = n;
+    b = p[i];
+    e = p[i + 1];
+    if (optr) o = optr[t];
   }
+  int n = 0;
+  for (int j0 = b; __any_sync(0xffffffffu, j0 < e); j0 += VS) {
+    const int k = j0 + g;
+    const int m = k < e ? colmap[c[k]] : -1;
+    const unsigned bal = __ballot_sync(0xffffffffu, m >= 0) & gmask;
+    if (m >= 0 && oc) {
+      const int d = o + n + __popc(bal & ((1u << lane) - 1u));
+      oc[d] = m;
+      ov[d] = v[k];
+    }
+    n += __popc(bal);
+  }
+  if (cnt && g == 0 && t < nr) cnt[t] = n;
 }
 
 __global__ void colmap_kernel(int n, const signed char* __restrict__ labels, signed char want,
@@ -598,35 +610,52 @@ __global__ void colmap_kernel(int n, const signed char* __restrict__ labels, sig
     map[i] = labels[i] == want ? pos[i] : -1;
 }
 
-// R row j = [Z row j mapped through f_idx | 1 at c_idx[j]] in fine ordering
+// R row j = [Z row j mapped through f_idx | 1 at c_idx[j]] in fine ordering:
+// the unit entry goes before the first mapped column > c_idx[j] (or last).
+// VS lanes per row, the insertion point found by ballot chunk by chunk.
+template <int VS>
 __global__ void restriction_kernel(int nc, const int* __restrict__ zp, const int* __restrict__ zc,
                                    const double* __restrict__ zv, const int* __restrict__ f_idx,
                                    const int* __restrict__ c_idx, int* __restrict__ rp,
                                    int* __restrict__ rc, double* __restrict__ rv) {
-  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < nc;
-       j += (long long)gridDim.x * blockDim.x) {
-    const int b = zp[j], e = zp[j + 1];
-    const int cj = c_idx[j];
-    long long o = (long long)b + j;
-    rp[j] = (int)o;
-    if (j == nc - 1) rp[nc] = (int)(e + nc);
-    bool done = false;
-    for (int k = b; k < e; ++k) {
-      const int col = f_idx[zc[k]];
-      if (!done && col > cj) {
-        rc[o] = cj;
-        rv[o] = 1.0;
-        ++o;
-        done = true;
+  const long long j = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / VS;
+  const int lane = threadIdx.x & 31, g = lane & (VS - 1), sh = lane - g;
+  const unsigned gmask = (VS == 32 ? 0xffffffffu : ((1u << VS) - 1u)) << sh;
+  int b = 0, e = 0, cj = 0;
+  if (j < nc) {
+    b = zp[j];
+    e = zp[j + 1];
+    cj = c_idx[j];
+    if (g == 0) {
+      rp[j] = (int)(b + j);
+      if (j == nc - 1) rp[nc] = (int)(e + nc);
+    }
+  }
+  const long long o = (long long)b + j;
+  bool done = false;  // unit entry already placed (uniform within the group)
+  for (int k0 = b; __any_sync(0xffffffffu, k0 < e); k0 += VS) {
+    const int k = k0 + g;
+    const bool in = k < e;
+    const int col = in ? f_idx[zc[k]] : 0;
+    const unsigned gt = __ballot_sync(0xffffffffu, in && col > cj) & gmask;
+    int shift = done ? 1 : 0;
+    if (!done && gt) {
+      const int first = __ffs(gt) - 1;  // lane holding the first column > cj
+      if (lane >= first) shift = 1;
+      if (lane == first) {
+        rc[o + (k - b)] = cj;
+        rv[o + (k - b)] = 1.0;
       }
-      rc[o] = col;
-      rv[o] = zv[k];
-      ++o;
     }
-    if (!done) {
-      rc[o] = cj;
-      rv[o] = 1.0;
+    if (in) {
+      rc[o + (k - b) + shift] = col;
+      rv[o + (k - b) + shift] = zv[k];
     }
+    done = done || gt != 0;
+  }
+  if (j < nc && !done && g == 0) {
+    rc[o + (e - b)] = cj;
+    rv[o + (e - b)] = 1.0;
   }
 }
 
@@ -804,14 +833,14 @@ int airg_extract(int nr_sel, const int32_t* rows, const int32_t* p, const int32_
   airg_csr_result* r = new_result(nr_sel, ncols_sel, s);
   int* cnt = nullptr;
   AIRG_TRY(scratch(&cnt, nr_sel + 1, s));
-  const int nb = blocks_for(nr_sel, 256);
+  const int nb = (int)(((long long)nr_sel * 8 + 255) / 256);
   if (nr_sel > 0)
-    extract_kernel<<<nb, 256, 0, s>>>(nr_sel, rows, p, c, v, colmap, nullptr, nullptr, nullptr, cnt);
+    extract_kernel<8><<<nb, 256, 0, s>>>(nr_sel, rows, p, c, v, colmap, nullptr, nullptr, nullptr, cnt);
   long long nnz = 0;
   AIRG_TRY(scan_counts(cnt, r->ptr, nr_sel, &nnz, s));
   AIRG_TRY(result_alloc_entries(r, nnz, true));
   if (nr_sel > 0)
-    extract_kernel<<<nb, 256, 0, s>>>(nr_sel, rows, p, c, v, colmap, r->ptr, r->col, r->val, nullptr);
+    extract_kernel<8><<<nb, 256, 0, s>>>(nr_sel, rows, p, c, v, colmap, r->ptr, r->col, r->val, nullptr);
   AIRG_LAUNCH_CHECK();
   release(cnt, s);
   *out = r;
@@ -838,8 +867,8 @@ int airg_restriction(int n, int nc, const int32_t* zp, const int32_t* zc, const 
   airg_csr_result* r = new_result(nc, n, s);
   AIRG_TRY(result_alloc_entries(r, (long long)znnz + nc, true));
   if (nc > 0)
-    restriction_kernel<<<blocks_for(nc, 256), 256, 0, s>>>(nc, zp, zc, zv, f_idx, c_idx, r->ptr, r->col,
-                                                          r->val);
+    restriction_kernel<8><<<(int)(((long long)nc * 8 + 255) / 256), 256, 0, s>>>(
+        nc, zp, zc, zv, f_idx, c_idx, r->ptr, r->col, r->val);
   else
     AIRG_CUDA(cudaMemsetAsync(r->ptr, 0, sizeof(int), s));
   AIRG_LAUNCH_CHECK();
