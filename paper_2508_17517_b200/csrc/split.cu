@@ -9,36 +9,66 @@
 namespace airg {
 
 // ---- strength graph (splitting.py:86-109) ----------------------------------
+// VS lanes per row (one group per row, no grid stride: every lane of a warp
+// reaches the shuffles and ballots)
+#define AIRG_GROUP(VS)                                                              \
+  const int lane = threadIdx.x & 31, g = lane & (VS - 1), sh = lane - g;           \
+  const unsigned gmask = (VS == 32 ? 0xffffffffu : ((1u << VS) - 1u)) << sh;       \
+  (void)gmask
+
+template <int VS>
 __global__ void strength_count_kernel(int n, const int* __restrict__ ptr, const int* __restrict__ col,
                                       const double* __restrict__ val, double theta,
                                       unsigned char* __restrict__ keep, int* __restrict__ cnt) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int b = ptr[i], e = ptr[i + 1];
-    double mx = 0.0;
-    for (int k = b; k < e; ++k)
-      if (col[k] != i) mx = fmax(mx, fabs(val[k]));
-    const double thr = mul_rn(theta, mx);
-    int c = 0;
-    for (int k = b; k < e; ++k) {
-      const bool s = col[k] != i && val[k] != 0.0 && fabs(val[k]) >= thr;
-      keep[k] = s;
-      c += s;
-    }
-    cnt[i] = c;
+  AIRG_GROUP(VS);
+  const long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / VS;
+  int b = 0, e = 0;
+  if (i < n) {
+    b = ptr[i];
+    e = ptr[i + 1];
   }
+  double mx = 0.0;  // max is order-free: lanes stride the row, then reduce
+  for (int k = b + g; k < e; k += VS)
+    if (col[k] != i) mx = fmax(mx, fabs(val[k]));
+#pragma unroll
+  for (int o = VS / 2; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const double thr = mul_rn(theta, mx);
+  int c = 0;
+  for (int k0 = b; __any_sync(0xffffffffu, k0 < e); k0 += VS) {
+    const int k = k0 + g;
+    bool st = false;
+    if (k < e) {
+      const double v = val[k];
+      st = col[k] != i && v != 0.0 && fabs(v) >= thr;
+      keep[k] = st;
+    }
+    c += __popc(__ballot_sync(0xffffffffu, st) & gmask);
+  }
+  if (i < n && g == 0) cnt[i] = c;
 }
 
+template <int VS>
 __global__ void compact_cols_kernel(int n, const int* __restrict__ ptr, const int* __restrict__ col,
                                     const unsigned char* __restrict__ keep,
                                     const int* __restrict__ optr, int* __restrict__ ocol) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    int o = optr[i];
-    for (int k = ptr[i]; k < ptr[i + 1]; ++k)
-      if (keep[k]) ocol[o++] = col[k];
+  AIRG_GROUP(VS);
+  const long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / VS;
+  int b = 0, e = 0, o = 0;
+  if (i < n) {
+    b = ptr[i];
+    e = ptr[i + 1];
+    o = optr[i];
+  }
+  for (int k0 = b; __any_sync(0xffffffffu, k0 < e); k0 += VS) {
+    const int k = k0 + g;
+    const bool kp = k < e && keep[k];
+    const unsigned bal = __ballot_sync(0xffffffffu, kp) & gmask;
+    if (kp) ocol[o + __popc(bal & ((1u << lane) - 1u))] = col[k];
+    o += __popc(bal);
   }
 }
+
+static int group_blocks(long long n, int vs) { return (int)((n * vs + 255) / 256); }
 
 __global__ void col_count_kernel(long long nnz, const int* __restrict__ col, int* __restrict__ cnt) {
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < nnz;
@@ -112,14 +142,14 @@ static int strength_closure(int n, const int* ptr, const int* col, const double*
   AIRG_TRY(scratch(&keep, nnz, s));
   AIRG_TRY(scratch(&cnt, n + 1, s));
   const int nb = blocks_for(n, 256);
-  strength_count_kernel<<<nb, 256, 0, s>>>(n, ptr, col, val, theta, keep, cnt);
+  strength_count_kernel<8><<<group_blocks(n, 8), 256, 0, s>>>(n, ptr, col, val, theta, keep, cnt);
   AIRG_LAUNCH_CHECK();
   airg_csr_result* S = new_result(n, n, s);
   if (!S) return AIRG_ERR_CUDA;
   long long snnz = 0;
   AIRG_TRY(scan_counts(cnt, S->ptr, n, &snnz, s));
   AIRG_TRY(result_alloc_entries(S, snnz, false));
-  compact_cols_kernel<<<nb, 256, 0, s>>>(n, ptr, col, keep, S->ptr, S->col);
+  compact_cols_kernel<8><<<group_blocks(n, 8), 256, 0, s>>>(n, ptr, col, keep, S->ptr, S->col);
   AIRG_LAUNCH_CHECK();
   // transpose
   AIRG_TRY(scratch(&tcnt, n + 1, s));
@@ -295,20 +325,46 @@ int split_index(int n, const signed char* labels, int* pos, int* f_idx, int* c_i
 }
 
 // ---- DDC (splitting.py:162-207) --------------------------------------------
+// VS lanes load a row chunk coalesced; the group's first lane adds the
+// off-diagonal F entries in entry order (bincount's sequential sum)
+template <int VS>
 __global__ void ddc_ratio_kernel(int nf, const int* __restrict__ f_idx, const int* __restrict__ ptr,
                                  const int* __restrict__ col, const double* __restrict__ val,
                                  const signed char* __restrict__ labels, double* __restrict__ ratio,
                                  int* __restrict__ bad) {
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nf;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int i = f_idx[t];
-    double sum = 0.0, d = 0.0;
-    for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+  AIRG_GROUP(VS);
+  const long long t = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / VS;
+  int i = 0, b = 0, e = 0;
+  if (t < nf) {
+    i = f_idx[t];
+    b = ptr[i];
+    e = ptr[i + 1];
+  }
+  double sum = 0.0, d = 0.0;
+  for (int k0 = b; __any_sync(0xffffffffu, k0 < e); k0 += VS) {
+    const int k = k0 + g;
+    bool off = false, dia = false;
+    double a = 0.0;
+    if (k < e) {
       const int j = col[k];
-      if (labels[j] != 0) continue;
-      if (j == i) d = val[k];
-      else sum = add_rn(sum, fabs(val[k]));  // bincount: sequential in entry order
+      if (labels[j] == 0) {
+        a = val[k];
+        dia = j == i;
+        off = !dia;
+      }
     }
+    const unsigned bo = __ballot_sync(0xffffffffu, off) & gmask;
+    const unsigned bd = __ballot_sync(0xffffffffu, dia) & gmask;
+    if (bd) d = __shfl_sync(0xffffffffu, a, __ffs(bd) - 1);
+    else __shfl_sync(0xffffffffu, a, lane);  // keep every lane in the shuffle
+    const double fa = fabs(a);
+#pragma unroll
+    for (int q = 0; q < VS; ++q) {
+      const double x = __shfl_sync(0xffffffffu, fa, sh + q);
+      if ((bo >> (sh + q)) & 1u) sum = add_rn(sum, x);
+    }
+  }
+  if (t < nf && g == 0) {
     if (d == 0.0) atomicMin(bad, i);
     ratio[t] = __ddiv_rn(sum, fabs(d));
   }
@@ -396,7 +452,8 @@ static int ddc_pass_run(int n, const int* ptr, const int* col, const double* val
   int init[2] = {0x7fffffff, 0};
   AIRG_CUDA(cudaMemcpyAsync(ibuf, init, sizeof init, cudaMemcpyHostToDevice, s));
   const int nb = blocks_for(nf, 256);
-  if (nf > 0) ddc_ratio_kernel<<<nb, 256, 0, s>>>(nf, f_idx, ptr, col, val, labels, ratio, ibuf);
+  if (nf > 0)
+    ddc_ratio_kernel<8><<<group_blocks(nf, 8), 256, 0, s>>>(nf, f_idx, ptr, col, val, labels, ratio, ibuf);
   AIRG_LAUNCH_CHECK();
   int bad = 0;
   AIRG_CUDA(cudaMemcpyAsync(&bad, ibuf, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -531,29 +588,50 @@ __global__ void repair_kernel(int n, const int* __restrict__ ptr, const int* __r
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(changed, c);
 }
 
+// VS lanes per row: each lane keeps its first maximum of |a_ij| over the C
+// neighbours it strides over, then the group keeps the larger value, the
+// earlier entry on ties -- the sequential "first maximum wins" scan.
+template <int VS>
 __global__ void onepoint_kernel(int n, const int* __restrict__ ptr, const int* __restrict__ col,
                                 const double* __restrict__ val, const signed char* __restrict__ labels,
                                 const int* __restrict__ pos, int* __restrict__ pcol,
                                 int* __restrict__ bad) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    if (labels[i] == 1) {
+  AIRG_GROUP(VS);
+  const long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / VS;
+  const bool fine = i < n && labels[i] != 1;
+  int b = 0, e = 0;
+  if (fine) {
+    b = ptr[i];
+    e = ptr[i + 1];
+  }
+  double bm = -1.0;
+  int bk = 0x7fffffff;
+  for (int k = b + g; k < e; k += VS) {
+    const int j = col[k];
+    if (labels[j] != 1) continue;
+    const double a = fabs(val[k]);
+    if (a > bm) {
+      bm = a;
+      bk = k;
+    }
+  }
+#pragma unroll
+  for (int o = VS / 2; o > 0; o >>= 1) {
+    const double om = __shfl_xor_sync(0xffffffffu, bm, o);
+    const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
+    if (om > bm || (om == bm && ok < bk)) {
+      bm = om;
+      bk = ok;
+    }
+  }
+  if (i < n && g == 0) {
+    if (!fine) {
       pcol[i] = pos[i];
-      continue;
+    } else {
+      const int best = bk != 0x7fffffff ? pos[col[bk]] : -1;
+      pcol[i] = best;
+      if (best < 0) atomicMin(bad, (int)i);
     }
-    int best = -1;
-    double bm = -1.0;
-    for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
-      const int j = col[k];
-      if (labels[j] != 1) continue;
-      const double a = fabs(val[k]);
-      if (a > bm) {  // strict: first maximum wins (lowest C index)
-        bm = a;
-        best = pos[j];
-      }
-    }
-    pcol[i] = best;
-    if (best < 0) atomicMin(bad, (int)i);
   }
 }
 
@@ -643,8 +721,8 @@ int airg_prolong_onepoint(int n, const int32_t* ptr, const int32_t* col, const d
   AIRG_TRY(scratch(&bad, 1, s));
   int init = 0x7fffffff;
   AIRG_CUDA(cudaMemcpyAsync(bad, &init, sizeof(int), cudaMemcpyHostToDevice, s));
-  onepoint_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, ptr, col, val, (const signed char*)labels,
-                                                     pos, pcol, bad);
+  onepoint_kernel<8><<<group_blocks(n, 8), 256, 0, s>>>(n, ptr, col, val, (const signed char*)labels,
+                                                        pos, pcol, bad);
   AIRG_LAUNCH_CHECK();
   int b = 0;
   AIRG_CUDA(cudaMemcpyAsync(&b, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
