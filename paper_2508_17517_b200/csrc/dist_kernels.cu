@@ -6,6 +6,7 @@
 // so a distributed hierarchy equals the serial one bit for bit.
 // ref: splitting.py:86-207, problems.py:48-85
 #include "setup_common.cuh"
+#include "rowgroup.cuh"
 #include <vector>
 
 namespace airg {
@@ -46,40 +47,6 @@ static long long stencil_before(long long idx, int nx, double vx, double vy) {
   if (vx > 0) before += j * (nx - 1) + (i > 0 ? i - 1 : 0);
   if (vy > 0) before += idx - nx > 0 ? idx - nx : 0;
   return before;
-}
-
-// strength graph rows with a global row offset (diagonal = column row0 + i)
-__global__ void strength_rows_kernel(int n, int row0, const int* __restrict__ ptr,
-                                     const int* __restrict__ col, const double* __restrict__ val,
-                                     double theta, unsigned char* __restrict__ keep,
-                                     int* __restrict__ cnt) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int gi = row0 + (int)i;
-    const int b = ptr[i], e = ptr[i + 1];
-    double mx = 0.0;
-    for (int k = b; k < e; ++k)
-      if (col[k] != gi) mx = fmax(mx, fabs(val[k]));
-    const double thr = mul_rn(theta, mx);
-    int c = 0;
-    for (int k = b; k < e; ++k) {
-      const bool s = col[k] != gi && val[k] != 0.0 && fabs(val[k]) >= thr;
-      keep[k] = s;
-      c += s;
-    }
-    cnt[i] = c;
-  }
-}
-
-__global__ void compact_keep_cols_kernel(int n, const int* __restrict__ ptr, const int* __restrict__ col,
-                                         const unsigned char* __restrict__ keep,
-                                         const int* __restrict__ optr, int* __restrict__ ocol) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    int o = optr[i];
-    for (int k = ptr[i]; k < ptr[i + 1]; ++k)
-      if (keep[k]) ocol[o++] = col[k];
-  }
 }
 
 __global__ void union_sorted_rows_kernel(int n, const int* __restrict__ ap, const int* __restrict__ ac,
@@ -169,26 +136,6 @@ __global__ void luby_finish_ext_kernel(int n, const signed char* __restrict__ st
        i += (long long)gridDim.x * blockDim.x) {
     const signed char v = st[i];
     labels[i] = (v == 1 || v >= 3) ? 0 : 1;
-  }
-}
-
-__global__ void ddc_ratio_ext_kernel(int nf, int row0, const int* __restrict__ f_loc,
-                                     const int* __restrict__ ptr, const int* __restrict__ col,
-                                     const double* __restrict__ val,
-                                     const signed char* __restrict__ labels, double* __restrict__ ratio,
-                                     int* __restrict__ bad) {
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nf;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int i = f_loc[t];
-    double sum = 0.0, d = 0.0;
-    for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
-      const int j = col[k];
-      if (labels[j] != 0) continue;
-      if (j == i) d = val[k];
-      else sum = add_rn(sum, fabs(val[k]));
-    }
-    if (d == 0.0) atomicMin(bad, row0 + i);
-    ratio[t] = __ddiv_rn(sum, fabs(d));
   }
 }
 
@@ -311,13 +258,13 @@ int airg_strength_rows(int n, int row0, const int32_t* ptr, const int32_t* col, 
   AIRG_TRY(scratch(&keep, nnz, s));
   AIRG_TRY(scratch(&cnt, n + 1, s));
   const int nb = blocks_for(n, 256);
-  if (n > 0) strength_rows_kernel<<<nb, 256, 0, s>>>(n, row0, ptr, col, val, theta, keep, cnt);
+  if (n > 0) strength_count_kernel<8><<<group_blocks(n, 8), 256, 0, s>>>(n, row0, ptr, col, val, theta, keep, cnt);
   AIRG_LAUNCH_CHECK();
   airg_csr_result* S = new_result(n, 0, s);
   long long snnz = 0;
   AIRG_TRY(scan_counts(cnt, S->ptr, n, &snnz, s));
   AIRG_TRY(result_alloc_entries(S, snnz, false));
-  if (n > 0) compact_keep_cols_kernel<<<nb, 256, 0, s>>>(n, ptr, col, keep, S->ptr, S->col);
+  if (n > 0) compact_cols_kernel<8><<<group_blocks(n, 8), 256, 0, s>>>(n, ptr, col, keep, S->ptr, S->col);
   AIRG_LAUNCH_CHECK();
   release(keep, s);
   release(cnt, s);
@@ -403,7 +350,7 @@ int airg_ddc_ratios(int nf, int row0, const int32_t* f_loc, const int32_t* ptr, 
   const int init = 0x7fffffff;
   AIRG_CUDA(cudaMemcpyAsync(bad, &init, sizeof(int), cudaMemcpyHostToDevice, s));
   if (nf > 0) {
-    ddc_ratio_ext_kernel<<<blocks_for(nf, 256), 256, 0, s>>>(nf, row0, f_loc, ptr, col_ext, val,
+    ddc_ratio_kernel<8><<<group_blocks(nf, 8), 256, 0, s>>>(nf, row0, f_loc, ptr, col_ext, val,
                                                             (const signed char*)labels_ext, ratio, bad);
     minmaxsum_kernel<<<np, 256, 0, s>>>(nf, ratio, parts);
   }

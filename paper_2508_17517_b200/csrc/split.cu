@@ -3,73 +3,13 @@
 // maps and the one-point prolongator.
 // ref: splitting.py:86-238, hierarchy.py:250-305
 #include "setup_common.cuh"
+#include "rowgroup.cuh"
 #include <vector>
 #include <cmath>
 
 namespace airg {
 
 // ---- strength graph (splitting.py:86-109) ----------------------------------
-// VS lanes per row (one group per row, no grid stride: every lane of a warp
-// reaches the shuffles and ballots)
-#define AIRG_GROUP(VS)                                                              \
-  const int lane = threadIdx.x & 31, g = lane & (VS - 1), sh = lane - g;           \
-  const unsigned gmask = (VS == 32 ? 0xffffffffu : ((1u << VS) - 1u)) << sh;       \
-  (void)gmask
-
-template <int VS>
-__global__ void strength_count_kernel(int n, const int* __restrict__ ptr, const int* __restrict__ col,
-                                      const double* __restrict__ val, double theta,
-                                      unsigned char* __restrict__ keep, int* __restrict__ cnt) {
-  AIRG_GROUP(VS);
-  const long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / VS;
-  int b = 0, e = 0;
-  if (i < n) {
-    b = ptr[i];
-    e = ptr[i + 1];
-  }
-  double mx = 0.0;  // max is order-free: lanes stride the row, then reduce
-  for (int k = b + g; k < e; k += VS)
-    if (col[k] != i) mx = fmax(mx, fabs(val[k]));
-#pragma unroll
-  for (int o = VS / 2; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  const double thr = mul_rn(theta, mx);
-  int c = 0;
-  for (int k0 = b; __any_sync(0xffffffffu, k0 < e); k0 += VS) {
-    const int k = k0 + g;
-    bool st = false;
-    if (k < e) {
-      const double v = val[k];
-      st = col[k] != i && v != 0.0 && fabs(v) >= thr;
-      keep[k] = st;
-    }
-    c += __popc(__ballot_sync(0xffffffffu, st) & gmask);
-  }
-  if (i < n && g == 0) cnt[i] = c;
-}
-
-template <int VS>
-__global__ void compact_cols_kernel(int n, const int* __restrict__ ptr, const int* __restrict__ col,
-                                    const unsigned char* __restrict__ keep,
-                                    const int* __restrict__ optr, int* __restrict__ ocol) {
-  AIRG_GROUP(VS);
-  const long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / VS;
-  int b = 0, e = 0, o = 0;
-  if (i < n) {
-    b = ptr[i];
-    e = ptr[i + 1];
-    o = optr[i];
-  }
-  for (int k0 = b; __any_sync(0xffffffffu, k0 < e); k0 += VS) {
-    const int k = k0 + g;
-    const bool kp = k < e && keep[k];
-    const unsigned bal = __ballot_sync(0xffffffffu, kp) & gmask;
-    if (kp) ocol[o + __popc(bal & ((1u << lane) - 1u))] = col[k];
-    o += __popc(bal);
-  }
-}
-
-static int group_blocks(long long n, int vs) { return (int)((n * vs + 255) / 256); }
-
 __global__ void col_count_kernel(long long nnz, const int* __restrict__ col, int* __restrict__ cnt) {
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < nnz;
        k += (long long)gridDim.x * blockDim.x)
@@ -142,7 +82,7 @@ static int strength_closure(int n, const int* ptr, const int* col, const double*
   AIRG_TRY(scratch(&keep, nnz, s));
   AIRG_TRY(scratch(&cnt, n + 1, s));
   const int nb = blocks_for(n, 256);
-  strength_count_kernel<8><<<group_blocks(n, 8), 256, 0, s>>>(n, ptr, col, val, theta, keep, cnt);
+  strength_count_kernel<8><<<group_blocks(n, 8), 256, 0, s>>>(n, 0, ptr, col, val, theta, keep, cnt);
   AIRG_LAUNCH_CHECK();
   airg_csr_result* S = new_result(n, n, s);
   if (!S) return AIRG_ERR_CUDA;
@@ -325,51 +265,6 @@ int split_index(int n, const signed char* labels, int* pos, int* f_idx, int* c_i
 }
 
 // ---- DDC (splitting.py:162-207) --------------------------------------------
-// VS lanes load a row chunk coalesced; the group's first lane adds the
-// off-diagonal F entries in entry order (bincount's sequential sum)
-template <int VS>
-__global__ void ddc_ratio_kernel(int nf, const int* __restrict__ f_idx, const int* __restrict__ ptr,
-                                 const int* __restrict__ col, const double* __restrict__ val,
-                                 const signed char* __restrict__ labels, double* __restrict__ ratio,
-                                 int* __restrict__ bad) {
-  AIRG_GROUP(VS);
-  const long long t = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / VS;
-  int i = 0, b = 0, e = 0;
-  if (t < nf) {
-    i = f_idx[t];
-    b = ptr[i];
-    e = ptr[i + 1];
-  }
-  double sum = 0.0, d = 0.0;
-  for (int k0 = b; __any_sync(0xffffffffu, k0 < e); k0 += VS) {
-    const int k = k0 + g;
-    bool off = false, dia = false;
-    double a = 0.0;
-    if (k < e) {
-      const int j = col[k];
-      if (labels[j] == 0) {
-        a = val[k];
-        dia = j == i;
-        off = !dia;
-      }
-    }
-    const unsigned bo = __ballot_sync(0xffffffffu, off) & gmask;
-    const unsigned bd = __ballot_sync(0xffffffffu, dia) & gmask;
-    if (bd) d = __shfl_sync(0xffffffffu, a, __ffs(bd) - 1);
-    else __shfl_sync(0xffffffffu, a, lane);  // keep every lane in the shuffle
-    const double fa = fabs(a);
-#pragma unroll
-    for (int q = 0; q < VS; ++q) {
-      const double x = __shfl_sync(0xffffffffu, fa, sh + q);
-      if ((bo >> (sh + q)) & 1u) sum = add_rn(sum, x);
-    }
-  }
-  if (t < nf && g == 0) {
-    if (d == 0.0) atomicMin(bad, i);
-    ratio[t] = __ddiv_rn(sum, fabs(d));
-  }
-}
-
 __global__ void ddc_hist_kernel(int nf, const double* __restrict__ ratio, const double* __restrict__ edges,
                                 int nedges, unsigned long long* __restrict__ hist) {
   extern __shared__ unsigned long long sh[];
@@ -453,7 +348,7 @@ static int ddc_pass_run(int n, const int* ptr, const int* col, const double* val
   AIRG_CUDA(cudaMemcpyAsync(ibuf, init, sizeof init, cudaMemcpyHostToDevice, s));
   const int nb = blocks_for(nf, 256);
   if (nf > 0)
-    ddc_ratio_kernel<8><<<group_blocks(nf, 8), 256, 0, s>>>(nf, f_idx, ptr, col, val, labels, ratio, ibuf);
+    ddc_ratio_kernel<8><<<group_blocks(nf, 8), 256, 0, s>>>(nf, 0, f_idx, ptr, col, val, labels, ratio, ibuf);
   AIRG_LAUNCH_CHECK();
   int bad = 0;
   AIRG_CUDA(cudaMemcpyAsync(&bad, ibuf, sizeof(int), cudaMemcpyDeviceToHost, s));
