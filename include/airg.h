@@ -279,6 +279,7 @@ int airg_ddc_ratios(int nf, int row0, const int32_t* f_loc, const int32_t* ptr, 
                     double* minmaxsum_h, void* stream);
 int airg_ddc_hist(int nf, const double* ratio, const double* edges_h, int nedges, uint64_t* hist,
                   void* stream);
+/* converted_h may be NULL (no host read, no stream synchronisation) */
 int airg_ddc_convert(int nf, const int32_t* f_loc, const double* ratio, double cut, int all,
                      int8_t* labels, int32_t* converted_h, void* stream);
 /* elements [start, start+n) of the PCG64 stream (a + b*random()) */

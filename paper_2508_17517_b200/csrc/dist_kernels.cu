@@ -406,8 +406,10 @@ int airg_ddc_convert(int nf, const int32_t* f_loc, const double* ratio, double c
     ddc_convert_ext_kernel<<<blocks_for(nf, 256), 256, 0, s>>>(nf, f_loc, ratio, cut, all,
                                                                (signed char*)labels, c);
   AIRG_LAUNCH_CHECK();
-  AIRG_CUDA(cudaMemcpyAsync(converted_h, c, sizeof(int), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
+  if (converted_h) {  // NULL: no host read (the caller counts the labels itself)
+    AIRG_CUDA(cudaMemcpyAsync(converted_h, c, sizeof(int), cudaMemcpyDeviceToHost, s));
+    AIRG_CUDA(cudaStreamSynchronize(s));
+  }
   release(c, s);
   return AIRG_OK;
 }

@@ -62,6 +62,25 @@ class Comm:
         h = out.view(self.world, t.numel()).cpu().tolist()
         return h if many else [x[0] for x in h]
 
+    def sum_dev(self, t):
+        """Sum over ranks of a device integer scalar; one host read."""
+        return int(self.allreduce(t.reshape(1).to(I64)).item())
+
+    def allgather_dev(self, t):
+        """All-gather of a device integer vector -> host list over ranks; one
+        host read."""
+        t = t.reshape(-1).to(I64)
+        out = torch.empty(self.world * t.numel(), dtype=I64, device=t.device)
+        dist.all_gather_into_tensor(out, t, group=self.group)
+        return out.view(self.world, t.numel()).cpu().tolist()
+
+    def allgather_f(self, vals):
+        """Per-rank list of floats -> list over ranks; one host read."""
+        t = torch.tensor([float(x) for x in vals], dtype=VAL, device=self.device)
+        out = torch.empty(self.world * t.numel(), dtype=VAL, device=self.device)
+        dist.all_gather_into_tensor(out, t, group=self.group)
+        return out.view(self.world, t.numel()).cpu().tolist()
+
     def sum_ints(self, vals):
         """Elementwise sum over ranks of a list of integers; one host read."""
         t = torch.tensor([int(x) for x in vals], dtype=I64, device=self.device)
@@ -111,9 +130,10 @@ class Halo:
         self.n_loc = part.hi(r) - part.lo(r)
         self.n = int(self.ghost.numel())
         owners = part.owner(self.ghost) if self.n else torch.zeros(0, dtype=I64, device=comm.device)
-        self.recv_counts = torch.bincount(owners, minlength=W).cpu().tolist()
-        sc = comm.a2a(torch.tensor(self.recv_counts, dtype=I64, device=comm.device), [1] * W, [1] * W)
-        self.send_counts = sc.cpu().tolist()
+        # mat[q][p]: ghosts rank q needs from rank p (one all-gather, one host read)
+        mat = comm.allgather_dev(torch.bincount(owners, minlength=W))
+        self.recv_counts = mat[r]
+        self.send_counts = [mat[q][r] for q in range(W)]
         req = comm.a2a(self.ghost, self.recv_counts, self.send_counts)
         self.send_idx = req - part.lo(r)
 
@@ -133,7 +153,8 @@ class Halo:
         # element counts per peer (one segmented sum, one host copy)
         def per_peer(counts, lengths):
             seg = torch.repeat_interleave(torch.arange(len(counts), device=dev),
-                                          torch.tensor(counts, device=dev))
+                                          torch.tensor(counts, device=dev),
+                                          output_size=int(sum(counts)))
             tot = torch.zeros(len(counts), dtype=I64, device=dev)
             if lengths.numel():
                 tot.index_add_(0, seg, lengths)
@@ -142,11 +163,12 @@ class Halo:
         both = both.cpu().tolist()
         se, re_ = both[:self.comm.world], both[self.comm.world:]
         starts = M.row_offsets[:-1].to(I64)[self.send_idx]
-        tot = int(slen.sum().item())
+        tot = int(sum(se))
         if tot:
             first = torch.cumsum(slen, 0) - slen
-            idx = (torch.arange(tot, device=dev) - torch.repeat_interleave(first, slen)
-                   + torch.repeat_interleave(starts, slen))
+            idx = (torch.arange(tot, device=dev)
+                   - torch.repeat_interleave(first, slen, output_size=tot)
+                   + torch.repeat_interleave(starts, slen, output_size=tot))
             scol, sval = M.col_indices[idx], M.values[idx]
         else:
             scol = torch.zeros(0, dtype=IDX, device=dev)
@@ -285,8 +307,28 @@ def _local_index(labels, which):
     return torch.nonzero(labels == which).flatten().to(IDX)
 
 
+def stable_buckets(owner, counts):
+    """Permutation that orders ``owner`` (values 0..k-1, device) by bucket,
+    keeping the original order inside each bucket; ``counts`` = bincount
+    (device).  Elementwise + cumsum only: no host read."""
+    start = torch.cumsum(counts, 0) - counts
+    dest = torch.empty_like(owner)
+    for q in range(counts.numel()):
+        m = owner == q
+        dest = torch.where(m, start[q] + torch.cumsum(m.to(I64), 0) - 1, dest)
+    perm = torch.empty_like(owner)
+    perm[dest] = torch.arange(owner.numel(), device=owner.device, dtype=owner.dtype)
+    return perm
+
+
 def strength_closure(comm, A, theta):
-    """Local rows of pattern(S + S^T) (global columns).  ref: splitting.py:86-109"""
+    """Local rows of pattern(S + S^T) (global columns).  ref: splitting.py:86-109
+
+    S^T's local rows come from an all-to-all of the (j, i) pairs by the owner
+    of j; the received pairs are ordered by i (rank chunks in rank order,
+    each in its sender's row order), so a stable sort by the local row j
+    leaves every transposed row sorted.  Host reads: S's size, the
+    world x world pair counts."""
     r = comm.rank
     n, lo = A.M.nrows, A.rows.lo(r)
     res = L.C.c_void_p()
@@ -295,19 +337,22 @@ def strength_closure(comm, A, theta):
     S = take(res, values=False)
     dev = S.row_offsets.device
     lens = (S.row_offsets[1:] - S.row_offsets[:-1]).to(I64)
-    i_glob = lo + torch.repeat_interleave(torch.arange(n, device=dev, dtype=I64), lens)
+    i_glob = lo + torch.repeat_interleave(torch.arange(n, device=dev, dtype=I64), lens,
+                                          output_size=S.nnz)
     j_glob = S.col_indices.to(I64)
-    owners = A.rows.owner(j_glob)
-    order = torch.argsort(owners, stable=True)
-    sc = torch.bincount(owners, minlength=comm.world).cpu().tolist()
-    rc = comm.a2a(torch.tensor(sc, dtype=I64, device=dev), [1] * comm.world,
-                  [1] * comm.world).cpu().tolist()
-    rj = comm.a2a(j_glob[order], sc, rc)
-    ri = comm.a2a(i_glob[order], sc, rc)
-    key = (rj - lo) * A.rows.n + ri
-    key, _ = torch.sort(key)
-    trow = key // A.rows.n
-    tcol = (key % A.rows.n).to(IDX)
+    if comm.world > 1:
+        owners = A.rows.owner(j_glob)
+        cnt = torch.bincount(owners, minlength=comm.world)
+        mat = comm.allgather_dev(cnt)
+        sc = mat[r]
+        rc = [mat[q][r] for q in range(comm.world)]
+        perm = stable_buckets(owners, cnt)
+        rj = comm.a2a(j_glob[perm], sc, rc)
+        ri = comm.a2a(i_glob[perm], sc, rc)
+    else:
+        rj, ri = j_glob, i_glob
+    trow, p2 = torch.sort((rj - lo).to(IDX), stable=True)
+    tcol = ri[p2].to(IDX)
     tptr = torch.zeros(n + 1, dtype=I64, device=dev)
     tptr[1:] = torch.cumsum(torch.bincount(trow, minlength=n), 0)
     res = L.C.c_void_p()
@@ -356,39 +401,40 @@ def pmisr(comm, A, clo, seed, max_luby_loops=None):
     return labels
 
 
-def ddc_pass(comm, A_ext, labels_ext, n, row0, fraction, nbins):
-    """One distributed DDC pass (splitting.py:177-207); labels updated in place."""
+def ddc_pass(comm, A_ext, labels_ext, n, row0, fraction, nbins, nf, halo):
+    """One distributed DDC pass (splitting.py:177-207); labels updated in place
+    (ghosts refreshed through ``halo``).  ``nf`` is the global F count before
+    the pass; returns (stats, global F count after).  Host reads: the F index
+    list, the local ratio extrema, one all-gather of [bad, min, max, sum], the
+    histogram, the F count after."""
     from .cfsplit import DDCPassStats
     f_loc = _local_index(labels_ext[:n], 0)
     nf_loc = int(f_loc.numel())
-    nf = comm.sum_int(nf_loc)
+    if nf == 0:
+        raise ValueError('zero-size array to reduction operation minimum which has no identity')
     ratio = empty(nf_loc, VAL)
     bad = L.i32()
     mms = np.zeros(3)
     L.call('airg_ddc_ratios', nf_loc, row0, L.ptr(f_loc), L.ptr(A_ext.row_offsets),
            L.ptr(A_ext.col_indices), L.ptr(A_ext.values), L.ptr(labels_ext), L.ptr(ratio),
            L.C.byref(bad), L.hptr(mms), L.stream_handle())
-    dev = ratio.device
-    # one MIN allreduce carries the zero-diagonal flag and the ratio extrema
-    mn = comm.allreduce(torch.tensor([float(bad.value), mms[0], -mms[1]], dtype=VAL, device=dev),
-                        'min').cpu().numpy()
-    b = int(mn[0])
+    g = comm.allgather_f([float(bad.value), mms[0], mms[1], mms[2] if nf_loc else 0.0])
+    b = int(min(x[0] for x in g))
     if b != 0x7fffffff:
         raise ValueError(f'zero diagonal in fine-fine block (fine row {b}); splitting is not '
                          'usable for reduction')
-    if nf == 0:
-        raise ValueError('zero-size array to reduction operation minimum which has no identity')
-    lo, hi = float(mn[1]), float(-mn[2])
-    sm = float(comm.allreduce(torch.tensor([mms[2] if nf_loc else 0.0], dtype=VAL,
-                                           device=dev)).item())
+    lo, hi = min(x[1] for x in g), max(x[2] for x in g)
+    sm = 0.0
+    for x in g:
+        sm += x[3]
     target = fraction * nf
-    conv = L.i32()
+    dev = ratio.device
     if lo == hi:
         allc = abs(nf - target) < target
         cut = lo if allc else hi
         if allc:
             L.call('airg_ddc_convert', nf_loc, L.ptr(f_loc), L.ptr(ratio), cut, 1, L.ptr(labels_ext),
-                   L.C.byref(conv), L.stream_handle())
+                   None, L.stream_handle())
     else:
         edges = lo + (hi - lo) * np.arange(nbins + 1) / nbins
         edges = np.ascontiguousarray(edges)
@@ -400,10 +446,11 @@ def ddc_pass(comm, A_ext, labels_ext, n, row0, fraction, nbins):
         k = nbins - int(np.argmin(np.abs(above - target)[::-1]))
         cut = float(edges[k])
         L.call('airg_ddc_convert', nf_loc, L.ptr(f_loc), L.ptr(ratio), cut, 0, L.ptr(labels_ext),
-               L.C.byref(conv), L.stream_handle())
-    converted = comm.sum_int(conv.value)
-    return DDCPassStats(n_f_before=nf, converted=converted, ratio_min=lo, ratio_max=hi,
-                        ratio_mean=sm / nf, cut=cut)
+               None, L.stream_handle())
+    labels_ext[n:] = halo.values(labels_ext[:n])
+    nf_after = comm.sum_dev((labels_ext[:n] == 0).sum())
+    return DDCPassStats(n_f_before=nf, converted=nf - nf_after, ratio_min=lo, ratio_max=hi,
+                        ratio_mean=sm / nf, cut=cut), nf_after
 
 
 def dist_arnoldi_coeffs(comm, A_ff, halo, order, seed):
@@ -553,12 +600,14 @@ def setup_distributed(comm, A, cfg, poly_inject=None, replicate_below=20000, for
         A_ext = with_cols(cur.M, halo_a.ext_cols(cur.M.col_indices), n + halo_a.n)
         lab_ext = halo_a.ext(labels)
         stats = []
+        nf_glob = comm.sum_dev((lab_ext[:n] == 0).sum())
         for _ in range(cfg.ddc_its):
-            if int(comm.allreduce((lab_ext[:n] == 0).sum().reshape(1).to(I64)).item()) == 0:
+            if nf_glob == 0:
                 break
-            stats.append(ddc_pass(comm, A_ext, lab_ext, n, lo, cfg.ddc_fraction, cfg.ddc_bins))
-            lab_ext[n:] = halo_a.values(lab_ext[:n])
-        nc_glob = int(comm.allreduce((lab_ext[:n] == 1).sum().reshape(1).to(I64)).item())
+            st_, nf_glob = ddc_pass(comm, A_ext, lab_ext, n, lo, cfg.ddc_fraction, cfg.ddc_bins,
+                                    nf_glob, halo_a)
+            stats.append(st_)
+        nc_glob = cur.rows.n - nf_glob
         tick('cf_split.ddc')
         if nc_glob == cur.rows.n:
             raise ValueError(f'splitting produced no F points at level {level}')

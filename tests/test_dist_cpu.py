@@ -103,3 +103,12 @@ def test_halo_exchange_gloo_world2():
     out = mgr.dict()
     mp.spawn(_worker, args=(2, port, out), nprocs=2, join=True)
     assert dict(out) == {0: 'ok', 1: 'ok'}, dict(out)
+
+
+def test_stable_buckets_is_a_stable_sort_by_owner():
+    from paper_2508_17517_b200.dist import stable_buckets
+    g = torch.Generator().manual_seed(7)
+    for world in (1, 2, 4):
+        owner = torch.randint(0, world, (1000,), generator=g)
+        perm = stable_buckets(owner, torch.bincount(owner, minlength=world))
+        assert torch.equal(perm, torch.argsort(owner, stable=True))
