@@ -51,6 +51,12 @@ __device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long
   return v;
 }
 
+__device__ __forceinline__ double ld_relaxed_sys_d(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // spin on one peer's message count (relaxed polls, one acquire fence once it
 // is reached: an acquire per poll would keep invalidating the SM's L1 under
 // the CTAs sharing it); traps (fails the context) after ~20 s instead of
@@ -1589,10 +1595,15 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
 }
 
 // gathers and stores the send entries into the peers' ghost tails, then (last
-// CTA) publishes the new message counts and raises the expected counts of the
-// messages this exchange receives (the consumer kernel waits on those)
-__global__ void put_kernel(PutDesc d, const double* __restrict__ x, unsigned long long* sent,
-                           unsigned long long* expect, unsigned int* ticket) {
+// CTA) publishes the new message counts, raises the expected counts of the
+// messages this exchange receives and waits for them: the kernel completes
+// only once the peers' ghost values have landed, so the consuming kernel needs
+// no separate wait launch (its griddepcontrol.wait / stream order is the
+// acquire edge)
+__global__ void put_kernel(PutDesc d, WaitDesc w, const double* __restrict__ x,
+                           unsigned long long* sent, unsigned long long* expect,
+                           unsigned int* ticket, const unsigned long long* flags) {
+  pdl_enter();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d.nsend; i += gridDim.x * blockDim.x) {
     int q = 0;
     while (i >= d.sofs[q + 1]) ++q;
@@ -1610,20 +1621,117 @@ __global__ void put_kernel(PutDesc d, const double* __restrict__ x, unsigned lon
           st_release_sys(d.rflag[j], ++sent[d.peer[j]]);
           ++expect[d.peer[j]];
         }
+      for (int j = 0; j < w.npeer; ++j) wait_count(flags + w.peer[j], expect[w.peer[j]]);
     }
   }
 }
 
-// wait for the listed peers' messages (counts raised by the matching put)
-__global__ void wait_kernel(WaitDesc w, const unsigned long long* flags, const unsigned long long* expect) {
-  const int t = threadIdx.x;
-  if (t < w.npeer) wait_count(flags + w.peer[t], expect[w.peer[t]]);
+// ---- LL halo exchange (no system-scope fences) -------------------------------
+// Every ghost value travels as one 16-byte slot {lo32, flag, hi32, flag}
+// written with a single vector store (NCCL's LL format: each 8-byte
+// (data, flag) half lands atomically), so the receiver needs no fence: it polls
+// the slots of its own LL region until both flags equal the exchange's
+// sequence number and copies the values into the vector's ghost tail.  Each
+// message also carries a header slot, so every exchange is a two-way handshake
+// between halo partners even when one direction has no data.  Per partner
+// pair the sequence number counts the exchanges; its parity selects one of two
+// slot banks: the sender can only reuse a bank after the receiver has sent the
+// next message, i.e. finished the kernel that drained it.
+struct LLDesc {
+  int nsend = 0, nrecv = 0;
+  const int* idx = nullptr;
+  int npeer = 0;
+  int peer[kMaxPeers] = {};
+  int sofs[kMaxPeers + 1] = {};          // send segments per partner
+  int rofs[kMaxPeers + 1] = {};          // ghost-tail segments per partner
+  uint4* rdst[kMaxPeers] = {};           // partner's LL region for me
+  int rcap[kMaxPeers] = {};              // slots per bank there
+  const uint4* lsrc[kMaxPeers] = {};     // my LL region for the partner
+  int lcap[kMaxPeers] = {};
+  double* ghost = nullptr;               // target vector + n_loc
+};
+
+__device__ __forceinline__ void st_ll(uint4* p, double v, unsigned f) {
+  const unsigned long long u = __double_as_longlong(v);
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"((unsigned)u), "r"(f),
+               "r"((unsigned)(u >> 32)), "r"(f)
+               : "memory");
 }
 
-// norm allreduce, step 1: my partial sum into every peer's slot (parity of the
-// local call count keeps consecutive reductions apart)
-__global__ void norm_put_kernel(NormDesc d, const double* loc, const unsigned long long* ncount,
-                                unsigned long long* sent, unsigned long long* expect) {
+__device__ __forceinline__ double ld_ll(const uint4* p, unsigned f) {
+  unsigned a, b, c, d;
+  const long long t0 = clock64();
+  for (;;) {
+    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+                 : "l"(p)
+                 : "memory");
+    if (b == f && d == f) break;
+    if (clock64() - t0 > 40000000000ll) __trap();
+  }
+  return __longlong_as_double((long long)(((unsigned long long)c << 32) | a));
+}
+
+__global__ void ll_halo_kernel(LLDesc d, const double* __restrict__ x, unsigned long long* seq,
+                               unsigned int* ticket) {
+  pdl_enter();
+  unsigned f[kMaxPeers];
+#pragma unroll
+  for (int j = 0; j < kMaxPeers; ++j) f[j] = j < d.npeer ? (unsigned)seq[d.peer[j]] + 1u : 0u;
+  const int stride = gridDim.x * blockDim.x;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int i = tid; i < d.nsend + d.npeer; i += stride) {
+    int j, slot;
+    double v = 0.0;
+    if (i < d.nsend) {
+      j = 0;
+      while (i >= d.sofs[j + 1]) ++j;
+      slot = 1 + i - d.sofs[j];
+      v = x[d.idx[i]];
+    } else {
+      j = i - d.nsend;
+      slot = 0;
+    }
+    unsigned fj = 0;
+#pragma unroll
+    for (int q = 0; q < kMaxPeers; ++q)
+      if (q == j) fj = f[q];
+    st_ll(d.rdst[j] + (size_t)(fj & 1u) * d.rcap[j] + slot, v, fj);
+  }
+  for (int i = tid; i < d.nrecv + d.npeer; i += stride) {
+    int j, slot;
+    if (i < d.nrecv) {
+      j = 0;
+      while (i >= d.rofs[j + 1]) ++j;
+      slot = 1 + i - d.rofs[j];
+    } else {
+      j = i - d.nrecv;
+      slot = 0;
+    }
+    unsigned fj = 0;
+#pragma unroll
+    for (int q = 0; q < kMaxPeers; ++q)
+      if (q == j) fj = f[q];
+    const double v = ld_ll(d.lsrc[j] + (size_t)(fj & 1u) * d.lcap[j] + slot, fj);
+    if (slot) d.ghost[i] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(ticket, 1u);
+    if (t == gridDim.x - 1) {  // every CTA has read the sequence numbers
+      *ticket = 0u;
+      for (int j = 0; j < d.npeer; ++j) seq[d.peer[j]] += 1ull;
+    }
+  }
+}
+
+// norm allreduce in one single-thread kernel: my partial sum into every
+// peer's slot (the parity of the local call count keeps consecutive
+// reductions apart), publish, wait for the peers' partials, rank-ordered sum
+__global__ void norm_kernel(NormDesc d, WaitDesc w, const double* loc, double* slots_mine,
+                            unsigned long long* ncount, unsigned long long* sent,
+                            unsigned long long* expect, const unsigned long long* flags, double* out) {
+  pdl_enter();
   const int par = (int)(*ncount & 1ull);
   const double v = *loc;
   for (int j = 0; j < d.npeer; ++j) d.slots[j][par * d.world + d.me] = v;
@@ -1632,14 +1740,9 @@ __global__ void norm_put_kernel(NormDesc d, const double* loc, const unsigned lo
     st_release_sys(d.rflag[j], ++sent[d.peer[j]]);
     ++expect[d.peer[j]];
   }
-}
-
-// step 2 (after the wait): rank-ordered sum of the partials -> out
-__global__ void norm_sum_kernel(int me, int world, const double* loc, const double* slots,
-                                unsigned long long* ncount, double* out) {
-  const int par = (int)(*ncount & 1ull);
+  for (int j = 0; j < w.npeer; ++j) wait_count(flags + w.peer[j], expect[w.peer[j]]);
   double s = 0.0;
-  for (int q = 0; q < world; ++q) s += q == me ? *loc : slots[par * world + q];
+  for (int q = 0; q < d.world; ++q) s += q == d.me ? v : ld_relaxed_sys_d(slots_mine + par * d.world + q);
   *out = s;
   *ncount += 1ull;
 }
@@ -1651,6 +1754,7 @@ __global__ void pack_kernel(int n, const int* __restrict__ idx, const double* __
 }
 
 __global__ void finish_sum_kernel(int nparts, const double* __restrict__ parts, double* __restrict__ out) {
+  pdl_enter();
   __shared__ double red[32];
   double s = 0.0;
   for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += parts[i];
@@ -1679,6 +1783,7 @@ __global__ void unpad_kernel(int world, int tmax, const int* __restrict__ cnt, c
 struct P2PHalo {
   PutDesc put;
   WaitDesc wait;
+  LLDesc ll;
 };
 
 struct DLev {
@@ -1736,6 +1841,11 @@ struct airg_dplan {
   double* nslots = nullptr;
   unsigned long long *flags = nullptr, *sent = nullptr, *recvd = nullptr, *ncount = nullptr;
   unsigned int* ticket = nullptr;
+  unsigned long long* lseq = nullptr;  // LL exchanges per partner
+  unsigned int* llticket = nullptr;
+  bool ll = true;
+  std::vector<size_t> ll_off;  // my LL region per sender (doubles into the arena)
+  std::vector<int> ll_cap;     // its bank size (slots)
   std::vector<void*> owned;  // dmalloc'd buffers freed at destroy
   cudaStream_t cs = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
@@ -1751,40 +1861,35 @@ static int dalloc_owned(airg_dplan* p, T** ptr, size_t count) {
   return AIRG_OK;
 }
 
-// put half of a P2P exchange (the consumer waits: wait_into / wait_kernel)
-static int wait_now(airg_dplan* p, const WaitDesc& w, cudaStream_t s);
-
+// one P2P exchange: the put kernel stores, publishes and waits (put_kernel)
 static int halo_put(airg_dplan* p, const P2PHalo& h, const double* x, cudaStream_t s) {
   const PutDesc& d = h.put;
   if (d.npeer == 0) return AIRG_OK;
   // measured: spreading the gather over CTAs beats one CTA (dependent
   // idx -> x -> remote-store chains); at most 16 CTAs
-  put_kernel<<<std::max(1, blocks_for(d.nsend, 256, 16)), 256, 0, s>>>(d, x, p->sent, p->recvd,
-                                                                      p->ticket);
-  AIRG_LAUNCH_CHECK();
+  AIRG_CUDA(launch_pdl(put_kernel, std::max(1, blocks_for(d.nsend, 256, 16)), 256, s, d, h.wait, x,
+                       p->sent, p->recvd, p->ticket, (const unsigned long long*)p->flags));
   ++p->launches;
   return AIRG_OK;
 }
 
 
-static int wait_now(airg_dplan* p, const WaitDesc& w, cudaStream_t s) {
-  if (!w.npeer) return AIRG_OK;
-  wait_kernel<<<1, 32, 0, s>>>(w, p->flags, p->recvd);
-  AIRG_LAUNCH_CHECK();
-  ++p->launches;
-  return AIRG_OK;
-}
-
-// P2P: put kernel + one-CTA wait kernel.  Waiting inside the consuming SpMV
+// P2P: one put kernel whose last CTA also waits for the incoming ghosts (a
+// separate one-CTA wait kernel per exchange measured slower).  Waiting inside the consuming SpMV
 // was measured slower both with every CTA polling (2x SpMV time) and with only
 // the CTAs that read ghost columns polling (solve 30 vs 21 ms at N = 2: the
 // peer wait lands inside the large kernels).  NCCL: pack + send/recv
 static int halo_exchange(airg_dplan* p, HaloX& h, const P2PHalo* ph, double* x_ext, cudaStream_t s) {
   if (p->world == 1) return AIRG_OK;
-  if (p->p2p) {
-    AIRG_TRY(halo_put(p, *ph, x_ext, s));
-    return wait_now(p, ph->wait, s);
+  if (p->p2p && p->ll) {
+    const LLDesc& d = ph->ll;
+    if (d.npeer == 0) return AIRG_OK;
+    AIRG_CUDA(launch_pdl(ll_halo_kernel, std::max(1, blocks_for(d.nsend + d.nrecv, 256, 16)), 256, s, d,
+                         (const double*)x_ext, p->lseq, p->llticket));
+    ++p->launches;
+    return AIRG_OK;
   }
+  if (p->p2p) return halo_put(p, *ph, x_ext, s);  // the put kernel also waits
   if (h.nsend) {
     pack_kernel<<<blocks_for(h.nsend, 256, 1024), 256, 0, s>>>(h.nsend, h.send_idx, x_ext, h.sendbuf);
     AIRG_LAUNCH_CHECK();
@@ -1809,12 +1914,9 @@ static int norm_allreduce(airg_dplan* p, cudaStream_t s) {
     AIRG_NCCL(ncclAllReduce(p->nrm_loc, p->nrm_glob, 1, ncclDouble, ncclSum, p->comm, s));
     return AIRG_OK;
   }
-  norm_put_kernel<<<1, 1, 0, s>>>(p->nd, p->nrm_loc, p->ncount, p->sent, p->recvd);
-  AIRG_LAUNCH_CHECK();
-  AIRG_TRY(wait_now(p, p->nwait, s));
-  norm_sum_kernel<<<1, 1, 0, s>>>(p->rank, p->world, p->nrm_loc, p->nslots, p->ncount, p->nrm_glob);
-  AIRG_LAUNCH_CHECK();
-  p->launches += 2;
+  AIRG_CUDA(launch_pdl(norm_kernel, 1, 1, s, p->nd, p->nwait, (const double*)p->nrm_loc, p->nslots,
+                       p->ncount, p->sent, p->recvd, (const unsigned long long*)p->flags, p->nrm_glob));
+  ++p->launches;
   return AIRG_OK;
 }
 
@@ -1824,8 +1926,7 @@ static int dplan_vcycle(airg_dplan* p, int l, cudaStream_t s);
 static int dplan_tail(airg_dplan* p, const double* in, double* out, cudaStream_t s) {
   const int mine = p->tcnt[p->rank];
   if (p->p2p) {
-    AIRG_TRY(halo_put(p, p->pTail, in, s));
-    AIRG_TRY(wait_now(p, p->pTail.wait, s));
+    AIRG_TRY(halo_put(p, p->pTail, in, s));  // waits for the peers' parts too
   } else {
     AIRG_CUDA(cudaMemcpyAsync(p->tsend, in, (size_t)mine * sizeof(double), cudaMemcpyDeviceToDevice, s));
     AIRG_NCCL(ncclAllGather(p->tsend, p->trecv, p->tmax, ncclDouble, p->comm, s));
@@ -1883,10 +1984,10 @@ static int dplan_vcycle(airg_dplan* p, int l, cudaStream_t s) {
 static int dplan_residual(airg_dplan* p, const double* b, cudaStream_t s) {
   AIRG_TRY(halo_exchange(p, p->hT, &p->pT, p->x_ext, s));
   const int nb = spmv_blocks(p->top);
-  Epi ep{p->r, nullptr, -1.0, 1.0, b, nullptr, nullptr, p->parts};
+  // written straight into level 0's input vector (no copy per iteration)
+  Epi ep{p->lv[0].r_ext, nullptr, -1.0, 1.0, b, nullptr, nullptr, p->parts};
   AIRG_TRY(launch_spmv(p->top, p->x_ext, 1.0, ep, s));
-  finish_sum_kernel<<<1, 1024, 0, s>>>(nb, p->parts, p->nrm_loc);
-  AIRG_LAUNCH_CHECK();
+  AIRG_CUDA(launch_pdl(finish_sum_kernel, 1, 1024, s, nb, (const double*)p->parts, p->nrm_loc));
   return norm_allreduce(p, s);
 }
 
@@ -1925,7 +2026,8 @@ static int dalloc(airg_dplan* p, HaloX& h, int n_loc, int nsend, const int* send
 //   offsets of tr_full, norm slots, flags
 enum { kDirLev = 5 };
 
-static size_t dir_len(int nd, int W) { return (size_t)nd * (kDirLev + 3 * (1 + W)) + (2 + W) + 3; }
+// ... then per sender q: offset and bank size (slots) of my LL region for q
+static size_t dir_len(int nd, int W) { return (size_t)nd * (kDirLev + 3 * (1 + W)) + (2 + W) + 2 * W + 3; }
 
 static int p2p_peers(const HaloX& h, int me, int W, std::vector<int>& out) {
   out.clear();
@@ -1964,6 +2066,33 @@ static int build_p2p_halo(airg_dplan* p, const HaloX& h, const std::vector<long 
   out.put = d;
   out.wait.npeer = d.npeer;
   for (int j = 0; j < d.npeer; ++j) out.wait.peer[j] = peers[j];
+  // LL form of the same exchange
+  LLDesc l{};
+  l.nsend = h.nsend;
+  l.nrecv = h.nrecv;
+  l.idx = h.send_idx;
+  l.npeer = d.npeer;
+  const size_t llb = dl - 3 - 2 * (size_t)W;  // directory: LL offsets, then bank sizes
+  for (int j = 0; j < l.npeer; ++j) {
+    const int q = peers[j];
+    const long long* D = dir.data() + (size_t)q * dl;
+    l.peer[j] = q;
+    l.sofs[j] = h.sofs[q];
+    l.rofs[j] = h.rofs[q];
+    l.rdst[j] = (uint4*)(p->peer_base[q] + D[llb + me]);
+    l.rcap[j] = (int)D[llb + W + me];
+    l.lsrc[j] = (const uint4*)(p->arena + p->ll_off[q]);
+    l.lcap[j] = p->ll_cap[q];
+  }
+  l.sofs[l.npeer] = h.nsend;
+  l.rofs[l.npeer] = h.nrecv;
+  for (int j = l.npeer - 1; j >= 0; --j) {
+    if (h.scnt[l.peer[j]] == 0) l.sofs[j] = l.sofs[j + 1];
+    if (h.rcnt[l.peer[j]] == 0) l.rofs[j] = l.rofs[j + 1];
+  }
+  const long long* Dm = dir.data() + (size_t)me * dl;
+  l.ghost = p->arena + Dm[vec_slot] + Dm[hslot];
+  out.ll = l;
   return AIRG_OK;
 }
 
@@ -1994,6 +2123,19 @@ static int p2p_setup(airg_dplan* p) {
   off += up((size_t)p->n_top + p->hT.nrecv + 1);
   mine[k++] = p->hT.n_loc;
   for (int q = 0; q < W; ++q) mine[k++] = p->hT.rofs[q];
+  // LL regions: per sender, two banks of (1 header + largest message) 16-byte slots
+  p->ll_off.assign(W, 0);
+  p->ll_cap.assign(W, 0);
+  for (int q = 0; q < W; ++q) {
+    if (q == me) continue;
+    int mx = p->hT.rcnt[q];
+    for (const DLev& L : p->lv) mx = std::max({mx, L.hR.rcnt[q], L.hC.rcnt[q], L.hF.rcnt[q]});
+    p->ll_cap[q] = 1 + mx;
+    p->ll_off[q] = off;
+    off += up((size_t)4 * p->ll_cap[q]);
+  }
+  for (int q = 0; q < W; ++q) mine[k++] = (long long)p->ll_off[q];
+  for (int q = 0; q < W; ++q) mine[k++] = p->ll_cap[q];
   const size_t tr_off = off;
   mine[k++] = (long long)off;
   off += up((size_t)p->tail_n + 1);
@@ -2123,13 +2265,15 @@ static int p2p_setup(airg_dplan* p) {
   }
   if (!p->sent) {
     unsigned long long* ctr = nullptr;
-    AIRG_TRY(dalloc_owned(p, &ctr, (size_t)3 * W + 2));
+    AIRG_TRY(dalloc_owned(p, &ctr, (size_t)4 * W + 3));
     p->sent = ctr;
     p->recvd = ctr + W;
     p->ncount = ctr + 2 * W;
     p->ticket = (unsigned int*)(ctr + 2 * W + 1);
+    p->lseq = ctr + 2 * W + 2;
+    p->llticket = (unsigned int*)(ctr + 3 * W + 2);
   }
-  AIRG_CUDA(cudaMemset(p->sent, 0, ((size_t)3 * W + 2) * sizeof(unsigned long long)));
+  AIRG_CUDA(cudaMemset(p->sent, 0, ((size_t)4 * W + 3) * sizeof(unsigned long long)));
   AIRG_CUDA(cudaDeviceSynchronize());
   return AIRG_OK;
 }
@@ -2245,6 +2389,8 @@ int airg_dplan_finish(airg_dplan* p, airg_plan* tail, const int32_t* counts_h) {
   p->tmax = mx;
   static const bool force_nccl = getenv("AIRG_DPLAN_NCCL") != nullptr;
   p->p2p = p->world > 1 && !force_nccl;
+  static const bool no_ll = getenv("AIRG_DPLAN_LL") && atoi(getenv("AIRG_DPLAN_LL")) == 0;
+  p->ll = !no_ll;  // AIRG_DPLAN_LL=0: fenced put kernels instead of LL slots
   if (p->p2p) {
     const int rc = p2p_setup(p);
     if (rc != AIRG_OK) return rc;
@@ -2337,7 +2483,6 @@ int airg_dplan_richardson(airg_dplan* p, const double* b, double* x, double rtol
   }
   auto iteration = [&](cudaStream_t t) -> int {
     DLev& L0 = p->lv[0];
-    AIRG_CUDA(cudaMemcpyAsync(L0.r_ext, p->r, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, t));
     AIRG_TRY(dplan_vcycle(p, 0, t));
     AIRG_TRY(launch_axpby(n, p->x_ext, nullptr, 1.0, p->x_ext, nullptr, 1.0, L0.e, t));
     return dplan_residual(p, b, t);
