@@ -137,6 +137,50 @@ class Halo:
         req = comm.a2a(self.ghost, self.recv_counts, self.send_counts)
         self.send_idx = req - part.lo(r)
 
+    @classmethod
+    def many(cls, comm, items):
+        """Halo(comm, part, need) for every (part, need) of ``items`` with ONE
+        all-gather of the count matrices and ONE all-to-all of the requests
+        (instead of two collectives per plan).  Same plans as the per-item
+        constructor: ghosts sorted, per-peer requests in ghost order."""
+        W, r, K = comm.world, comm.rank, len(items)
+        if K == 0:
+            return []
+        dev = comm.device
+        hs, owners = [], []
+        for part, need in items:
+            h = cls.__new__(cls)
+            h.comm, h.part = comm, part
+            h.ghost = need.to(I64)
+            h.n_loc = part.hi(r) - part.lo(r)
+            h.n = int(h.ghost.numel())
+            hs.append(h)
+            owners.append(part.owner(h.ghost) if h.n else torch.zeros(0, dtype=I64, device=dev))
+        counts = torch.stack([torch.bincount(o, minlength=W) for o in owners])  # [K, W]
+        mat = np.asarray(comm.allgather_dev(counts)).reshape(W, K, W)  # [q, i, p]
+        # send buffer ordered by (peer, item); within one item the ghosts of a
+        # peer are contiguous (sorted ids, contiguous partition)
+        key = torch.cat([o * K + i for i, o in enumerate(owners)])
+        ghosts = torch.cat([h.ghost for h in hs])
+        send = ghosts[torch.argsort(key, stable=True)] if ghosts.numel() else ghosts
+        send_tot = [int(mat[r, :, p].sum()) for p in range(W)]
+        recv_tot = [int(mat[q, :, r].sum()) for q in range(W)]
+        req = comm.a2a(send, send_tot, recv_tot)
+        # received: peer q, then item i; regroup per item in peer order
+        seg = mat[:, :, r]  # [q, i] requests of q for item i
+        off = np.concatenate([[0], np.cumsum(seg.reshape(-1))])[:-1].reshape(W, K)
+        parts = [np.arange(off[q, i], off[q, i] + seg[q, i]) for i in range(K) for q in range(W)]
+        perm = torch.from_numpy(np.concatenate(parts).astype(np.int64)).to(dev) if parts else None
+        req = req[perm] if perm is not None and req.numel() else req
+        pos = 0
+        for i, h in enumerate(hs):
+            h.recv_counts = [int(mat[r, i, p]) for p in range(W)]
+            h.send_counts = [int(mat[q, i, r]) for q in range(W)]
+            ns = int(sum(h.send_counts))
+            h.send_idx = req[pos:pos + ns] - h.part.lo(r)
+            pos += ns
+        return hs
+
     def values(self, local):
         """Ghost values (in ghost order) of a per-local-row array."""
         return self.comm.a2a(local[self.send_idx], self.send_counts, self.recv_counts)
@@ -763,11 +807,23 @@ class DistSolver:
         r = comm.rank
         self.comm = comm
         self.lv = []
+        top = H.top
+        # every ghost plan the setup did not leave behind, built in one batch
+        # (one all-gather + one all-to-all): the R and A_ff plans of the setup
+        # are the solve's; A_fc and the top operator need new ones
+        want = []
         for d in H.dlevels:
-            # the R and A_ff ghost plans of the setup are the solve's
-            hR = d.halo_R or Halo(comm, d.fine, remote_cols(d.R.col_indices, d.fine, r))
-            hC = Halo(comm, d.cpart, remote_cols(d.A_fc.col_indices, d.cpart, r))
-            hF = d.halo_F or Halo(comm, d.fpart, remote_cols(d.A_ff.col_indices, d.fpart, r))
+            if d.halo_R is None:
+                want.append((d.fine, remote_cols(d.R.col_indices, d.fine, r)))
+            want.append((d.cpart, remote_cols(d.A_fc.col_indices, d.cpart, r)))
+            if d.halo_F is None:
+                want.append((d.fpart, remote_cols(d.A_ff.col_indices, d.fpart, r)))
+        want.append((top.rows, remote_cols(top.M.col_indices, top.rows, r)))
+        built = iter(Halo.many(comm, want))
+        for d in H.dlevels:
+            hR = d.halo_R if d.halo_R is not None else next(built)
+            hC = next(built)
+            hF = d.halo_F if d.halo_F is not None else next(built)
             self.lv.append(dict(
                 R=with_cols(d.R, hR.ext_cols(d.R.col_indices), hR.n_loc + hR.n),
                 hR=hR,
@@ -775,8 +831,7 @@ class DistSolver:
                 Aff=with_cols(d.A_ff, hF.ext_cols(d.A_ff.col_indices), hF.n_loc + hF.n), hF=hF,
                 f=d.f_loc.long(), c=d.c_loc.long(), n=d.fine.hi(r) - d.fine.lo(r),
                 coef=np.asarray(d.f_smoother.coeffs, dtype=np.float64)))
-        top = H.top
-        self.htop = Halo(comm, top.rows, remote_cols(top.M.col_indices, top.rows, r))
+        self.htop = next(built)
         self.Atop = with_cols(top.M, self.htop.ext_cols(top.M.col_indices),
                               self.htop.n_loc + self.htop.n)
         # partition of the first replicated level (the tail's top matrix)

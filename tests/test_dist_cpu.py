@@ -89,6 +89,23 @@ def _worker(rank, world, port, out):
         # local rows followed by ghost rows
         R = D.cat_rows(M, gp, gc, gv, n)
         assert R.nrows == (hi - lo) + len(expect_need)
+        # batched plans (one all-gather + one all-to-all) == one plan per item
+        part2 = D.Part.from_counts([30, 7], cpu)
+        rng = np.random.default_rng(11 + rank)
+        lo2, hi2 = part2.lo(rank), part2.hi(rank)
+        need2 = torch.tensor(sorted({int(c) for c in rng.integers(0, n, 25)
+                                     if not lo2 <= c < hi2}), dtype=torch.int64)
+        items = [(part, need), (part2, need2), (part, torch.zeros(0, dtype=torch.int64)),
+                 (part2, need2[:3])]
+        single = [D.Halo(comm, p_, q_) for p_, q_ in items]
+        batch = D.Halo.many(comm, items)
+        for s_, b_ in zip(single, batch):
+            assert s_.n == b_.n and s_.n_loc == b_.n_loc
+            assert list(s_.recv_counts) == list(b_.recv_counts)
+            assert list(s_.send_counts) == list(b_.send_counts)
+            assert s_.send_idx.tolist() == b_.send_idx.tolist()
+            loc2 = 0.25 * torch.arange(b_.part.lo(rank), b_.part.hi(rank), dtype=torch.float64)
+            assert b_.values(loc2).tolist() == s_.values(loc2).tolist()
         out[rank] = 'ok'
     except Exception as e:  # surface the failing assertion in the parent
         import traceback
