@@ -415,7 +415,8 @@ class DistWorkload:
         # the inflow strip builds ~12 % less work per row (measured at N = 2
         # and 4, tools/dist_kprof.py): it gets proportionally more grid rows
         self.Ad = D.advection_2d_strips(self.comm, nx, nx * world, *PI4,
-                                        weights=[1.14] + [1.0] * (world - 1))
+                                        weights=[float(os.environ.get('AIRG_STRIP_W0', 1.14))]
+                                        + [1.0] * (world - 1))
         self.n = self.Ad.M.nrows
         self.n_total = self.Ad.rows.n
         self.b = torch.zeros(self.n, dtype=torch.float64, device='cuda')
