@@ -29,6 +29,25 @@ __device__ double block_sum(double v, double* red) {
   return red[32];
 }
 
+// block_sum for an 8-warp CTA with ONE barrier: warp totals go to one of two
+// alternating slot sets (a fast warp's next write cannot meet a slow warp's
+// read of the current set: reusing a set needs the barrier in between), and
+// every thread adds the 8 totals in the xor-butterfly order of block_sum's
+// final warp_sum (lanes >= 8 contribute exact zeros), so the value is
+// bitwise block_sum's.
+struct Sum8 {
+  double* red;  // 16 slots
+  int buf;
+  __device__ __forceinline__ double operator()(double v) {
+    v = warp_sum(v);
+    double* r = red + 8 * buf;
+    if ((threadIdx.x & 31) == 0) r[threadIdx.x >> 5] = v;
+    buf ^= 1;
+    __syncthreads();
+    return ((r[0] + r[4]) + (r[2] + r[6])) + ((r[1] + r[5]) + (r[3] + r[7]));
+  }
+};
+
 __device__ __forceinline__ double rowdot(const int* __restrict__ p, const int* __restrict__ c,
                                          const double* __restrict__ v, const double* x, int i) {
   double s = 0.0;
@@ -37,74 +56,121 @@ __device__ __forceinline__ double rowdot(const int* __restrict__ p, const int* _
 }
 
 // H is (m+1) x m row-major.  info[0] = k, info[1] = error code, dinfo[0] = beta
-__global__ void __launch_bounds__(1024) arnoldi_cta_kernel(int n, const int* __restrict__ p,
-                                                           const int* __restrict__ c,
-                                                           const double* __restrict__ v,
-                                                           const double* __restrict__ b, int m,
-                                                           double* V, double* w, double* H,
-                                                           int* info, double* dinfo) {
+// Thread t owns entries i = t + e*NT (e < E) of the working vector w, kept in
+// registers; the Gram-Schmidt step q forms w -= h_q V_q and the next basis
+// vector's partial dot in the same pass, with V_{q+1} loaded before the
+// reduction of step q, so each step costs one block reduction instead of two
+// dependent L2 round trips.  Per-thread summation order is unchanged (entries
+// in e order), so H is bitwise what the two-pass loop produced.
+template <int NT, int E>
+__global__ void __launch_bounds__(NT) arnoldi_cta_kernel(int n, const int* __restrict__ p,
+                                                         const int* __restrict__ c,
+                                                         const double* __restrict__ v,
+                                                         const double* __restrict__ b, int m,
+                                                         double* V, double* w, double* H,
+                                                         int* info, double* dinfo) {
+  static_assert(NT == 256, "Sum8 reduces 8 warps");
   __shared__ double red[33];
+  __shared__ double red8[16];
+  extern __shared__ double hcol[];  // column j of H (m + 1), thread 0 only
+  Sum8 bsum{red8, 0};
+  const int tid = threadIdx.x;
   double sq = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) sq = fma(b[i], b[i], sq);
-  const double beta = sqrt(block_sum(sq, red));
-  if (threadIdx.x == 0) {
+  for (int i = tid; i < n; i += NT) sq = fma(b[i], b[i], sq);
+  const double beta = sqrt(bsum(sq));
+  if (tid == 0) {
     dinfo[0] = beta;
     info[0] = m;
     info[1] = 0;
   }
   if (beta == 0.0) {
-    if (threadIdx.x == 0) info[1] = 1;
+    if (tid == 0) info[1] = 1;
     return;
   }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) V[i] = b[i] / beta;
-  for (int i = threadIdx.x; i < (m + 1) * m; i += blockDim.x) H[i] = 0.0;
+  for (int i = tid; i < n; i += NT) V[i] = b[i] / beta;
+  for (int i = tid; i < (m + 1) * m; i += NT) H[i] = 0.0;
   __syncthreads();
   double hmax = 0.0;
   int k = m;
+  double wr[E], vq[E], vn[E];
   for (int j = 0; j < m; ++j) {
     const double* Vj = V + (size_t)j * n;
     sq = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const double t = rowdot(p, c, v, Vj, i);
-      w[i] = t;
-      sq = fma(t, t, sq);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = tid + e * NT;
+      wr[e] = 0.0;
+      if (i < n) {
+        const double t = rowdot(p, c, v, Vj, i);
+        wr[e] = t;
+        sq = fma(t, t, sq);
+      }
     }
-    const double before = sqrt(block_sum(sq, red));
+    const double before = sqrt(bsum(sq));
+    if (tid == 0)
+      for (int q = 0; q <= j; ++q) hcol[q] = 0.0;
     double hn = 0.0;
     for (int sweep = 0; sweep < 2; ++sweep) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = tid + e * NT;
+        vq[e] = i < n ? V[i] : 0.0;
+      }
       for (int q = 0; q <= j; ++q) {
-        const double* Vq = V + (size_t)q * n;
         double d = 0.0;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) d = fma(Vq[i], w[i], d);
-        const double h = block_sum(d, red);
-        if (threadIdx.x == 0) H[q * m + j] += h;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] -= h * Vq[i];
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+          if (tid + e * NT < n) d = fma(vq[e], wr[e], d);
+        if (q < j) {
+          const double* Vn = V + (size_t)(q + 1) * n;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int i = tid + e * NT;
+            vn[e] = i < n ? Vn[i] : 0.0;
+          }
+        }
+        const double h = bsum(d);
+        if (tid == 0) hcol[q] += h;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          wr[e] -= h * vq[e];
+          vq[e] = vn[e];
+        }
       }
       sq = 0.0;
-      for (int i = threadIdx.x; i < n; i += blockDim.x) sq = fma(w[i], w[i], sq);
-      hn = sqrt(block_sum(sq, red));
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (tid + e * NT < n) sq = fma(wr[e], wr[e], sq);
+      hn = sqrt(bsum(sq));
       if (!(sweep == 0 && hn < 0.7 * before)) break;  // "twice is enough"
     }
     __syncthreads();
     double cn = 0.0;
-    if (threadIdx.x == 0) {
-      H[(j + 1) * m + j] = hn;
-      for (int q = 0; q <= j + 1; ++q) cn = fma(H[q * m + j], H[q * m + j], cn);
+    if (tid == 0) {
+      hcol[j + 1] = hn;
+      for (int q = 0; q <= j + 1; ++q) {
+        H[q * m + j] = hcol[q];
+        cn = fma(hcol[q], hcol[q], cn);
+      }
       red[32] = sqrt(cn);
     }
     __syncthreads();
     hmax = fmax(hmax, red[32]);
     __syncthreads();
     if (hn <= 1e-14 * hmax) {
-      if (threadIdx.x == 0) H[(j + 1) * m + j] = 0.0;
+      if (tid == 0) H[(j + 1) * m + j] = 0.0;
       k = j + 1;
       break;
     }
     double* Vn = V + (size_t)(j + 1) * n;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) Vn[i] = w[i] / hn;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = tid + e * NT;
+      if (i < n) Vn[i] = wr[e] / hn;
+    }
     __syncthreads();
   }
-  if (threadIdx.x == 0) info[0] = k;
+  if (tid == 0) info[0] = k;
 }
 
 // ---- multi-kernel path ----------------------------------------------------
@@ -301,8 +367,8 @@ extern "C" int airg_arnoldi(int n, const int32_t* p, const int32_t* c, const dou
     AIRG_TRY(scratch(&H, (size_t)(m + 1) * m, s));
     AIRG_TRY(scratch(&dinfo, 1, s));
     AIRG_TRY(scratch(&info, 2, s));
-    const int thr = n <= 4096 ? 256 : 1024;
-    arnoldi_cta_kernel<<<1, thr, 0, s>>>(n, p, c, v, b, m, V, w, H, info, dinfo);
+    static_assert(kArnoldiCta <= 256 * 16, "one CTA of 256 threads, 16 entries each");
+    arnoldi_cta_kernel<256, 16><<<1, 256, (size_t)(m + 1) * sizeof(double), s>>>(n, p, c, v, b, m, V, w, H, info, dinfo);
     AIRG_LAUNCH_CHECK();
     int hi[2];
     AIRG_CUDA(cudaMemcpyAsync(H_h, H, (size_t)(m + 1) * m * sizeof(double), cudaMemcpyDeviceToHost, s));
