@@ -45,35 +45,39 @@ struct CountCheckOp {
 
 // Long rows (product upper bound > 512): one CTA per row sharing one
 // shared-memory key set.  Counting has no ordering constraint, so warps take
-// different chunks of A entries concurrently.
+// chunks of kCountChunk A entries from a shared cursor (dynamic balance: the
+// B rows behind the entries vary in length, a static split left warps idle at
+// the end-of-row barrier).
+constexpr int kCountChunk = 8;
 __global__ void __launch_bounds__(128) spgemm_count_block_kernel(CountArgs a) {
   extern __shared__ int keys[];
-  __shared__ int total, ovf;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+  __shared__ int total, ovf, cursor;
+  const int tid = threadIdx.x, lane = tid & 31;
   const int bits = a.bits, T = 1 << bits;
   for (long long t = blockIdx.x; t < a.nrows; t += gridDim.x) {
     const int row = a.rows[t];
     for (int i = tid; i < T; i += blockDim.x) keys[i] = kEmpty;
+    const int ab0 = a.Ap[row], ae = a.Ap[row + 1];
     if (tid == 0) {
       total = 0;
       ovf = 0;
+      cursor = ab0;
     }
     __syncthreads();
-    const int ab0 = a.Ap[row], ae0 = a.Ap[row + 1];
-    // warp w takes a contiguous quarter of the A row (balanced), walked in
-    // chunks of 32 entries: the B-row bounds of a chunk are loaded
-    // lane-parallel, the next B row's first 32 columns are prefetched while the
-    // current row is inserted
-    const int len = ae0 - ab0;
-    const int ab = ab0 + (int)((long long)len * w / nw), ae = ab0 + (int)((long long)len * (w + 1) / nw);
-    for (int base = ab; base < ae; base += 32) {
+    // per chunk: the B-row bounds are loaded lane-parallel, the next B row's
+    // first 32 columns are prefetched while the current row is inserted
+    while (true) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&cursor, kCountChunk);
+      base = __shfl_sync(kFull, base, 0);
+      if (base >= ae) break;
       int bb = 0, be = 0;
-      if (base + lane < ae) {
+      if (lane < kCountChunk && base + lane < ae) {
         const int k = a.Ac[base + lane];
         bb = a.Bp[k];
         be = a.Bp[k + 1];
       }
-      const int cnt = min(32, ae - base);
+      const int cnt = min(kCountChunk, ae - base);
       int cb = __shfl_sync(kFull, bb, 0), ce = __shfl_sync(kFull, be, 0);
       int pc = cb + lane < ce ? a.Bc[cb + lane] : -1;
       int added = 0;
