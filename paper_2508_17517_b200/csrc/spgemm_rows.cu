@@ -49,7 +49,7 @@ struct CountCheckOp {
 // B rows behind the entries vary in length, a static split left warps idle at
 // the end-of-row barrier).
 constexpr int kCountChunk = 8;
-__global__ void __launch_bounds__(128) spgemm_count_block_kernel(CountArgs a) {
+__global__ void __launch_bounds__(256) spgemm_count_block_kernel(CountArgs a) {
   extern __shared__ int keys[];
   __shared__ int total, ovf, cursor;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -452,7 +452,8 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
       CountArgs a{A.p, A.c, B.p, B.c, cl.list(c), nr, cbits[c], (1 << cbits[c]) * 3 / 4, cnt,
                   ovf_rows, ovf_n, nullptr, nullptr, nullptr};
       if (c == 2) {  // long rows: CTA per row, one shared key set
-        spgemm_count_block_kernel<<<std::min(nr, 148 * 16), 128, (size_t)(1 << cbits[c]) * 4,
+        static const int cnt_nt = getenv("AIRG_COUNT_NT") ? atoi(getenv("AIRG_COUNT_NT")) : 256;  // swept 64-512: 90 / 53 / 41 / 43 ms
+        spgemm_count_block_kernel<<<std::min(nr, 148 * 16), std::max(32, std::min(256, cnt_nt)), (size_t)(1 << cbits[c]) * 4,
                                     fk.stream(c)>>>(a);
       } else {
         spgemm_count_kernel<<<blocks_for(nr, cwarps[c], 148 * 32), cwarps[c] * 32, shm,
