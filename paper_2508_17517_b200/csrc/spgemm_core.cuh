@@ -374,7 +374,7 @@ static __global__ void rowlen_kernel(int m, const int* __restrict__ ptr, long lo
     out[i] = ptr[i + 1] - ptr[i];
 }
 
-constexpr int kMaxCls = 8;
+constexpr int kMaxCls = 24;
 
 // block-aggregated append of row ids to per-class lists (lists[c*m + ...])
 static __global__ void classify_kernel(int m, const long long* __restrict__ size, const long long* __restrict__ th,
@@ -387,6 +387,24 @@ static __global__ void classify_kernel(int m, const long long* __restrict__ size
   if (i < m) {
     const long long v = size[i];
     while (c < ncls - 1 && v > th[c]) ++c;
+    slot = atomicAdd(scnt + c, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < ncls) sbase[threadIdx.x] = atomicAdd(counts + threadIdx.x, scnt[threadIdx.x]);
+  __syncthreads();
+  if (i < m) lists[(long long)c * m + sbase[c] + slot] = (int)i;
+}
+
+// same with a precomputed class id per row
+static __global__ void classify_ids_kernel(int m, const int* __restrict__ ids, int ncls,
+                                           int* __restrict__ lists, int* __restrict__ counts) {
+  __shared__ int scnt[kMaxCls], sbase[kMaxCls];
+  if (threadIdx.x < ncls) scnt[threadIdx.x] = 0;
+  __syncthreads();
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  int c = 0, slot = 0;
+  if (i < m) {
+    c = ids[i];
     slot = atomicAdd(scnt + c, 1);
   }
   __syncthreads();
@@ -422,6 +440,24 @@ static int classify(int m, const long long* size, const std::vector<long long>& 
   AIRG_CUDA(cudaStreamSynchronize(s));
   out.m = m;
   release(dth, s);
+  release(cnt, s);
+  return AIRG_OK;
+}
+
+// class lists from per-row ids in [0, ncls); extra_dev as in classify
+static int classify_ids(int m, const int* ids, int ncls, Classes& out, cudaStream_t s,
+                        const int* extra_dev = nullptr, int* extra_h = nullptr) {
+  int* cnt = nullptr;
+  AIRG_TRY(scratch(&out.lists, (size_t)ncls * (m > 0 ? m : 1), s));
+  AIRG_TRY(scratch(&cnt, ncls, s));
+  AIRG_CUDA(cudaMemsetAsync(cnt, 0, ncls * sizeof(int), s));
+  if (m > 0) classify_ids_kernel<<<(m + 255) / 256, 256, 0, s>>>(m, ids, ncls, out.lists, cnt);
+  AIRG_LAUNCH_CHECK();
+  out.count.assign(ncls, 0);
+  AIRG_CUDA(cudaMemcpyAsync(out.count.data(), cnt, ncls * sizeof(int), cudaMemcpyDeviceToHost, s));
+  if (extra_dev) AIRG_CUDA(cudaMemcpyAsync(extra_h, extra_dev, sizeof(int), cudaMemcpyDeviceToHost, s));
+  AIRG_CUDA(cudaStreamSynchronize(s));
+  out.m = m;
   release(cnt, s);
   return AIRG_OK;
 }

@@ -1,7 +1,7 @@
 // General SpGEMM (Z = -A_cf Ahat, A P, R (A P)) and the fused Galerkin
 // product with drop/lump.  Kernel design in spgemm_core.cuh.
 // ref: sparse.py:222-240 (spgemm), hierarchy.py:281-286 (coarse_matrix)
-#include "spgemm_core.cuh"
+#include "spgemm_span.cuh"
 #include <vector>
 #include <algorithm>
 
@@ -422,42 +422,154 @@ static int gather_ll(const long long* d, const std::vector<int>& rows, std::vect
   return AIRG_OK;
 }
 
+// count-pass class of a row: span path (window <= 4096 / <= 16384 columns)
+// or the hash classes by product upper bound
+enum { kCntHash64 = 0, kCntSpan4k = 1, kCntSpan16k = 2, kCntHash512 = 3, kCntHashBlk = 4, kCntClasses = 5 };
+
+__global__ void count_class_kernel(int m, const long long* __restrict__ ub,
+                                   const long long* __restrict__ words, int* __restrict__ ids) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long w = words[i], u = ub[i];
+    ids[i] = w > 0 ? (w * 32 <= 4096 ? kCntSpan4k : kCntSpan16k)
+                   : (u <= 64 ? kCntHash64 : u <= 512 ? kCntHash512 : kCntHashBlk);
+  }
+}
+
+// numeric-pass class: span rows by output length (kSpanCaps), then the hash
+// classes (<= 32, <= 128 warp per row; <= 512 ... <= 8192 CTA per row;
+// longer: global tables)
+constexpr int kNumSpanCls = 10;
+__constant__ int kSpanCapsDev[kNumSpanCls] = {128, 256, 384, 512, 768, 1024, 1536, 2048, 3072, 4096};
+static const int kSpanCaps[kNumSpanCls] = {128, 256, 384, 512, 768, 1024, 1536, 2048, 3072, 4096};
+constexpr int kNumHashCls = 8;
+__global__ void numeric_class_kernel(int m, const int* __restrict__ Cp,
+                                     const long long* __restrict__ words, int* __restrict__ ids) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int n = Cp[i + 1] - Cp[i];
+    int c;
+    if (words[i] > 0 && n <= kSpanNmax) {
+      c = 0;
+      while (n > kSpanCapsDev[c]) ++c;
+    } else {
+      c = kNumSpanCls + (n <= 32 ? 0 : n <= 128 ? 1 : n <= 512 ? 2 : n <= 1024 ? 3 : n <= 2048 ? 4
+                         : n <= 4096 ? 5 : n <= 8192 ? 6 : 7);
+    }
+    ids[i] = c;
+  }
+}
+
+template <int NW, int KP, int D>
+static int launch_span_numeric_t(const SpanNumArgs& a, cudaStream_t s) {
+  const size_t shm = span_num_bytes(a.ncap) * NW;
+  static bool attr = false;
+  if (!attr) {
+    AIRG_CUDA(cudaFuncSetAttribute(span_numeric_kernel<NW, KP, D>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)span_num_bytes(kSpanNmax) * NW));
+    attr = true;
+  }
+  span_numeric_kernel<NW, KP, D><<<blocks_for(a.nrows, NW, 148 * 64), 32 * NW, shm, s>>>(a);
+  AIRG_LAUNCH_CHECK();
+  return AIRG_OK;
+}
+
+// B-row prefetch shape (KP x 32 entries, D steps ahead); AIRG_SPAN_KD="KP,D"
+// selects another instantiation (measurement only)
+static int launch_span_numeric(SpanNumArgs a, int ncap, cudaStream_t s) {
+  a.ncap = ncap;
+  int kp = 4, d = 4;
+  if (const char* e = getenv("AIRG_SPAN_KD")) sscanf(e, "%d,%d", &kp, &d);
+  const int kd = kp * 10 + d;
+  switch (kd) {
+    case 42: return launch_span_numeric_t<2, 4, 2>(a, s);
+    case 46: return launch_span_numeric_t<2, 4, 6>(a, s);
+    case 63: return launch_span_numeric_t<2, 6, 3>(a, s);
+    case 82: return launch_span_numeric_t<2, 8, 2>(a, s);
+    case 21: return launch_span_numeric_t<2, 2, 1>(a, s);
+    default: return launch_span_numeric_t<2, 4, 4>(a, s);
+  }
+}
+
+template <int NT>
+static int launch_span_count(const SpanCountArgs& a, int span, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    AIRG_CUDA(cudaFuncSetAttribute(span_count_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kSpanMax));
+    attr = true;
+  }
+  span_count_kernel<NT><<<std::min(a.nrows, 148 * 16), NT, (size_t)span, s>>>(a);
+  AIRG_LAUNCH_CHECK();
+  return AIRG_OK;
+}
+
+// rows with at least this many products may take the span path (below it
+// the hash set of 128 slots is cheaper than sweeping a window)
+static int span_min_ub() {
+  static const int v = getenv("AIRG_SPAN_MIN_UB") ? atoi(getenv("AIRG_SPAN_MIN_UB")) : 65;
+  return v;
+}
+
 // C = A B (mode 0, optionally negated) or drop_and_lump(A B) (mode 1).
 static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double tol, int lump,
                        airg_csr_result** out, cudaStream_t s, int row0 = 0) {
   const int m = A.nrows;
-  long long *ub = nullptr, *rl = nullptr;
-  int *cnt = nullptr, *Cp = nullptr;
+  long long *ub = nullptr, *rl = nullptr, *words = nullptr, *bmoff = nullptr;
+  int *cnt = nullptr, *Cp = nullptr, *cmin = nullptr, *ids = nullptr;
+  unsigned* gbm = nullptr;
   AIRG_TRY(scratch(&ub, m, s));
   AIRG_TRY(scratch(&cnt, m + 1, s));
   AIRG_TRY(scratch(&Cp, m + 1, s));
-  if (m > 0) product_ub_kernel<<<blocks_for(m, 256), 256, 0, s>>>(m, A.p, A.c, B.p, ub);
+  AIRG_TRY(scratch(&cmin, m, s));
+  AIRG_TRY(scratch(&words, m, s));
+  AIRG_TRY(scratch(&bmoff, m + 1, s));
+  AIRG_TRY(scratch(&ids, m, s));
+  if (m > 0)
+    span_ub_kernel<8><<<blocks_for((long long)m * 8, 256), 256, 0, s>>>(m, A.p, A.c, B.p, B.c, ub,
+                                                                         cmin, words, span_min_ub());
   AIRG_LAUNCH_CHECK();
+  long long totw = 0;
+  AIRG_TRY(scan_counts64(words, bmoff, m, &totw, s));
+  AIRG_TRY(scratch(&gbm, totw, s));
   // ---- pass 1 ----
   {
+    if (m > 0) count_class_kernel<<<blocks_for(m, 256), 256, 0, s>>>(m, ub, words, ids);
+    AIRG_LAUNCH_CHECK();
     Classes cl;
-    AIRG_TRY(classify(m, ub, {64, 512}, cl, s));
+    AIRG_TRY(classify_ids(m, ids, kCntClasses, cl, s));
     int *ovf_rows = nullptr, *ovf_n = nullptr;
     AIRG_TRY(scratch(&ovf_rows, m > 0 ? m : 1, s));
     AIRG_TRY(scratch(&ovf_n, 1, s));
     AIRG_CUDA(cudaMemsetAsync(ovf_n, 0, sizeof(int), s));
-    const int cbits[3] = {7, 10, 12}, cwarps[3] = {8, 8, 4};
     AIRG_TRY(set_smem((const void*)spgemm_count_kernel, (size_t)8 * 4096 * sizeof(int)));
     Fork fk;
     AIRG_TRY(fk.begin(s));
-    for (int c = 0; c < 3; ++c) {
+    for (int c = 0; c < kCntClasses; ++c) {
       const int nr = cl.count[c];
       if (!nr) continue;
-      const size_t shm = (size_t)cwarps[c] * (1 << cbits[c]) * sizeof(int);
-      CountArgs a{A.p, A.c, B.p, B.c, cl.list(c), nr, cbits[c], (1 << cbits[c]) * 3 / 4, cnt,
+      if (c == kCntSpan4k || c == kCntSpan16k) {
+        SpanCountArgs a{A.p, A.c, B.p, B.c, cl.list(c), nr, cmin, words, bmoff, gbm, cnt};
+        if (c == kCntSpan4k) AIRG_TRY((launch_span_count<128>(a, 4096, fk.stream(c))));
+        else AIRG_TRY((launch_span_count<256>(a, kSpanMax, fk.stream(c))));
+        continue;
+      }
+      const int bits = c == kCntHash64 ? 7 : c == kCntHash512 ? 10 : 12;
+      const int warps = c == kCntHashBlk ? 4 : 8;
+      const size_t shm = (size_t)warps * (1 << bits) * sizeof(int);
+      CountArgs a{A.p, A.c, B.p, B.c, cl.list(c), nr, bits, (1 << bits) * 3 / 4, cnt,
                   ovf_rows, ovf_n, nullptr, nullptr, nullptr};
-      if (c == 2) {  // long rows: CTA per row, one shared key set
-        static const int cnt_nt = getenv("AIRG_COUNT_NT") ? atoi(getenv("AIRG_COUNT_NT")) : 256;  // swept 64-512: 90 / 53 / 41 / 43 ms
-        spgemm_count_block_kernel<<<std::min(nr, 148 * 16), std::max(32, std::min(256, cnt_nt)), (size_t)(1 << cbits[c]) * 4,
+      if (c == kCntHashBlk) {  // long rows: CTA per row, one shared key set
+        // threads per row: swept 64-512 (90 / 53 / 41 / 43 ms); must be a multiple of 32
+        static const int cnt_nt = [] {
+          const int v = getenv("AIRG_COUNT_NT") ? atoi(getenv("AIRG_COUNT_NT")) : 256;
+          return std::max(32, std::min(256, v)) & ~31;
+        }();
+        spgemm_count_block_kernel<<<std::min(nr, 148 * 16), cnt_nt, (size_t)(1 << bits) * 4,
                                     fk.stream(c)>>>(a);
       } else {
-        spgemm_count_kernel<<<blocks_for(nr, cwarps[c], 148 * 32), cwarps[c] * 32, shm,
-                              fk.stream(c)>>>(a);
+        spgemm_count_kernel<<<blocks_for(nr, warps, 148 * 32), warps * 32, shm, fk.stream(c)>>>(a);
       }
       AIRG_LAUNCH_CHECK();
     }
@@ -484,16 +596,15 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
     release(cl.lists, s);
   }
   // ---- pass 2 ----
-  // the scan total (output nnz) is read back with the class counts: one sync
   AIRG_TRY(scan_counts(cnt, Cp, m, nullptr, s));
   AIRG_TRY(scratch(&rl, m, s));
   if (m > 0) rowlen_kernel<<<blocks_for(m, 256), 256, 0, s>>>(m, Cp, rl);
+  if (m > 0) numeric_class_kernel<<<blocks_for(m, 256), 256, 0, s>>>(m, Cp, words, ids);
+  AIRG_LAUNCH_CHECK();
   Classes cl;
-  // output-length classes: <= 32 / 128 warp per row; <= 512 ... 8192 CTA per
-  // row with a shared table of 2 x class slots (bits 10 .. 14; the 8192 class
-  // takes 197 KB, one CTA per SM); longer rows use global tables
+  // the scan total (output nnz) is read back with the class counts: one sync
   int nnz32 = 0;
-  AIRG_TRY(classify(m, rl, {32, 128, 512, 1024, 2048, 4096, 8192}, cl, s, Cp + m, &nnz32));
+  AIRG_TRY(classify_ids(m, ids, kNumSpanCls + kNumHashCls, cl, s, Cp + m, &nnz32));
   const long long nnz = nnz32;
   airg_csr_result* r = new airg_csr_result();
   r->nrows = m;
@@ -508,11 +619,18 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
   AIRG_TRY(scratch(&anyd, 1, s));
   AIRG_CUDA(cudaMemsetAsync(anyd, 0, sizeof(int), s));
   {
+    Fork fk;
+    AIRG_TRY(fk.begin(s));
+    for (int c = 0; c < kNumSpanCls; ++c) {
+      const int nr = cl.count[c];
+      if (!nr) continue;
+      SpanNumArgs a{A.p, A.c, A.v, B.p, B.c, B.v, cl.list(c), nr, 0, cmin, words, bmoff, gbm, Cp,
+                    ocol, oval, negate, mode, tol, lump, cnt, anyd, row0};
+      AIRG_TRY(launch_span_numeric(a, kSpanCaps[c], fk.stream(c)));
+    }
     const int cbits[7] = {6, 8, 10, 11, 12, 13, 14}, cwarps[2] = {8, 8};
     constexpr int kGlobalClass = 7;
     AIRG_TRY(set_smem((const void*)spgemm_numeric_kernel, 200 * 1024));
-    Fork fk;
-    AIRG_TRY(fk.begin(s));
     static bool attr = false;
     if (!attr) {
       const int lim = 200 * 1024;  // >= the 8192-class table (193 KB)
@@ -524,10 +642,11 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
       attr = true;
     }
     for (int c = 0; c < kGlobalClass; ++c) {
-      const int nr = cl.count[c];
+      const int nr = cl.count[kNumSpanCls + c];
       if (!nr) continue;
-      NumArgs a{A.p, A.c, A.v, B.p, B.c, B.v, cl.list(c), nr, cbits[c], Cp, ocol, oval, negate,
-                mode, tol, lump, cnt, anyd, nullptr, nullptr, nullptr, nullptr, row0};
+      NumArgs a{A.p, A.c, A.v, B.p, B.c, B.v, cl.list(kNumSpanCls + c), nr, cbits[c], Cp, ocol, oval,
+                negate, mode, tol, lump, cnt, anyd, nullptr, nullptr, nullptr, nullptr, row0};
+      cudaStream_t st = fk.stream(kNumSpanCls + c);
       if (c >= 2) {
         // one CTA per row, table shared by the CTA.  Threads per row measured
         // at 2048^2 (level-5 Galerkin, tools/nt_sweep.sh): the steps carry one
@@ -543,7 +662,7 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
           parsed = true;
         }
         const int nt = nts[c];
-#define AIRG_NUMBLK(T, B) spgemm_numeric_block_kernel<T, B><<<grid, T, shm, fk.stream(c)>>>(a)
+#define AIRG_NUMBLK(T, B) spgemm_numeric_block_kernel<T, B><<<grid, T, shm, st>>>(a)
 #define AIRG_NUMBLK3(B) \
   if (nt == 64) AIRG_NUMBLK(64, B); else if (nt == 128) AIRG_NUMBLK(128, B); else AIRG_NUMBLK(256, B)
         if (c == 2) { AIRG_NUMBLK3(10); }
@@ -555,16 +674,15 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
 #undef AIRG_NUMBLK
       } else {
         const size_t shm = (size_t)cwarps[c] * ((1 << cbits[c]) * 12 + 1024);
-        spgemm_numeric_kernel<<<blocks_for(nr, cwarps[c], 148 * 32), cwarps[c] * 32, shm,
-                                fk.stream(c)>>>(a);
+        spgemm_numeric_kernel<<<blocks_for(nr, cwarps[c], 148 * 32), cwarps[c] * 32, shm, st>>>(a);
       }
       AIRG_LAUNCH_CHECK();
     }
     AIRG_TRY(fk.end(s));
-    const int nr = cl.count[kGlobalClass];
+    const int nr = cl.count[kNumSpanCls + kGlobalClass];
     if (nr) {
       std::vector<int> rows(nr);
-      AIRG_CUDA(cudaMemcpyAsync(rows.data(), cl.list(kGlobalClass), nr * sizeof(int),
+      AIRG_CUDA(cudaMemcpyAsync(rows.data(), cl.list(kNumSpanCls + kGlobalClass), nr * sizeof(int),
                                 cudaMemcpyDeviceToHost, s));
       std::vector<long long> sizes;
       AIRG_TRY(gather_ll(rl, rows, sizes, s, m));
@@ -597,10 +715,9 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
     release(oval, s);
     release(Cp, s);
   }
-  release(anyd, s);
-  release(ub, s);
-  release(rl, s);
-  release(cnt, s);
+  for (void* q : {(void*)anyd, (void*)ub, (void*)rl, (void*)cnt, (void*)cmin, (void*)words,
+                  (void*)bmoff, (void*)ids, (void*)gbm})
+    release(q, s);
   *out = r;
   return AIRG_OK;
 }
