@@ -20,7 +20,6 @@
 
 namespace airg {
 
-static int smem_limit() { return 200 * 1024; }
 
 // raw rows live at [ptr[r] + r, ...) (one spare slot per row for a lumped diagonal)
 __global__ void compact_rows_kernel(int m, const int* __restrict__ rawp, const int* __restrict__ optr,
@@ -153,6 +152,58 @@ __global__ void pattern_diag_kernel(int n, const int* __restrict__ p, const int*
   }
 }
 
+// Position of a column in the (sorted) pattern row of the current row, held
+// in shared memory: a hash table (any column window) or a bitmap of the
+// row's window [pmin, pmax] (windows <= kPolySpan columns -- every row of the
+// advection hierarchies).  The bitmap answers with a bit test (misses, most
+// products) and a rank (hits); the hash table needs a probe sequence, which
+// for a miss runs until an empty slot.
+constexpr int kPolySpan = 8192;
+constexpr int kPolyWords = kPolySpan / 32;
+
+struct HashPos {
+  int* keys;
+  int* pv;
+  int bits;
+  static __host__ __device__ size_t bytes(int cap) { return (size_t)8 << ceil_log2(2ll * cap); }
+  __device__ void bind(unsigned char* p, int cap) {
+    bits = ceil_log2(2ll * cap);
+    keys = (int*)p;
+    pv = keys + (1 << bits);
+  }
+  __device__ void clear(const int*, int, int, int tid, int nt) {
+    for (int i = tid; i < (1 << bits); i += nt) keys[i] = kEmpty;
+  }
+  __device__ void insert(const int* pc, int i) { map_insert(keys, pv, bits, pc[i], i); }
+  __device__ int find(int c) const { return map_find(keys, pv, bits, c); }
+};
+
+struct BitPos {
+  uint2* bm;  // per window word: (position of its first column, bits)
+  int pmin;
+  unsigned span;
+  static __host__ __device__ size_t bytes(int) { return (size_t)kPolyWords * sizeof(uint2); }
+  __device__ void bind(unsigned char* p, int) { bm = (uint2*)p; }
+  // pc: the pattern row (m sorted columns)
+  __device__ void clear(const int* pc, int m, int, int tid, int nt) {
+    pmin = m ? pc[0] : 0;
+    span = m ? (unsigned)(pc[m - 1] - pmin + 1) : 0u;
+    for (int i = tid; i < (int)((span + 31) >> 5); i += nt) bm[i] = make_uint2(0u, 0u);
+  }
+  __device__ void insert(const int* pc, int i) {
+    const unsigned off = (unsigned)(pc[i] - pmin);
+    atomicOr(&bm[off >> 5].y, 1u << (off & 31u));
+    if (i == 0 || ((unsigned)(pc[i - 1] - pmin) >> 5) != (off >> 5)) bm[off >> 5].x = (unsigned)i;
+  }
+  __device__ int find(int c) const {
+    const unsigned off = (unsigned)(c - pmin);
+    if (off >= span) return -1;
+    const uint2 e = bm[off >> 5];
+    if (!((e.y >> (off & 31u)) & 1u)) return -1;
+    return (int)e.x + __popc(e.y & ((1u << (off & 31u)) - 1u));
+  }
+};
+
 // Per row (warp): positions of the pattern row in shared memory; for each
 // power k = 2..d: next[pos(j)] += P_{k-1}[i,q] * A[q,j] over q ascending
 // (present entries only), lanes over A row q.  Accumulate
@@ -183,32 +234,36 @@ struct PolyArgs {
   // rows handled by this launch (one length class); null = all n rows
   const int* rows;
   int nrows;
+  // block kernel only: per-CTA working set in global memory (rows whose
+  // working set exceeds shared memory), gstride bytes per CTA; null = smem
+  unsigned char* gmem;
+  size_t gstride;
 };
 
+template <class PM>
 __global__ void __launch_bounds__(128) poly_assemble_kernel(PolyArgs a) {
   extern __shared__ unsigned char smraw[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int T = 1 << a.bits;
   const int cap = a.cap;
-  // per warp: keys[T], pos[T], cur[cap], nxt[cap], acc[cap], flags cur/nxt/acc (3*cap bytes)
-  const size_t per = (size_t)T * 8 + (size_t)cap * 24 + (size_t)cap * 3;
+  // per warp: position map, cur[cap], nxt[cap], acc[cap], flags cur/nxt/acc (3*cap bytes)
+  const size_t per = PM::bytes(cap) + (size_t)cap * 24 + (size_t)cap * 3;
   unsigned char* base = smraw + (size_t)w * ((per + 15) & ~(size_t)15);
   double* cur = (double*)base;
   double* nxt = cur + cap;
   double* acc = nxt + cap;
-  int* keys = (int*)(acc + cap);
-  int* pv = keys + T;
-  unsigned char* fcur = (unsigned char*)(pv + T);
+  PM pm;
+  pm.bind((unsigned char*)(acc + cap), cap);
+  unsigned char* fcur = (unsigned char*)(acc + cap) + PM::bytes(cap);
   unsigned char* fnxt = fcur + cap;
   unsigned char* facc = fnxt + cap;
   for (long long r = (long long)blockIdx.x * nw + w; r < a.nrows; r += (long long)gridDim.x * nw) {
     const int row = a.rows ? a.rows[r] : (int)r;
     const int pb = a.Pp[row], pe = a.Pp[row + 1], m = pe - pb;
     if (m > cap) continue;  // handled by the global pass (flag via out_cnt = -1)
-    for (int i = lane; i < T; i += 32) keys[i] = kEmpty;
+    pm.clear(a.Pc + pb, m, cap, lane, 32);
     __syncwarp();
     for (int i = lane; i < m; i += 32) {
-      map_insert(keys, pv, a.bits, a.Pc[pb + i], i);
+      pm.insert(a.Pc + pb, i);
       cur[i] = 0.0;
       nxt[i] = 0.0;
       acc[i] = 0.0;
@@ -224,7 +279,7 @@ __global__ void __launch_bounds__(128) poly_assemble_kernel(PolyArgs a) {
         const int q = a.Lc[qq];
         const double lv = a.Lv[qq];
         for (int jj = a.Ap[q] + lane; jj < a.Ap[q + 1]; jj += 32) {
-          const int p = map_find(keys, pv, a.bits, a.Ac[jj]);
+          const int p = pm.find(a.Ac[jj]);
           if (p >= 0) {
             nxt[p] = add_rn(nxt[p], mul_rn(lv, a.Av[jj]));
             fnxt[p] = 1;
@@ -247,7 +302,7 @@ __global__ void __launch_bounds__(128) poly_assemble_kernel(PolyArgs a) {
     // term 0: c0 * I (diagonal is always in the pattern)
     const double c0 = a.coef[0];
     if (lane == 0) {
-      const int p = map_find(keys, pv, a.bits, a.row0 + row);
+      const int p = pm.find(a.row0 + row);
       acc[p] = add_rn(acc[p], c0);  // 0 + c0 (=c0; -0 -> +0 is pruned anyway)
       facc[p] = 1;
     }
@@ -255,7 +310,7 @@ __global__ void __launch_bounds__(128) poly_assemble_kernel(PolyArgs a) {
     if (d >= 1) {
       const double c1 = a.coef[1];
       for (int kk = a.Ap[row] + lane; kk < a.Ap[row + 1]; kk += 32) {
-        const int p = map_find(keys, pv, a.bits, a.Ac[kk]);
+        const int p = pm.find(a.Ac[kk]);
         const double v = a.Av[kk];
         acc[p] = add_rn(acc[p], mul_rn(c1, v));
         facc[p] = 1;
@@ -299,14 +354,14 @@ __global__ void __launch_bounds__(128) poly_assemble_kernel(PolyArgs a) {
             hv = cb + lane < ce ? a.Av[cb + lane] : 0.0;
           }
           if (c0 >= 0) {
-            const int p = map_find(keys, pv, a.bits, c0);
+            const int p = pm.find(c0);
             if (p >= 0) {
               nxt[p] = add_rn(nxt[p], mul_rn(l, v0));
               fnxt[p] = 1;
             }
           }
           for (int jj = tb + 32 + lane; jj < te; jj += 32) {
-            const int p = map_find(keys, pv, a.bits, a.Ac[jj]);
+            const int p = pm.find(a.Ac[jj]);
             if (p >= 0) {
               nxt[p] = add_rn(nxt[p], mul_rn(l, a.Av[jj]));
               fnxt[p] = 1;
@@ -347,20 +402,29 @@ __global__ void __launch_bounds__(128) poly_assemble_kernel(PolyArgs a) {
 // row of col_q (distinct columns -> distinct positions), a barrier between
 // consecutive q.  The present positions of a power and their A-row bounds are
 // staged in shared memory first, so a step issues no dependent global loads.
-// Shared memory per CTA: keys/pos T ints each, cur/nxt/acc cap doubles,
-// list/rb/re cap ints, flags 3 cap bytes.
+// Working set per CTA (block_bytes): position map, cur/nxt/acc cap doubles,
+// list/rb/re cap ints, flags 3 cap bytes -- in shared memory, or for rows
+// beyond it (any length, as the reference, polynomial.py:379-416) in a
+// global-memory slab per CTA.  masked=1: the plain masked product, one
+// barrier per left-row entry.
+template <class PM>
+__host__ __device__ __forceinline__ size_t block_bytes(int cap) {
+  return (PM::bytes(cap) + (size_t)cap * (24 + 12 + 3) + 15) & ~(size_t)15;
+}
+
+template <class PM>
 __global__ void __launch_bounds__(256) poly_assemble_block_kernel(PolyArgs a) {
   extern __shared__ unsigned char smraw[];
   __shared__ int s_np, s_cnt;
   const int tid = threadIdx.x, NT = blockDim.x;
-  const int T = 1 << a.bits;
   const int cap = a.cap;
-  double* cur = (double*)smraw;
+  unsigned char* wbase = a.gmem ? a.gmem + (size_t)blockIdx.x * a.gstride : smraw;
+  double* cur = (double*)wbase;
   double* nxt = cur + cap;
   double* acc = nxt + cap;
-  int* keys = (int*)(acc + cap);
-  int* pv = keys + T;
-  int* list = pv + T;
+  PM pm;
+  pm.bind((unsigned char*)(acc + cap), cap);
+  int* list = (int*)((unsigned char*)(acc + cap) + PM::bytes(cap));
   int* rbs = list + cap;
   int* res = rbs + cap;
   unsigned char* fcur = (unsigned char*)(res + cap);
@@ -369,10 +433,10 @@ __global__ void __launch_bounds__(256) poly_assemble_block_kernel(PolyArgs a) {
   for (long long r = blockIdx.x; r < a.nrows; r += gridDim.x) {
     const int row = a.rows ? a.rows[r] : (int)r;
     const int pb = a.Pp[row], pe = a.Pp[row + 1], m = pe - pb;
-    for (int i = tid; i < T; i += NT) keys[i] = kEmpty;
+    pm.clear(a.Pc + pb, m, cap, tid, NT);
     __syncthreads();
     for (int i = tid; i < m; i += NT) {
-      map_insert(keys, pv, a.bits, a.Pc[pb + i], i);
+      pm.insert(a.Pc + pb, i);
       cur[i] = 0.0;
       nxt[i] = 0.0;
       acc[i] = 0.0;
@@ -381,9 +445,37 @@ __global__ void __launch_bounds__(256) poly_assemble_block_kernel(PolyArgs a) {
       facc[i] = 0;
     }
     __syncthreads();
+    if (a.masked) {  // one masked product: left row L_i (in order), right rows A_q
+      for (int qq = a.Lp[row]; qq < a.Lp[row + 1]; ++qq) {
+        const int q = a.Lc[qq];
+        const double lv = a.Lv[qq];
+        for (int jj = a.Ap[q] + tid; jj < a.Ap[q + 1]; jj += NT) {
+          const int p = pm.find(a.Ac[jj]);
+          if (p >= 0) {
+            nxt[p] = add_rn(nxt[p], mul_rn(lv, a.Av[jj]));
+            fnxt[p] = 1;
+          }
+        }
+        __syncthreads();
+      }
+      if (tid == 0) s_cnt = 0;
+      __syncthreads();
+      int c = 0;
+      for (int i = tid; i < m; i += NT) {
+        a.out_val[pb + i] = nxt[i];
+        a.out_keep[pb + i] = fnxt[i];
+        c += fnxt[i];
+      }
+      c = warp_sum(c);
+      if ((tid & 31) == 0 && c) atomicAdd(&s_cnt, c);
+      __syncthreads();
+      if (tid == 0) a.out_cnt[row] = s_cnt;
+      __syncthreads();
+      continue;
+    }
     const int d = a.ncoef - 1;
     if (tid == 0) {  // term 0: c0 * I (the diagonal is always in the pattern)
-      const int p = map_find(keys, pv, a.bits, a.row0 + row);
+      const int p = pm.find(a.row0 + row);
       acc[p] = add_rn(acc[p], a.coef[0]);
       facc[p] = 1;
     }
@@ -391,7 +483,7 @@ __global__ void __launch_bounds__(256) poly_assemble_block_kernel(PolyArgs a) {
     if (d >= 1) {
       const double c1 = a.coef[1];
       for (int kk = a.Ap[row] + tid; kk < a.Ap[row + 1]; kk += NT) {
-        const int p = map_find(keys, pv, a.bits, a.Ac[kk]);
+        const int p = pm.find(a.Ac[kk]);
         const double v = a.Av[kk];
         acc[p] = add_rn(acc[p], mul_rn(c1, v));
         facc[p] = 1;
@@ -427,7 +519,7 @@ __global__ void __launch_bounds__(256) poly_assemble_block_kernel(PolyArgs a) {
         const double l = cur[list[t]];
         const int rb = rbs[t], re = res[t];
         for (int jj = rb + tid; jj < re; jj += NT) {
-          const int p = map_find(keys, pv, a.bits, a.Ac[jj]);
+          const int p = pm.find(a.Ac[jj]);
           if (p >= 0) {
             nxt[p] = add_rn(nxt[p], mul_rn(l, a.Av[jj]));
             fnxt[p] = 1;
@@ -503,66 +595,103 @@ static int max_row_len(int m, const int* p, int* out, cudaStream_t s) {
 }
 
 // Rows are classified by pattern length (caps 32, 64, ..., next pow2 >= the
-// longest row) and each class runs with its own shared-memory footprint
-// (43 B x cap per warp), so a few long rows no longer cut the occupancy of
-// every row of the level.
+// longest row) and by column window (bitmap position map when the window is
+// <= kPolySpan, hash table otherwise), and each class runs with its own
+// working-set size, so a few long rows do not cut the occupancy of every row
+// of the level.  Warp per row below kPolyBlockCap entries, CTA per row above;
+// CTA rows whose working set exceeds the shared-memory opt-in limit run from
+// global memory.
 static const int kPolyBlockCap = getenv("AIRG_POLY_BLOCK_CAP") ? atoi(getenv("AIRG_POLY_BLOCK_CAP")) : 256;
 
-static int run_poly_kernel(PolyArgs& a, int maxlen, cudaStream_t s) {
-  int capmax = 32;
-  while (capmax < maxlen) capmax <<= 1;
-  auto per_warp = [](int cap) {
-    const size_t T = (size_t)1 << ceil_log2(2ll * cap);
-    return (T * 8 + (size_t)cap * 27 + 15) & ~(size_t)15;
-  };
-  if (per_warp(capmax) > (size_t)smem_limit()) {
-    set_error("pattern row of %d entries exceeds the shared-memory assembly kernel", maxlen);
-    return AIRG_ERR_VALUE;
+__global__ void poly_class_kernel(int n, const int* __restrict__ Pp, const int* __restrict__ Pc,
+                                  int ncap, int* __restrict__ ids) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int b = Pp[i], m = Pp[i + 1] - b;
+    int c = 0;
+    while ((32 << c) < m) ++c;
+    const bool bit = m == 0 || (long long)Pc[b + m - 1] - Pc[b] < kPolySpan;
+    ids[i] = c + (bit ? 0 : ncap);
   }
+}
+
+// dynamic shared memory a kernel of this file may request: the device opt-in
+// limit less room for the kernels' static shared variables
+static int smem_optin() {
+  static int v = -1;
+  if (v < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+      v = 227 * 1024;
+    v -= 1024;
+  }
+  return v;
+}
+
+template <class PM>
+static int launch_poly_class(PolyArgs b, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    AIRG_CUDA(cudaFuncSetAttribute(poly_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   smem_limit()));
-    AIRG_CUDA(cudaFuncSetAttribute(poly_assemble_block_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem_limit()));
+    AIRG_CUDA(cudaFuncSetAttribute(poly_assemble_kernel<PM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   smem_optin()));
+    AIRG_CUDA(cudaFuncSetAttribute(poly_assemble_block_kernel<PM>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin()));
     attr = true;
   }
-  std::vector<long long> th;
-  for (long long c = 32; c < capmax; c <<= 1) th.push_back(c);
-  long long* len = nullptr;
-  AIRG_TRY(scratch(&len, a.n > 0 ? a.n : 1, s));
-  if (a.n > 0) rowlen_kernel<<<blocks_for(a.n, 256), 256, 0, s>>>(a.n, a.Pp, len);
+  const size_t per = (PM::bytes(b.cap) + (size_t)b.cap * 27 + 15) & ~(size_t)15;
+  if (b.cap < kPolyBlockCap && per <= (size_t)smem_optin()) {
+    int warps = 4;
+    while (warps > 1 && per * warps > (size_t)smem_optin()) warps >>= 1;
+    poly_assemble_kernel<PM><<<blocks_for(b.nrows, warps, 148 * 32), warps * 32, per * warps, st>>>(b);
+    AIRG_LAUNCH_CHECK();
+    return AIRG_OK;
+  }
+  static const int nt128 = getenv("AIRG_POLY_NT128") ? atoi(getenv("AIRG_POLY_NT128")) : 64;
+  static const int nt256 = getenv("AIRG_POLY_NT256") ? atoi(getenv("AIRG_POLY_NT256")) : 128;
+  const int nt = b.cap >= 512 ? 256 : b.cap >= 256 ? nt256 : nt128;
+  const size_t shm = block_bytes<PM>(b.cap);
+  if (shm <= (size_t)smem_optin()) {
+    poly_assemble_block_kernel<PM><<<std::min(b.nrows, 148 * 16), nt, shm, st>>>(b);
+    AIRG_LAUNCH_CHECK();
+    return AIRG_OK;
+  }
+  const int grid = std::min(b.nrows, 148 * 2);
+  AIRG_TRY(scratch(&b.gmem, shm * grid, st));
+  b.gstride = shm;
+  poly_assemble_block_kernel<PM><<<grid, 256, 0, st>>>(b);
+  AIRG_LAUNCH_CHECK();
+  release(b.gmem, st);
+  return AIRG_OK;
+}
+
+static int run_poly_kernel(PolyArgs& a, int maxlen, cudaStream_t s) {
+  int ncap = 1;
+  while ((32 << (ncap - 1)) < maxlen) ++ncap;
+  if (2 * ncap > kMaxCls) {
+    set_error("pattern row of %d entries exceeds the assembly classes", maxlen);
+    return AIRG_ERR_VALUE;
+  }
+  int* ids = nullptr;
+  AIRG_TRY(scratch(&ids, a.n > 0 ? a.n : 1, s));
+  if (a.n > 0) poly_class_kernel<<<blocks_for(a.n, 256), 256, 0, s>>>(a.n, a.Pp, a.Pc, ncap, ids);
   AIRG_LAUNCH_CHECK();
   Classes cl;
-  AIRG_TRY(classify(a.n, len, th, cl, s));
+  AIRG_TRY(classify_ids(a.n, ids, 2 * ncap, cl, s));
   Fork fk;
   AIRG_TRY(fk.begin(s));
-  for (int c = 0; c < (int)cl.count.size(); ++c) {
+  for (int c = 0; c < 2 * ncap; ++c) {
     const int nr = cl.count[c];
     if (!nr) continue;
     PolyArgs b = a;
-    b.cap = 32 << c;
-    b.bits = ceil_log2(2ll * b.cap);
+    b.cap = 32 << (c % ncap);
     b.rows = cl.list(c);
     b.nrows = nr;
-    if (b.cap >= kPolyBlockCap && !b.masked) {  // long rows: CTA per row
-      const size_t T = (size_t)1 << b.bits;
-      const size_t shm = T * 8 + (size_t)b.cap * (24 + 12 + 3);
-      static const int nt128 = getenv("AIRG_POLY_NT128") ? atoi(getenv("AIRG_POLY_NT128")) : 64;
-      static const int nt256 = getenv("AIRG_POLY_NT256") ? atoi(getenv("AIRG_POLY_NT256")) : 128;
-      const int nt = b.cap >= 512 ? 256 : b.cap >= 256 ? nt256 : nt128;
-      poly_assemble_block_kernel<<<std::min(nr, 148 * 16), nt, shm, fk.stream(c)>>>(b);
-    } else {
-      const size_t per = per_warp(b.cap);
-      int warps = 4;
-      while (warps > 1 && per * warps > (size_t)smem_limit()) warps >>= 1;
-      poly_assemble_kernel<<<blocks_for(nr, warps, 148 * 32), warps * 32, per * warps,
-                             fk.stream(c)>>>(b);
-    }
-    AIRG_LAUNCH_CHECK();
+    if (c < ncap) AIRG_TRY(launch_poly_class<BitPos>(b, fk.stream(c)));
+    else AIRG_TRY(launch_poly_class<HashPos>(b, fk.stream(c)));
   }
   AIRG_TRY(fk.end(s));
-  release(len, s);
+  release(ids, s);
   release(cl.lists, s);
   return AIRG_OK;
 }
