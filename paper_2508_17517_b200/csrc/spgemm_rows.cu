@@ -475,19 +475,18 @@ static int launch_span_numeric_t(const SpanNumArgs& a, cudaStream_t s) {
   return AIRG_OK;
 }
 
-// B-row prefetch shape (KP x 32 entries, D steps ahead); AIRG_SPAN_KD="KP,D"
-// selects another instantiation (measurement only)
-static int launch_span_numeric(SpanNumArgs a, int ncap, cudaStream_t s) {
+// B-row prefetch shape kd = 10 KP + D (KP x 32 entries, D steps ahead);
+// AIRG_SPAN_KD="KP,D" overrides it (measurement only)
+static int launch_span_numeric(SpanNumArgs a, int ncap, int kd, cudaStream_t s) {
   a.ncap = ncap;
-  int kp = 4, d = 4;
-  if (const char* e = getenv("AIRG_SPAN_KD")) sscanf(e, "%d,%d", &kp, &d);
-  const int kd = kp * 10 + d;
+  if (const char* e = getenv("AIRG_SPAN_KD")) {
+    int kp = 4, d = 4;
+    sscanf(e, "%d,%d", &kp, &d);
+    kd = kp * 10 + d;
+  }
   switch (kd) {
     case 42: return launch_span_numeric_t<2, 4, 2>(a, s);
-    case 46: return launch_span_numeric_t<2, 4, 6>(a, s);
-    case 63: return launch_span_numeric_t<2, 6, 3>(a, s);
     case 82: return launch_span_numeric_t<2, 8, 2>(a, s);
-    case 21: return launch_span_numeric_t<2, 2, 1>(a, s);
     default: return launch_span_numeric_t<2, 4, 4>(a, s);
   }
 }
@@ -526,12 +525,21 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
   AIRG_TRY(scratch(&words, m, s));
   AIRG_TRY(scratch(&bmoff, m + 1, s));
   AIRG_TRY(scratch(&ids, m, s));
+  unsigned long long* tot = nullptr;
+  AIRG_TRY(scratch(&tot, 2, s));
+  AIRG_CUDA(cudaMemsetAsync(tot, 0, 2 * sizeof(unsigned long long), s));
   if (m > 0)
     span_ub_kernel<8><<<blocks_for((long long)m * 8, 256), 256, 0, s>>>(m, A.p, A.c, B.p, B.c, ub,
-                                                                         cmin, words, span_min_ub());
+                                                                         cmin, words, span_min_ub(), tot);
   AIRG_LAUNCH_CHECK();
+  unsigned long long tot_h[2] = {0, 0};
+  AIRG_CUDA(cudaMemcpyAsync(tot_h, tot, sizeof(tot_h), cudaMemcpyDeviceToHost, s));
   long long totw = 0;
-  AIRG_TRY(scan_counts64(words, bmoff, m, &totw, s));
+  AIRG_TRY(scan_counts64(words, bmoff, m, &totw, s));  // synchronises (tot_h too)
+  release(tot, s);
+  // mean B-row length of the span rows sets the numeric prefetch shape: rows
+  // longer than 4 x 32 entries would run their tail with exposed latency
+  const int span_kd = tot_h[1] && tot_h[0] > 112ull * tot_h[1] ? 82 : 44;
   AIRG_TRY(scratch(&gbm, totw, s));
   // ---- pass 1 ----
   {
@@ -626,7 +634,7 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
       if (!nr) continue;
       SpanNumArgs a{A.p, A.c, A.v, B.p, B.c, B.v, cl.list(c), nr, 0, cmin, words, bmoff, gbm, Cp,
                     ocol, oval, negate, mode, tol, lump, cnt, anyd, row0};
-      AIRG_TRY(launch_span_numeric(a, kSpanCaps[c], fk.stream(c)));
+      AIRG_TRY(launch_span_numeric(a, kSpanCaps[c], span_kd, fk.stream(c)));
     }
     const int cbits[7] = {6, 8, 10, 11, 12, 13, 14}, cwarps[2] = {8, 8};
     constexpr int kGlobalClass = 7;

@@ -63,7 +63,8 @@ template <int VS>
 __global__ void span_ub_kernel(int m, const int* __restrict__ Ap, const int* __restrict__ Ac,
                                const int* __restrict__ Bp, const int* __restrict__ Bc,
                                long long* __restrict__ ub, int* __restrict__ cmin_out,
-                               long long* __restrict__ words, int span_min_ub) {
+                               long long* __restrict__ words, int span_min_ub,
+                               unsigned long long* __restrict__ totals) {
   const int sub = threadIdx.x & (VS - 1);
   const unsigned gmask = VS == 32 ? 0xffffffffu : (((1u << VS) - 1u) << (threadIdx.x & 31 & ~(VS - 1)));
   for (long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / VS; r < m;
@@ -93,6 +94,10 @@ __global__ void span_ub_kernel(int m, const int* __restrict__ Ap, const int* __r
       const bool use = s >= span_min_ub && span > 0 && span <= kSpanMax && span <= 32 * s &&
                        s >= 8ll * (ae - ab);
       words[r] = use ? (span + 31) / 32 : 0;
+      if (use) {  // products and steps of the span rows (B-row prefetch shape)
+        atomicAdd(totals, (unsigned long long)s);
+        atomicAdd(totals + 1, (unsigned long long)(ae - ab));
+      }
     }
   }
 }
