@@ -104,6 +104,18 @@ int airg_plan_richardson(airg_plan* plan, const double* b, double* x, double rto
 int airg_plan_set_exact(airg_plan* plan, int exact);
 /* Number of kernel launches issued by the last airg_plan_richardson call. */
 int64_t airg_plan_launches(airg_plan* plan);
+/* 1 when the fast-mode coarse solve of this plan is the dense q(A) GEMV,
+ * 0 when it runs the Newton apply (exact mode, a large coarse grid, or an
+ * identity column of q(A) that stopped early, polynomial.py:312-355). */
+int airg_plan_coarse_mode(airg_plan* plan);
+/* Number of CUDA graphs the plan holds (bounded: least recently used evicted). */
+int airg_plan_graph_count(airg_plan* plan);
+/* The plan's staging vectors (finest-level size): airg_plan_vcycle called
+ * with r = *vin, e = *vout runs the captured V-cycle without copying the
+ * caller's vectors in and out (measurement). */
+int airg_plan_staging(airg_plan* plan, double** vin, double** vout);
+/* Stream-ordered device-to-device copy (bench / test helper). */
+int airg_copy_d2d(void* dst, const void* src, int64_t bytes, void* stream);
 
 /* ---- distributed (row-strip) solve over NCCL ----------------
  * One plan per rank: per distributed level R / A_fc / A_ff on local rows with

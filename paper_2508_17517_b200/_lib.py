@@ -139,6 +139,10 @@ sig('airg_plan_set_coarse', vp, i32, vp, vp, vp, C.c_int, C.c_int, vp, C.c_int, 
 sig('airg_plan_vcycle', vp, C.c_int, vp, vp, C.c_int, vp)
 sig('airg_plan_richardson', vp, vp, vp, f64, f64, C.c_int, C.c_int, vp, vp, vp, vp)
 sig('airg_plan_launches', vp, ret=i64)
+sig('airg_plan_coarse_mode', vp)
+sig('airg_plan_graph_count', vp)
+sig('airg_plan_staging', vp, C.POINTER(vp), C.POINTER(vp))
+sig('airg_copy_d2d', vp, vp, i64, vp)
 sig('airg_nccl_unique_id', C.c_char_p)
 sig('airg_comm_create', C.c_char_p, C.c_int, C.c_int, C.POINTER(vp))
 sig('airg_comm_destroy', vp)

@@ -384,10 +384,9 @@ def setup(A, cfg, poly_inject=None, keep_level_matrices=False):
     The recorded polynomials of a run are in ``H.polys``.
     """
     from .cfsplit import cf_split
-    from .csr import SparseMatrix, to_dev, IDX, VAL
+    from .csr import as_matrix
     cfg.validate()
-    if not isinstance(A, SparseMatrix):
-        raise TypeError('setup expects a paper_2508_17517_b200.SparseMatrix')
+    A = as_matrix(A)  # a reference airmg.SparseMatrix (host, int64) is uploaded
     if A.nrows != A.ncols:
         raise ValueError('require a square matrix')
     if A.nrows == 0:

@@ -13,7 +13,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib as L
-from .csr import VAL, empty, to_dev
+from .csr import VAL, empty, is_host_array, to_dev
 from .gmres_poly import poly_args
 
 _DIVERGENCE_FACTOR = 1e8
@@ -114,13 +114,67 @@ class Plan:
         return int(L.load().airg_plan_launches(self.h))
 
 
-def plan_for(H, exact=False):
-    p = getattr(H, '_plan', None)
-    if p is None:
-        p = Plan(H)
-        H._plan = p
-    L.call('airg_plan_set_exact', p.h, 1 if exact else 0)
-    return p
+class _PlanPool:
+    """Native plans of one Hierarchy, one per concurrent solve.
+
+    The reference's Hierarchy is immutable and usable by concurrent solves,
+    each owning its work vectors (SPEC.md concurrency model, solve.py:113-167).
+    A plan holds work vectors, a stream and its captured graphs, so a solve
+    takes a plan from the pool for its whole duration (creating one when all
+    are busy) and returns it afterwards; the arithmetic mode is set on the
+    taken plan, never on a shared one."""
+
+    def __init__(self):
+        import threading
+        self.lock = threading.Lock()
+        self.free = []
+        self.all = []
+
+    def acquire(self, H, exact):
+        with self.lock:
+            p = self.free.pop() if self.free else None
+        if p is None:
+            p = Plan(H)
+            with self.lock:
+                self.all.append(p)
+        L.call('airg_plan_set_exact', p.h, 1 if exact else 0)
+        return p
+
+    def release(self, p):
+        with self.lock:
+            self.free.append(p)
+
+
+def _pool(H):
+    pool = H.__dict__.get('_plans')
+    if pool is None:
+        pool = H.__dict__.setdefault('_plans', _PlanPool())
+    return pool
+
+
+class plan_for:
+    """Context manager: ``with plan_for(H, exact) as p`` holds a plan of H's
+    pool for the duration of one solve."""
+
+    def __init__(self, H, exact=False):
+        self.H, self.exact = H, exact
+
+    def __enter__(self):
+        self.p = _pool(self.H).acquire(self.H, self.exact)
+        return self.p
+
+    def __exit__(self, *exc):
+        _pool(self.H).release(self.p)
+        return False
+
+
+def coarse_mode(H):
+    """'dense' when the fast-mode coarse solve of H's plans is the dense q(A)
+    GEMV, 'newton' otherwise (after a solve has built a plan)."""
+    pool = H.__dict__.get('_plans')
+    if pool is None or not pool.all:
+        return None
+    return 'dense' if L.load().airg_plan_coarse_mode(pool.all[0].h) == 1 else 'newton'
 
 
 def _level_size(H, level):
@@ -135,13 +189,15 @@ def vcycle(H, level, r, cfg, exact=False):
     if level < 0 or level > len(H.levels):
         raise ValueError(f'level {level} out of range')
     n = _level_size(H, level)
+    host = is_host_array(r)
     r = to_dev(r, VAL)
     if r.numel() != n:
         raise ValueError('residual has wrong length for this level')
     e = empty(n, VAL)
-    L.call('airg_plan_vcycle', plan_for(H, exact).h, level, L.ptr(r), L.ptr(e), cfg.f_smooth_its,
-           L.stream_handle())
-    return e
+    with plan_for(H, exact) as p:
+        L.call('airg_plan_vcycle', p.h, level, L.ptr(r), L.ptr(e), cfg.f_smooth_its,
+               L.stream_handle())
+    return e.cpu().numpy() if host else e
 
 
 def richardson_solve(H, b, x0, cfg, exact=False):
@@ -153,17 +209,18 @@ def richardson_solve(H, b, x0, cfg, exact=False):
     vector/FMA path."""
     cfg.validate()
     A = H.top_A
+    host = is_host_array(x0)
     b = to_dev(b, VAL)
     x = to_dev(x0, VAL).clone()
     if b.numel() != A.nrows or x.numel() != A.nrows:
         raise ValueError('right-hand side or initial guess has wrong length')
-    plan = plan_for(H, exact)
     hist = np.zeros(cfg.max_iters + 1)
     its = C.c_int(0)
     conv = C.c_int(0)
-    st = L.load().airg_plan_richardson(plan.h, L.ptr(b), L.ptr(x), cfg.rtol, cfg.atol,
-                                       cfg.max_iters, cfg.f_smooth_its, L.hptr(hist),
-                                       C.byref(its), C.byref(conv), L.stream_handle())
+    with plan_for(H, exact) as plan:
+        st = L.load().airg_plan_richardson(plan.h, L.ptr(b), L.ptr(x), cfg.rtol, cfg.atol,
+                                           cfg.max_iters, cfg.f_smooth_its, L.hptr(hist),
+                                           C.byref(its), C.byref(conv), L.stream_handle())
     if st == L.ERR_DIVERGED:
         raise DivergenceError(L.last_error(), its.value)
     L.check(st, 'airg_plan_richardson')
@@ -171,7 +228,8 @@ def richardson_solve(H, b, x0, cfg, exact=False):
                        converged=bool(conv.value), cycle_complexity=H.cycle_complexity,
                        storage_complexity=H.storage_complexity,
                        flops_per_cycle=count_cycle_flops(H, f_smooth_its=cfg.f_smooth_its))
-    return x, stats
+    # the reference returns an ndarray: numpy in, numpy out; device in, device out
+    return (x.cpu().numpy() if host else x), stats
 
 
 def _poly_apply_flops(p, nnz, n):
@@ -211,10 +269,14 @@ def _spmat_bytes(M):
     return 12 * M.nnz + 4 * (M.nrows + 1)
 
 
-def count_cycle_bytes(H, include_top=True):
+def count_cycle_bytes(H, include_top=True, coarse=None):
     """Algorithmic HBM bytes of one V-cycle (+ the top residual), the
     roofline numerator of SURVEY.md 8(d): 12 B/nnz + 4 B/row per matrix pass,
-    every vector operand read or written once."""
+    every vector operand read or written once.  ``coarse``: the coarse solve
+    that runs -- 'dense' (fast mode's q(A) GEMV: 8 n^2 + 16 n) or 'newton'
+    (the root-by-root apply); default: what H's solve plans use."""
+    if coarse is None:
+        coarse = coarse_mode(H) or 'newton'
     tot = 0
     for lv in H.levels:
         nf, nc = lv.split.n_f, lv.split.n_c
@@ -232,7 +294,9 @@ def count_cycle_bytes(H, include_top=True):
             else:
                 tot += 16 * lv.n
     Cm, p = H.coarsest_A, H.coarse_solver
-    if p.kind == 'newton_roots':
+    if p.kind == 'newton_roots' and coarse == 'dense':
+        tot += 8 * Cm.nrows * Cm.nrows + 16 * Cm.nrows
+    elif p.kind == 'newton_roots':
         i = 0
         while i < len(p.roots):
             if p.roots[i].imag == 0:

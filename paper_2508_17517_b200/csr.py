@@ -142,6 +142,31 @@ def validate(A):
     return A
 
 
+def as_matrix(A):
+    """The device form of ``A``: a SparseMatrix passes through; a host CSR
+    object with the reference's attributes (``airmg.SparseMatrix``:
+    nrows, ncols, int64 row_offsets / col_indices, float64 values --
+    sparse.py:44-73) is uploaded, so reference callers can pass their own
+    matrices.  Indices must fit int32 (the device CSR's index type)."""
+    if isinstance(A, SparseMatrix):
+        return A
+    try:
+        nr, nc = int(A.nrows), int(A.ncols)
+        p, c, v = A.row_offsets, A.col_indices, A.values
+    except AttributeError:
+        raise TypeError(f'expected a CSR matrix (nrows, ncols, row_offsets, col_indices, values), '
+                        f'got {type(A).__name__}') from None
+    p = np.asarray(p) if not isinstance(p, torch.Tensor) else p
+    if max(nr, nc, int(p[-1]) if len(p) else 0) > np.iinfo(np.int32).max:
+        raise ValueError('matrix too large for 32-bit device indices')
+    return SparseMatrix.csr(nr, nc, p, c, v, check=False)
+
+
+def is_host_array(x):
+    """True for inputs the reference API takes as numpy arrays (not device tensors)."""
+    return not isinstance(x, torch.Tensor)
+
+
 def as_vector(x, n=None):
     t = to_dev(x, VAL)
     if t.dim() != 1 or (n is not None and t.numel() != n):
@@ -152,6 +177,7 @@ def as_vector(x, n=None):
 def spmv(A, x, exact=False):
     """y = A x (sparse.py:206-212).  ``exact=True`` reproduces scipy's
     sequential non-FMA row sums bitwise; the default is the vector kernel."""
+    A = as_matrix(A)
     x = to_dev(x, VAL)
     if x.dim() != 1 or x.numel() != A.ncols:
         raise ValueError(f'vector of length {x.numel()} incompatible with '
@@ -230,6 +256,7 @@ def _args(A):
 
 def spgemm(A, B, negate=False):
     """Structural product, cancellation zeros kept (sparse.py:222-240)."""
+    A, B = as_matrix(A), as_matrix(B)
     if A.ncols != B.nrows:
         raise ValueError(f'cannot multiply {A.nrows}x{A.ncols} by {B.nrows}x{B.ncols}')
     r = new_result()
@@ -240,6 +267,7 @@ def spgemm(A, B, negate=False):
 
 def spgemm_fixed_sparsity(A, B, pattern):
     """A @ B restricted to the stored positions of ``pattern`` (sparse.py:243-263)."""
+    A, B, pattern = as_matrix(A), as_matrix(B), as_matrix(pattern)
     if A.ncols != B.nrows:
         raise ValueError(f'cannot multiply {A.nrows}x{A.ncols} by {B.nrows}x{B.ncols}')
     if pattern.nrows != A.nrows or pattern.ncols != B.ncols:
@@ -273,6 +301,7 @@ def extract_mapped(A, rows, colmap, ncols):
 
 def extract(A, rows, cols):
     """Submatrix A[rows, cols], renumbered, entry order kept (sparse.py:278-304)."""
+    A = as_matrix(A)
     rows = _index_set(rows, A.nrows, 'row')
     cols = _index_set(cols, A.ncols, 'column')
     colmap = torch.full((A.ncols,), -1, dtype=IDX, device=rows.device)
@@ -282,6 +311,7 @@ def extract(A, rows, cols):
 
 def drop_and_lump(A, rel_tol, lump):
     """Row-relative drop, optional sequential lump onto the diagonal (sparse.py:307-352)."""
+    A = as_matrix(A)
     if rel_tol < 0:
         raise ValueError('rel_tol must be non-negative')
     if lump and A.nrows != A.ncols:
@@ -298,6 +328,7 @@ def drop_and_lump(A, rel_tol, lump):
 
 def diagonal(A):
     """Main diagonal as a device vector (sparse.py:360-367)."""
+    A = as_matrix(A)
     n = min(A.nrows, A.ncols)
     d = empty(n, VAL)
     L.call('airg_diagonal', n, *_args(A), L.ptr(d), L.stream_handle())

@@ -38,7 +38,18 @@ void set_error(const char* fmt, ...);
     if (_s != AIRG_OK) return _s;                                                \
   } while (0)
 
-constexpr int kNumSMs = 148;
+// SMs of the current device (148 on B200), queried once per device
+inline int num_sms() {
+  static int cache[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& v = cache[dev & 63];
+  if (v == 0) {
+    int n = 0;
+    v = cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0 ? n : 148;
+  }
+  return v;
+}
 
 inline int blocks_for(long long n, int threads, long long cap = 148LL * 64) {
   long long b = (n + threads - 1) / threads;
@@ -66,27 +77,19 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
-// Keep freed scratch mapped in the stream-ordered pool: with the default
-// release threshold (0) every synchronisation unmaps it and the next large
-// cudaMallocAsync pays for re-mapping GBs of HBM.
-inline void keep_pool_warm() {
-  static thread_local int done_dev = -1;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    unsigned long long thr = ~0ull;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
-  done_dev = dev;
-}
+// The library's own stream-ordered memory pool (one per device), with the
+// release threshold raised so freed scratch stays mapped across
+// synchronisations (with the default threshold 0 every synchronisation
+// unmaps it and the next large allocation pays for re-mapping GBs of HBM).
+// A private pool, so the process's default pool -- torch's and every other
+// user's -- keeps its own settings.
+cudaMemPool_t lib_pool();
 
-// Scratch memory from the stream-ordered pool (freed by the caller of alloc).
+// Scratch memory from the library pool (freed by the caller of alloc).
 template <typename T>
 inline int scratch(T** p, size_t count, cudaStream_t s) {
-  keep_pool_warm();
   if (count == 0) count = 1;
-  AIRG_CUDA(cudaMallocAsync((void**)p, count * sizeof(T), s));
+  AIRG_CUDA(cudaMallocFromPoolAsync((void**)p, count * sizeof(T), lib_pool(), s));
   return AIRG_OK;
 }
 inline void release(void* p, cudaStream_t s) {
@@ -96,8 +99,7 @@ inline void release(void* p, cudaStream_t s) {
 // Long-lived plan buffers: pool-backed (no device-wide sync on free).
 template <typename T>
 inline cudaError_t dmalloc(T** p, size_t bytes) {
-  keep_pool_warm();
-  cudaError_t e = cudaMallocAsync((void**)p, bytes ? bytes : 1, 0);
+  cudaError_t e = cudaMallocFromPoolAsync((void**)p, bytes ? bytes : 1, lib_pool(), 0);
   if (e == cudaSuccess) e = cudaStreamSynchronize(0);
   return e;
 }

@@ -22,6 +22,29 @@ void set_error(const char* fmt, ...) {
   g_err = buf;
 }
 
+cudaMemPool_t lib_pool() {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  cudaMemPool_t& p = pools[dev & 63];
+  if (!p) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    if (cudaMemPoolCreate(&p, &props) != cudaSuccess) {
+      p = nullptr;
+      cudaDeviceGetDefaultMemPool(&p, dev);  // fallback: the device pool, untouched
+      return p;
+    }
+    unsigned long long thr = ~0ull;
+    cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  return p;
+}
+
 // ---------------------------------------------------------------------------
 // SpMV with a fused epilogue:
 //   out[omap ? omap[i] : i] = alpha * (A (xs*x))_i + beta * v[vmap ? vmap[i] : i]
@@ -209,7 +232,8 @@ struct Csr {
   int vs = 1;
 };
 
-static long long g_launches = 0;
+// kernels launched by this thread (per-call deltas are taken on the calling thread)
+static thread_local long long g_launches = 0;
 
 static int launch_spmv(const Csr& A, const double* x, double xs, const Epi& ep, cudaStream_t s,
                        bool exact = false) {
@@ -430,7 +454,7 @@ __global__ void __launch_bounds__(1024) newton_smem_kernel(
     int n, const int* __restrict__ gptr, const int* __restrict__ gcol, const double* __restrict__ gval,
     int mat_smem, const double* __restrict__ b, double* __restrict__ xout, int nunits,
     const int* __restrict__ utype, const double* __restrict__ up1, const double* __restrict__ up2,
-    int identity_cols = 0) {
+    int identity_cols = 0, int* stopped = nullptr) {
   extern __shared__ double sm[];
   __shared__ double red[2][32];
   const int tid = threadIdx.x, nthr = blockDim.x, nw = nthr >> 5;
@@ -499,7 +523,10 @@ __global__ void __launch_bounds__(1024) newton_smem_kernel(
     if (utype[k] == 0) {
       const double t = up1[k];
       const double sc = scale / t;
-      if (!isfinite(mul<E>(sc, nrm))) break;
+      if (!isfinite(mul<E>(sc, nrm))) {
+        if (stopped && tid == 0) atomicOr(stopped, 1);
+        break;
+      }
       for (int r = g; r < rows_pad; r += ng) {
         const double s = rowdot(u, r);
         if (gl == 0 && r < n) w[r] = s;
@@ -524,7 +551,10 @@ __global__ void __launch_bounds__(1024) newton_smem_kernel(
           bad |= !isfinite(d);
         }
       }
-      if (__syncthreads_or(bad)) break;
+      if (__syncthreads_or(bad)) {
+        if (stopped && tid == 0) atomicOr(stopped, 1);
+        break;
+      }
       for (int r = g; r < rows_pad; r += ng) {
         const double z = rowdot(w, r);
         if (gl == 0 && r < n) {
@@ -547,7 +577,10 @@ __global__ void __launch_bounds__(1024) newton_smem_kernel(
       scale = E ? mul_rn(scale, nrm) : scale * nrm;
       nrm = 1.0;  // max|u/nrm| == 1 exactly
       __syncthreads();
-      if (!isfinite(scale) || scale == 0.0) break;
+      if (!isfinite(scale) || scale == 0.0) {
+        if (stopped && tid == 0) atomicOr(stopped, 1);
+        break;
+      }
     }
   }
   __syncthreads();
@@ -923,7 +956,13 @@ struct GraphEntry {
   bool exact;
   cudaGraphExec_t exec;
   long long nk;  // kernels per replay
+  unsigned long long used;  // LRU tick
 };
+
+// graphs kept per plan (least recently used evicted); the keys use the
+// plan's own staging vectors, so a plan needs one per (operation, level,
+// smoothing sweeps, arithmetic mode)
+constexpr size_t kMaxGraphs = 32;
 
 struct airg_plan {
   cudaStream_t cs = nullptr;  // plan stream: captures and replays
@@ -948,6 +987,12 @@ struct airg_plan {
   bool ready_top = false, ready_coarse = false;
   bool exact = false;  // reference arithmetic order (parity mode)
   double* coarseQ = nullptr;  // dense q(A_coarse) for the fast coarse solve
+  int dense_state = 0;  // 0 not built, 1 dense q(A) in use, -1 Newton apply (an
+                        // identity column stopped early: q(A) is not linear there)
+  // staging vectors: Richardson b / x, V-cycle API input / output; the
+  // captured graphs name these, never the caller's buffers
+  double *sb = nullptr, *sx = nullptr, *vin = nullptr, *vout = nullptr;
+  unsigned long long tick = 0;
 };
 
 static int alloc_vec(double** p, long long n) {
@@ -1131,7 +1176,8 @@ int airg_plan_destroy(airg_plan* p) {
     free_poly(L.sm);
   }
   free_poly(p->coarse_poly);
-  for (double* q : {p->cw0, p->cw1, p->cw2, p->cw3, p->r, p->e, p->parts, p->norm_d, p->coarseQ})
+  for (double* q : {p->cw0, p->cw1, p->cw2, p->cw3, p->r, p->e, p->parts, p->norm_d, p->coarseQ,
+                    p->sb, p->sx, p->vin, p->vout})
     if (q) dfree(q);
   if (p->iflag) dfree(p->iflag);
   if (p->nst) dfree(p->nst);
@@ -1247,6 +1293,7 @@ __global__ void __launch_bounds__(256) dense_gemv_kernel(int n, const double* __
 static int build_dense_coarse(airg_plan* p, cudaStream_t s) {
   const int n = p->coarse.nrows;
   AIRG_CUDA(dmalloc(&p->coarseQ, (size_t)n * n * sizeof(double)));
+  AIRG_CUDA(cudaMemsetAsync(p->iflag, 0, sizeof(int), s));
   const Poly& cp = p->coarse_poly;
   const Csr& A = p->coarse;
   const size_t vec_bytes = (size_t)3 * n * sizeof(double);
@@ -1258,9 +1305,19 @@ static int build_dense_coarse(airg_plan* p, cudaStream_t s) {
                                  (int)cap));
   newton_smem_kernel<false><<<n, 256, shm, s>>>(n, A.ptr, A.col, A.val, mat_smem, nullptr,
                                                 p->coarseQ, (int)cp.utype.size(), cp.d_utype,
-                                                cp.d_p1, cp.d_p2, 1);
+                                                cp.d_p1, cp.d_p2, 1, p->iflag);
   ++g_launches;
   AIRG_LAUNCH_CHECK();
+  int stopped = 0;
+  AIRG_CUDA(cudaMemcpyAsync(&stopped, p->iflag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  AIRG_CUDA(cudaStreamSynchronize(s));
+  if (stopped) {  // the reference stops per right-hand side (polynomial.py:312-355)
+    dfree(p->coarseQ);
+    p->coarseQ = nullptr;
+    p->dense_state = -1;
+  } else {
+    p->dense_state = 1;
+  }
   return AIRG_OK;
 }
 
@@ -1272,9 +1329,12 @@ static int vcycle_rec(airg_plan* p, int level, const double* r, double* e, int f
       set_error("plan has no coarse solver");
       return AIRG_ERR_ARG;
     }
-    if (!p->exact && p->coarse_poly.kind == 1 && p->coarse.nrows <= kDenseCoarseMax) {
+    if (!p->exact && p->coarse_poly.kind == 1 && p->coarse.nrows <= kDenseCoarseMax &&
+        p->dense_state >= 0) {
       // fast mode: y = Q r with Q = q(A_coarse) precomputed column by column
-      if (!p->coarseQ) AIRG_TRY(build_dense_coarse(p, s));
+      if (p->dense_state == 0) AIRG_TRY(build_dense_coarse(p, s));
+    }
+    if (!p->exact && p->coarse_poly.kind == 1 && p->dense_state == 1) {
       const int n = p->coarse.nrows;
       dense_gemv_kernel<<<(n + 31) / 32, 256, 0, s>>>(n, p->coarseQ, r, e);
       ++g_launches;
@@ -1344,10 +1404,8 @@ static int plan_streams(airg_plan* p) {
 // things a capture must not do (synchronous allocation) are done up front
 static int prepare_capture(airg_plan* p, cudaStream_t s) {
   if (!p->exact && p->ready_coarse && p->coarse_poly.kind == 1 &&
-      p->coarse.nrows <= kDenseCoarseMax && !p->coarseQ) {
+      p->coarse.nrows <= kDenseCoarseMax && p->dense_state == 0)
     AIRG_TRY(build_dense_coarse(p, s));
-    AIRG_CUDA(cudaStreamSynchronize(s));
-  }
   return AIRG_OK;
 }
 
@@ -1360,6 +1418,13 @@ static int run_graph(airg_plan* p, int kind, int level, const void* a, const voi
     if (g.kind == kind && g.level == level && g.a == a && g.b == b && g.fits == fits &&
         g.exact == p->exact)
       ent = &g;
+  if (!ent && p->graphs.size() >= kMaxGraphs) {  // evict the least recently used
+    auto lru = std::min_element(p->graphs.begin(), p->graphs.end(),
+                                [](const GraphEntry& x, const GraphEntry& y) { return x.used < y.used; });
+    AIRG_CUDA(cudaStreamSynchronize(cs));
+    cudaGraphExecDestroy(lru->exec);
+    p->graphs.erase(lru);
+  }
   if (!ent) {
     const long long l0 = g_launches;
     AIRG_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
@@ -1374,10 +1439,11 @@ static int run_graph(airg_plan* p, int kind, int level, const void* a, const voi
     cudaGraphExec_t ex = nullptr;
     AIRG_CUDA(cudaGraphInstantiate(&ex, graph, 0));
     cudaGraphDestroy(graph);
-    p->graphs.push_back(GraphEntry{kind, level, a, b, fits, p->exact, ex, g_launches - l0});
+    p->graphs.push_back(GraphEntry{kind, level, a, b, fits, p->exact, ex, g_launches - l0, 0});
     ent = &p->graphs.back();
     g_launches = l0;
   }
+  ent->used = ++p->tick;
   AIRG_CUDA(cudaGraphLaunch(ent->exec, cs));
   g_launches += ent->nk;
   return AIRG_OK;
@@ -1395,13 +1461,48 @@ int airg_plan_vcycle(airg_plan* p, int level, const double* r, double* e, int f_
   const int fits = f_smooth_its < 1 ? 1 : f_smooth_its;
   AIRG_TRY(plan_streams(p));
   AIRG_TRY(prepare_capture(p, s));
+  const int n = level == p->nlevels ? p->coarse.nrows : p->lv[level].n;
+  const int nmax = p->nlevels ? p->lv[0].n : p->coarse.nrows;
+  if (!p->vin) {
+    AIRG_TRY(alloc_vec(&p->vin, nmax));
+    AIRG_TRY(alloc_vec(&p->vout, nmax));
+  }
+  if (r != p->vin)
+    AIRG_CUDA(cudaMemcpyAsync(p->vin, r, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   AIRG_CUDA(cudaEventRecord(p->ev_in, s));
   AIRG_CUDA(cudaStreamWaitEvent(p->cs, p->ev_in, 0));
-  AIRG_TRY(run_graph(p, 0, level, r, e, fits, p->cs,
-                     [&](cudaStream_t t) { return vcycle_rec(p, level, r, e, fits, t); }));
+  AIRG_TRY(run_graph(p, 0, level, p->vin, p->vout, fits, p->cs,
+                     [&](cudaStream_t t) { return vcycle_rec(p, level, p->vin, p->vout, fits, t); }));
   AIRG_CUDA(cudaEventRecord(p->ev_out, p->cs));
   AIRG_CUDA(cudaStreamWaitEvent(s, p->ev_out, 0));
+  if (e != p->vout)
+    AIRG_CUDA(cudaMemcpyAsync(e, p->vout, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   return AIRG_OK;
+}
+
+// the plan's staging vectors (size of the finest level); a V-cycle called on
+// them runs without copying in / out
+int airg_plan_staging(airg_plan* p, double** vin, double** vout) {
+  const int nmax = p->nlevels ? p->lv[0].n : p->coarse.nrows;
+  if (!p->vin) {
+    AIRG_TRY(alloc_vec(&p->vin, nmax));
+    AIRG_TRY(alloc_vec(&p->vout, nmax));
+  }
+  *vin = p->vin;
+  *vout = p->vout;
+  return AIRG_OK;
+}
+
+int airg_copy_d2d(void* dst, const void* src, int64_t bytes, void* stream) {
+  AIRG_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return AIRG_OK;
+}
+
+int airg_plan_graph_count(airg_plan* p) { return p ? (int)p->graphs.size() : 0; }
+
+int airg_plan_coarse_mode(airg_plan* p) {
+  // 1: fast-mode coarse solve is the dense q(A) GEMV; 0: Newton apply
+  return p && p->dense_state == 1 ? 1 : 0;
 }
 
 int64_t airg_plan_launches(airg_plan* p) { return p ? p->launches : 0; }
@@ -1458,8 +1559,16 @@ extern "C" int airg_plan_richardson(airg_plan* p, const double* b, double* x, do
   AIRG_CUDA(cudaEventRecord(p->ev_in, caller));
   AIRG_CUDA(cudaStreamWaitEvent(p->cs, p->ev_in, 0));
   cudaStream_t s = p->cs;
-  const int st = richardson_body(p, b, x, rtol, atol, max_iters, f_smooth_its, history, iterations,
-                                 converged, s);
+  const int n = p->top.nrows;
+  if (!p->sb) {
+    AIRG_TRY(alloc_vec(&p->sb, n));
+    AIRG_TRY(alloc_vec(&p->sx, n));
+  }
+  AIRG_CUDA(cudaMemcpyAsync(p->sb, b, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  AIRG_CUDA(cudaMemcpyAsync(p->sx, x, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  const int st = richardson_body(p, p->sb, p->sx, rtol, atol, max_iters, f_smooth_its, history,
+                                 iterations, converged, s);
+  cudaMemcpyAsync(x, p->sx, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, s);
   cudaEventRecord(p->ev_out, s);
   cudaStreamWaitEvent(caller, p->ev_out, 0);
   return st;

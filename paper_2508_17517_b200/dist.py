@@ -875,7 +875,7 @@ class DistSolver:
     def _native(self):
         if getattr(self, '_dplan', None) is not None:
             return self._dplan
-        from .amg_solve import plan_for
+        from .amg_solve import _pool
         comm = self.comm
         h = L.C.c_void_p()
         L.call('airg_dplan_create', native_comm(comm), len(self.lv), L.C.byref(h))
@@ -906,7 +906,8 @@ class DistSolver:
         T = self.Atop
         L.call('airg_dplan_set_top', h, T.nrows, L.ptr(T.row_offsets), L.ptr(T.col_indices),
                L.ptr(T.values), T.nnz)
-        tail = plan_for(self.H.tail)
+        # a plan of the tail's pool dedicated to this distributed plan (never released)
+        tail = _pool(self.H.tail).acquire(self.H.tail, False)
         p = self.tail_part
         counts = np.ascontiguousarray(np.diff(p.off), dtype=np.int32)
         L.call('airg_dplan_finish', h, tail.h, L.hptr(counts))

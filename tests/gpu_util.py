@@ -52,3 +52,8 @@ def rel(a, b):
     a = np.asarray(a, dtype=np.float64)
     b = np.asarray(b, dtype=np.float64)
     return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)))
+
+
+def tonp(x):
+    """Host copy of a solve result (numpy in -> numpy out, device in -> device out)."""
+    return x if isinstance(x, np.ndarray) else x.cpu().numpy()

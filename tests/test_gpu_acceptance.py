@@ -2,6 +2,8 @@
 /root/reference/pkg/tests/test_acceptance.py) run against the GPU package."""
 
 import numpy as np
+
+from tests.gpu_util import tonp
 import pytest
 import scipy.sparse as sps
 import scipy.sparse.linalg as spla
@@ -43,7 +45,7 @@ def test_criterion_03_cyclic_reduction_exactness(G):
         x, st = G.richardson_solve(H, b, np.zeros(n), G.SolveConfig(rtol=1e-10))
         assert st.converged and st.iterations <= 2
         expected = spla.spsolve_triangular(host_scipy(A), b, lower=True)
-        x = x.cpu().numpy()
+        x = tonp(x)
         assert np.linalg.norm(x - expected) <= 1e-10 * np.linalg.norm(expected)
 
 
@@ -120,7 +122,7 @@ def test_criterion_10_determinism(G):
     for _ in range(2):
         H = G.setup(A, G.SetupConfig(seed=0))
         x, st = G.richardson_solve(H, b, np.ones(A.nrows), G.SolveConfig())
-        runs.append((st.residual_history, x.cpu().numpy().tobytes(),
+        runs.append((st.residual_history, tonp(x).tobytes(),
                      G.hierarchy_summary(H)))
     assert runs[0][0] == runs[1][0]
     assert runs[0][1] == runs[1][1]

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 from oracle import airg_oracle as O
-from tests.gpu_util import dev_csr, dev_poly, host_csr, oracle_poly, rel, upload_hierarchy
+from tests.gpu_util import dev_csr, dev_poly, host_csr, oracle_poly, rel, upload_hierarchy, tonp
 
 pytestmark = pytest.mark.gpu
 
@@ -279,7 +279,7 @@ def test_setup_matches_reference_fixtures(G, golden, case):
     # reference's bit for bit; only the norm reduction order differs.
     x, st = G.richardson_solve(H, b, np.ones(A.nrows), G.SolveConfig(), exact=True)
     assert st.iterations == int(g['iterations'])
-    h = hashlib.sha256(np.ascontiguousarray(x.cpu().numpy()).tobytes()).hexdigest()
+    h = hashlib.sha256(np.ascontiguousarray(tonp(x)).tobytes()).hexdigest()
     assert h == str(g['x_digest'])
     assert rel(st.residual_history, g['history']) < 1e-13
     # fast mode (vector SpMV + FMA): same iterations, history within 1e-10 of
@@ -350,7 +350,7 @@ def test_krylov_free_setup_bitwise_without_injection(G, nx, v):
     x, st = G.richardson_solve(H, b, np.ones(A.nrows), G.SolveConfig(max_iters=60), exact=True)
     xo, hist, conv, its = O.richardson(Ho, np.zeros(Ao.nrows), np.ones(Ao.nrows), max_iters=60)
     assert st.iterations == its
-    assert x.cpu().numpy().tobytes() == xo.tobytes()
+    assert tonp(x).tobytes() == xo.tobytes()
 
 
 def test_setup_errors(G):
@@ -395,3 +395,32 @@ def test_ap_onepoint_structural_zeros(G, seed):
     same(take(res), ref)
     assert np.any(ref.val == 0.0)          # the case exercises cancellations
     assert not np.any(np.signbit(ref.val[ref.val == 0.0]))
+
+
+def test_gpu_setup_replayed_by_oracle_512():
+    """The benchmark configuration one size down (512^2, default SetupConfig,
+    order 6; the reference fixtures stop at 128^2): GPU setup with its own
+    device Krylov coefficients, the oracle replays it with those coefficients
+    injected.  Every level's labels / R / P / A_ff / A_fc / A and the
+    coarsest matrix must be bitwise equal -- this exercises the long-row
+    SpGEMM / drop-lump / assembly classes the 2048^2 bench runs (pre-drop
+    R(AP) rows up to ~1300 entries) -- and the residual history within
+    1e-10 of the initial residual."""
+    import paper_2508_17517_b200 as G
+    nx = 512
+    A, b = G.build_advection_2d(G.AdvectionProblem(nx=nx, ny=nx, vx=PI4[0], vy=PI4[1]))
+    H = G.setup(A, G.SetupConfig(), keep_level_matrices=True)
+    inj = {k: oracle_poly(p) for k, p in H.polys.items()}
+    Ao = O.advection_2d(nx, nx, *PI4)
+    Ho = O.setup(Ao, O.Cfg(), poly_inject=inj, keep_level_matrices=True)
+    assert H.num_levels == len(Ho.levels)
+    assert H.truncated_at == Ho.truncated_at
+    for L, Lo in zip(H.levels, Ho.levels):
+        assert np.array_equal(L.split.labels_host(), Lo.labels)
+        for a, o in ((L.R, Lo.R), (L.P, Lo.P), (L.A_ff, Lo.A_ff), (L.A_fc, Lo.A_fc), (L.A, Lo.A)):
+            same(a, o)
+    same(H.coarsest_A, Ho.coarsest_A)
+    x, st = G.richardson_solve(H, b, np.ones(A.nrows), G.SolveConfig())
+    xo, hist, conv, its = O.richardson(Ho, np.zeros(Ao.nrows), np.ones(Ao.nrows))
+    assert st.iterations == its
+    assert np.max(np.abs(np.array(st.residual_history) - hist)) <= 1e-10 * hist[0]

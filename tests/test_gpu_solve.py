@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 from oracle import airg_oracle as O
-from tests.gpu_util import dev_csr, dev_poly, rel, upload_hierarchy
+from tests.gpu_util import dev_csr, dev_poly, rel, upload_hierarchy, tonp
 
 pytestmark = pytest.mark.gpu
 
@@ -109,7 +109,7 @@ def test_vcycle_every_level(G, hier64):
         n = hier64.levels[lev].n if lev < len(hier64.levels) else hier64.coarsest_A.nrows
         r = rng.standard_normal(n)
         want = O.vcycle(hier64, lev, r)
-        got = G.vcycle(H, lev, r, G.SolveConfig()).cpu().numpy()
+        got = tonp(G.vcycle(H, lev, r, G.SolveConfig()))
         assert np.max(np.abs(got - want)) <= 1e-10 * np.max(np.abs(want)), lev
 
 
@@ -126,7 +126,7 @@ def test_richardson_matches_oracle(G, nx, ny, v, order, its):
                                G.SolveConfig(f_smooth_its=its))
     assert st.iterations == its_o and st.converged == conv_o
     assert rel(st.residual_history, hist_o) < 1e-10
-    x = x.cpu().numpy()
+    x = tonp(x)
     assert np.max(np.abs(x - x_o)) <= 1e-10 * max(np.max(np.abs(x_o)), 1e-300) + 1e-14
 
 
@@ -142,10 +142,10 @@ def test_richardson_exact_mode_bitwise(G, nx, ny, v, order, its):
     x, st = G.richardson_solve(H, np.zeros(A.nrows), np.ones(A.nrows),
                                G.SolveConfig(f_smooth_its=its), exact=True)
     assert st.iterations == its_o
-    assert x.cpu().numpy().tobytes() == x_o.tobytes()
+    assert tonp(x).tobytes() == x_o.tobytes()
     assert rel(st.residual_history, hist_o) < 1e-13
     r = np.random.default_rng(4).standard_normal(A.nrows)
-    e = G.vcycle(H, 0, r, G.SolveConfig(), exact=True).cpu().numpy()
+    e = tonp(G.vcycle(H, 0, r, G.SolveConfig(), exact=True))
     assert e.tobytes() == O.vcycle(Hh, 0, r).tobytes()
 
 
@@ -165,7 +165,7 @@ def test_divergence_guard(G):
     H = upload_hierarchy(Hh)
     bad = O._mk(A.nrows, A.ncols, A.ptr, A.col, -50.0 * A.val)
     H.top_A = dev_csr(bad)
-    H._plan = None
+    H._plans = None  # fresh plans for the modified top operator
     with pytest.raises(G.DivergenceError) as ei:
         G.richardson_solve(H, np.zeros(A.nrows), np.ones(A.nrows), G.SolveConfig(max_iters=50))
     assert ei.value.iteration >= 1
@@ -177,4 +177,74 @@ def test_solve_bitwise_deterministic(G):
     x1, s1 = G.richardson_solve(H, np.zeros(A.nrows), np.ones(A.nrows), G.SolveConfig())
     x2, s2 = G.richardson_solve(H, np.zeros(A.nrows), np.ones(A.nrows), G.SolveConfig())
     assert s1.residual_history == s2.residual_history
-    assert x1.cpu().numpy().tobytes() == x2.cpu().numpy().tobytes()
+    assert tonp(x1).tobytes() == tonp(x2).tobytes()
+
+
+def test_concurrent_solves_on_one_hierarchy(G):
+    """The reference's Hierarchy is immutable and usable by concurrent solves,
+    each owning its work vectors (SPEC.md concurrency model): two threads
+    solving on one H on their own streams both reproduce the single-thread
+    result bitwise (each solve takes its own plan from H's pool)."""
+    import threading
+    import torch
+    A, b = G.build_advection_2d(G.AdvectionProblem(nx=96, ny=96, vx=PI4[0], vy=PI4[1]))
+    H = G.setup(A, G.SetupConfig(poly_order=4))
+    x_ref, st_ref = G.richardson_solve(H, b, np.ones(A.nrows), G.SolveConfig())
+    out, errs = {}, []
+
+    def run(i):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(3):
+                    x, st = G.richardson_solve(H, b, np.ones(A.nrows) * (1 + 0 * i),
+                                               G.SolveConfig())
+                s.synchronize()
+            out[i] = (tonp(x), st.residual_history)
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for i in range(2):
+        assert out[i][0].tobytes() == tonp(x_ref).tobytes()
+        assert out[i][1] == st_ref.residual_history
+
+
+def test_graph_cache_bounded_and_host_in_host_out(G):
+    """vcycle() / richardson_solve() with fresh vectors every call reuse the
+    plan's captured graphs (they name the plan's staging vectors), and numpy
+    inputs give numpy outputs like the reference's API."""
+    from paper_2508_17517_b200 import _lib as L
+    A, b = G.build_advection_2d(G.AdvectionProblem(nx=64, ny=64, vx=PI4[0], vy=PI4[1]))
+    H = G.setup(A, G.SetupConfig(poly_order=4))
+    rng = np.random.default_rng(0)
+    for _ in range(40):
+        e = G.vcycle(H, 0, rng.standard_normal(A.nrows), G.SolveConfig())
+        assert isinstance(e, np.ndarray)
+        x, _ = G.richardson_solve(H, b, rng.standard_normal(A.nrows), G.SolveConfig())
+        assert isinstance(x, np.ndarray)
+    pool = H.__dict__['_plans']
+    assert len(pool.all) == 1
+    assert L.load().airg_plan_graph_count(pool.all[0].h) <= 4
+
+
+def test_setup_accepts_reference_style_host_matrix(G):
+    """A reference caller's matrix (host CSR with int64 indices, the
+    attributes of airmg.SparseMatrix, sparse.py:44-73) is accepted by
+    setup() and the sparse kernels, with the same result as the device one."""
+    from types import SimpleNamespace
+    Ao = O.advection_2d(48, 48, *PI4)
+    Ah = SimpleNamespace(nrows=Ao.nrows, ncols=Ao.ncols, row_offsets=Ao.ptr.astype(np.int64),
+                         col_indices=Ao.col.astype(np.int64), values=Ao.val)
+    H1 = G.setup(Ah, G.SetupConfig(poly_order=4))
+    H2 = G.setup(dev_csr(Ao), G.SetupConfig(poly_order=4))
+    assert H1.num_levels == H2.num_levels
+    for L1, L2 in zip(H1.levels, H2.levels):
+        assert np.array_equal(L1.split.labels_host(), L2.split.labels_host())
+    y = tonp(G.spmv(Ah, np.ones(Ao.ncols)))
+    assert np.max(np.abs(y - O.spmv(Ao, np.ones(Ao.ncols)))) <= 1e-14

@@ -10,6 +10,8 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
+
+from tests.gpu_util import tonp
 import torch
 import torch.distributed as dist
 
@@ -66,7 +68,7 @@ def main():
     assert std.iterations == sts.iterations, (std.iterations, sts.iterations)
     assert np.max(np.abs(hd - hs)) <= 1e-10 * hs[0], (hd, hs)
     xg = comm.allgather_v(xd).cpu().numpy()
-    assert np.max(np.abs(xg - xs.cpu().numpy())) <= 1e-9 * np.max(np.abs(xs.cpu().numpy())) + 1e-12
+    assert np.max(np.abs(xg - tonp(xs))) <= 1e-9 * np.max(np.abs(tonp(xs))) + 1e-12
     # native plan (C++ V-cycle, NCCL halos, captured graphs)
     for rep in range(2):
         xn, stn = S.solve(torch.zeros(hi - lo, dtype=torch.float64, device='cuda'),
@@ -75,7 +77,7 @@ def main():
         assert stn.iterations == sts.iterations, (stn.iterations, sts.iterations)
         assert np.max(np.abs(hn - hs)) <= 1e-10 * hs[0], (hn, hs)
         xg = comm.allgather_v(xn).cpu().numpy()
-        assert np.max(np.abs(xg - xs.cpu().numpy())) <= 1e-9 * np.max(np.abs(xs.cpu().numpy())) + 1e-12
+        assert np.max(np.abs(xg - tonp(xs))) <= 1e-9 * np.max(np.abs(tonp(xs))) + 1e-12
     if comm.rank == 0:
         print(f'DIST OK world={comm.world} nx={nx} dist_levels={nd} total_levels={H.num_levels} '
               f'its={std.iterations} hist_diff={np.max(np.abs(hd - hs)) / hs[0]:.2e}', flush=True)
