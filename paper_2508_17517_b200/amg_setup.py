@@ -205,18 +205,25 @@ class _Timer:
         if self.sink is not None:
             e1 = torch.cuda.Event(enable_timing=True)
             e1.record()
-            self.sink.setdefault('_pending', []).append((self.phase, self.e0, e1))
+            self.sink.setdefault('_pending', []).append((self.phase, self.sink.get('_level'),
+                                                         self.e0, e1))
         return False
 
 
 def _flush_timings(sink):
-    """Sum the recorded phase events into seconds (one synchronisation)."""
+    """Sum the recorded phase events into seconds (one synchronisation);
+    per-level sums go to sink['_per_level'][level][phase]."""
     pend = sink.pop('_pending', None) if sink is not None else None
     if not pend:
         return
-    pend[-1][2].synchronize()
-    for phase, e0, e1 in pend:
-        sink[phase] = sink.get(phase, 0.0) + e0.elapsed_time(e1) / 1e3
+    pend[-1][3].synchronize()
+    per = sink.setdefault('_per_level', {})
+    for phase, level, e0, e1 in pend:
+        dt = e0.elapsed_time(e1) / 1e3
+        sink[phase] = sink.get(phase, 0.0) + dt
+        if level is not None:
+            d = per.setdefault(level, {})
+            d[phase] = d.get(phase, 0.0) + dt
 
 
 def resolve_truncate_start(cfg, n_top):
@@ -397,8 +404,10 @@ def setup(A, cfg, poly_inject=None, keep_level_matrices=False):
     truncate_start = resolve_truncate_start(cfg, A.nrows)
     levels, current, coarse_solver, truncated_at = build_levels(
         A, cfg, 0, truncate_start, inj, polys, timings, keep_level_matrices)
+    per_level = timings.pop('_per_level', {})
     H = Hierarchy(levels=levels, coarsest_A=current, coarse_solver=coarse_solver, top_A=A,
                   truncated_at=truncated_at, config=cfg, setup_breakdown=timings)
+    H.setup_levels = per_level  # {level: {phase: seconds}}
     H.polys = polys
     return finalize_complexities(H)
 
@@ -421,6 +430,7 @@ def build_levels(A, cfg, level0, truncate_start, inj, polys, timings, keep_level
         return s
 
     while True:
+        timings['_level'] = level
         if current.nrows <= cfg.min_coarse_size:
             coarse_solver = coarse_here(current, level)
             break
@@ -469,4 +479,5 @@ def build_levels(A, cfg, level0, truncate_start, inj, polys, timings, keep_level
         current = coarse
         level += 1
     _flush_timings(timings)
+    timings.pop('_level', None)
     return levels, current, coarse_solver, truncated_at

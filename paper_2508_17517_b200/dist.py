@@ -766,6 +766,7 @@ def setup_distributed(comm, A, cfg, poly_inject=None, replicate_below=20000, for
     tick('gather_tail')
     levels, coarsest, solver, trunc = build_levels(full, cfg, level, truncate_start, inj, polys,
                                                    timings)
+    timings.pop('_per_level', None)
     tail = Hierarchy(levels=levels, coarsest_A=coarsest, coarse_solver=solver, top_A=full,
                      truncated_at=trunc, config=cfg, setup_breakdown=timings)
     tail.polys = polys
