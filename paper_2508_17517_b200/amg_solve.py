@@ -145,10 +145,21 @@ class _PlanPool:
             self.free.append(p)
 
 
+_POOL_LOCK = None
+
+
 def _pool(H):
+    global _POOL_LOCK
     pool = H.__dict__.get('_plans')
     if pool is None:
-        pool = H.__dict__.setdefault('_plans', _PlanPool())
+        import threading
+        if _POOL_LOCK is None:
+            _POOL_LOCK = threading.Lock()
+        with _POOL_LOCK:
+            pool = H.__dict__.get('_plans')
+            if pool is None:
+                pool = _PlanPool()
+                H._plans = pool
     return pool
 
 

@@ -11,7 +11,7 @@ int scan_counts(const int* in, int* out, int n, long long* total_h, cudaStream_t
   AIRG_CUDA(cudaMemsetAsync(out, 0, sizeof(int), s));
   if (n > 0) {
     AIRG_CUDA(cub::DeviceScan::InclusiveSum(tmp, bytes, in, out + 1, n, s));
-    AIRG_CUDA(cudaMallocAsync(&tmp, bytes, s));
+    AIRG_CUDA(cudaMallocFromPoolAsync(&tmp, bytes, lib_pool(), s));
     AIRG_CUDA(cub::DeviceScan::InclusiveSum(tmp, bytes, in, out + 1, n, s));
     cudaFreeAsync(tmp, s);
   }
@@ -30,7 +30,7 @@ int scan_counts64(const long long* in, long long* out, int n, long long* total_h
   AIRG_CUDA(cudaMemsetAsync(out, 0, sizeof(long long), s));
   if (n > 0) {
     AIRG_CUDA(cub::DeviceScan::InclusiveSum(tmp, bytes, in, out + 1, n, s));
-    AIRG_CUDA(cudaMallocAsync(&tmp, bytes, s));
+    AIRG_CUDA(cudaMallocFromPoolAsync(&tmp, bytes, lib_pool(), s));
     AIRG_CUDA(cub::DeviceScan::InclusiveSum(tmp, bytes, in, out + 1, n, s));
     cudaFreeAsync(tmp, s);
   }
@@ -48,7 +48,7 @@ airg_csr_result* new_result(int nrows, int ncols, cudaStream_t s) {
   r->nrows = nrows;
   r->ncols = ncols;
   r->stream = s;
-  if (cudaMallocAsync((void**)&r->ptr, (size_t)(nrows + 1) * sizeof(int), s) != cudaSuccess) {
+  if (cudaMallocFromPoolAsync((void**)&r->ptr, (size_t)(nrows + 1) * sizeof(int), lib_pool(), s) != cudaSuccess) {
     delete r;
     set_error("out of device memory (result ptr)");
     return nullptr;
@@ -58,9 +58,9 @@ airg_csr_result* new_result(int nrows, int ncols, cudaStream_t s) {
 
 int result_alloc_entries(airg_csr_result* r, long long nnz, bool values) {
   r->nnz = nnz;
-  AIRG_CUDA(cudaMallocAsync((void**)&r->col, (size_t)(nnz > 0 ? nnz : 1) * sizeof(int), r->stream));
+  AIRG_CUDA(cudaMallocFromPoolAsync((void**)&r->col, (size_t)(nnz > 0 ? nnz : 1) * sizeof(int), lib_pool(), r->stream));
   if (values)
-    AIRG_CUDA(cudaMallocAsync((void**)&r->val, (size_t)(nnz > 0 ? nnz : 1) * sizeof(double),
+    AIRG_CUDA(cudaMallocFromPoolAsync((void**)&r->val, (size_t)(nnz > 0 ? nnz : 1) * sizeof(double), lib_pool(),
                               r->stream));
   return AIRG_OK;
 }

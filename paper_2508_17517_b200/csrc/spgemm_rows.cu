@@ -711,7 +711,7 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
     r->val = oval;
     r->nnz = nnz;
   } else {
-    AIRG_CUDA(cudaMallocAsync((void**)&r->ptr, (size_t)(m + 1) * sizeof(int), s));
+    AIRG_CUDA(cudaMallocFromPoolAsync((void**)&r->ptr, (size_t)(m + 1) * sizeof(int), lib_pool(), s));
     long long fn = 0;
     AIRG_TRY(scan_counts(cnt, r->ptr, m, &fn, s));
     AIRG_TRY(result_alloc_entries(r, fn, true));

@@ -370,7 +370,7 @@ static int ddc_pass_run(int n, const int* ptr, const int* col, const double* val
     size_t b1 = 0, b2 = 0;
     AIRG_CUDA(cub::DeviceReduce::Min(tmp, b1, ratio, mm, nf, s));
     AIRG_CUDA(cub::DeviceReduce::Max(tmp, b2, ratio, mm + 1, nf, s));
-    AIRG_CUDA(cudaMallocAsync(&tmp, b1 > b2 ? b1 : b2, s));
+    AIRG_CUDA(cudaMallocFromPoolAsync(&tmp, b1 > b2 ? b1 : b2, lib_pool(), s));
     AIRG_CUDA(cub::DeviceReduce::Min(tmp, b1, ratio, mm, nf, s));
     AIRG_CUDA(cub::DeviceReduce::Max(tmp, b2, ratio, mm + 1, nf, s));
     const int pb = blocks_for(nf, 256, 1024);
@@ -547,7 +547,7 @@ int airg_strength(int n, const int32_t* ptr, const int32_t* col, const double* v
   airg_csr_result *S = nullptr, *Cl = nullptr;
   AIRG_TRY(strength_closure(n, ptr, col, val, nnz, theta, &S, &Cl, s));
   for (airg_csr_result* r : {S, Cl}) {
-    AIRG_CUDA(cudaMallocAsync((void**)&r->val, (size_t)(r->nnz > 0 ? r->nnz : 1) * sizeof(double), s));
+    AIRG_CUDA(cudaMallocFromPoolAsync((void**)&r->val, (size_t)(r->nnz > 0 ? r->nnz : 1) * sizeof(double), lib_pool(), s));
     fill_ones_kernel<<<blocks_for(r->nnz, 256), 256, 0, s>>>(r->nnz, r->val);
   }
   AIRG_LAUNCH_CHECK();

@@ -73,7 +73,8 @@ def test_distributed_path_on_one_rank_is_the_serial_hierarchy(single_rank):
     n = A.nrows
     xd, sd = S.solve(torch.zeros(n, dtype=torch.float64, device='cuda'),
                      torch.ones(n, dtype=torch.float64, device='cuda'), G.SolveConfig())
-    xs, ss = G.richardson_solve(H, b, np.ones(n), G.SolveConfig())
+    xs, ss = G.richardson_solve(H, b, torch.ones(n, dtype=torch.float64, device='cuda'),
+                                G.SolveConfig())
     hd, hs = np.array(sd.residual_history), np.array(ss.residual_history)
     assert sd.iterations == ss.iterations
     assert np.max(np.abs(hd - hs)) <= 1e-10 * hs[0]

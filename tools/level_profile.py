@@ -7,7 +7,8 @@ import paper_2508_17517_b200 as G
 nx = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
 v = (float(np.cos(np.pi / 4)), float(np.sin(np.pi / 4)))
 A, b = G.build_advection_2d(G.AdvectionProblem(nx=nx, ny=nx, vx=v[0], vy=v[1]))
-for _ in range(2):
+G.reserve_memory(nx * nx * 1600, nx * nx * 4000)
+for _ in range(3):
     H = G.setup(A, G.SetupConfig())
 tot = {}
 for lev in sorted(H.setup_levels):
