@@ -8,8 +8,11 @@
 // use a device-resident multi-kernel path: SpMV, fixed-order dot partials,
 // axpy, with the reorthogonalisation / breakdown decisions taken on the device.
 #include "setup_common.cuh"
+#include <cooperative_groups.h>
 #include <vector>
 #include <cmath>
+
+namespace cg = cooperative_groups;
 
 namespace airg {
 
@@ -345,6 +348,151 @@ static int arnoldi_multi(int n, const int* p, const int* c, const double* v, con
   return AIRG_OK;
 }
 
+// ---- one cooperative kernel for large operators -------------------------
+// The multi-kernel recurrence above (same per-element assignment: NP blocks
+// of 256 threads, grid-stride; warp per row for the SpMV; dot partials per
+// block summed in the dot_finish order), with a grid barrier where a kernel
+// boundary was: H and the basis are bitwise the multi-kernel path's, but an
+// order-m Arnoldi is one launch instead of ~3 m^2 + 10 m.  The dot reduction
+// double-buffers its partials (a block can only rewrite a buffer after the
+// barrier of the next dot).  Decisions (second sweep, breakdown) are taken
+// redundantly by every block from the same reduced values.
+struct ArnoldiGridArgs {
+  int n, m;
+  const int *p, *c;
+  const double* v;
+  const double* b;
+  double beta;
+  double* V;
+  double* w;
+  double* H;     // (m + 1) x m
+  double* parts; // 2 x gridDim.x
+  int* info;     // [0] k
+};
+
+__global__ void __launch_bounds__(256) arnoldi_grid_kernel(ArnoldiGridArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[33];
+  const int tid = threadIdx.x, np = gridDim.x;
+  const long long n = a.n, stride = (long long)np * 256, i0 = (long long)blockIdx.x * 256 + tid;
+  int buf = 0;
+  auto gdot = [&](const double* x, const double* y) -> double {
+    double s = 0.0;
+    for (long long i = i0; i < n; i += stride) s = fma(x[i], y[i], s);
+    s = block_sum(s, red);
+    double* parts = a.parts + (size_t)buf * np;
+    buf ^= 1;
+    if (tid == 0) parts[blockIdx.x] = s;
+    grid.sync();
+    double t = 0.0;
+    for (int i = tid; i < np; i += 256) t += parts[i];
+    return block_sum(t, red);
+  };
+  const int m = a.m;
+  double* V = a.V;
+  double* w = a.w;
+  for (long long i = i0; i < n; i += stride) V[i] = a.b[i] / a.beta;
+  double hmax = 0.0;
+  int k = m;
+  const int lane = tid & 31;
+  const long long warp0 = ((long long)blockIdx.x * 256 + tid) >> 5, nwarps = stride >> 5;
+  for (int j = 0; j < m; ++j) {
+    grid.sync();  // V_j complete
+    const double* Vj = V + (size_t)j * n;
+    for (long long r = warp0; r < n; r += nwarps) {
+      double sacc = 0.0;
+      for (int q = a.p[r] + lane; q < a.p[r + 1]; q += 32) sacc = fma(a.v[q], Vj[a.c[q]], sacc);
+      sacc = warp_sum(sacc);
+      if (lane == 0) w[r] = sacc;
+    }
+    grid.sync();  // w complete
+    const double before2 = gdot(w, w);
+    double hcolj = 0.0;  // unused by blocks > 0
+    double after2 = 0.0;
+    for (int sweep = 0; sweep < 2; ++sweep) {
+      if (sweep == 1 && !(sqrt(after2) < 0.7 * sqrt(before2))) break;
+      for (int q = 0; q <= j; ++q) {
+        const double* Vq = V + (size_t)q * n;
+        const double h = gdot(Vq, w);
+        if (blockIdx.x == 0 && tid == 0) a.H[(size_t)q * m + j] += h;
+        for (long long i = i0; i < n; i += stride) w[i] -= h * Vq[i];
+      }
+      after2 = gdot(w, w);
+    }
+    (void)hcolj;
+    const double hn = sqrt(after2);
+    // column norm of H(:, j) in the control kernel's order
+    grid.sync();  // block 0's H writes visible
+    double cn = 0.0;
+    for (int q = 0; q <= j; ++q) {
+      const double h = a.H[(size_t)q * m + j];
+      cn = __dadd_rn(cn, __dmul_rn(h, h));
+    }
+    cn = __dadd_rn(cn, __dmul_rn(hn, hn));
+    hmax = fmax(hmax, sqrt(cn));
+    if (hn <= 1e-14 * hmax) {  // lucky breakdown
+      k = j + 1;
+      break;
+    }
+    if (blockIdx.x == 0 && tid == 0) a.H[(size_t)(j + 1) * m + j] = hn;
+    double* Vn = V + (size_t)(j + 1) * n;
+    for (long long i = i0; i < n; i += stride) Vn[i] = w[i] / hn;
+  }
+  if (blockIdx.x == 0 && tid == 0) a.info[0] = k;
+}
+
+static int arnoldi_grid(int n, const int* p, const int* c, const double* v, const double* b, int m,
+                        double* H_h, int* k_h, double* beta_h, cudaStream_t s) {
+  double *V = nullptr, *w = nullptr, *sc = nullptr, *Hd = nullptr;
+  int* info = nullptr;
+  const int np = blocks_for(n, 256, 148 * 4);
+  AIRG_TRY(scratch(&V, (size_t)(m + 1) * n, s));
+  AIRG_TRY(scratch(&w, n, s));
+  AIRG_TRY(scratch(&sc, 2 * np + 8, s));
+  AIRG_TRY(scratch(&Hd, (size_t)(m + 1) * m, s));
+  AIRG_TRY(scratch(&info, 2, s));
+  AIRG_CUDA(cudaMemsetAsync(Hd, 0, (size_t)(m + 1) * m * sizeof(double), s));
+  // beta with the multi-kernel dot (same partials, same finish)
+  DotCtx d{sc + 8, np};
+  const Gate always{nullptr, nullptr};
+  double bb = 0;
+  AIRG_TRY(dev_dot(n, b, b, sc, nullptr, d, always, s));
+  AIRG_CUDA(cudaMemcpyAsync(&bb, sc, sizeof(double), cudaMemcpyDeviceToHost, s));
+  AIRG_CUDA(cudaStreamSynchronize(s));
+  const double beta = std::sqrt(bb);
+  *beta_h = beta;
+  if (beta == 0.0) {
+    set_error("cannot build a Krylov space from a zero vector");
+    return AIRG_ERR_VALUE;
+  }
+  ArnoldiGridArgs a{n, m, p, c, v, b, beta, V, w, Hd, sc + 8, info};
+  void* args[] = {&a};
+  AIRG_CUDA(cudaLaunchCooperativeKernel((const void*)arnoldi_grid_kernel, np, 256, args, 0, s));
+  int k = 0;
+  AIRG_CUDA(cudaMemcpyAsync(H_h, Hd, (size_t)(m + 1) * m * sizeof(double), cudaMemcpyDeviceToHost, s));
+  AIRG_CUDA(cudaMemcpyAsync(&k, info, sizeof(int), cudaMemcpyDeviceToHost, s));
+  AIRG_CUDA(cudaStreamSynchronize(s));
+  *k_h = k;
+  for (void* q : {(void*)V, (void*)w, (void*)sc, (void*)Hd, (void*)info}) release(q, s);
+  return AIRG_OK;
+}
+
+// whether the cooperative kernel fits co-resident (it always does on B200:
+// at most 592 blocks of 256 threads); otherwise the multi-kernel path
+static bool grid_arnoldi_ok(int n) {
+  static int max_blocks = -1;
+  if (max_blocks < 0) {
+    int per_sm = 0, dev = 0, coop = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    if (!coop ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arnoldi_grid_kernel, 256, 0) != cudaSuccess)
+      per_sm = 0;
+    max_blocks = per_sm * num_sms();
+  }
+  return !getenv("AIRG_ARNOLDI_MULTI") && blocks_for(n, 256, 148 * 4) <= max_blocks;
+}
+
 }  // namespace airg
 
 using namespace airg;
@@ -382,7 +530,8 @@ extern "C" int airg_arnoldi(int n, const int32_t* p, const int32_t* c, const dou
     }
     *k_h = hi[0];
   } else {
-    st = arnoldi_multi(n, p, c, v, b, m, H_h, k_h, beta_h, s);
+    st = grid_arnoldi_ok(n) ? arnoldi_grid(n, p, c, v, b, m, H_h, k_h, beta_h, s)
+                            : arnoldi_multi(n, p, c, v, b, m, H_h, k_h, beta_h, s);
     if (st != AIRG_OK) return st;
   }
   // numerically zero on the Krylov space? (polynomial.py:108-109)

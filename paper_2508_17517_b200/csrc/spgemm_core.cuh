@@ -180,6 +180,19 @@ __device__ void warp_radix_sort(int* k, V* v, int* k2, V* v2, int n, int* cnt, i
   }
 }
 
+// Predicated global loads straight into the destination register (value
+// kept when the predicate is off).  Written as PTX so the compiler cannot
+// load into a temporary and move it to the destination, which would wait
+// for the load and defeat a software-pipelined walk.
+__device__ __forceinline__ void ld_pred(int& v, const int* p, bool pr) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.nc.b32 %0, [%1];\n\t}"
+               : "+r"(v) : "l"(p), "r"((int)pr));
+}
+__device__ __forceinline__ void ld_pred(double& v, const double* p, bool pr) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.nc.f64 %0, [%1];\n\t}"
+               : "+d"(v) : "l"(p), "r"((int)pr));
+}
+
 __host__ __device__ __forceinline__ int ceil_log2(long long x) {
   int b = 0;
   while ((1ll << b) < x) ++b;

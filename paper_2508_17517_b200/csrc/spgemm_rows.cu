@@ -461,18 +461,33 @@ __global__ void numeric_class_kernel(int m, const int* __restrict__ Cp,
 }
 
 template <int NW, int KP, int D>
-static int launch_span_numeric_t(const SpanNumArgs& a, cudaStream_t s) {
+static int launch_span_numeric_nw(const SpanNumArgs& a, cudaStream_t s) {
   const size_t shm = span_num_bytes(a.ncap) * NW;
-  static bool attr = false;
-  if (!attr) {
+  static size_t attr = 0;
+  if (shm > attr) {
     AIRG_CUDA(cudaFuncSetAttribute(span_numeric_kernel<NW, KP, D>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)span_num_bytes(kSpanNmax) * NW));
-    attr = true;
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    attr = shm;
   }
   span_numeric_kernel<NW, KP, D><<<blocks_for(a.nrows, NW, 148 * 64), 32 * NW, shm, s>>>(a);
   AIRG_LAUNCH_CHECK();
   return AIRG_OK;
+}
+
+// warps per CTA: consecutive output rows share most B rows, so the warps of
+// one CTA (same SM, same L1) take consecutive rows; as many as fit in
+// shared memory up to AIRG_SPAN_NW (measurement knob)
+template <int KP, int D>
+static int launch_span_numeric_t(const SpanNumArgs& a, cudaStream_t s) {
+  static const int nw_max = getenv("AIRG_SPAN_NW") ? atoi(getenv("AIRG_SPAN_NW")) : 2;
+  int nw = nw_max;
+  while (nw > 1 && span_num_bytes(a.ncap) * nw > 200 * 1024) nw >>= 1;
+  switch (nw) {
+    case 8: return launch_span_numeric_nw<8, KP, D>(a, s);
+    case 4: return launch_span_numeric_nw<4, KP, D>(a, s);
+    case 2: return launch_span_numeric_nw<2, KP, D>(a, s);
+    default: return launch_span_numeric_nw<1, KP, D>(a, s);
+  }
 }
 
 // B-row prefetch shape kd = 10 KP + D (KP x 32 entries, D steps ahead);
@@ -485,9 +500,8 @@ static int launch_span_numeric(SpanNumArgs a, int ncap, int kd, cudaStream_t s) 
     kd = kp * 10 + d;
   }
   switch (kd) {
-    case 42: return launch_span_numeric_t<2, 4, 2>(a, s);
-    case 82: return launch_span_numeric_t<2, 8, 2>(a, s);
-    default: return launch_span_numeric_t<2, 4, 4>(a, s);
+    case 82: return launch_span_numeric_t<8, 2>(a, s);
+    default: return launch_span_numeric_t<4, 4>(a, s);
   }
 }
 

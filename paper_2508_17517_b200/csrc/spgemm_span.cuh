@@ -36,19 +36,6 @@ constexpr int kSpanNmax = 4096;              // longest output row handled here
 // land on distinct bit positions)
 __device__ __forceinline__ unsigned flag_nibble(unsigned x) { return (x * 0x10204080u) >> 28; }
 
-// Predicated global loads straight into the destination register (value
-// kept when the predicate is off).  Written as PTX so the compiler cannot
-// load into a temporary and move it to the destination, which would wait
-// for the load and defeat the software pipeline below.
-__device__ __forceinline__ void ld_pred(int& v, const int* p, bool pr) {
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.nc.b32 %0, [%1];\n\t}"
-               : "+r"(v) : "l"(p), "r"((int)pr));
-}
-__device__ __forceinline__ void ld_pred(double& v, const double* p, bool pr) {
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.nc.f64 %0, [%1];\n\t}"
-               : "+d"(v) : "l"(p), "r"((int)pr));
-}
-
 // rank of window offset `off` in the bitmap (prefix, bits) pairs
 __device__ __forceinline__ int span_rank(const uint2* bm, unsigned off) {
   const uint2 e = bm[off >> 5];

@@ -424,3 +424,23 @@ def test_gpu_setup_replayed_by_oracle_512():
     xo, hist, conv, its = O.richardson(Ho, np.zeros(Ao.nrows), np.ones(Ao.nrows))
     assert st.iterations == its
     assert np.max(np.abs(np.array(st.residual_history) - hist)) <= 1e-10 * hist[0]
+
+
+@pytest.mark.parametrize('order', [6, 40])
+def test_grid_arnoldi_bitwise_multi_kernel(G, order):
+    """The one-launch cooperative Arnoldi (operators > 4096 rows) computes the
+    multi-kernel recurrence with the same per-element assignment and
+    reduction order: H, k and beta bitwise equal."""
+    import os
+    from paper_2508_17517_b200.csr import random_unit_vector
+    from paper_2508_17517_b200.gmres_poly import hessenberg
+    A, _ = G.build_advection_2d(G.AdvectionProblem(nx=120, ny=110, vx=HARD[0], vy=HARD[1]))
+    b = random_unit_vector(A.nrows, 3)
+    H1, k1, b1 = hessenberg(A, order + 1, b)
+    os.environ['AIRG_ARNOLDI_MULTI'] = '1'
+    try:
+        H2, k2, b2 = hessenberg(A, order + 1, b)
+    finally:
+        del os.environ['AIRG_ARNOLDI_MULTI']
+    assert (k1, b1) == (k2, b2)
+    assert H1.tobytes() == H2.tobytes()
