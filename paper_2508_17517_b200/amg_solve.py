@@ -179,6 +179,12 @@ class plan_for:
         return False
 
 
+def held_plan(H, exact=False):
+    """A plan of H's pool taken for good (measurement tools that drive the
+    native plan directly)."""
+    return _pool(H).acquire(H, exact)
+
+
 def coarse_mode(H):
     """'dense' when the fast-mode coarse solve of H's plans is the dense q(A)
     GEMV, 'newton' otherwise (after a solve has built a plan)."""

@@ -60,6 +60,12 @@ struct Epi {
   const int* vmap;
   double* acc;      // optional: acc[o] += value
   double* partial;  // optional: per-block sum of squares of value
+  // optional independent scatter done by the same launch (saves a kernel):
+  // sc_dst[sc_idx[i]] = sc_src[i], i < sc_n
+  const double* sc_src = nullptr;
+  const int* sc_idx = nullptr;
+  double* sc_dst = nullptr;
+  long long sc_n = 0;
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
@@ -145,6 +151,11 @@ __global__ void __launch_bounds__(256) spmv_vec_kernel(int nrows, const int* __r
                                                        const double* __restrict__ x, double xs,
                                                        Epi ep) {
   pdl_enter();
+  if (ep.sc_n) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < ep.sc_n;
+         i += (long long)gridDim.x * blockDim.x)
+      ep.sc_dst[ep.sc_idx[i]] = ep.sc_src[i];
+  }
   const int lane = threadIdx.x & (VS - 1);
   const long long row = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / VS;
   double s = 0.0;
@@ -578,7 +589,9 @@ __global__ void __launch_bounds__(1024) newton_smem_kernel(
       nrm = 1.0;  // max|u/nrm| == 1 exactly
       __syncthreads();
       if (!isfinite(scale) || scale == 0.0) {
-        if (stopped && tid == 0) atomicOr(stopped, 1);
+        // scale underflowing to 0 only drops terms that would add 0 * u;
+        // an infinite scale drops real terms
+        if (stopped && tid == 0) atomicOr(stopped, isfinite(scale) ? 2 : 1);
         break;
       }
     }
@@ -1311,7 +1324,7 @@ static int build_dense_coarse(airg_plan* p, cudaStream_t s) {
   int stopped = 0;
   AIRG_CUDA(cudaMemcpyAsync(&stopped, p->iflag, sizeof(int), cudaMemcpyDeviceToHost, s));
   AIRG_CUDA(cudaStreamSynchronize(s));
-  if (stopped) {  // the reference stops per right-hand side (polynomial.py:312-355)
+  if (stopped & 1) {  // the reference stops per right-hand side (polynomial.py:312-355)
     dfree(p->coarseQ);
     p->coarseQ = nullptr;
     p->dense_state = -1;
@@ -1351,16 +1364,21 @@ static int vcycle_rec(airg_plan* p, int level, const double* r, double* e, int f
     AIRG_TRY(launch_spmv(L.R, r, 1.0, ep, s, p->exact));
   }
   AIRG_TRY(vcycle_rec(p, level + 1, L.rc, L.ec, fits, s));
-  // rhs = r[f] - A_fc e_c
+  // rhs = r[f] - A_fc e_c, and (same launch) the scatter e[c] = e_c
   {
     Epi ep{L.rhs, nullptr, -1.0, 1.0, r, L.f_idx, nullptr, nullptr};
+    ep.sc_src = L.ec;
+    ep.sc_idx = L.c_idx;
+    ep.sc_dst = e;
+    ep.sc_n = L.Afc.nrows > 0 ? L.n_c : 0;
     AIRG_TRY(launch_spmv(L.Afc, L.ec, 1.0, ep, s, p->exact));
+    if (L.Afc.nrows == 0)
+      AIRG_TRY(launch_axpby(L.n_c, e, L.c_idx, 1.0, L.ec, nullptr, 0.0, nullptr, s, p->exact));
   }
   if (fits == 1 && !L.has_asm && L.sm.kind == 0) {
     // e[f] = q(A_ff) rhs written straight through f_idx by the last Horner step
     AIRG_TRY(poly_apply_dev(L.sm, L.Aff, L.rhs, e, L.t0, L.t1, L.t2, L.t2, p->iflag, p->parts,
                             p->nst, s, p->exact, L.f_idx));
-    AIRG_TRY(launch_axpby(L.n_c, e, L.c_idx, 1.0, L.ec, nullptr, 0.0, nullptr, s, p->exact));
     return AIRG_OK;
   }
   AIRG_TRY(smooth_level(p, L, L.rhs, L.ef, s));
@@ -1376,9 +1394,8 @@ static int vcycle_rec(airg_plan* p, int level, const double* r, double* e, int f
     AIRG_TRY(launch_axpby(L.n_f, L.ef, nullptr, 1.0, L.ef, nullptr, 1.0, corr, s, p->exact));
     release(tmp, s);
   }
-  // scatter e[f] = ef, e[c] = ec
+  // scatter e[f] = ef (e[c] = ec went with the A_fc launch)
   AIRG_TRY(launch_axpby(L.n_f, e, L.f_idx, 1.0, L.ef, nullptr, 0.0, nullptr, s, p->exact));
-  AIRG_TRY(launch_axpby(L.n_c, e, L.c_idx, 1.0, L.ec, nullptr, 0.0, nullptr, s, p->exact));
   return AIRG_OK;
 }
 

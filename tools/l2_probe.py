@@ -6,7 +6,7 @@ import sys, os, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2508_17517_b200 as G
-from paper_2508_17517_b200.amg_solve import plan_for
+from paper_2508_17517_b200.amg_solve import held_plan
 from paper_2508_17517_b200 import _lib as L
 
 nx = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
@@ -44,7 +44,7 @@ for i, lv in enumerate(H.levels):
                      warm_us=round(tw * 1e3, 1), cold_gbs=round(byt / tc / 1e6), warm_gbs=round(byt / tw / 1e6)))
     print(json.dumps(rows[-1]), flush=True)
 
-p = plan_for(H)
+p = held_plan(H)
 r = torch.randn(A.nrows, dtype=torch.float64, device='cuda'); e = torch.empty_like(r)
 for _ in range(3):
     L.call('airg_plan_vcycle', p.h, 0, L.ptr(r), L.ptr(e), 1, L.stream_handle())

@@ -3,7 +3,7 @@ import sys, time, json
 sys.path.insert(0, '.')
 import numpy as np, torch
 import paper_2508_17517_b200 as G
-from paper_2508_17517_b200.amg_solve import plan_for, count_cycle_bytes
+from paper_2508_17517_b200.amg_solve import held_plan, count_cycle_bytes
 nx = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
 order = int(sys.argv[2]) if len(sys.argv) > 2 else 6
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
@@ -19,7 +19,7 @@ for rep in range(reps):
                       'levels': H.num_levels, 'trunc': H.truncated_at, 'cc': H.cycle_complexity,
                       'breakdown': {k: round(v, 4) for k, v in H.setup_breakdown.items()}}), flush=True)
 # V-cycle timing
-p = plan_for(H)
+p = held_plan(H)
 r = torch.randn(A.nrows, dtype=torch.float64, device='cuda')
 e = torch.empty_like(r)
 from paper_2508_17517_b200 import _lib as L
