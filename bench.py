@@ -10,7 +10,8 @@ default AIRG config (order-6 GMRES polynomial smoothers, order-100 Newton
 coarse solver, automatic truncation).
 
 value = DOFs / (setup s + solve s).  At N>1 the job is ONE global problem of
-2048 x (2048 N) grid points split into N row strips of 2048^2 (weak scaling):
+4096 x (4096 N) grid points split into N row strips of 4096^2 -- BASELINE.json
+configs[2], ~16.8M DOFs per GPU (weak scaling; --nx sets the strip size):
 distributed setup + native distributed Richardson with NCCL halo exchanges
 (paper_2508_17517_b200/dist.py), step time = max over ranks.  Inputs are
 resident in HBM before the timed region; every level operator of the
@@ -41,9 +42,17 @@ def parse():
     ap.add_argument('--steps', type=int, default=5)
     ap.add_argument('--warmup', type=int, default=3)
     ap.add_argument('--impl', default='ours', choices=['ours', 'reference'])
-    ap.add_argument('--nx', type=int, default=2048)
+    ap.add_argument('--nx', type=int, default=None,
+                    help='grid points per side per GPU (default: 2048 at N=1, configs[1]; '
+                         '4096 at N>1, configs[2]: ~16.8M DOFs per GPU)')
     ap.add_argument('--order', type=int, default=6)
-    ap.add_argument('--cpu-nx', type=int, default=256, help='CPU baseline sample grid')
+    ap.add_argument('--truncate-start', type=int, default=None,
+                    help='SetupConfig.auto_truncate_start_level (configs[3]: a low start, e.g. 4, '
+                         'gives a large coarsest grid solved by the order-100 Newton polynomial)')
+    ap.add_argument('--cpu-nx', type=int, default=512,
+                    help='CPU sample grid (reference arm and cpu_baseline): 512^2, whose per-DOF '
+                         'cost is within ~2x of the 2048^2 run; the full 2048^2 reference run '
+                         'takes ~19 min (profiles/)')
     ap.add_argument('--no-cpu', action='store_true')
     ap.add_argument('--problem', default='fd', choices=['fd', 'dg'],
                     help='fd: 2-D upwind finite differences (configs[1]); dg: upwind DG Q1 on '
@@ -95,20 +104,22 @@ def cpu_cores_note():
 
 
 def _ref_worker(job):
-    """One reference instance: W warm-up + K timed setup/solve runs on the
-    sample (one BLAS thread; scipy's sparse kernels are single-threaded)."""
+    """One reference instance: a small warm-up run (module import, caches;
+    when W > 0) and `steps` timed setup/solve runs on the sample (one BLAS
+    thread; scipy's sparse kernels are single-threaded)."""
     nx, order, problem, warmup, steps = job
     try:
         from threadpoolctl import threadpool_limits
         threadpool_limits(1)
     except Exception:
         pass
+    if warmup:
+        cpu_run(min(nx, 64), order, problem)
     setup_s, solve_s, its = [], [], 0
-    for i in range(warmup + steps):
+    for _ in range(steps):
         a, b, its = cpu_run(nx, order, problem)
-        if i >= warmup:
-            setup_s.append(a)
-            solve_s.append(b)
+        setup_s.append(a)
+        solve_s.append(b)
     return float(np.mean(setup_s)), float(np.mean(solve_s)), its
 
 
@@ -121,7 +132,10 @@ def reference_arm(args, rank, world):
         return 0
     problem = getattr(args, 'problem', 'fd')
     procs = int(os.environ.get('AIRG_REF_PROCS', os.cpu_count() or 1))
-    job = (args.cpu_nx, args.order, problem, args.warmup, args.steps)
+    # the K timed steps are spread over the concurrent instances (at least one
+    # each), so the run takes about one sample's time, not K of them
+    per = max(1, -(-args.steps // procs))
+    job = (args.cpu_nx, args.order, problem, args.warmup, per)
     if procs > 1:
         import multiprocessing as mp
         with mp.get_context('fork').Pool(procs) as pool:
@@ -146,8 +160,8 @@ def reference_arm(args, rank, world):
         'setup_s': float(np.mean([a for a, _, _ in res])),
         'solve_s': float(np.mean([b for _, b, _ in res])), 'iterations': its,
         'cpu_baseline': {'value': v, 'unit': 'DOF/s', 'cores': procs, 'kind': 'port',
-                         'sample': f'{procs} concurrent instances (one per host core) of '
-                                   f'setup + solve at {args.cpu_nx}^2 of the {args.nx}^2 workload '
+                         'sample': f'{procs} concurrent instances (one per host core), {per} timed '
+                                   f'setup + solve each at {args.cpu_nx}^2 of the {args.nx}^2 workload '
                                    f'(oracle/airg_oracle.py = numpy/scipy restatement of airmg, '
                                    f'pinned bitwise to it; scipy sparse kernels single-threaded, '
                                    f'1 BLAS thread per instance; host has {ncpu} cpus); value = '
@@ -305,7 +319,7 @@ class SerialWorkload:
         import paper_2508_17517_b200 as G
         self.G, self.args = G, args
         nx = args.nx
-        self.cfg = G.SetupConfig(poly_order=args.order)
+        self.cfg = G.SetupConfig(poly_order=args.order, auto_truncate_start_level=args.truncate_start)
         self.scfg = G.SolveConfig()
         prob = G.AdvectionProblem(nx=nx, ny=nx, vx=PI4[0], vy=PI4[1])
         if args.problem == 'dg':
@@ -316,6 +330,10 @@ class SerialWorkload:
             self.A, self.b = G.build_advection_2d(prob)
             self.workload = (f'AIRG pi/4 advection {nx}x{nx}, order {args.order}, default '
                              'SetupConfig (BASELINE.json configs[1])')
+            if args.truncate_start is not None:
+                self.workload = (f'AIRG pi/4 advection {nx}x{nx}, order {args.order}, truncation '
+                                 f'start level {args.truncate_start}: order-100 Newton coarse '
+                                 'solver on a large coarsest grid (BASELINE.json configs[3])')
         self.n = self.n_total = self.A.nrows
         self.x0 = torch.ones(self.n, dtype=torch.float64, device='cuda')
         self.parallelism = 'single GPU'
@@ -414,7 +432,7 @@ class DistWorkload:
         self.G, self.D, self.args = G, D, args
         self.comm = D.Comm()
         nx = args.nx
-        self.cfg = G.SetupConfig(poly_order=args.order)
+        self.cfg = G.SetupConfig(poly_order=args.order, auto_truncate_start_level=args.truncate_start)
         self.scfg = G.SolveConfig()
         # the inflow strip builds ~12 % less work per row (measured at N = 2
         # and 4, tools/dist_kprof.py): it gets proportionally more grid rows
@@ -426,7 +444,10 @@ class DistWorkload:
         self.b = torch.zeros(self.n, dtype=torch.float64, device='cuda')
         self.x0 = torch.ones(self.n, dtype=torch.float64, device='cuda')
         self.workload = (f'AIRG pi/4 advection {nx}x{nx * world} global grid ({world} row strips '
-                         f'of {nx}x{nx}), order {args.order}, default SetupConfig')
+                         f'of {nx}x{nx}), order {args.order}, '
+                         + ('default SetupConfig (BASELINE.json configs[2] weak scaling)'
+                            if args.truncate_start is None else
+                            f'truncation start level {args.truncate_start} (BASELINE.json configs[3])'))
         self.parallelism = (f'row-strip domain decomposition over {world} GPUs, NCCL halo '
                             'exchanges; replicated coarse tail')
 
@@ -627,6 +648,8 @@ def ours_arm(args, rank, world, local):
 def main():
     args = parse()
     rank, world, local = dist_env()
+    if args.nx is None:  # BASELINE configs[1] on one GPU, configs[2] (weak scaling) on N
+        args.nx = 2048 if world == 1 else 4096
     if args.impl == 'reference':
         return reference_arm(args, rank, world)
     return ours_arm(args, rank, world, local)

@@ -7,6 +7,7 @@ import os
 import socket
 
 import numpy as np
+import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -20,12 +21,12 @@ def _free_port():
     return p
 
 
-def _global_csr(n, seed=3):
+def _global_csr(n, seed=3, kmax=6):
     """A random global CSR (sorted columns, every row non-empty)."""
     rng = np.random.default_rng(seed)
     ptr, col, val = [0], [], []
     for i in range(n):
-        k = int(rng.integers(1, 6))
+        k = int(rng.integers(1, kmax))
         c = np.unique(np.concatenate([[i], rng.integers(0, n, size=k)]))
         col.extend(c.tolist())
         val.extend((1000.0 * i + c).tolist())
@@ -41,25 +42,30 @@ def _worker(rank, world, port, out):
         from paper_2508_17517_b200.csr import SparseMatrix
         cpu = torch.device('cpu')
         comm = D.Comm(device=cpu)
-        n = 37
-        counts = [17, 20]
+        # uneven strips (world 2: 17 + 20 rows; world 8: 5..16 rows)
+        counts = [17, 20] if world == 2 else [5 + (3 * r) % 12 for r in range(world)]
+        n = sum(counts)
         part = D.Part.from_counts(counts, cpu)
         lo, hi = part.lo(rank), part.hi(rank)
         # owner lookup
         g = torch.arange(n)
-        assert part.owner(g).tolist() == [0] * 17 + [1] * 20
+        assert part.owner(g).tolist() == sum(([r] * c for r, c in enumerate(counts)), [])
         # collectives
-        assert comm.allgather_int(rank + 5) == [5, 6]
-        assert comm.sum_int(rank + 1) == 3
+        assert comm.allgather_int(rank + 5) == [5 + r for r in range(world)]
+        assert comm.sum_int(rank + 1) == world * (world + 1) // 2
         v = torch.arange(lo, hi, dtype=torch.float64)
         assert comm.allgather_v(v).tolist() == list(range(n))
-        # the global matrix; this rank's rows with global column ids
-        P, C, V = _global_csr(n)
+        # the global matrix; this rank's rows with global column ids (columns
+        # drawn from the whole range: every rank couples to every other, the
+        # all-to-all pattern of the coarse levels at 8 ranks)
+        P, C, V = _global_csr(n, kmax=6 if world == 2 else 14)
         lp = torch.tensor(P[lo:hi + 1] - P[lo], dtype=torch.int32)
         lc = torch.tensor(C[P[lo]:P[hi]], dtype=torch.int32)
         lv = torch.tensor(V[P[lo]:P[hi]], dtype=torch.float64)
         M = SparseMatrix(hi - lo, n, lp, lc, lv)
         need = D.remote_cols(M.col_indices, part, rank)
+        if world == 8:  # the case exercises all-to-all couplings
+            assert set(part.owner(need).tolist()) == set(range(world)) - {rank}
         expect_need = sorted({int(c) for c in lc.tolist() if not lo <= c < hi})
         assert need.tolist() == expect_need
         halo = D.Halo(comm, part, need)
@@ -90,7 +96,7 @@ def _worker(rank, world, port, out):
         R = D.cat_rows(M, gp, gc, gv, n)
         assert R.nrows == (hi - lo) + len(expect_need)
         # batched plans (one all-gather + one all-to-all) == one plan per item
-        part2 = D.Part.from_counts([30, 7], cpu)
+        part2 = D.Part.from_counts([30, 7] if world == 2 else counts[::-1], cpu)
         rng = np.random.default_rng(11 + rank)
         lo2, hi2 = part2.lo(rank), part2.hi(rank)
         need2 = torch.tensor(sorted({int(c) for c in rng.integers(0, n, 25)
@@ -114,12 +120,15 @@ def _worker(rank, world, port, out):
         dist.destroy_process_group()
 
 
-def test_halo_exchange_gloo_world2():
+@pytest.mark.parametrize('world', [2, 8])
+def test_halo_exchange_gloo(world):
+    """Partitions, halos (ghost values and ghost rows), batched halo plans and
+    [local | ghost] renumbering at 2 and 8 ranks."""
     port = _free_port()
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(2, port, out), nprocs=2, join=True)
-    assert dict(out) == {0: 'ok', 1: 'ok'}, dict(out)
+    mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
+    assert dict(out) == {r: 'ok' for r in range(world)}, dict(out)
 
 
 def test_stable_buckets_is_a_stable_sort_by_owner():

@@ -90,3 +90,16 @@ def test_two_gpu_strips_match_serial():
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=420)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert 'DIST OK world=2' in r.stdout + r.stderr
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 4,
+                    reason='needs four GPUs')
+def test_four_gpu_strips_match_serial():
+    """4 ranks: the coarse levels couple non-adjacent strips; hierarchy bitwise
+    the serial one under injection, solve within 1e-10 (tools/dist_check.py)."""
+    cmd = [sys.executable, '-m', 'torch.distributed.run', '--nnodes=1', '--nproc-per-node', '4',
+           '--master-addr', '127.0.0.1', '--master-port', str(_free_port()),
+           os.path.join(ROOT, 'tools', 'dist_check.py'), '256', '1500', 'weighted']
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert 'DIST OK world=4' in r.stdout + r.stderr
