@@ -424,14 +424,15 @@ static int gather_ll(const long long* d, const std::vector<int>& rows, std::vect
 
 // count-pass class of a row: span path (window <= 4096 / <= 16384 columns)
 // or the hash classes by product upper bound
-enum { kCntHash64 = 0, kCntSpan4k = 1, kCntSpan16k = 2, kCntHash512 = 3, kCntHashBlk = 4, kCntClasses = 5 };
+enum { kCntHash64 = 0, kCntSpan4k = 1, kCntSpan16k = 2, kCntHash512 = 3, kCntHashBlk = 4,
+       kCntSpan64k = 5, kCntClasses = 6 };
 
 __global__ void count_class_kernel(int m, const long long* __restrict__ ub,
                                    const long long* __restrict__ words, int* __restrict__ ids) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
        i += (long long)gridDim.x * blockDim.x) {
     const long long w = words[i], u = ub[i];
-    ids[i] = w > 0 ? (w * 32 <= 4096 ? kCntSpan4k : kCntSpan16k)
+    ids[i] = w > 0 ? (w * 32 <= 4096 ? kCntSpan4k : w * 32 <= 16384 ? kCntSpan16k : kCntSpan64k)
                    : (u <= 64 ? kCntHash64 : u <= 512 ? kCntHash512 : kCntHashBlk);
   }
 }
@@ -462,7 +463,7 @@ __global__ void numeric_class_kernel(int m, const int* __restrict__ Cp,
 
 template <int NW, int KP, int D>
 static int launch_span_numeric_nw(const SpanNumArgs& a, cudaStream_t s) {
-  const size_t shm = span_num_bytes(a.ncap) * NW;
+  const size_t shm = span_num_bytes(a.ncap, a.wcap) * NW;
   static size_t attr = 0;
   if (shm > attr) {
     AIRG_CUDA(cudaFuncSetAttribute(span_numeric_kernel<NW, KP, D>,
@@ -481,7 +482,7 @@ template <int KP, int D>
 static int launch_span_numeric_t(const SpanNumArgs& a, cudaStream_t s) {
   static const int nw_max = getenv("AIRG_SPAN_NW") ? atoi(getenv("AIRG_SPAN_NW")) : 2;
   int nw = nw_max;
-  while (nw > 1 && span_num_bytes(a.ncap) * nw > 200 * 1024) nw >>= 1;
+  while (nw > 1 && span_num_bytes(a.ncap, a.wcap) * nw > 200 * 1024) nw >>= 1;
   switch (nw) {
     case 8: return launch_span_numeric_nw<8, KP, D>(a, s);
     case 4: return launch_span_numeric_nw<4, KP, D>(a, s);
@@ -540,13 +541,13 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
   AIRG_TRY(scratch(&bmoff, m + 1, s));
   AIRG_TRY(scratch(&ids, m, s));
   unsigned long long* tot = nullptr;
-  AIRG_TRY(scratch(&tot, 2, s));
-  AIRG_CUDA(cudaMemsetAsync(tot, 0, 2 * sizeof(unsigned long long), s));
+  AIRG_TRY(scratch(&tot, 3, s));
+  AIRG_CUDA(cudaMemsetAsync(tot, 0, 3 * sizeof(unsigned long long), s));
   if (m > 0)
     span_ub_kernel<8><<<blocks_for((long long)m * 8, 256), 256, 0, s>>>(m, A.p, A.c, B.p, B.c, ub,
                                                                          cmin, words, span_min_ub(), tot);
   AIRG_LAUNCH_CHECK();
-  unsigned long long tot_h[2] = {0, 0};
+  unsigned long long tot_h[3] = {0, 0, 0};
   AIRG_CUDA(cudaMemcpyAsync(tot_h, tot, sizeof(tot_h), cudaMemcpyDeviceToHost, s));
   long long totw = 0;
   AIRG_TRY(scan_counts64(words, bmoff, m, &totw, s));  // synchronises (tot_h too)
@@ -571,9 +572,10 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
     for (int c = 0; c < kCntClasses; ++c) {
       const int nr = cl.count[c];
       if (!nr) continue;
-      if (c == kCntSpan4k || c == kCntSpan16k) {
+      if (c == kCntSpan4k || c == kCntSpan16k || c == kCntSpan64k) {
         SpanCountArgs a{A.p, A.c, B.p, B.c, cl.list(c), nr, cmin, words, bmoff, gbm, cnt};
         if (c == kCntSpan4k) AIRG_TRY((launch_span_count<128>(a, 4096, fk.stream(c))));
+        else if (c == kCntSpan16k) AIRG_TRY((launch_span_count<256>(a, 16384, fk.stream(c))));
         else AIRG_TRY((launch_span_count<256>(a, kSpanMax, fk.stream(c))));
         continue;
       }
@@ -646,8 +648,8 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
     for (int c = 0; c < kNumSpanCls; ++c) {
       const int nr = cl.count[c];
       if (!nr) continue;
-      SpanNumArgs a{A.p, A.c, A.v, B.p, B.c, B.v, cl.list(c), nr, 0, cmin, words, bmoff, gbm, Cp,
-                    ocol, oval, negate, mode, tol, lump, cnt, anyd, row0};
+      SpanNumArgs a{A.p, A.c, A.v, B.p, B.c, B.v, cl.list(c), nr, 0, (int)tot_h[2], cmin, words, bmoff,
+                    gbm, Cp, ocol, oval, negate, mode, tol, lump, cnt, anyd, row0};
       AIRG_TRY(launch_span_numeric(a, kSpanCaps[c], span_kd, fk.stream(c)));
     }
     const int cbits[7] = {6, 8, 10, 11, 12, 13, 14}, cwarps[2] = {8, 8};

@@ -28,7 +28,8 @@
 
 namespace airg {
 
-constexpr int kSpanMax = 16384;              // window columns handled here
+constexpr int kSpanMax = 65536;              // window columns handled here (the 4096^2
+                                             // hierarchy's windows reach ~30k)
 constexpr int kSpanWords = kSpanMax / 32;    // bitmap words per row (max)
 constexpr int kSpanNmax = 4096;              // longest output row handled here
 
@@ -81,9 +82,10 @@ __global__ void span_ub_kernel(int m, const int* __restrict__ Ap, const int* __r
       const bool use = s >= span_min_ub && span > 0 && span <= kSpanMax && span <= 32 * s &&
                        s >= 8ll * (ae - ab);
       words[r] = use ? (span + 31) / 32 : 0;
-      if (use) {  // products and steps of the span rows (B-row prefetch shape)
+      if (use) {  // products and steps of the span rows (B-row prefetch shape), widest window
         atomicAdd(totals, (unsigned long long)s);
         atomicAdd(totals + 1, (unsigned long long)(ae - ab));
+        atomicMax(totals + 2, (unsigned long long)((span + 31) / 32));
       }
     }
   }
@@ -307,6 +309,7 @@ struct SpanNumArgs {
   const int* rows;
   int nrows;
   int ncap;  // longest output row of this launch (sizes the accumulators)
+  int wcap;  // widest window of this product in bitmap words (sizes the bitmap)
   const int* cmin;
   const long long* words;
   const long long* bmoff;
@@ -325,8 +328,8 @@ struct SpanNumArgs {
 
 // shared memory per warp of the numeric kernel: bitmap (prefix, bits) pairs,
 // ncap + 1 accumulators (the last one the dummy slot), the drop mask
-__host__ __device__ __forceinline__ size_t span_num_bytes(int ncap) {
-  return ((size_t)kSpanWords * sizeof(uint2) + (size_t)(ncap + 2) * sizeof(double) +
+__host__ __device__ __forceinline__ size_t span_num_bytes(int ncap, int wcap) {
+  return ((size_t)wcap * sizeof(uint2) + (size_t)(ncap + 2) * sizeof(double) +
           (size_t)(ncap / 32 + 1) * sizeof(unsigned) + 15) & ~(size_t)15;
 }
 
@@ -439,9 +442,9 @@ template <int NW, int KP, int D>
 __global__ void __launch_bounds__(32 * NW) span_numeric_kernel(SpanNumArgs a) {
   extern __shared__ uint4 span_smem4[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  unsigned char* base = (unsigned char*)span_smem4 + (size_t)w * span_num_bytes(a.ncap);
+  unsigned char* base = (unsigned char*)span_smem4 + (size_t)w * span_num_bytes(a.ncap, a.wcap);
   uint2* bm = (uint2*)base;
-  double* acc = (double*)(base + (size_t)kSpanWords * sizeof(uint2));
+  double* acc = (double*)(base + (size_t)a.wcap * sizeof(uint2));
   unsigned* dm = (unsigned*)(acc + a.ncap + 2);
   for (long long t = (long long)blockIdx.x * NW + w; t < a.nrows; t += (long long)gridDim.x * NW) {
     const int row = a.rows[t];

@@ -3,16 +3,16 @@ csr_matmat semantics, sparse.py:222-240) -- plain products and the fused
 drop/lump epilogue (sparse.py:307-352) of the Galerkin product.
 
 The library routes each output row by its column window and length:
-  count:   hash set (<= 64 products), span bitmap (window <= 4096 / <= 16384
-           columns), hash set (<= 512 products), CTA hash set (longer),
+  count:   hash set (<= 64 products), span bitmap (window <= 4096 / <= 16384 /
+           <= 65536 columns), hash set (<= 512 products), CTA hash set (longer),
            global tables (overflow);
   numeric: span path by output length (<= 256 ... <= 4096), hash warp per
            row (<= 32, <= 128), CTA per row (<= 512 ... <= 8192), global
            tables (> 8192).
 The synthetic rows below are built so every one of these classes receives
 rows: each A row owns private B rows whose columns are drawn from a pool of
-about L columns inside a window of W columns (W <= 16384 -> span path,
-W > 16384 -> hash path), values from a small set so that sums cancel exactly
+about L columns inside a window of W columns (W <= 65536 -> span path,
+W > 65536 -> hash path), values from a small set so that sums cancel exactly
 (structural zeros) and magnitudes from 1e-12 to 1 so that the drop rule
 fires."""
 
@@ -90,18 +90,20 @@ def _drop_lump_rows(M, tol, lump):
 CASES = [
     ('hash<=32', 300, 24, 200, 6, 8),
     ('hash<=128', 200, 100, 600, 8, 8),
-    ('hash512cnt', 100, 300, 30000, 4, 100),
+    ('hash512cnt', 100, 300, 90000, 4, 100),
     ('span<=256', 120, 200, 3000, 12, 60),
     ('span<=512', 80, 450, 4000, 10, 120),
     ('span<=1024', 48, 900, 12000, 12, 200),
     ('span<=2048', 24, 1800, 15000, 12, 400),
     ('span<=4096', 8, 3600, 16000, 10, 900),
-    ('hashblk<=512', 40, 400, 40000, 8, 120),
-    ('hashblk<=1024', 24, 900, 40000, 10, 220),
-    ('hashblk<=2048', 12, 1800, 60000, 10, 450),
-    ('hashblk<=4096', 6, 3500, 60000, 10, 900),
+    ('span64k<=1024', 24, 900, 40000, 10, 220),
+    ('span64k<=4096', 6, 3500, 60000, 10, 900),
+    ('hashblk<=512', 40, 400, 90000, 8, 120),
+    ('hashblk<=1024', 24, 900, 90000, 10, 220),
+    ('hashblk<=2048', 12, 1800, 90000, 10, 450),
+    ('hashblk<=4096', 6, 3500, 90000, 10, 900),
     ('span>4096->hash<=8192', 4, 7000, 16000, 10, 1800),
-    ('hash>8192->global', 2, 12000, 80000, 10, 3000),
+    ('hash>8192->global', 2, 12000, 100000, 10, 3000),
 ]
 
 
@@ -125,7 +127,7 @@ def test_spgemm_mixed_classes_one_call():
     streams write disjoint rows of the same output)."""
     import paper_2508_17517_b200 as G
     rng = np.random.default_rng(11)
-    parts = [_case(rng, n // 4 + 1, L, W, ka, bl, 90000, cancel=(i % 2 == 0))
+    parts = [_case(rng, n // 4 + 1, L, W, ka, bl, 110000, cancel=(i % 2 == 0))
              for i, (_, n, L, W, ka, bl) in enumerate(CASES[:-1])]
     import scipy.sparse as sps
     A = O.from_scipy(sps.block_diag([p[0].sp() for p in parts], format='csr'))
