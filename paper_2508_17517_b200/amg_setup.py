@@ -153,6 +153,28 @@ def finalize_complexities(H):
     return H
 
 
+def setup_compulsory_bytes(H):
+    """Compulsory HBM traffic of the setup: every level operator read once
+    and every retained output (R, P, A_ff, A_fc and the next level's
+    operator) written once, 12 B/nnz + 4 B/row (int32 CSR, fp64 values).
+    Intermediates (Z, A P, the assembled polynomial, pre-drop R A P rows)
+    are not counted: this is the lower bound a memory-bound setup would
+    approach, not the bytes the kernels move."""
+    def spm(nnz, rows):
+        return 12 * int(nnz) + 4 * (int(rows) + 1)
+    tot = 0
+    for i, lv in enumerate(H.levels):
+        nxt = H.levels[i + 1] if i + 1 < len(H.levels) else None
+        tot += spm(lv.nnz_A, lv.n)
+        for M in (lv.R, lv.P, lv.A_ff, lv.A_fc):
+            tot += spm(M.nnz, M.nrows)
+        tot += spm(nxt.nnz_A, nxt.n) if nxt is not None else spm(H.coarsest_A.nnz,
+                                                                  H.coarsest_A.nrows)
+    if not H.levels:
+        tot += spm(H.top_A.nnz, H.top_A.nrows)
+    return int(tot)
+
+
 def hierarchy_summary(H):
     """JSON-serialisable summary (hierarchy.py:451-490)."""
     levels = []
