@@ -65,17 +65,23 @@ __device__ __forceinline__ double rowdot(const int* __restrict__ p, const int* _
 // reduction of step q, so each step costs one block reduction instead of two
 // dependent L2 round trips.  Per-thread summation order is unchanged (entries
 // in e order), so H is bitwise what the two-pass loop produced.
+// The first vsm basis vectors live in shared memory (after H's column): the
+// Gram-Schmidt sweeps re-read every earlier vector, and an order-100
+// Arnoldi on a few hundred rows otherwise waits on L2 at every step.
 template <int NT, int E>
 __global__ void __launch_bounds__(NT) arnoldi_cta_kernel(int n, const int* __restrict__ p,
                                                          const int* __restrict__ c,
                                                          const double* __restrict__ v,
                                                          const double* __restrict__ b, int m,
-                                                         double* V, double* w, double* H,
-                                                         int* info, double* dinfo) {
+                                                         double* Vg, double* w, double* H,
+                                                         int* info, double* dinfo, int vsm) {
   static_assert(NT == 256, "Sum8 reduces 8 warps");
   __shared__ double red[33];
   __shared__ double red8[16];
-  extern __shared__ double hcol[];  // column j of H (m + 1), thread 0 only
+  extern __shared__ double hcol[];  // column j of H (m + 1), thread 0 only; then vsm vectors
+  double* Vs = hcol + ((m + 2) & ~1);
+  auto vrow = [&](int q) -> double* { return q < vsm ? Vs + (size_t)q * n : Vg + (size_t)q * n; };
+  double* V = vrow(0);
   Sum8 bsum{red8, 0};
   const int tid = threadIdx.x;
   double sq = 0.0;
@@ -97,7 +103,7 @@ __global__ void __launch_bounds__(NT) arnoldi_cta_kernel(int n, const int* __res
   int k = m;
   double wr[E], vq[E], vn[E];
   for (int j = 0; j < m; ++j) {
-    const double* Vj = V + (size_t)j * n;
+    const double* Vj = vrow(j);
     sq = 0.0;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
@@ -125,7 +131,7 @@ __global__ void __launch_bounds__(NT) arnoldi_cta_kernel(int n, const int* __res
         for (int e = 0; e < E; ++e)
           if (tid + e * NT < n) d = fma(vq[e], wr[e], d);
         if (q < j) {
-          const double* Vn = V + (size_t)(q + 1) * n;
+          const double* Vn = vrow(q + 1);
 #pragma unroll
           for (int e = 0; e < E; ++e) {
             const int i = tid + e * NT;
@@ -165,7 +171,7 @@ __global__ void __launch_bounds__(NT) arnoldi_cta_kernel(int n, const int* __res
       k = j + 1;
       break;
     }
-    double* Vn = V + (size_t)(j + 1) * n;
+    double* Vn = vrow(j + 1);
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const int i = tid + e * NT;
@@ -516,7 +522,25 @@ extern "C" int airg_arnoldi(int n, const int32_t* p, const int32_t* c, const dou
     AIRG_TRY(scratch(&dinfo, 1, s));
     AIRG_TRY(scratch(&info, 2, s));
     static_assert(kArnoldiCta <= 256 * 16, "one CTA of 256 threads, 16 entries each");
-    arnoldi_cta_kernel<256, 16><<<1, 256, (size_t)(m + 1) * sizeof(double), s>>>(n, p, c, v, b, m, V, w, H, info, dinfo);
+    // as many basis vectors in shared memory as fit
+    const size_t hbytes = (size_t)((m + 2) & ~1) * sizeof(double);
+    const size_t cap = 200 * 1024;
+    const int vsm = (int)std::min<size_t>((size_t)(m + 1), (cap - hbytes) / ((size_t)n * sizeof(double)));
+    const size_t shm = hbytes + (size_t)vsm * n * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      AIRG_CUDA(cudaFuncSetAttribute(arnoldi_cta_kernel<256, 16>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap));
+      AIRG_CUDA(cudaFuncSetAttribute(arnoldi_cta_kernel<256, 2>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap));
+      attr = true;
+    }
+    // entries per thread: 2 for the coarsest grids (<= 512 rows; the per-step
+    // loops then issue 8x fewer predicated-off instructions), 16 up to 4096
+    if (n <= 512)
+      arnoldi_cta_kernel<256, 2><<<1, 256, shm, s>>>(n, p, c, v, b, m, V, w, H, info, dinfo, vsm);
+    else
+      arnoldi_cta_kernel<256, 16><<<1, 256, shm, s>>>(n, p, c, v, b, m, V, w, H, info, dinfo, vsm);
     AIRG_LAUNCH_CHECK();
     int hi[2];
     AIRG_CUDA(cudaMemcpyAsync(H_h, H, (size_t)(m + 1) * m * sizeof(double), cudaMemcpyDeviceToHost, s));
