@@ -607,12 +607,20 @@ def ours_arm(args, rank, world, local):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
+        try:  # one core: the path is single-threaded Python/scipy (and 1 BLAS thread)
+            from threadpoolctl import threadpool_limits
+            lim = threadpool_limits(1)
+        except Exception:
+            lim = None
         a, bs, its = cpu_run(args.cpu_nx, args.order, args.problem)
+        if lim is not None:
+            lim.restore_original_limits()
         ncpu, blas = cpu_cores_note()
         cpu = {'value': args.cpu_nx ** 2 * (4 if args.problem == 'dg' else 1) / (a + bs), 'unit': 'DOF/s', 'cores': 1, 'kind': 'port',
                'sample': f'one setup + timed second solve at {args.cpu_nx}^2 (of the {args.nx}^2 '
                          f'workload) with oracle/airg_oracle.py (numpy/scipy restatement of airmg; '
-                         f'scipy sparse kernels single-threaded; BLAS {blas}; {ncpu} host cpus); '
+                         f'scipy sparse kernels single-threaded, BLAS limited to 1 thread; '
+                         f'{ncpu} host cpus); '
                          f'setup {a:.2f} s, solve {bs:.3f} s, {its} its'}
 
     if rank == 0:

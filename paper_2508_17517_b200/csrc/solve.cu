@@ -757,21 +757,29 @@ static int newton_multi(const Poly& p, const Csr& A, const double* b, double* y,
   const int nb = blocks_for(n, thr, 148 * 8);
   newton_init_kernel<<<nb, thr, 0, s>>>(n, b, t0, y, nst);
   ++g_launches;
+  // SpMVs: the reference-order row kernel in exact mode; otherwise the
+  // vector SpMV (lanes per row sized to the operator: the coarsest grids of a
+  // truncated hierarchy have hundreds of entries per row).  After a stop the
+  // vector SpMV still runs but its output is never used (the update and
+  // rescale kernels are gated on the state).
+  auto spmv = [&](const double* in, double* out) -> int {
+    if (E) {
+      newton_rowspmv_kernel<E><<<nb, thr, 0, s>>>(n, A.ptr, A.col, A.val, in, out, nst, iflag);
+      ++g_launches;
+      AIRG_LAUNCH_CHECK();
+      return AIRG_OK;
+    }
+    Epi ep{out, nullptr, 1.0, 0.0, nullptr, nullptr, nullptr, nullptr};
+    return launch_spmv(A, in, 1.0, ep, s, false);
+  };
   for (int k = 0; k < nunits; ++k) {
     const int ty = p.utype[k];
     AIRG_CUDA(cudaMemsetAsync(iflag, 0, sizeof(int), s));
-    if (ty == 1) {
-      newton_rowspmv_kernel<E><<<nb, thr, 0, s>>>(n, A.ptr, A.col, A.val, t0, t1, nst, iflag);
-      ++g_launches;
-    }
+    if (ty == 1) AIRG_TRY(spmv(t0, t1));
     newton_check_kernel<<<nb, thr, 0, s>>>(n, ty, p.p1[k], p.p2[k], t0, t1, nst, iflag);
     ++g_launches;
-    if (ty == 0) {
-      newton_rowspmv_kernel<E><<<nb, thr, 0, s>>>(n, A.ptr, A.col, A.val, t0, t1, nst, iflag);
-    } else {
-      newton_rowspmv_kernel<E><<<nb, thr, 0, s>>>(n, A.ptr, A.col, A.val, t1, t2, nst, iflag);
-    }
-    ++g_launches;
+    if (ty == 0) AIRG_TRY(spmv(t0, t1));
+    else AIRG_TRY(spmv(t1, t2));
     newton_update_kernel<E><<<nb, thr, 0, s>>>(n, ty, p.p1[k], p.p2[k], y, t0, t1, t2, nst, iflag,
                                             parts);
     newton_rescale_kernel<<<1, 1024, 0, s>>>(n, nb, parts, t0, nst, iflag);
