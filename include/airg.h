@@ -139,6 +139,15 @@ int airg_dplan_set_level(airg_dplan* plan, int level, int n_loc, int nf, int nc,
                          const int32_t* c_idx, int ncoef, const double* coef_h);
 int airg_dplan_set_top(airg_dplan* plan, int n_loc, const int32_t* ptr, const int32_t* col,
                        const double* val, int64_t nnz);
+/* Distributed coarsest grid for a Newton coarse solver (configs[3]): the
+ * rank's rows of the coarsest operator with columns [local | ghost], its halo
+ * (as airg_dplan_set_halo) and the Newton units (as airg_plan_set_coarse).
+ * The tail V-cycle then applies q(C) on the row strips instead of gathering
+ * the coarsest grid (ref: polynomial.py:312-355, hierarchy.py:308-362). */
+int airg_dplan_set_dcoarse(airg_dplan* plan, int n_loc, const int32_t* ptr, const int32_t* col,
+                           const double* val, int64_t nnz, int nsend, const int32_t* send_idx,
+                           const int32_t* scnt_h, const int32_t* rcnt_h, int nunits,
+                           const int32_t* type_h, const double* p1_h, const double* p2_h);
 int airg_dplan_finish(airg_dplan* plan, airg_plan* tail, const int32_t* counts_h);
 int airg_dplan_richardson(airg_dplan* plan, const double* b, double* x, double rtol, double atol,
                           int max_iters, double* history_h, int* iterations_h, int* converged_h,

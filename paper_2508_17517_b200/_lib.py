@@ -151,6 +151,7 @@ sig('airg_dplan_set_halo', vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp)
 sig('airg_dplan_set_level', vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, vp, i64, vp, vp, vp,
     i64, vp, vp, vp, i64, vp, vp, C.c_int, vp)
 sig('airg_dplan_set_top', vp, C.c_int, vp, vp, vp, i64)
+sig('airg_dplan_set_dcoarse', vp, C.c_int, vp, vp, vp, i64, C.c_int, vp, vp, vp, C.c_int, vp, vp, vp)
 sig('airg_dplan_finish', vp, vp, vp)
 sig('airg_dplan_richardson', vp, vp, vp, f64, f64, C.c_int, vp, vp, vp, vp)
 sig('airg_dplan_destroy', vp)

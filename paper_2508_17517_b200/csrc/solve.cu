@@ -1948,6 +1948,26 @@ struct airg_comm {
   long long owner = -1, next_id = 0;
 };
 
+// Distributed Newton coarse solve (configs[3]: a truncated hierarchy whose
+// coarsest grid is too large to replicate): the coarsest operator stays on
+// its row strips, u's ghosts travel per SpMV (NCCL send/recv), and the
+// per-root decisions of polynomial.py:312-355 (non-finite delta -> stop, max
+// |u| -> rescale / stop) need global facts.  They are taken speculatively:
+// every rank applies the root, then ONE allreduce(max) of (max|u_new|, bad)
+// decides; a root whose delta was non-finite anywhere is undone from the
+// saved x / u, which is what stopping before it gives.
+struct DCoarse {
+  bool on = false;
+  int n_loc = 0;
+  Csr C;  // local rows, columns [local | ghost]
+  HaloX h;
+  std::vector<int> utype;
+  std::vector<double> p1, p2;
+  double *u = nullptr, *w = nullptr, *z = nullptr, *x0 = nullptr, *u0 = nullptr;
+  unsigned long long* red = nullptr;  // [0..1] local (max bits, bad), [2..3] global
+  double* state = nullptr;            // [0] scale, [1] stop
+};
+
 struct airg_dplan {
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
@@ -1986,6 +2006,7 @@ struct airg_dplan {
   cudaGraphExec_t graph = nullptr;
   const void* gkey[2] = {nullptr, nullptr};
   long long launches = 0;
+  DCoarse dc;
 };
 
 template <typename T>
@@ -2038,6 +2059,24 @@ static int halo_exchange(airg_dplan* p, HaloX& h, const P2PHalo* ph, double* x_e
   return AIRG_OK;
 }
 
+// the NCCL form of a halo exchange (pack + grouped send/recv), whatever the
+// plan's transport: the distributed coarse solve is not in the P2P layout
+static int halo_nccl(airg_dplan* p, HaloX& h, double* x_ext, cudaStream_t s) {
+  if (p->world == 1) return AIRG_OK;
+  if (h.nsend) {
+    pack_kernel<<<blocks_for(h.nsend, 256, 1024), 256, 0, s>>>(h.nsend, h.send_idx, x_ext, h.sendbuf);
+    AIRG_LAUNCH_CHECK();
+  }
+  AIRG_NCCL(ncclGroupStart());
+  for (int q = 0; q < p->world; ++q) {
+    if (h.scnt[q]) AIRG_NCCL(ncclSend(h.sendbuf + h.sofs[q], h.scnt[q], ncclDouble, q, p->comm, s));
+    if (h.rcnt[q])
+      AIRG_NCCL(ncclRecv(x_ext + h.n_loc + h.rofs[q], h.rcnt[q], ncclDouble, q, p->comm, s));
+  }
+  AIRG_NCCL(ncclGroupEnd());
+  return AIRG_OK;
+}
+
 // nrm_loc -> nrm_glob (sum over ranks)
 static int norm_allreduce(airg_dplan* p, cudaStream_t s) {
   if (p->world == 1) {
@@ -2054,10 +2093,142 @@ static int norm_allreduce(airg_dplan* p, cudaStream_t s) {
   return AIRG_OK;
 }
 
+__global__ void dn_init_kernel(int n, const double* __restrict__ in, double* __restrict__ u,
+                               double* __restrict__ x, double* state, unsigned long long* red) {
+  pdl_enter();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    u[i] = in[i];
+    x[i] = 0.0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    state[0] = 1.0;
+    state[1] = 0.0;
+    red[0] = red[1] = 0ull;
+  }
+}
+
+// x += delta, u = u_new for one unit (real root: p1 = theta; pair: p1 = 2a,
+// p2 = |theta|^2), saving the previous x / u; local max|u_new| (as the bits
+// of a non-negative double: uint64 order == double order, NaN above inf) and
+// the non-finite-delta flag into red[0..1]
+__global__ void dn_update_kernel(int n, int type, double p1, double p2, double* __restrict__ x,
+                                 double* __restrict__ u, const double* __restrict__ w,
+                                 const double* __restrict__ z, double* __restrict__ x0,
+                                 double* __restrict__ u0, const double* state,
+                                 unsigned long long* red) {
+  pdl_enter();
+  if (state[1] != 0.0) return;
+  const double sc = state[0] / (type == 0 ? p1 : p2);
+  double lmax = 0.0;
+  int bad = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double ui = u[i], xi = x[i];
+    x0[i] = xi;
+    u0[i] = ui;
+    double d, un;
+    if (type == 0) {
+      d = sc * ui;
+      un = ui - w[i] / p1;
+    } else {
+      d = sc * (p1 * ui - w[i]);
+      un = ui + (z[i] - p1 * w[i]) / p2;
+    }
+    bad |= !isfinite(d);
+    x[i] = xi + d;
+    u[i] = un;
+    const double a = fabs(un);
+    lmax = (a != a || a > lmax) ? a : lmax;
+  }
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(lmax);
+  unsigned long long m = bits;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long y = __shfl_xor_sync(0xffffffffu, m, o);
+    m = y > m ? y : m;
+  }
+  bad = __any_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0) {
+    if (m) atomicMax(red, m);
+    if (bad) atomicOr(red + 1, 1ull);
+  }
+}
+
+// one CTA: the global decision of the unit (undo + stop / stop / rescale)
+__global__ void dn_decide_kernel(int n, double* __restrict__ x, double* __restrict__ u,
+                                 const double* __restrict__ x0, const double* __restrict__ u0,
+                                 double* state, unsigned long long* red) {
+  pdl_enter();
+  __shared__ int act;
+  __shared__ double nrm;
+  if (state[1] != 0.0) return;
+  if (threadIdx.x == 0) {
+    act = 0;
+    if (red[3]) {
+      act = 2;  // a non-finite delta somewhere: stop before this unit
+    } else {
+      const double m = __longlong_as_double((long long)red[2]);
+      nrm = m;
+      if (m == 0.0) state[1] = 1.0;
+      else if (m > 1e150 || m < 1e-150) act = 1;
+    }
+  }
+  __syncthreads();
+  if (act == 2) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      x[i] = x0[i];
+      u[i] = u0[i];
+    }
+  } else if (act == 1) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) u[i] /= nrm;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (act == 2) state[1] = 1.0;
+    if (act == 1) {
+      const double sc = state[0] * nrm;
+      state[0] = sc;
+      if (!isfinite(sc) || sc == 0.0) state[1] = 1.0;
+    }
+    red[0] = red[1] = 0ull;
+  }
+}
+
 static int dplan_vcycle(airg_dplan* p, int l, cudaStream_t s);
+static int halo_nccl(airg_dplan* p, HaloX& h, double* x_ext, cudaStream_t s);
+
+// e = q(C) r on the row strips of the coarsest operator (see DCoarse)
+static int dist_newton(airg_dplan* p, const double* in, double* out, cudaStream_t s) {
+  DCoarse& D = p->dc;
+  const int n = D.n_loc;
+  const int nb = blocks_for(n, 256, 148 * 4);
+  AIRG_CUDA(launch_pdl(dn_init_kernel, nb, 256, s, n, in, D.u, out, D.state, D.red));
+  for (size_t k = 0; k < D.utype.size(); ++k) {
+    const int ty = D.utype[k];
+    AIRG_TRY(halo_nccl(p, D.h, D.u, s));
+    {
+      Epi ep{D.w, nullptr, 1.0, 0.0, nullptr, nullptr, nullptr, nullptr};
+      AIRG_TRY(launch_spmv(D.C, D.u, 1.0, ep, s));
+    }
+    if (ty == 1) {
+      AIRG_TRY(halo_nccl(p, D.h, D.w, s));
+      Epi ep{D.z, nullptr, 1.0, 0.0, nullptr, nullptr, nullptr, nullptr};
+      AIRG_TRY(launch_spmv(D.C, D.w, 1.0, ep, s));
+    }
+    AIRG_CUDA(launch_pdl(dn_update_kernel, nb, 256, s, n, ty, D.p1[k], D.p2[k], out, D.u,
+                         (const double*)D.w, (const double*)D.z, D.x0, D.u0,
+                         (const double*)D.state, D.red));
+    AIRG_NCCL(ncclAllReduce(D.red, D.red + 2, 2, ncclUint64, ncclMax, p->comm, s));
+    AIRG_CUDA(launch_pdl(dn_decide_kernel, 1, 1024, s, n, out, D.u, (const double*)D.x0,
+                         (const double*)D.u0, D.state, D.red));
+    p->launches += 4 + (ty == 1 ? 1 : 0);
+  }
+  AIRG_LAUNCH_CHECK();
+  return AIRG_OK;
+}
 
 // V-cycle of the replicated tail: in = local part (tcnt[rank] entries), out = local part
 static int dplan_tail(airg_dplan* p, const double* in, double* out, cudaStream_t s) {
+  if (p->dc.on) return dist_newton(p, in, out, s);
   const int mine = p->tcnt[p->rank];
   if (p->p2p) {
     AIRG_TRY(halo_put(p, p->pTail, in, s));  // waits for the peers' parts too
@@ -2492,6 +2663,32 @@ int airg_dplan_set_level(airg_dplan* p, int level, int n_loc, int nf, int nc, co
     AIRG_TRY(dalloc_owned(p, &L.e, (size_t)n_loc + 1));
     L.own_e = true;
   }
+  return AIRG_OK;
+}
+
+// distributed coarsest grid (Newton coarse solver on row strips): local rows
+// with columns [local | ghost] (halo: nsend entries, per-rank counts), the
+// units of the Newton form (type, p1, p2 as airg_plan_set_coarse)
+int airg_dplan_set_dcoarse(airg_dplan* p, int n_loc, const int32_t* ptr, const int32_t* col,
+                           const double* val, int64_t nnz, int nsend, const int32_t* send_idx,
+                           const int32_t* scnt_h, const int32_t* rcnt_h, int nunits,
+                           const int32_t* type_h, const double* p1_h, const double* p2_h) {
+  DCoarse& D = p->dc;
+  AIRG_TRY(dalloc(p, D.h, n_loc, nsend, send_idx, scnt_h, rcnt_h, p->world));
+  D.n_loc = n_loc;
+  D.C = make_csr(n_loc, n_loc + D.h.nrecv, ptr, col, val, nnz);
+  D.utype.assign(type_h, type_h + nunits);
+  D.p1.assign(p1_h, p1_h + nunits);
+  D.p2.assign(p2_h, p2_h + nunits);
+  const size_t ext = (size_t)n_loc + D.h.nrecv + 1;
+  AIRG_TRY(dalloc_owned(p, &D.u, ext));
+  AIRG_TRY(dalloc_owned(p, &D.w, ext));
+  AIRG_TRY(dalloc_owned(p, &D.z, (size_t)n_loc + 1));
+  AIRG_TRY(dalloc_owned(p, &D.x0, (size_t)n_loc + 1));
+  AIRG_TRY(dalloc_owned(p, &D.u0, (size_t)n_loc + 1));
+  AIRG_TRY(dalloc_owned(p, &D.red, 4));
+  AIRG_TRY(dalloc_owned(p, &D.state, 2));
+  D.on = true;
   return AIRG_OK;
 }
 

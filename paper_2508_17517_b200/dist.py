@@ -300,6 +300,7 @@ class DHierarchy:
     truncated_at: int = None
     config: object = None
     setup_breakdown: dict = None
+    tail_dmat: object = None  # the tail's top level on its row strips (before the gather)
 
     @property
     def num_levels(self):
@@ -773,7 +774,7 @@ def setup_distributed(comm, A, cfg, poly_inject=None, replicate_below=20000, for
     finalize_complexities(tail)
     tick(None)
     return DHierarchy(dlevels=dlevels, tail=tail, tail_level=level, top=A, comm=comm, polys=polys,
-                      truncated_at=trunc, config=cfg, setup_breakdown=timings)
+                      truncated_at=trunc, config=cfg, setup_breakdown=timings, tail_dmat=cur)
 
 
 # ---------------------------------------------------------------------------
@@ -904,6 +905,7 @@ class DistSolver:
                    L.ptr(Ff.row_offsets), L.ptr(Ff.col_indices), L.ptr(Ff.values), Ff.nnz,
                    L.ptr(f32), L.ptr(c32), len(coef), L.hptr(coef))
         set_halo(0, 3, self.htop)
+        self._set_dist_coarse(h, keep)
         T = self.Atop
         L.call('airg_dplan_set_top', h, T.nrows, L.ptr(T.row_offsets), L.ptr(T.col_indices),
                L.ptr(T.values), T.nnz)
@@ -915,6 +917,34 @@ class DistSolver:
         self._keep = keep
         self._dplan = h
         return h
+
+    def _set_dist_coarse(self, h, keep):
+        """configs[3]: when the tail is the coarsest grid alone (the hierarchy
+        was truncated at the first replicated level) and its solver is the
+        Newton polynomial, apply it on the row strips of the coarsest
+        operator instead of gathering the grid to every rank
+        (AIRG_DIST_COARSE=0 keeps the replicated solve)."""
+        import os
+        from .gmres_poly import newton_units
+        H, comm = self.H, self.comm
+        T = H.tail
+        if (comm.world == 1 or T is None or T.num_levels != 0 or H.tail_dmat is None
+                or T.coarse_solver.kind != 'newton_roots'
+                or os.environ.get('AIRG_DIST_COARSE', '1') == '0'):
+            return
+        Cd = H.tail_dmat
+        r = comm.rank
+        halo = Halo(comm, Cd.rows, remote_cols(Cd.M.col_indices, Cd.rows, r))
+        Cx = with_cols(Cd.M, halo.ext_cols(Cd.M.col_indices), halo.n_loc + halo.n)
+        si = halo.send_idx.to(IDX).contiguous()
+        sc = np.ascontiguousarray(halo.send_counts, dtype=np.int32)
+        rc = np.ascontiguousarray(halo.recv_counts, dtype=np.int32)
+        t, a1, a2 = newton_units(T.coarse_solver.roots)
+        keep.extend([Cx, si, sc, rc, t, a1, a2])
+        L.call('airg_dplan_set_dcoarse', h, Cx.nrows, L.ptr(Cx.row_offsets), L.ptr(Cx.col_indices),
+               L.ptr(Cx.values), Cx.nnz, si.numel(), L.ptr(si), L.hptr(sc), L.hptr(rc), len(t),
+               L.hptr(t), L.hptr(a1), L.hptr(a2))
+        self.dist_coarse = True
 
     def __del__(self):
         try:
@@ -987,7 +1017,17 @@ def dist_cycle_bytes(S, include_top=True):
         tot += _spmat_bytes(Lv['Afc']) + 8 * nc + 16 * nf
         tot += 16 * nf + d * (_spmat_bytes(Lv['Aff']) + 24 * nf)
         tot += 16 * n
-    tot += count_cycle_bytes(S.H.tail, include_top=False)
+    if getattr(S, 'dist_coarse', False):
+        # the Newton units on this rank's strip of the coarsest operator: per
+        # unit the SpMV(s) plus x, u, w (z) read and x, u, x0, u0 written
+        from .gmres_poly import newton_units
+        C = S.H.tail_dmat.M
+        t, _, _ = newton_units(S.H.tail.coarse_solver.roots)
+        spm = _spmat_bytes(C)
+        for ty in t:
+            tot += (2 * spm + 72 * C.nrows) if ty else (spm + 56 * C.nrows)
+    else:
+        tot += count_cycle_bytes(S.H.tail, include_top=False)
     if include_top:
         tot += _spmat_bytes(S.Atop) + 40 * S.Atop.nrows
     return int(tot)

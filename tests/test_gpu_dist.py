@@ -103,3 +103,18 @@ def test_four_gpu_strips_match_serial():
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert 'DIST OK world=4' in r.stdout + r.stderr
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason='needs two GPUs')
+def test_two_gpu_distributed_newton_coarse():
+    """configs[3] shape at 2 ranks: truncation at level 2 leaves a coarsest grid
+    of ~10k rows solved by the order-100 Newton polynomial.  Its distributed
+    application (row strips, ghost exchange per SpMV, one max-allreduce per
+    root) must give the same residual history as the replicated one."""
+    cmd = [sys.executable, '-m', 'torch.distributed.run', '--nnodes=1', '--nproc-per-node', '2',
+           '--master-addr', '127.0.0.1', '--master-port', str(_free_port()),
+           os.path.join(ROOT, 'tools', 'dist_coarse_check.py'), '256', '3']
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=420)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert 'DIST COARSE OK world=2' in r.stdout + r.stderr
