@@ -19,6 +19,7 @@ hierarchy (> 1 GB per GPU) exceeds L2.
 """
 
 import argparse
+import glob
 import json
 import os
 import subprocess
@@ -385,15 +386,20 @@ class SerialWorkload:
         ms = e0.elapsed_time(e1) / nv
         vbytes = count_cycle_bytes(H, include_top=False)
         self.traffic = None
-        try:  # ncu DRAM bytes of one V-cycle of this configuration (profiles/)
-            t = json.load(open(os.path.join(ROOT, 'profiles', 'r01_vcycle_traffic.json')))
-            if int(t['algorithmic_bytes']) == int(vbytes):
-                self.traffic = int(t['dram_total_bytes'])
-        except Exception:
-            pass
+        src = None
+        # ncu DRAM bytes of one V-cycle of this configuration (profiles/, newest round first)
+        for fn in sorted(glob.glob(os.path.join(ROOT, 'profiles', 'r*_vcycle_traffic.json')),
+                         reverse=True):
+            try:
+                t = json.load(open(fn))
+                if int(t['algorithmic_bytes']) == int(vbytes):
+                    self.traffic, src = int(t['dram_total_bytes']), os.path.basename(fn)
+                    break
+            except Exception:
+                pass
         return ms, vbytes, ('one V-cycle (R/A_fc/A_ff SpMV chains + Newton coarse solve); '
                             f'algorithmic bytes {vbytes} (count_cycle_bytes); traffic = ncu '
-                            'dram__bytes_read+write of the same V-cycle (profiles/r01_vcycle_traffic.json)')
+                            f'dram__bytes_read+write of the same V-cycle (profiles/{src or "r*_vcycle_traffic.json: none matches"})')
 
     def e2e(self):
         """Step through the public API from pinned host buffers."""

@@ -182,6 +182,128 @@ __global__ void __launch_bounds__(NT) arnoldi_cta_kernel(int n, const int* __res
   if (tid == 0) info[0] = k;
 }
 
+// ---- one-warp Gram-Schmidt (n <= 512: coarsest grids, order-100 Newton) ----
+// The CTA does the SpMV; warp 0 alone runs the Gram-Schmidt sweeps with the
+// working vector in registers (E entries per lane), so each of the ~m^2/2
+// projections of an order-m Arnoldi costs a 5-step shuffle reduction instead
+// of a block barrier (an order-100 Arnoldi on 330 rows: 5 ms -> ~1 ms).
+template <int E>
+__global__ void __launch_bounds__(256) arnoldi_warp_kernel(int n, const int* __restrict__ p,
+                                                           const int* __restrict__ c,
+                                                           const double* __restrict__ v,
+                                                           const double* __restrict__ b, int m,
+                                                           double* Vg, double* H, int* info,
+                                                           double* dinfo, int vsm) {
+  extern __shared__ double hcol[];  // (m + 2) & ~1 | ws (n, even) | vsm vectors
+  __shared__ int done;
+  double* ws = hcol + ((m + 2) & ~1);
+  double* Vs = ws + ((n + 1) & ~1);
+  auto vrow = [&](int q) -> double* { return q < vsm ? Vs + (size_t)q * n : Vg + (size_t)q * n; };
+  const int tid = threadIdx.x, lane = tid & 31;
+  const bool w0 = tid < 32;
+  double wr[E], vq[E], vn[E];
+  if (w0) {
+    double sq = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = lane + 32 * e;
+      wr[e] = i < n ? b[i] : 0.0;
+      sq = fma(wr[e], wr[e], sq);
+    }
+    const double beta = sqrt(warp_sum(sq));
+    if (lane == 0) {
+      dinfo[0] = beta;
+      info[0] = m;
+      info[1] = beta == 0.0 ? 1 : 0;
+      done = beta == 0.0;
+    }
+    if (beta != 0.0) {
+      double* V0 = vrow(0);
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (lane + 32 * e < n) V0[lane + 32 * e] = wr[e] / beta;
+    }
+  }
+  for (int i = tid; i < (m + 1) * m; i += blockDim.x) H[i] = 0.0;
+  __syncthreads();
+  if (done) return;
+  double hmax = 0.0;
+  int k = m;
+  for (int j = 0; j < m; ++j) {
+    const double* Vj = vrow(j);
+    for (int i = tid; i < n; i += blockDim.x) ws[i] = rowdot(p, c, v, Vj, i);
+    __syncthreads();
+    if (w0) {
+      double sq = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = lane + 32 * e;
+        wr[e] = i < n ? ws[i] : 0.0;
+        sq = fma(wr[e], wr[e], sq);
+      }
+      const double before = sqrt(warp_sum(sq));
+      for (int q = lane; q <= j; q += 32) hcol[q] = 0.0;
+      __syncwarp();
+      double hn = 0.0;
+      for (int sweep = 0; sweep < 2; ++sweep) {
+        const double* V0 = vrow(0);
+#pragma unroll
+        for (int e = 0; e < E; ++e) vq[e] = lane + 32 * e < n ? V0[lane + 32 * e] : 0.0;
+        for (int q = 0; q <= j; ++q) {
+          double d0 = 0.0, d1 = 0.0;  // two chains: half the dependent FMA latency
+#pragma unroll
+          for (int e = 0; e < E; e += 2) {
+            d0 = fma(vq[e], wr[e], d0);
+            if (e + 1 < E) d1 = fma(vq[e + 1], wr[e + 1], d1);
+          }
+          if (q < j) {
+            const double* Vn = vrow(q + 1);
+#pragma unroll
+            for (int e = 0; e < E; ++e) vn[e] = lane + 32 * e < n ? Vn[lane + 32 * e] : 0.0;
+          }
+          const double h = warp_sum(d0 + d1);
+          if (lane == 0) hcol[q] += h;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            wr[e] -= h * vq[e];
+            vq[e] = vn[e];
+          }
+        }
+        sq = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) sq = fma(wr[e], wr[e], sq);
+        hn = sqrt(warp_sum(sq));
+        if (!(sweep == 0 && hn < 0.7 * before)) break;  // "twice is enough"
+      }
+      __syncwarp();
+      double cn = 0.0;
+      if (lane == 0) {
+        hcol[j + 1] = hn;
+        for (int q = 0; q <= j + 1; ++q) {
+          H[q * m + j] = hcol[q];
+          cn = fma(hcol[q], hcol[q], cn);
+        }
+      }
+      hmax = fmax(hmax, sqrt(__shfl_sync(0xffffffffu, cn, 0)));
+      if (hn <= 1e-14 * hmax) {
+        if (lane == 0) {
+          H[(j + 1) * m + j] = 0.0;
+          done = 1;
+        }
+        k = j + 1;
+      } else {
+        double* Vn = vrow(j + 1);
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+          if (lane + 32 * e < n) Vn[lane + 32 * e] = wr[e] / hn;
+      }
+    }
+    __syncthreads();
+    if (done) break;
+  }
+  if (tid == 0) info[0] = k;
+}
+
 // ---- multi-kernel path ----------------------------------------------------
 // The modified Gram-Schmidt recurrence of the single-CTA kernel, spread over
 // the GPU (SpMV, fixed-order dot partials + finish, axpy).  The selective
@@ -535,9 +657,21 @@ extern "C" int airg_arnoldi(int n, const int32_t* p, const int32_t* c, const dou
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap));
       attr = true;
     }
-    // entries per thread: 2 for the coarsest grids (<= 512 rows; the per-step
-    // loops then issue 8x fewer predicated-off instructions), 16 up to 4096
-    if (n <= 512)
+    // up to 512 rows (coarsest grids): one-warp Gram-Schmidt; else 16 entries
+    // per thread of the CTA up to 4096
+    if (n <= 512 && !getenv("AIRG_ARNOLDI_CTA")) {
+      const size_t wbytes = hbytes + (size_t)((n + 1) & ~1) * sizeof(double);
+      const int vw = (int)std::min<size_t>((size_t)(m + 1), (cap - wbytes) / ((size_t)n * sizeof(double)));
+      const size_t shw = wbytes + (size_t)vw * n * sizeof(double);
+      static bool wattr = false;
+      if (!wattr) {
+        for (auto k : {arnoldi_warp_kernel<4>, arnoldi_warp_kernel<8>, arnoldi_warp_kernel<16>})
+          AIRG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap));
+        wattr = true;
+      }
+      auto k = n <= 128 ? arnoldi_warp_kernel<4> : n <= 256 ? arnoldi_warp_kernel<8> : arnoldi_warp_kernel<16>;
+      k<<<1, 256, shw, s>>>(n, p, c, v, b, m, V, H, info, dinfo, vw);
+    } else if (n <= 512)
       arnoldi_cta_kernel<256, 2><<<1, 256, shm, s>>>(n, p, c, v, b, m, V, w, H, info, dinfo, vsm);
     else
       arnoldi_cta_kernel<256, 16><<<1, 256, shm, s>>>(n, p, c, v, b, m, V, w, H, info, dinfo, vsm);

@@ -3,6 +3,7 @@
 // driver.  ref: /root/reference/pkg/src/airmg/solve.py:89-167,
 // polynomial.py:295-369, sparse.py:206-212.
 #include "airg_common.cuh"
+#include "chain.cuh"
 #include <nccl.h>
 #include <vector>
 #include <algorithm>
@@ -967,6 +968,11 @@ struct LevelOps {
   double* t0 = nullptr;   // n_f
   double* t1 = nullptr;   // n_f
   double* t2 = nullptr;   // n_f (extra smooths)
+  // fused smoother chain (fast mode): CTA row partition + grid-barrier counter
+  int chain_G = 0;        // 0: not prepared / not eligible
+  int chain_smem = 0;     // dynamic shared bytes of its launches
+  int* chain_part = nullptr;
+  unsigned long long* chain_bar = nullptr;
 };
 
 struct GraphEntry {
@@ -1194,6 +1200,8 @@ int airg_plan_destroy(airg_plan* p) {
   for (auto& L : p->lv) {
     for (double* q : {L.rc, L.ec, L.rhs, L.ef, L.t0, L.t1, L.t2})
       if (q) dfree(q);
+    if (L.chain_part) dfree(L.chain_part);
+    if (L.chain_bar) dfree(L.chain_bar);
     free_poly(L.sm);
   }
   free_poly(p->coarse_poly);
@@ -1272,6 +1280,118 @@ int airg_plan_set_coarse(airg_plan* p, int n, const int32_t* ptr, const int32_t*
 }
 
 }  // extern "C"
+
+// ---- fused smoother chain (chain.cuh) ---------------------------------------
+static int chain_smem() {
+  static int v = 0;
+  if (!v) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    v = std::max(48 * 1024, optin - 1024);
+  }
+  return v;
+}
+// AIRG_CHAIN: 0 off, 1 (default) where it measured faster, 2 every eligible level
+static int chain_mode() {
+  const char* e = getenv("AIRG_CHAIN");
+  return e ? atoi(e) : 1;
+}
+// CTAs for a chain: about kb KB of A_ff per CTA, at most one per SM
+static int chain_ctas(const Csr& A) {
+  const int kb = getenv("AIRG_CHAIN_KB") ? std::max(1, atoi(getenv("AIRG_CHAIN_KB"))) : 64;
+  const long long bytes = 12LL * A.nnz + 12LL * A.nrows;
+  const long long g = (bytes + kb * 1024LL - 1) / (kb * 1024LL);
+  return (int)std::max(1LL, std::min<long long>(g, num_sms()));
+}
+// Measured per level at 2048^2 (profiles/r02_vcycle.md): the chain wins on
+// the short-row levels (<= 8 entries per row: the per-degree kernels there
+// are launch- and L2-miss-bound), and loses or ties where rows are long
+// (one row's gathers are the latency chain of every step, and a grid barrier
+// costs about what a graph-replayed kernel boundary does).
+static bool chain_eligible(const LevelOps& L) {
+  const int d = (int)L.sm.coef.size() - 1;
+  const int mode = chain_mode();
+  return mode > 0 && (mode == 2 || L.Aff.vs <= 2) && !L.has_asm && L.sm.kind == 0 && d >= 2 &&
+         d <= kChainMaxDeg && L.n_f > 0;
+}
+static int prepare_chain(LevelOps& L, cudaStream_t s) {
+  if (L.chain_G || !chain_eligible(L)) return AIRG_OK;
+  const int G = chain_ctas(L.Aff);
+  // only where the whole A_ff stages into shared memory: a partly staged
+  // chain re-reads the rest every step and measured no faster than the
+  // one-launch-per-degree path (tools/micro/chain_bench.cu)
+  const bool partial = getenv("AIRG_CHAIN_CAP") || getenv("AIRG_CHAIN_PARTIAL");
+  if (!partial && 12LL * L.Aff.nnz + 4LL * L.n_f + 256LL * G > (long long)G * (chain_smem() - 128))
+    return AIRG_OK;
+  AIRG_CUDA(dmalloc(&L.chain_part, sizeof(int) * (3 * G + 1)));
+  AIRG_CUDA(cudaMemsetAsync(L.chain_part + 3 * G, 0, sizeof(int), s));
+  AIRG_CUDA(dmalloc(&L.chain_bar, sizeof(unsigned long long)));
+  AIRG_CUDA(cudaMemsetAsync(L.chain_bar, 0, sizeof(unsigned long long), s));
+  // staging capacity per CTA (AIRG_CHAIN_CAP lowers it: tests of the unstaged rows)
+  long long cap = chain_smem() - 128;
+  if (getenv("AIRG_CHAIN_CAP")) cap = std::min(cap, atoll(getenv("AIRG_CHAIN_CAP")));
+  long long* w = nullptr;
+  AIRG_TRY(scratch(&w, (size_t)L.n_f + 1, s));
+  chain_partition_kernel<<<1, 1024, 0, s>>>(L.n_f, L.Aff.ptr, L.Aff.vs, G, cap, w, L.chain_part);
+  AIRG_LAUNCH_CHECK();
+  release(w, s);
+  int need = 0;  // one read per level at plan build: the launch's shared bytes
+  AIRG_CUDA(cudaMemcpyAsync(&need, L.chain_part + 3 * G, sizeof(int), cudaMemcpyDeviceToHost, s));
+  AIRG_CUDA(cudaStreamSynchronize(s));
+  L.chain_smem = std::min(chain_smem(), ((need + 1023) / 1024) * 1024 + 1024);
+  L.chain_G = G;
+  return AIRG_OK;
+}
+template <int VS>
+static cudaError_t chain_launch_vs(const ChainArgs& a, int G, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(chain_kernel<VS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         chain_smem());
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(kChainThreads);
+  cfg.dynamicSmemBytes = a.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, chain_kernel<VS>, a);
+}
+// e[ymap] = q(A_ff) rhs in one launch
+static int launch_chain(LevelOps& L, const double* rhs, double* y, const int* ymap, cudaStream_t s) {
+  ChainArgs a{};
+  a.n = L.n_f;
+  a.ptr = L.Aff.ptr;
+  a.col = L.Aff.col;
+  a.val = L.Aff.val;
+  a.b = rhs;
+  a.t0 = L.t0;
+  a.t1 = L.t1;
+  a.y = y;
+  a.ymap = ymap;
+  a.part = L.chain_part;
+  a.bar = L.chain_bar;
+  a.d = (int)L.sm.coef.size() - 1;
+  a.smem = L.chain_smem;
+  for (int j = 0; j <= a.d; ++j) a.coef[j] = L.sm.coef[j];
+  switch (L.Aff.vs) {
+    case 1: AIRG_CUDA(chain_launch_vs<1>(a, L.chain_G, s)); break;
+    case 2: AIRG_CUDA(chain_launch_vs<2>(a, L.chain_G, s)); break;
+    case 4: AIRG_CUDA(chain_launch_vs<4>(a, L.chain_G, s)); break;
+    case 8: AIRG_CUDA(chain_launch_vs<8>(a, L.chain_G, s)); break;
+    case 16: AIRG_CUDA(chain_launch_vs<16>(a, L.chain_G, s)); break;
+    default: AIRG_CUDA(chain_launch_vs<32>(a, L.chain_G, s)); break;
+  }
+  ++g_launches;
+  return AIRG_OK;
+}
 
 // smoother application on one level: ef = q(A_ff) rhs  (or assembled SpMV)
 static int smooth_level(airg_plan* p, LevelOps& L, const double* rhs, double* out, cudaStream_t s) {
@@ -1383,6 +1503,8 @@ static int vcycle_rec(airg_plan* p, int level, const double* r, double* e, int f
     if (L.Afc.nrows == 0)
       AIRG_TRY(launch_axpby(L.n_c, e, L.c_idx, 1.0, L.ec, nullptr, 0.0, nullptr, s, p->exact));
   }
+  if (fits == 1 && !p->exact && L.chain_G > 0)  // fused chain: A_ff staged once
+    return launch_chain(L, L.rhs, e, L.f_idx, s);
   if (fits == 1 && !L.has_asm && L.sm.kind == 0) {
     // e[f] = q(A_ff) rhs written straight through f_idx by the last Horner step
     AIRG_TRY(poly_apply_dev(L.sm, L.Aff, L.rhs, e, L.t0, L.t1, L.t2, L.t2, p->iflag, p->parts,
@@ -1431,6 +1553,8 @@ static int prepare_capture(airg_plan* p, cudaStream_t s) {
   if (!p->exact && p->ready_coarse && p->coarse_poly.kind == 1 &&
       p->coarse.nrows <= kDenseCoarseMax && p->dense_state == 0)
     AIRG_TRY(build_dense_coarse(p, s));
+  if (!p->exact)
+    for (auto& L : p->lv) AIRG_TRY(prepare_chain(L, s));
   return AIRG_OK;
 }
 

@@ -248,3 +248,25 @@ def test_setup_accepts_reference_style_host_matrix(G):
         assert np.array_equal(L1.split.labels_host(), L2.split.labels_host())
     y = tonp(G.spmv(Ah, np.ones(Ao.ncols)))
     assert np.max(np.abs(y - O.spmv(Ao, np.ones(Ao.ncols)))) <= 1e-14
+
+
+@pytest.mark.parametrize('kb,cap', [(64, None), (1, None), (1, 600), (4, 0)])
+def test_fused_smoother_chain_partitions(G, hier64, kb, cap, monkeypatch):
+    """The fused q(A_ff) chain (chain.cuh) under forced partitions: many CTAs
+    (kb: KB of A_ff per CTA), partly staged (cap: staged bytes per CTA) and
+    fully unstaged (cap 0) -- the V-cycle stays within 1e-10 of the oracle and
+    matches the unfused multi-launch path."""
+    monkeypatch.setenv('AIRG_CHAIN', '2')  # every level, whatever its row length
+    monkeypatch.setenv('AIRG_CHAIN_KB', str(kb))
+    if cap is not None:
+        monkeypatch.setenv('AIRG_CHAIN_CAP', str(cap))
+    H = upload_hierarchy(hier64)
+    rng = np.random.default_rng(5)
+    r = rng.standard_normal(hier64.levels[0].n)
+    want = O.vcycle(hier64, 0, r)
+    got = tonp(G.vcycle(H, 0, r, G.SolveConfig()))
+    assert np.max(np.abs(got - want)) <= 1e-10 * np.max(np.abs(want))
+    monkeypatch.setenv('AIRG_CHAIN', '0')
+    H2 = upload_hierarchy(hier64)
+    ref = tonp(G.vcycle(H2, 0, r, G.SolveConfig()))
+    assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
