@@ -16,7 +16,7 @@ namespace cg = cooperative_groups;
 
 namespace airg {
 
-constexpr int kArnoldiCta = 4096;
+constexpr int kArnoldiCta = 1024;  // above: the cooperative grid kernel (measured faster from ~1k rows)
 
 __device__ double block_sum(double v, double* red) {
   v = warp_sum(v);
@@ -362,19 +362,39 @@ __global__ void scale_div_kernel(long long n, const double* __restrict__ x, doub
     y[i] = x[i] / dd;
 }
 
+// lanes per row from the mean row length (the rule of the solve's SpMV):
+// the fine levels' A_ff have 1-8 entries per row, the coarse ones 100+
+static int arnoldi_vs(long long nnz, int n) {
+  const double mean = n > 0 ? (double)nnz / n : 0.0;
+  return mean <= 6 ? 1 : mean <= 12 ? 2 : mean <= 24 ? 4 : mean <= 48 ? 8 : mean <= 96 ? 16 : 32;
+}
+
+// y = A x with vs lanes per row (lane-strided FMA, xor-tree over the vs
+// lanes).  `gthread` / `gthreads` index the calling threads; trip counts are
+// warp-uniform (the row groups of a warp shuffle together).  The grid and
+// multi-kernel Arnoldi both use this, so their H stay bitwise equal.
+__device__ __forceinline__ void arnoldi_spmv(long long n, const int* __restrict__ p,
+                                             const int* __restrict__ c, const double* __restrict__ v,
+                                             const double* x, double* y, int vs,
+                                             long long gthread, long long gthreads) {
+  const int lane = (int)(gthread & 31), sub = lane / vs, sl = lane & (vs - 1);
+  const long long per = 32 / vs;  // rows per warp per sweep
+  for (long long rb = (gthread >> 5) * per; rb < n; rb += (gthreads >> 5) * per) {
+    const long long r = rb + sub;
+    double s = 0.0;
+    if (r < n)
+      for (int k = p[r] + sl; k < p[r + 1]; k += vs) s = fma(v[k], x[c[k]], s);
+    for (int o = vs >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, vs);
+    if (r < n && sl == 0) y[r] = s;
+  }
+}
+
 __global__ void spmv_rows_kernel(int n, const int* __restrict__ p, const int* __restrict__ c,
                                  const double* __restrict__ v, const double* __restrict__ x,
-                                 double* __restrict__ y, Gate g) {
+                                 double* __restrict__ y, int vs, Gate g) {
   if (g.off()) return;
-  // warp per row (rows of coarse operators are long)
-  const int lane = threadIdx.x & 31;
-  for (long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; r < n;
-       r += ((long long)gridDim.x * blockDim.x) >> 5) {
-    double s = 0.0;
-    for (int k = p[r] + lane; k < p[r + 1]; k += 32) s = fma(v[k], x[c[k]], s);
-    s = warp_sum(s);
-    if (lane == 0) y[r] = s;
-  }
+  arnoldi_spmv(n, p, c, v, x, y, vs, blockIdx.x * (long long)blockDim.x + threadIdx.x,
+               (long long)gridDim.x * blockDim.x);
 }
 
 // dsc: [0] scratch, [1] projection h, [2] ||w||^2 before, [3] ||w||^2 after, [4] hmax, [5] hn
@@ -414,11 +434,15 @@ static int dev_dot(long long n, const double* x, const double* y, double* out, d
   return AIRG_OK;
 }
 
+// dot-product partials: one per CTA of the cooperative kernel, which has
+// enough threads for one vs-lane group per row (the SpMV), at most 4 per SM
+static int arnoldi_parts(int n, int vs) { return blocks_for((long long)n * vs, 256, 148 * 4); }
+
 static int arnoldi_multi(int n, const int* p, const int* c, const double* v, const double* b, int m,
-                         double* H_h, int* k_h, double* beta_h, cudaStream_t s) {
+                         double* H_h, int* k_h, double* beta_h, int vs, cudaStream_t s) {
   double *V = nullptr, *w = nullptr, *sc = nullptr, *Hd = nullptr;
   int* ctl = nullptr;
-  const int np = blocks_for(n, 256, 148 * 4);
+  const int np = arnoldi_parts(n, vs);
   AIRG_TRY(scratch(&V, (size_t)(m + 1) * n, s));
   AIRG_TRY(scratch(&w, n, s));
   AIRG_TRY(scratch(&sc, np + 8, s));
@@ -447,7 +471,7 @@ static int arnoldi_multi(int n, const int* p, const int* c, const double* v, con
   scale_div_kernel<<<nb, 256, 0, s>>>(n, b, beta, nullptr, V, always);
   for (int j = 0; j < m; ++j) {
     const double* Vj = V + (size_t)j * n;
-    spmv_rows_kernel<<<blocks_for((long long)n * 32, 256), 256, 0, s>>>(n, p, c, v, Vj, w, live);
+    spmv_rows_kernel<<<blocks_for((long long)n * vs, 256), 256, 0, s>>>(n, p, c, v, Vj, w, vs, live);
     AIRG_LAUNCH_CHECK();
     AIRG_TRY(dev_dot(n, w, w, dsc + 2, nullptr, d, live, s));
     for (int sweep = 0; sweep < 2; ++sweep) {
@@ -496,6 +520,7 @@ struct ArnoldiGridArgs {
   double* H;     // (m + 1) x m
   double* parts; // 2 x gridDim.x
   int* info;     // [0] k
+  int vs;        // lanes per row of the SpMV
 };
 
 __global__ void __launch_bounds__(256) arnoldi_grid_kernel(ArnoldiGridArgs a) {
@@ -522,17 +547,10 @@ __global__ void __launch_bounds__(256) arnoldi_grid_kernel(ArnoldiGridArgs a) {
   for (long long i = i0; i < n; i += stride) V[i] = a.b[i] / a.beta;
   double hmax = 0.0;
   int k = m;
-  const int lane = tid & 31;
-  const long long warp0 = ((long long)blockIdx.x * 256 + tid) >> 5, nwarps = stride >> 5;
   for (int j = 0; j < m; ++j) {
     grid.sync();  // V_j complete
     const double* Vj = V + (size_t)j * n;
-    for (long long r = warp0; r < n; r += nwarps) {
-      double sacc = 0.0;
-      for (int q = a.p[r] + lane; q < a.p[r + 1]; q += 32) sacc = fma(a.v[q], Vj[a.c[q]], sacc);
-      sacc = warp_sum(sacc);
-      if (lane == 0) w[r] = sacc;
-    }
+    arnoldi_spmv(n, a.p, a.c, a.v, Vj, w, a.vs, i0, stride);
     grid.sync();  // w complete
     const double before2 = gdot(w, w);
     double hcolj = 0.0;  // unused by blocks > 0
@@ -570,10 +588,10 @@ __global__ void __launch_bounds__(256) arnoldi_grid_kernel(ArnoldiGridArgs a) {
 }
 
 static int arnoldi_grid(int n, const int* p, const int* c, const double* v, const double* b, int m,
-                        double* H_h, int* k_h, double* beta_h, cudaStream_t s) {
+                        double* H_h, int* k_h, double* beta_h, int vs, cudaStream_t s) {
   double *V = nullptr, *w = nullptr, *sc = nullptr, *Hd = nullptr;
   int* info = nullptr;
-  const int np = blocks_for(n, 256, 148 * 4);
+  const int np = arnoldi_parts(n, vs);
   AIRG_TRY(scratch(&V, (size_t)(m + 1) * n, s));
   AIRG_TRY(scratch(&w, n, s));
   AIRG_TRY(scratch(&sc, 2 * np + 8, s));
@@ -593,7 +611,7 @@ static int arnoldi_grid(int n, const int* p, const int* c, const double* v, cons
     set_error("cannot build a Krylov space from a zero vector");
     return AIRG_ERR_VALUE;
   }
-  ArnoldiGridArgs a{n, m, p, c, v, b, beta, V, w, Hd, sc + 8, info};
+  ArnoldiGridArgs a{n, m, p, c, v, b, beta, V, w, Hd, sc + 8, info, vs};
   void* args[] = {&a};
   AIRG_CUDA(cudaLaunchCooperativeKernel((const void*)arnoldi_grid_kernel, np, 256, args, 0, s));
   int k = 0;
@@ -607,7 +625,7 @@ static int arnoldi_grid(int n, const int* p, const int* c, const double* v, cons
 
 // whether the cooperative kernel fits co-resident (it always does on B200:
 // at most 592 blocks of 256 threads); otherwise the multi-kernel path
-static bool grid_arnoldi_ok(int n) {
+static bool grid_arnoldi_ok(int n, int vs) {
   static int max_blocks = -1;
   if (max_blocks < 0) {
     int per_sm = 0, dev = 0, coop = 0;
@@ -618,7 +636,7 @@ static bool grid_arnoldi_ok(int n) {
       per_sm = 0;
     max_blocks = per_sm * num_sms();
   }
-  return !getenv("AIRG_ARNOLDI_MULTI") && blocks_for(n, 256, 148 * 4) <= max_blocks;
+  return !getenv("AIRG_ARNOLDI_MULTI") && arnoldi_parts(n, vs) <= max_blocks;
 }
 
 }  // namespace airg
@@ -688,8 +706,12 @@ extern "C" int airg_arnoldi(int n, const int32_t* p, const int32_t* c, const dou
     }
     *k_h = hi[0];
   } else {
-    st = grid_arnoldi_ok(n) ? arnoldi_grid(n, p, c, v, b, m, H_h, k_h, beta_h, s)
-                            : arnoldi_multi(n, p, c, v, b, m, H_h, k_h, beta_h, s);
+    int nnz = 0;
+    AIRG_CUDA(cudaMemcpyAsync(&nnz, p + n, sizeof(int), cudaMemcpyDeviceToHost, s));
+    AIRG_CUDA(cudaStreamSynchronize(s));
+    const int vs = arnoldi_vs(nnz, n);
+    st = grid_arnoldi_ok(n, vs) ? arnoldi_grid(n, p, c, v, b, m, H_h, k_h, beta_h, vs, s)
+                                : arnoldi_multi(n, p, c, v, b, m, H_h, k_h, beta_h, vs, s);
     if (st != AIRG_OK) return st;
   }
   // numerically zero on the Krylov space? (polynomial.py:108-109)

@@ -426,15 +426,19 @@ def test_gpu_setup_replayed_by_oracle_512():
     assert np.max(np.abs(np.array(st.residual_history) - hist)) <= 1e-10 * hist[0]
 
 
-@pytest.mark.parametrize('order', [6, 40])
-def test_grid_arnoldi_bitwise_multi_kernel(G, order):
-    """The one-launch cooperative Arnoldi (operators > 4096 rows) computes the
+@pytest.mark.parametrize('order,power', [(6, 1), (40, 1), (6, 3), (6, 6)])
+def test_grid_arnoldi_bitwise_multi_kernel(G, order, power):
+    """The one-launch cooperative Arnoldi (operators > 1024 rows) computes the
     multi-kernel recurrence with the same per-element assignment and
-    reduction order: H, k and beta bitwise equal."""
+    reduction order: H, k and beta bitwise equal.  Powers of the stencil
+    give 3 / ~10 / ~28 entries per row (1, 2 and 8 SpMV lanes per row)."""
     import os
     from paper_2508_17517_b200.csr import random_unit_vector
     from paper_2508_17517_b200.gmres_poly import hessenberg
     A, _ = G.build_advection_2d(G.AdvectionProblem(nx=120, ny=110, vx=HARD[0], vy=HARD[1]))
+    A1 = A
+    for _ in range(power - 1):
+        A = G.spgemm(A, A1)
     b = random_unit_vector(A.nrows, 3)
     H1, k1, b1 = hessenberg(A, order + 1, b)
     os.environ['AIRG_ARNOLDI_MULTI'] = '1'

@@ -35,6 +35,7 @@ amg_setup.cf_split = split_hook  # build_levels imports it per call
 cfsplit.cf_split = split_hook
 orig_call = L.call
 per = {}
+per_level = {}
 
 
 def call_hook(name, *args):
@@ -44,6 +45,8 @@ def call_hook(name, *args):
         rec = per.setdefault(name, [0, 0.0])
         rec[0] += 1
         rec[1] += time.perf_counter() - t0
+    lvl = per_level.setdefault(state['level'], {})
+    lvl[name] = lvl.get(name, 0.0) + time.perf_counter() - t0
     return r
 
 
@@ -54,6 +57,7 @@ H = None
 for rep in range(3):
     H = None
     per.clear()
+    per_level.clear()
     state.update(level=-1, t_level=None)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -68,3 +72,10 @@ print(f'setup {1e3 * (t1 - t0):.1f} ms; levels >= {lv0} (incl. coarse build) wal
 print('per level wall (ms):', {k: round(1e3 * v, 2) for k, v in sorted(marks.items())})
 for k, v in sorted(per.items(), key=lambda kv: -kv[1][1]):
     print(f'{v[1] * 1e3:8.2f} ms {v[0]:4d} calls  {k}')
+top = ['airg_galerkin', 'airg_spgemm', 'airg_poly_assemble', 'airg_arnoldi', 'airg_restriction',
+       'airg_ddc_pass', 'airg_cf_pmisr', 'airg_extract']
+print('per level, ms in: ' + ' '.join(t[5:] for t in top) + ' other')
+for lv in sorted(per_level):
+    d = per_level[lv]
+    oth = sum(v for k, v in d.items() if k not in top)
+    print(f'{lv:>3} ' + ' '.join(f'{1e3 * d.get(t, 0):7.2f}' for t in top) + f' {1e3 * oth:7.2f}')
