@@ -240,7 +240,117 @@ struct PolyArgs {
   size_t gstride;
 };
 
-template <class PM>
+// One power of the warp-per-row assembly: nxt[pos(j)] += cur[q] * A[q, j]
+// over the present positions q in ascending order, lanes splitting the A
+// row of col_q (distinct columns -> distinct positions; rows in order, so
+// the summation order is the reference's).  Software-pipelined: while the
+// products of one A row are formed, the first KP x 32 entries of the
+// next present row are already loading into the other register set (two
+// named sets, no register copies of pending loads), and the next 32-position
+// block's row bounds are fetched when a block is entered.  Entries beyond
+// KP x 32 of a row load in place (KP from the class's pattern length).
+template <int KP>
+struct PolyRowRegs {
+  int c[KP];
+  double v[KP];
+  int b, e;
+  double l;
+};
+
+template <class PM, int KP>
+__device__ __forceinline__ void poly_power_walk(const PolyArgs& a, const PM& pm, int pb, int m,
+                                                int lane, const double* cur,
+                                                const unsigned char* fcur, double* nxt,
+                                                unsigned char* fnxt) {
+  // block metadata (per lane: position base + lane)
+  auto meta = [&](int base, int& rb, int& re, double& lv) -> unsigned {
+    const int q = base + lane;
+    const bool pres = q < m && fcur[q];
+    rb = re = 0;
+    lv = 0.0;
+    if (pres) {
+      const int col_q = a.Pc[pb + q];
+      const int rq = a.rowmap ? a.rowmap[col_q] : col_q;
+      rb = a.Ap[rq];
+      re = a.Ap[rq + 1];
+      lv = cur[q];
+    }
+    return __ballot_sync(0xffffffffu, pres);
+  };
+  int base = 0, rb, re, nrb = 0, nre = 0;
+  double lv, nlv = 0.0;
+  unsigned todo = meta(0, rb, re, lv), ntodo = 0;
+  if (m > 32) ntodo = meta(32, nrb, nre, nlv);
+  // next present position: (row bounds, coefficient) broadcast from its lane
+  auto next = [&](int& b, int& e, double& l) -> bool {
+    while (!todo) {
+      base += 32;
+      if (base >= m) return false;
+      todo = ntodo;
+      rb = nrb;
+      re = nre;
+      lv = nlv;
+      ntodo = 0;
+      if (base + 32 < m) ntodo = meta(base + 32, nrb, nre, nlv);
+    }
+    const int t = __ffs(todo) - 1;
+    todo &= todo - 1;
+    b = __shfl_sync(0xffffffffu, rb, t);
+    e = __shfl_sync(0xffffffffu, re, t);
+    l = __shfl_sync(0xffffffffu, lv, t);
+    return true;
+  };
+  auto issue = [&](PolyRowRegs<KP>& R) {
+    const int len = R.e - R.b;
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+      const bool p = 32 * q + lane < len;
+      R.c[q] = -1;
+      R.v[q] = 0.0;
+      ld_pred(R.c[q], a.Ac + R.b + 32 * q + lane, p);
+      ld_pred(R.v[q], a.Av + R.b + 32 * q + lane, p);
+    }
+  };
+  auto process = [&](const PolyRowRegs<KP>& R) {
+#pragma unroll
+    for (int q = 0; q < KP; ++q) {
+      if (R.c[q] >= 0) {
+        const int p = pm.find(R.c[q]);
+        if (p >= 0) {
+          nxt[p] = add_rn(nxt[p], mul_rn(R.l, R.v[q]));
+          fnxt[p] = 1;
+        }
+      }
+    }
+    for (int jj = R.b + 32 * KP + lane; jj < R.e; jj += 32) {
+      const int p = pm.find(a.Ac[jj]);
+      if (p >= 0) {
+        nxt[p] = add_rn(nxt[p], mul_rn(R.l, a.Av[jj]));
+        fnxt[p] = 1;
+      }
+    }
+    __syncwarp();
+  };
+  PolyRowRegs<KP> A, B;
+  if (!next(A.b, A.e, A.l)) return;
+  issue(A);
+  while (true) {
+    if (!next(B.b, B.e, B.l)) {
+      process(A);
+      return;
+    }
+    issue(B);
+    process(A);
+    if (!next(A.b, A.e, A.l)) {
+      process(B);
+      return;
+    }
+    issue(A);
+    process(B);
+  }
+}
+
+template <class PM, int KP>
 __global__ void __launch_bounds__(128) poly_assemble_kernel(PolyArgs a) {
   extern __shared__ unsigned char smraw[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -320,56 +430,9 @@ __global__ void __launch_bounds__(128) poly_assemble_kernel(PolyArgs a) {
       __syncwarp();
     }
     for (int k = 2; k <= d; ++k) {
-      // nxt = mask(cur * A): walk present entries of cur in column (= position)
-      // order; the A-row bounds of 32 positions are fetched at once (one per
-      // lane) and the next present row's head is loaded before the current
-      // row is processed.
-      for (int base = 0; base < m; base += 32) {
-        const int q = base + lane;
-        const bool pres = q < m && fcur[q];
-        int rb = 0, re = 0;
-        double lv = 0.0;
-        if (pres) {
-          const int col_q = a.Pc[pb + q];
-          const int rq = a.rowmap ? a.rowmap[col_q] : col_q;
-          rb = a.Ap[rq];
-          re = a.Ap[rq + 1];
-          lv = cur[q];
-        }
-        unsigned todo = __ballot_sync(0xffffffffu, pres);
-        int t = todo ? __ffs(todo) - 1 : 0;
-        int cb = __shfl_sync(0xffffffffu, rb, t), ce = __shfl_sync(0xffffffffu, re, t);
-        int hc = cb + lane < ce ? a.Ac[cb + lane] : -1;
-        double hv = cb + lane < ce ? a.Av[cb + lane] : 0.0;
-        while (todo) {
-          const double l = __shfl_sync(0xffffffffu, lv, t);
-          const int tb = cb, te = ce, c0 = hc;
-          const double v0 = hv;
-          todo &= todo - 1;
-          if (todo) {  // prefetch the head of the next present row
-            t = __ffs(todo) - 1;
-            cb = __shfl_sync(0xffffffffu, rb, t);
-            ce = __shfl_sync(0xffffffffu, re, t);
-            hc = cb + lane < ce ? a.Ac[cb + lane] : -1;
-            hv = cb + lane < ce ? a.Av[cb + lane] : 0.0;
-          }
-          if (c0 >= 0) {
-            const int p = pm.find(c0);
-            if (p >= 0) {
-              nxt[p] = add_rn(nxt[p], mul_rn(l, v0));
-              fnxt[p] = 1;
-            }
-          }
-          for (int jj = tb + 32 + lane; jj < te; jj += 32) {
-            const int p = pm.find(a.Ac[jj]);
-            if (p >= 0) {
-              nxt[p] = add_rn(nxt[p], mul_rn(l, a.Av[jj]));
-              fnxt[p] = 1;
-            }
-          }
-          __syncwarp();
-        }
-      }
+      // nxt = mask(cur * A): the present entries of cur in column (= position)
+      // order, software-pipelined (poly_power_walk)
+      poly_power_walk<PM, KP>(a, pm, pb, m, lane, cur, fcur, nxt, fnxt);
       const double ck = a.coef[k];
       for (int i = lane; i < m; i += 32) {
         if (fnxt[i]) {
@@ -633,8 +696,8 @@ template <class PM>
 static int launch_poly_class(PolyArgs b, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    AIRG_CUDA(cudaFuncSetAttribute(poly_assemble_kernel<PM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   smem_optin()));
+    for (auto k : {poly_assemble_kernel<PM, 1>, poly_assemble_kernel<PM, 2>, poly_assemble_kernel<PM, 4>})
+      AIRG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin()));
     AIRG_CUDA(cudaFuncSetAttribute(poly_assemble_block_kernel<PM>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin()));
     attr = true;
@@ -643,7 +706,10 @@ static int launch_poly_class(PolyArgs b, cudaStream_t st) {
   if (b.cap < kPolyBlockCap && per <= (size_t)smem_optin()) {
     int warps = 4;
     while (warps > 1 && per * warps > (size_t)smem_optin()) warps >>= 1;
-    poly_assemble_kernel<PM><<<blocks_for(b.nrows, warps, 148 * 32), warps * 32, per * warps, st>>>(b);
+    // A-row entries held per lane in the pipeline: the class's row length
+    auto k = b.cap <= 32 ? poly_assemble_kernel<PM, 1>
+                         : b.cap <= 64 ? poly_assemble_kernel<PM, 2> : poly_assemble_kernel<PM, 4>;
+    k<<<blocks_for(b.nrows, warps, 148 * 32), warps * 32, per * warps, st>>>(b);
     AIRG_LAUNCH_CHECK();
     return AIRG_OK;
   }
