@@ -57,69 +57,50 @@ __device__ __forceinline__ void chain_stamp(const ChainArgs& a, int p) {
 // (ceil(len / (kChainU VS)): a short row takes a full round trip like a long
 // one) plus a fixed overhead; w is the exclusive prefix of that cost, CTA g
 // gets rows [r0, r1) with w split evenly, and the staged prefix [r0, rs) is
-// the longest that fits `cap` bytes.  One CTA scans the rows (plan build).
+// the longest that fits `cap` bytes (plan build: cost kernel, device scan,
+// one thread per CTA of the chain).
 __device__ __forceinline__ long long chain_stage_bytes(const int* ptr, int r0, int rs) {
   const long long k = (long long)__ldg(ptr + rs) - __ldg(ptr + r0);
   return 4LL * (rs - r0 + 1) + 12LL * k + 48;
 }
-__global__ void __launch_bounds__(1024) chain_partition_kernel(int n, const int* __restrict__ ptr,
-                                                               int vs, int G, long long cap,
-                                                               long long* __restrict__ w,
-                                                               int* __restrict__ part) {
-  __shared__ long long sums[1024];
-  const int t = threadIdx.x, T = blockDim.x;
-  const int per = (n + T - 1) / T, lo = min(n, t * per), hi = min(n, lo + per);
+__global__ void chain_cost_kernel(int n, const int* __restrict__ ptr, int vs,
+                                  long long* __restrict__ cost) {
   const int step = kChainU * vs;
-  auto cost = [&](int i) -> long long {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
     const int len = __ldg(ptr + i + 1) - __ldg(ptr + i);
-    return (long long)((len + step - 1) / step) * step + 4;
-  };
-  long long acc = 0;
-  for (int i = lo; i < hi; ++i) acc += cost(i);
-  sums[t] = acc;
-  __syncthreads();
-  if (t == 0) {
-    long long run = 0;
-    for (int q = 0; q < T; ++q) {
-      const long long v = sums[q];
-      sums[q] = run;
-      run += v;
-    }
-    w[n] = run;
+    cost[i] = (long long)((len + step - 1) / step) * step + 4;
   }
-  __syncthreads();
-  acc = sums[t];
-  for (int i = lo; i < hi; ++i) {
-    w[i] = acc;
-    acc += cost(i);
-  }
-  __syncthreads();
+}
+// w: exclusive prefix of the row costs (n + 1 entries, w[n] the total)
+__global__ void chain_partition_kernel(int n, const int* __restrict__ ptr, int G, long long cap,
+                                       const long long* __restrict__ w, int* __restrict__ part) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= G) return;
   const long long W = w[n];
-  for (int g = t; g < G; g += T) {
-    auto bound = [&](int q) {  // first row i with w[i] >= q W / G
-      if (q <= 0) return 0;
-      if (q >= G) return n;
-      const long long tg = W * q / G;
-      int a = 0, b = n;
-      while (a < b) {
-        const int m = (a + b) >> 1;
-        if (w[m] < tg) a = m + 1; else b = m;
-      }
-      return a;
-    };
-    const int r0 = bound(g), r1 = bound(g + 1);
-    int a = r0, b = r1;  // largest rs in [r0, r1] with bytes(rs) <= cap
+  auto bound = [&](int q) {  // first row i with w[i] >= q W / G
+    if (q <= 0) return 0;
+    if (q >= G) return n;
+    const long long tg = W * q / G;
+    int a = 0, b = n;
     while (a < b) {
-      const int m = (a + b + 1) >> 1;
-      if (chain_stage_bytes(ptr, r0, m) <= cap) a = m; else b = m - 1;
+      const int m = (a + b) >> 1;
+      if (w[m] < tg) a = m + 1; else b = m;
     }
-    part[3 * g] = r0;
-    part[3 * g + 1] = a;
-    part[3 * g + 2] = r1;
-    // shared bytes this CTA stages (+ alignment slack): the launch asks for
-    // the maximum, leaving the rest of the SM's 256 KB to L1 (x gathers)
-    atomicMax(part + 3 * G, (int)(a > r0 ? chain_stage_bytes(ptr, r0, a) + 64 : 0));
+    return a;
+  };
+  const int r0 = bound(g), r1 = bound(g + 1);
+  int a = r0, b = r1;  // largest rs in [r0, r1] with bytes(rs) <= cap
+  while (a < b) {
+    const int m = (a + b + 1) >> 1;
+    if (chain_stage_bytes(ptr, r0, m) <= cap) a = m; else b = m - 1;
   }
+  part[3 * g] = r0;
+  part[3 * g + 1] = a;
+  part[3 * g + 2] = r1;
+  // shared bytes this CTA stages (+ alignment slack): the launch asks for
+  // the maximum, leaving the rest of the SM's 256 KB to L1 (x gathers)
+  atomicMax(part + 3 * G, (int)(a > r0 ? chain_stage_bytes(ptr, r0, a) + 64 : 0));
 }
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {

@@ -1282,6 +1282,9 @@ int airg_plan_set_coarse(airg_plan* p, int n, const int32_t* ptr, const int32_t*
 }  // extern "C"
 
 // ---- fused smoother chain (chain.cuh) ---------------------------------------
+namespace airg {
+int scan_counts64(const long long* in, long long* out, int n, long long* total_h, cudaStream_t s);
+}
 static int chain_smem() {
   static int v = 0;
   if (!v) {
@@ -1331,10 +1334,15 @@ static int prepare_chain(LevelOps& L, cudaStream_t s) {
   // staging capacity per CTA (AIRG_CHAIN_CAP lowers it: tests of the unstaged rows)
   long long cap = chain_smem() - 128;
   if (getenv("AIRG_CHAIN_CAP")) cap = std::min(cap, atoll(getenv("AIRG_CHAIN_CAP")));
-  long long* w = nullptr;
+  long long *cost = nullptr, *w = nullptr;
+  AIRG_TRY(scratch(&cost, (size_t)L.n_f, s));
   AIRG_TRY(scratch(&w, (size_t)L.n_f + 1, s));
-  chain_partition_kernel<<<1, 1024, 0, s>>>(L.n_f, L.Aff.ptr, L.Aff.vs, G, cap, w, L.chain_part);
+  chain_cost_kernel<<<blocks_for(L.n_f, 256), 256, 0, s>>>(L.n_f, L.Aff.ptr, L.Aff.vs, cost);
   AIRG_LAUNCH_CHECK();
+  AIRG_TRY(airg::scan_counts64(cost, w, L.n_f, nullptr, s));
+  chain_partition_kernel<<<(G + 127) / 128, 128, 0, s>>>(L.n_f, L.Aff.ptr, G, cap, w, L.chain_part);
+  AIRG_LAUNCH_CHECK();
+  release(cost, s);
   release(w, s);
   int need = 0;  // one read per level at plan build: the launch's shared bytes
   AIRG_CUDA(cudaMemcpyAsync(&need, L.chain_part + 3 * G, sizeof(int), cudaMemcpyDeviceToHost, s));

@@ -69,7 +69,13 @@ int main(int argc, char** argv) {
   const int smem = optin - 1024;
   long long* wbuf; cudaMalloc(&wbuf, 8 * (n + 1));
   const int vs = argc > 5 ? atoi(argv[5]) : 32;
-  chain_partition_kernel<<<1, 1024>>>(n, dp, vs, G, smem - 128, wbuf, part);
+  {  // exclusive prefix of the row costs on the host (test harness)
+    std::vector<long long> w(n + 1, 0);
+    const int step = kChainU * vs;
+    for (int i = 0; i < n; ++i) w[i + 1] = w[i] + (long long)((ptr[i + 1] - ptr[i] + step - 1) / step) * step + 4;
+    cudaMemcpy(wbuf, w.data(), 8 * (n + 1), cudaMemcpyHostToDevice);
+  }
+  chain_partition_kernel<<<(G + 127) / 128, 128>>>(n, dp, G, smem - 128, wbuf, part);
   int need = 0;
   cudaMemcpy(&need, part + 3 * G, 4, cudaMemcpyDeviceToHost);
   const int lsmem = argc > 6 && atoi(argv[6]) ? std::min(smem, ((need + 1023) / 1024) * 1024 + 1024) : smem;
