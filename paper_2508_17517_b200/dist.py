@@ -233,9 +233,15 @@ class Halo:
 
 
 def remote_cols(col, part, rank):
-    c = col.to(I64)
+    """Sorted distinct global columns outside this rank's range: a flag per
+    global column (one scatter over the column array, one compaction) -- no
+    int64 copy of the column array and no sort."""
     lo, hi = part.lo(rank), part.hi(rank)
-    return torch.unique(c[(c < lo) | (c >= hi)])
+    f = torch.zeros(part.n, dtype=torch.bool, device=col.device)
+    if col.numel():
+        f[col] = True
+    f[lo:hi] = False
+    return f.nonzero().squeeze(1)
 
 
 def cat_rows(M, gptr, gcol, gval, ncols):

@@ -12,8 +12,9 @@ def main():
     from paper_2508_17517_b200 import dist as D
     comm = D.Comm()
     v = (float(np.cos(np.pi / 4)), float(np.sin(np.pi / 4)))
-    G.reserve_memory(2048 * 2048 * 1600, 2048 * 2048 * 4000)
-    Ad = D.advection_2d_strips(comm, 2048, 2048 * comm.world, *v)
+    nx = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
+    G.reserve_memory(nx * nx * 1600, nx * nx * 4000)
+    Ad = D.advection_2d_strips(comm, nx, nx * comm.world, *v)
     for _ in range(2):
         DH = D.setup_distributed(comm, Ad, G.SetupConfig())
     torch.cuda.synchronize(); dist.barrier()
@@ -24,7 +25,7 @@ def main():
     pr.disable()
     if comm.rank == 0:
         s = io.StringIO()
-        pstats.Stats(pr, stream=s).sort_stats('cumulative').print_stats(40)
+        pstats.Stats(pr, stream=s).sort_stats(os.environ.get('SORT', 'cumulative')).print_stats(45)
         print(s.getvalue()[:9000])
     dist.destroy_process_group()
 
