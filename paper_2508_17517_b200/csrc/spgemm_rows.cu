@@ -804,16 +804,65 @@ __global__ void __launch_bounds__(32 * NW) ap_onepoint_kernel(
   }
 }
 
+// Short rows (L <= G entries, G lanes per row, 32 / G rows per warp): the
+// merge in registers.  Lane j holds A's j-th entry with its mapped column; a
+// lane is the head of its column if no earlier lane has it, its output
+// position is the number of head columns below it, and the head sums the
+// column's values over the lanes in order -- A's column order, the same sum
+// as the sorted-run path above (bitwise).
+template <int G>
+__global__ void __launch_bounds__(256) ap_small_kernel(
+    int nr, const int* __restrict__ rows, const int* __restrict__ Ap, const int* __restrict__ Ac,
+    const double* __restrict__ Av, const int* __restrict__ pcol, int* __restrict__ rcol,
+    double* __restrict__ rval, int* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31, j = lane & (G - 1);
+  const long long groups = ((long long)gridDim.x * blockDim.x) / G;
+  // warp-uniform trip count: the groups of a warp shuffle together
+  for (long long g0 = ((long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / G; g0 < nr;
+       g0 += groups) {
+    const long long r = g0 + lane / G;
+    const bool live = r < nr;
+    const int row = live ? rows[r] : 0;
+    const int b = live ? Ap[row] : 0, L = live ? Ap[row + 1] - b : 0;
+    const bool has = j < L;
+    const int c = has ? pcol[Ac[b + j]] : INT_MAX;
+    const double a = has ? Av[b + j] : 0.0;
+    bool head = has;
+    int pos = 0;
+    double sum = 0.0;
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      const int ci = __shfl_sync(kFull, c, i, G);
+      const double ai = __shfl_sync(kFull, a, i, G);
+      if (i < j && ci == c) head = false;
+      if (ci == c) sum = add_rn(sum, mul_rn(ai, 1.0));
+    }
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      const int ci = __shfl_sync(kFull, c, i, G);
+      const bool hi = __shfl_sync(kFull, head, i, G);
+      if (hi && ci < c) ++pos;
+    }
+    if (head) {
+      rcol[b + pos] = c;
+      rval[b + pos] = sum;
+    }
+    const unsigned bal = __ballot_sync(kFull, head);
+    if (live && j == 0) cnt[row] = __popc((bal >> (lane & ~(G - 1))) & (G == 32 ? kFull : ((1u << G) - 1u)));
+  }
+}
+
+// raw rows (at A's offsets) -> compacted output, vs lanes per row
 __global__ void ap_compact_kernel(int n, const int* __restrict__ Ap, const int* __restrict__ Cp,
                                   const int* __restrict__ rcol, const double* __restrict__ rval,
-                                  int* __restrict__ oc, double* __restrict__ ov) {
-  const int lane = threadIdx.x & 31;
-  for (long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; r < n;
-       r += ((long long)gridDim.x * blockDim.x) >> 5) {
+                                  int* __restrict__ oc, double* __restrict__ ov, int vs) {
+  const int j = threadIdx.x & (vs - 1);
+  for (long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / vs; r < n;
+       r += ((long long)gridDim.x * blockDim.x) / vs) {
     const int b = Ap[r], o = Cp[r], u = Cp[r + 1] - o;
-    for (int j = lane; j < u; j += 32) {
-      oc[o + j] = rcol[b + j];
-      ov[o + j] = rval[b + j];
+    for (int q = j; q < u; q += vs) {
+      oc[o + q] = rcol[b + q];
+      ov[o + q] = rval[b + q];
     }
   }
 }
@@ -828,13 +877,15 @@ static int ap_onepoint(const Mat& A, int nc, const int* pcol, airg_csr_result** 
   AIRG_LAUNCH_CHECK();
   Classes cl;
   int annz32 = 0;
-  AIRG_TRY(classify(n, len, {256, kApCap}, cl, s, A.p + n, &annz32));
+  // classes: <= 8 and <= 32 entries (register merge), <= 256 and <= kApCap
+  // (staged radix sort), longer (general product)
+  AIRG_TRY(classify(n, len, {8, 32, 256, kApCap}, cl, s, A.p + n, &annz32));
   release(len, s);
   // rows beyond the staging buffer, or (measurement knob AIRG_AP_AVG) a mean
   // row length above the cutoff, go to the general hash product
   static const long long avg_cap = getenv("AIRG_AP_AVG") ? atoll(getenv("AIRG_AP_AVG")) : (1ll << 40);
   const long long annz = annz32;
-  if (cl.count[2] > 0 || annz > avg_cap * n) {
+  if (cl.count[4] > 0 || annz > avg_cap * n) {
     release(cl.lists, s);
     int* Pp = nullptr;
     double* Pv = nullptr;
@@ -867,12 +918,20 @@ static int ap_onepoint(const Mat& A, int nc, const int* pcol, airg_csr_result** 
   Fork fk;
   AIRG_TRY(fk.begin(s));
   if (cl.count[0])
-    ap_onepoint_kernel<256, kW0><<<blocks_for(cl.count[0], kW0, 148 * 4), 32 * kW0, shm0, fk.stream(0)>>>(
+    ap_small_kernel<8><<<blocks_for((long long)cl.count[0] * 8, 256), 256, 0, fk.stream(0)>>>(
         cl.count[0], cl.list(0), A.p, A.c, A.v, pcol, rcol, rval, cnt);
   AIRG_LAUNCH_CHECK();
   if (cl.count[1])
-    ap_onepoint_kernel<kApCap, kW1><<<blocks_for(cl.count[1], kW1, 148 * 4), 32 * kW1, shm1,
-                                      fk.stream(1)>>>(cl.count[1], cl.list(1), A.p, A.c, A.v, pcol,
+    ap_small_kernel<32><<<blocks_for((long long)cl.count[1] * 32, 256), 256, 0, fk.stream(1)>>>(
+        cl.count[1], cl.list(1), A.p, A.c, A.v, pcol, rcol, rval, cnt);
+  AIRG_LAUNCH_CHECK();
+  if (cl.count[2])
+    ap_onepoint_kernel<256, kW0><<<blocks_for(cl.count[2], kW0, 148 * 4), 32 * kW0, shm0, fk.stream(2)>>>(
+        cl.count[2], cl.list(2), A.p, A.c, A.v, pcol, rcol, rval, cnt);
+  AIRG_LAUNCH_CHECK();
+  if (cl.count[3])
+    ap_onepoint_kernel<kApCap, kW1><<<blocks_for(cl.count[3], kW1, 148 * 4), 32 * kW1, shm1,
+                                      fk.stream(3)>>>(cl.count[3], cl.list(3), A.p, A.c, A.v, pcol,
                                                       rcol, rval, cnt);
   AIRG_LAUNCH_CHECK();
   AIRG_TRY(fk.end(s));
@@ -881,9 +940,11 @@ static int ap_onepoint(const Mat& A, int nc, const int* pcol, airg_csr_result** 
   long long nnz = 0;
   AIRG_TRY(scan_counts(cnt, r->ptr, n, &nnz, s));
   AIRG_TRY(result_alloc_entries(r, nnz, true));
-  if (n > 0)
-    ap_compact_kernel<<<blocks_for((long long)n * 32, 256), 256, 0, s>>>(n, A.p, r->ptr, rcol, rval,
-                                                                        r->col, r->val);
+  if (n > 0) {
+    const int vs = annz <= 4LL * n ? 4 : annz <= 16LL * n ? 8 : 32;  // lanes per row
+    ap_compact_kernel<<<blocks_for((long long)n * vs, 256), 256, 0, s>>>(n, A.p, r->ptr, rcol, rval,
+                                                                        r->col, r->val, vs);
+  }
   AIRG_LAUNCH_CHECK();
   release(rcol, s);
   release(rval, s);

@@ -364,11 +364,12 @@ def test_setup_errors(G):
     assert st.converged and st.iterations <= 2
 
 
-@pytest.mark.parametrize('seed', [0, 1, 2])
-def test_ap_onepoint_structural_zeros(G, seed):
-    """A P for a one-point P (the warp-per-row column merge): structure =
-    structural product, values summed in A's column order, exact
-    cancellations kept as +0.0 -- bitwise the oracle's spgemm(A, P)."""
+@pytest.mark.parametrize('seed,maxlen', [(0, 40), (1, 40), (2, 40), (3, 700), (4, 6)])
+def test_ap_onepoint_structural_zeros(G, seed, maxlen):
+    """A P for a one-point P (register merge for rows <= 8 / <= 32 entries,
+    staged radix sort up to 1024): structure = structural product, values
+    summed in A's column order, exact cancellations kept as +0.0 -- bitwise
+    the oracle's spgemm(A, P)."""
     import ctypes as C
     import torch
     from paper_2508_17517_b200 import _lib as L
@@ -376,8 +377,10 @@ def test_ap_onepoint_structural_zeros(G, seed):
     rng = np.random.default_rng(seed)
     n, nc = 300, 40
     rows, cols, vals = [], [], []
+    if maxlen > n:
+        n = 2 * maxlen
     for i in range(n):
-        k = int(rng.integers(1, 40))
+        k = int(rng.integers(1, maxlen))
         cs = np.unique(rng.integers(0, n, size=k))
         vs = rng.choice([1.0, -1.0, 0.5, -0.5, 1e-300, 3.0], size=len(cs))
         rows += [i] * len(cs)
