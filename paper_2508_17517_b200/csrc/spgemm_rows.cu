@@ -422,17 +422,188 @@ static int gather_ll(const long long* d, const std::vector<int>& rows, std::vect
   return AIRG_OK;
 }
 
+// ---- rows with few products: the whole row in registers ---------------------
+// G lanes per row (32 / G rows per warp), for rows with at most G products
+// and at most G entries in A's row.  Lane t forms product t in scipy's
+// generation order (A's row in order, each B row in order); a lane is the
+// head of its column if no earlier lane has the column, its output position
+// is the number of head columns below it, and the head sums the column's
+// products over the lanes in order: 0 + p_1 + p_2 + ... (separate roundings),
+// the order of the hash and span kernels -- bitwise the same rows.  Count
+// pass: the number of heads.  Numeric pass: the values, written at the
+// row's offset (mode 0), or drop/lump (drop_lump_row's rules, dropped values
+// summed in column order) at the raw offset Cp[row] + row (mode 1).
+struct RegArgs {
+  const int *Ap, *Ac;
+  const double* Av;
+  const int *Bp, *Bc;
+  const double* Bv;
+  const int* rows;
+  int nrows;
+  int count_only;
+  const int* Cp;
+  int* Cc;
+  double* Cv;
+  int negate, mode;
+  double tol;
+  int lump;
+  int* cnt;       // count pass: unique columns; mode 1: entries written
+  int* any_drop;
+  int row0;
+};
+
+template <int G>
+__global__ void __launch_bounds__(256) spgemm_reg_kernel(RegArgs a) {
+  const int lane = threadIdx.x & 31, j = lane & (G - 1), gbase = lane & ~(G - 1);
+  const unsigned gmask = G == 32 ? kFull : ((1u << G) - 1u) << gbase;
+  const long long groups = ((long long)gridDim.x * blockDim.x) / G;
+  for (long long g0 = ((long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / G; g0 < a.nrows;
+       g0 += groups) {  // warp-uniform trip count: the groups of a warp shuffle together
+    const long long r = g0 + lane / G;
+    const bool live = r < a.nrows;
+    const int row = live ? a.rows[r] : 0;
+    const int ab = live ? a.Ap[row] : 0, na = live ? a.Ap[row + 1] - ab : 0;
+    int bb = 0, bl = 0;
+    double av = 0.0;
+    if (j < na) {
+      const int k = a.Ac[ab + j];
+      av = a.Av[ab + j];
+      bb = a.Bp[k];
+      bl = a.Bp[k + 1] - bb;
+    }
+    int incl = bl;  // inclusive scan of the B-row lengths over the group
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, incl, o, G);
+      if (j >= o) incl += y;
+    }
+    const int excl = incl - bl;
+    const int P = __shfl_sync(kFull, incl, G - 1, G);
+    // product j: the A entry q with excl_q <= j < incl_q
+    int q = 0;
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      const int ei = __shfl_sync(kFull, excl, i, G), li = __shfl_sync(kFull, bl, i, G);
+      if (j >= ei && j < ei + li) q = i;
+    }
+    const int bq = __shfl_sync(kFull, bb, q, G), eq = __shfl_sync(kFull, excl, q, G);
+    const double aq = __shfl_sync(kFull, av, q, G);
+    const bool has = j < P;
+    const int c = has ? a.Bc[bq + j - eq] : INT_MAX;
+    const double pv = has ? mul_rn(aq, a.Bv[bq + j - eq]) : 0.0;
+    bool head = has;
+    double sum = 0.0;
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      const int ci = __shfl_sync(kFull, c, i, G);
+      const double pi = __shfl_sync(kFull, pv, i, G);
+      if (i < j && ci == c) head = false;
+      if (i < P && ci == c) sum = add_rn(sum, pi);
+    }
+    int pos = 0;
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      const int ci = __shfl_sync(kFull, c, i, G);
+      const bool hi = __shfl_sync(kFull, head, i, G);
+      if (hi && ci < c) ++pos;
+    }
+    const int U = __popc(__ballot_sync(kFull, head) & gmask);
+    if (a.count_only) {
+      if (live && j == 0) a.cnt[row] = U;
+      continue;
+    }
+    if (a.mode == 0) {
+      if (head) {
+        const long long o = (long long)a.Cp[row] + pos;
+        a.Cc[o] = c;
+        a.Cv[o] = a.negate ? -sum : sum;
+      }
+      continue;
+    }
+    // ---- mode 1: drop / lump (drop_lump_row) ----
+    const int diag = a.row0 + row;
+    double mx = head ? fabs(sum) : 0.0;
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(kFull, mx, o, G));
+    const unsigned dball = __ballot_sync(kFull, head && c == diag) & gmask;
+    const bool has_diag = dball != 0u;
+    const double thr = mul_rn(a.tol, mx);
+    const bool drop = head && c != diag && !(fabs(sum) >= thr);
+    const unsigned dropb = __ballot_sync(kFull, drop) & gmask;
+    const int ndrop = __popc(dropb);
+    double lumped = 0.0;  // dropped values in column order (ascending pos)
+    const int Umax = __reduce_max_sync(kFull, U);  // warp-uniform trip count
+    for (int qq = 0; qq < Umax; ++qq) {
+      const unsigned src = __ballot_sync(kFull, head && pos == qq) & gmask;
+      const int sl = __ffs(src) - 1 - gbase;
+      const double v = __shfl_sync(kFull, sum, sl < 0 ? 0 : sl, G);
+      const bool dq = __shfl_sync(kFull, drop, sl < 0 ? 0 : sl, G);
+      if (sl >= 0 && dq) lumped = add_rn(lumped, v);
+    }
+    const bool keep = head && !drop;
+    const bool insert = a.lump && ndrop > 0 && !has_diag && lumped != 0.0;
+    int krank = 0, before = 0;
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      const int ci = __shfl_sync(kFull, c, i, G);
+      const bool ki = __shfl_sync(kFull, keep, i, G);
+      if (ki && ci < c) ++krank;
+      if (ki && ci < diag) ++before;
+    }
+    const long long o = (long long)(live ? a.Cp[row] : 0) + row;
+    if (keep) {
+      double x = sum;
+      if (c == diag && a.lump && ndrop > 0) x = add_rn(x, lumped);
+      const int dst = krank + (insert && c > diag ? 1 : 0);
+      a.Cc[o + dst] = c;
+      a.Cv[o + dst] = x;
+    }
+    const int kept = __popc(__ballot_sync(kFull, keep) & gmask);
+    if (live && j == 0) {
+      if (insert) {
+        a.Cc[o + before] = diag;
+        a.Cv[o + before] = lumped;
+      }
+      a.cnt[row] = kept + (insert ? 1 : 0);
+      if (ndrop && a.any_drop) atomicOr(a.any_drop, 1);
+    }
+  }
+}
+
+template <int G>
+static int launch_reg(const RegArgs& a, cudaStream_t s) {
+  spgemm_reg_kernel<G><<<blocks_for((long long)a.nrows * G, 256), 256, 0, s>>>(a);
+  AIRG_LAUNCH_CHECK();
+  return AIRG_OK;
+}
+
+// rows of the register classes: not on the span path, <= 8 / <= kRegMax2
+// products and A entries (a 32-lane class measured slower than the hash
+// warp kernels: three 32-step shuffle loops per row)
+#ifndef AIRG_REG2
+#define AIRG_REG2 16
+#endif
+constexpr int kRegMax2 = AIRG_REG2;
+__device__ __forceinline__ int reg_class(long long words, long long ub, int na) {
+  if (words > 0) return -1;
+  if (ub <= 8 && na <= 8) return 0;
+  if (ub <= kRegMax2 && na <= kRegMax2) return 1;
+  return -1;
+}
+
 // count-pass class of a row: span path (window <= 4096 / <= 16384 columns)
 // or the hash classes by product upper bound
 enum { kCntHash64 = 0, kCntSpan4k = 1, kCntSpan16k = 2, kCntHash512 = 3, kCntHashBlk = 4,
-       kCntSpan64k = 5, kCntClasses = 6 };
+       kCntSpan64k = 5, kCntReg8 = 6, kCntReg32 = 7, kCntClasses = 8 };
 
-__global__ void count_class_kernel(int m, const long long* __restrict__ ub,
+__global__ void count_class_kernel(int m, const int* __restrict__ Ap, const long long* __restrict__ ub,
                                    const long long* __restrict__ words, int* __restrict__ ids) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
        i += (long long)gridDim.x * blockDim.x) {
     const long long w = words[i], u = ub[i];
-    ids[i] = w > 0 ? (w * 32 <= 4096 ? kCntSpan4k : w * 32 <= 16384 ? kCntSpan16k : kCntSpan64k)
+    const int rc = reg_class(w, u, Ap[i + 1] - Ap[i]);
+    ids[i] = rc >= 0 ? kCntReg8 + rc
+           : w > 0 ? (w * 32 <= 4096 ? kCntSpan4k : w * 32 <= 16384 ? kCntSpan16k : kCntSpan64k)
                    : (u <= 64 ? kCntHash64 : u <= 512 ? kCntHash512 : kCntHashBlk);
   }
 }
@@ -444,13 +615,18 @@ constexpr int kNumSpanCls = 10;
 __constant__ int kSpanCapsDev[kNumSpanCls] = {128, 256, 384, 512, 768, 1024, 1536, 2048, 3072, 4096};
 static const int kSpanCaps[kNumSpanCls] = {128, 256, 384, 512, 768, 1024, 1536, 2048, 3072, 4096};
 constexpr int kNumHashCls = 8;
-__global__ void numeric_class_kernel(int m, const int* __restrict__ Cp,
+constexpr int kNumRegCls = 2;  // after the span and hash classes
+__global__ void numeric_class_kernel(int m, const int* __restrict__ Cp, const int* __restrict__ Ap,
+                                     const long long* __restrict__ ub,
                                      const long long* __restrict__ words, int* __restrict__ ids) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
        i += (long long)gridDim.x * blockDim.x) {
     const int n = Cp[i + 1] - Cp[i];
+    const int rc = reg_class(words[i], ub[i], Ap[i + 1] - Ap[i]);
     int c;
-    if (words[i] > 0 && n <= kSpanNmax) {
+    if (rc >= 0) {
+      c = kNumSpanCls + kNumHashCls + rc;
+    } else if (words[i] > 0 && n <= kSpanNmax) {
       c = 0;
       while (n > kSpanCapsDev[c]) ++c;
     } else {
@@ -558,7 +734,7 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
   AIRG_TRY(scratch(&gbm, totw, s));
   // ---- pass 1 ----
   {
-    if (m > 0) count_class_kernel<<<blocks_for(m, 256), 256, 0, s>>>(m, ub, words, ids);
+    if (m > 0) count_class_kernel<<<blocks_for(m, 256), 256, 0, s>>>(m, A.p, ub, words, ids);
     AIRG_LAUNCH_CHECK();
     Classes cl;
     AIRG_TRY(classify_ids(m, ids, kCntClasses, cl, s));
@@ -572,6 +748,12 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
     for (int c = 0; c < kCntClasses; ++c) {
       const int nr = cl.count[c];
       if (!nr) continue;
+      if (c == kCntReg8 || c == kCntReg32) {
+        RegArgs a{A.p, A.c, A.v, B.p, B.c, B.v, cl.list(c), nr, 1, nullptr, nullptr, nullptr,
+                  0, 0, 0.0, 0, cnt, nullptr, row0};
+        AIRG_TRY(c == kCntReg8 ? launch_reg<8>(a, fk.stream(c)) : launch_reg<kRegMax2>(a, fk.stream(c)));
+        continue;
+      }
       if (c == kCntSpan4k || c == kCntSpan16k || c == kCntSpan64k) {
         SpanCountArgs a{A.p, A.c, B.p, B.c, cl.list(c), nr, cmin, words, bmoff, gbm, cnt};
         if (c == kCntSpan4k) AIRG_TRY((launch_span_count<128>(a, 4096, fk.stream(c))));
@@ -623,12 +805,12 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
   AIRG_TRY(scan_counts(cnt, Cp, m, nullptr, s));
   AIRG_TRY(scratch(&rl, m, s));
   if (m > 0) rowlen_kernel<<<blocks_for(m, 256), 256, 0, s>>>(m, Cp, rl);
-  if (m > 0) numeric_class_kernel<<<blocks_for(m, 256), 256, 0, s>>>(m, Cp, words, ids);
+  if (m > 0) numeric_class_kernel<<<blocks_for(m, 256), 256, 0, s>>>(m, Cp, A.p, ub, words, ids);
   AIRG_LAUNCH_CHECK();
   Classes cl;
   // the scan total (output nnz) is read back with the class counts: one sync
   int nnz32 = 0;
-  AIRG_TRY(classify_ids(m, ids, kNumSpanCls + kNumHashCls, cl, s, Cp + m, &nnz32));
+  AIRG_TRY(classify_ids(m, ids, kNumSpanCls + kNumHashCls + kNumRegCls, cl, s, Cp + m, &nnz32));
   const long long nnz = nnz32;
   airg_csr_result* r = new airg_csr_result();
   r->nrows = m;
@@ -651,6 +833,13 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
       SpanNumArgs a{A.p, A.c, A.v, B.p, B.c, B.v, cl.list(c), nr, 0, (int)tot_h[2], cmin, words, bmoff,
                     gbm, Cp, ocol, oval, negate, mode, tol, lump, cnt, anyd, row0};
       AIRG_TRY(launch_span_numeric(a, kSpanCaps[c], span_kd, fk.stream(c)));
+    }
+    for (int rc = 0; rc < kNumRegCls; ++rc) {
+      const int c = kNumSpanCls + kNumHashCls + rc, nr = cl.count[c];
+      if (!nr) continue;
+      RegArgs a{A.p, A.c, A.v, B.p, B.c, B.v, cl.list(c), nr, 0, Cp, ocol, oval, negate, mode, tol,
+                lump, cnt, anyd, row0};
+      AIRG_TRY(rc == 0 ? launch_reg<8>(a, fk.stream(c)) : launch_reg<kRegMax2>(a, fk.stream(c)));
     }
     const int cbits[7] = {6, 8, 10, 11, 12, 13, 14}, cwarps[2] = {8, 8};
     constexpr int kGlobalClass = 7;

@@ -3,6 +3,8 @@ csr_matmat semantics, sparse.py:222-240) -- plain products and the fused
 drop/lump epilogue (sparse.py:307-352) of the Galerkin product.
 
 The library routes each output row by its column window and length:
+  both:    registers (<= 8 / <= 16 products and A entries: the row merged
+           with shuffles, 8 / 16 lanes per row);
   count:   hash set (<= 64 products), span bitmap (window <= 4096 / <= 16384 /
            <= 65536 columns), hash set (<= 512 products), CTA hash set (longer),
            global tables (overflow);
@@ -88,6 +90,8 @@ def _drop_lump_rows(M, tol, lump):
 
 # (label, rows, L, W, ka, bl): output length ~L, window W
 CASES = [
+    ('reg<=8', 400, 8, 40, 2, 3),          # <= 8 products: register class, 8 lanes per row
+    ('reg<=16', 300, 14, 60, 4, 4),        # <= 16 products: register class, 16 lanes
     ('hash<=32', 300, 24, 200, 6, 8),
     ('hash<=128', 200, 100, 600, 8, 8),
     ('hash512cnt', 100, 300, 90000, 4, 100),
