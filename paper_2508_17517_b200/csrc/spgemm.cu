@@ -807,12 +807,15 @@ __global__ void colmap_kernel(int n, const signed char* __restrict__ labels, sig
 
 // R row j = [Z row j mapped through f_idx | 1 at c_idx[j]] in fine ordering:
 // the unit entry goes before the first mapped column > c_idx[j] (or last).
-// VS lanes per row, the insertion point found by ballot chunk by chunk.
+// VS lanes per row (from the mean row length); the loads of 4 chunks are
+// issued before any is used (the f_idx gather depends on the column load),
+// then the chunks are placed in order, the insertion point found by ballot.
 template <int VS>
 __global__ void restriction_kernel(int nc, const int* __restrict__ zp, const int* __restrict__ zc,
                                    const double* __restrict__ zv, const int* __restrict__ f_idx,
                                    const int* __restrict__ c_idx, int* __restrict__ rp,
                                    int* __restrict__ rc, double* __restrict__ rv) {
+  constexpr int U = 4;
   const long long j = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / VS;
   const int lane = threadIdx.x & 31, g = lane & (VS - 1), sh = lane - g;
   const unsigned gmask = (VS == 32 ? 0xffffffffu : ((1u << VS) - 1u)) << sh;
@@ -828,25 +831,37 @@ __global__ void restriction_kernel(int nc, const int* __restrict__ zp, const int
   }
   const long long o = (long long)b + j;
   bool done = false;  // unit entry already placed (uniform within the group)
-  for (int k0 = b; __any_sync(0xffffffffu, k0 < e); k0 += VS) {
-    const int k = k0 + g;
-    const bool in = k < e;
-    const int col = in ? f_idx[zc[k]] : 0;
-    const unsigned gt = __ballot_sync(0xffffffffu, in && col > cj) & gmask;
-    int shift = done ? 1 : 0;
-    if (!done && gt) {
-      const int first = __ffs(gt) - 1;  // lane holding the first column > cj
-      if (lane >= first) shift = 1;
-      if (lane == first) {
-        rc[o + (k - b)] = cj;
-        rv[o + (k - b)] = 1.0;
+  for (int k0 = b; __any_sync(0xffffffffu, k0 < e); k0 += U * VS) {
+    int col[U];
+    double val[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int k = k0 + q * VS + g;
+      col[q] = k < e ? zc[k] : -1;
+      val[q] = k < e ? zv[k] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) col[q] = col[q] >= 0 ? f_idx[col[q]] : -1;
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int k = k0 + q * VS + g;
+      const bool in = k < e;
+      const unsigned gt = __ballot_sync(0xffffffffu, in && col[q] > cj) & gmask;
+      int shift = done ? 1 : 0;
+      if (!done && gt) {
+        const int first = __ffs(gt) - 1;  // lane holding the first column > cj
+        if (lane >= first) shift = 1;
+        if (lane == first) {
+          rc[o + (k - b)] = cj;
+          rv[o + (k - b)] = 1.0;
+        }
       }
+      if (in) {
+        rc[o + (k - b) + shift] = col[q];
+        rv[o + (k - b) + shift] = val[q];
+      }
+      done = done || gt != 0;
     }
-    if (in) {
-      rc[o + (k - b) + shift] = col;
-      rv[o + (k - b) + shift] = zv[k];
-    }
-    done = done || gt != 0;
   }
   if (j < nc && !done && g == 0) {
     rc[o + (e - b)] = cj;
@@ -1061,8 +1076,15 @@ int airg_restriction(int n, int nc, const int32_t* zp, const int32_t* zc, const 
   AIRG_CUDA(cudaStreamSynchronize(s));
   airg_csr_result* r = new_result(nc, n, s);
   AIRG_TRY(result_alloc_entries(r, (long long)znnz + nc, true));
-  if (nc > 0)
+  const double mean = nc > 0 ? (double)znnz / nc : 0.0;  // lanes per row: 4 entries per lane
+  if (nc > 0 && mean > 64)
+    restriction_kernel<32><<<(int)(((long long)nc * 32 + 255) / 256), 256, 0, s>>>(
+        nc, zp, zc, zv, f_idx, c_idx, r->ptr, r->col, r->val);
+  else if (nc > 0 && mean > 16)
     restriction_kernel<8><<<(int)(((long long)nc * 8 + 255) / 256), 256, 0, s>>>(
+        nc, zp, zc, zv, f_idx, c_idx, r->ptr, r->col, r->val);
+  else if (nc > 0)
+    restriction_kernel<2><<<(int)(((long long)nc * 2 + 255) / 256), 256, 0, s>>>(
         nc, zp, zc, zv, f_idx, c_idx, r->ptr, r->col, r->val);
   else
     AIRG_CUDA(cudaMemsetAsync(r->ptr, 0, sizeof(int), s));
