@@ -664,7 +664,7 @@ static int max_row_len(int m, const int* p, int* out, cudaStream_t s) {
 // of the level.  Warp per row below kPolyBlockCap entries, CTA per row above;
 // CTA rows whose working set exceeds the shared-memory opt-in limit run from
 // global memory.
-static const int kPolyBlockCap = getenv("AIRG_POLY_BLOCK_CAP") ? atoi(getenv("AIRG_POLY_BLOCK_CAP")) : 256;
+static const int kPolyBlockCap = getenv("AIRG_POLY_BLOCK_CAP") ? atoi(getenv("AIRG_POLY_BLOCK_CAP")) : 512;
 
 __global__ void poly_class_kernel(int n, const int* __restrict__ Pp, const int* __restrict__ Pc,
                                   int ncap, int* __restrict__ ids) {
@@ -696,7 +696,8 @@ template <class PM>
 static int launch_poly_class(PolyArgs b, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    for (auto k : {poly_assemble_kernel<PM, 1>, poly_assemble_kernel<PM, 2>, poly_assemble_kernel<PM, 4>})
+    for (auto k : {poly_assemble_kernel<PM, 1>, poly_assemble_kernel<PM, 2>, poly_assemble_kernel<PM, 4>,
+                   poly_assemble_kernel<PM, 8>})
       AIRG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin()));
     AIRG_CUDA(cudaFuncSetAttribute(poly_assemble_block_kernel<PM>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin()));
@@ -707,8 +708,10 @@ static int launch_poly_class(PolyArgs b, cudaStream_t st) {
     int warps = 4;
     while (warps > 1 && per * warps > (size_t)smem_optin()) warps >>= 1;
     // A-row entries held per lane in the pipeline: the class's row length
+    static const int kp8 = getenv("AIRG_POLY_KP8") ? atoi(getenv("AIRG_POLY_KP8")) : 1;
     auto k = b.cap <= 32 ? poly_assemble_kernel<PM, 1>
-                         : b.cap <= 64 ? poly_assemble_kernel<PM, 2> : poly_assemble_kernel<PM, 4>;
+           : b.cap <= 64 ? poly_assemble_kernel<PM, 2>
+           : (b.cap <= 128 || !kp8) ? poly_assemble_kernel<PM, 4> : poly_assemble_kernel<PM, 8>;
     k<<<blocks_for(b.nrows, warps, 148 * 32), warps * 32, per * warps, st>>>(b);
     AIRG_LAUNCH_CHECK();
     return AIRG_OK;

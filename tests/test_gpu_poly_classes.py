@@ -1,9 +1,10 @@
 """Bitwise parity of every masked-polynomial-assembly row class against the
 oracle (polynomial.py:372-416 / sparse.py:243-263).
 
-The library classes each pattern row by length (warp per row below 256
-entries, CTA per row from 256, CTA with a global-memory working set when it
-exceeds shared memory) and by column window (bitmap position map for windows
+The library classes each pattern row by length (warp per row below 512
+entries -- its A rows held 1/2/4/8 x 32 entries per lane in the pipeline --,
+CTA per row from 512, CTA with a global-memory working set when it exceeds
+shared memory) and by column window (bitmap position map for windows
 <= 8192 columns, hash table beyond).  The matrices below have short local rows
 plus "hub" rows of chosen lengths in narrow or wide windows, so every class
 receives rows."""
@@ -49,6 +50,8 @@ def hub_matrix(seed, n, hubs):
 
 
 HUBS = [(1000, 100, 4000),      # warp (cap 128), bitmap
+        (1500, 200, 5000),      # warp (cap 256, 8 x 32 entries per lane), bitmap
+        (2500, 40, 3000),       # warp (cap 64), bitmap
         (2000, 300, 6000),      # CTA (cap 512), bitmap
         (3000, 700, 8000),      # CTA (cap 1024), bitmap
         (4000, 1500, 8100),     # CTA (cap 2048), bitmap
