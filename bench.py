@@ -397,7 +397,7 @@ class SerialWorkload:
                     break
             except Exception:
                 pass
-        return ms, vbytes, ('one V-cycle (R/A_fc/A_ff SpMV chains + Newton coarse solve); '
+        return ms, vbytes, ('one V-cycle (R / A_fc SpMVs, q(A_ff) smoother chains, coarse solve: the path the plan runs); '
                             f'algorithmic bytes {vbytes} (count_cycle_bytes); traffic = ncu '
                             f'dram__bytes_read+write of the same V-cycle (profiles/{src or "r*_vcycle_traffic.json: none matches"})')
 
