@@ -242,10 +242,66 @@ struct Csr {
   const int* col = nullptr;
   const double* val = nullptr;
   int vs = 1;
+  // optional ELL copy (fast mode, fixed-width stencil rows): slot k of row i
+  // at k * nrows + i; padding slots repeat a valid column with value 0
+  int ew = 0;
+  const int* ecol = nullptr;
+  const double* eval = nullptr;
 };
 
 // kernels launched by this thread (per-call deltas are taken on the calling thread)
 static thread_local long long g_launches = 0;
+
+// ELL SpMV with the CSR kernel's epilogue (fast mode): one thread per row,
+// column-major slots, so the loads of a warp are coalesced and no row
+// offsets are read (the stencil operators of the finest level, 2-3 entries
+// per row).
+__global__ void __launch_bounds__(256) spmv_ell_epi_kernel(int nrows, int w, const int* __restrict__ ecol,
+                                                           const double* __restrict__ eval,
+                                                           const double* __restrict__ x, double xs,
+                                                           Epi ep) {
+  pdl_enter();
+  if (ep.sc_n) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < ep.sc_n;
+         i += (long long)gridDim.x * blockDim.x)
+      ep.sc_dst[ep.sc_idx[i]] = ep.sc_src[i];
+  }
+  const long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  double sq = 0.0;
+  if (row < nrows) {
+    int c[4];
+    double a[4];
+    double s = 0.0;
+    for (int k0 = 0; k0 < w; k0 += 4) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool in = k0 + q < w;
+        c[q] = in ? __ldg(ecol + (size_t)(k0 + q) * nrows + row) : -1;
+        a[q] = in ? __ldg(eval + (size_t)(k0 + q) * nrows + row) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (c[q] >= 0) s = fma(a[q], xs * __ldg(x + c[q]), s);
+    }
+    double r = ep.alpha * s;
+    if (ep.v) r = fma(ep.beta, ep.v[ep.vmap ? ep.vmap[row] : row], r);
+    const long long o = ep.omap ? ep.omap[row] : row;
+    if (ep.out) ep.out[o] = r;
+    if (ep.acc) ep.acc[o] += r;
+    sq = r * r;
+  }
+  if (ep.partial) {
+    __shared__ double red[32];
+    sq = warp_sum(sq);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      double t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+      t = warp_sum(t);
+      if (threadIdx.x == 0) ep.partial[blockIdx.x] = t;
+    }
+  }
+}
 
 static int launch_spmv(const Csr& A, const double* x, double xs, const Epi& ep, cudaStream_t s,
                        bool exact = false) {
@@ -254,6 +310,13 @@ static int launch_spmv(const Csr& A, const double* x, double xs, const Epi& ep, 
   if (exact) {
     spmv_vec_kernel<1, true><<<(A.nrows + threads - 1) / threads, threads, 0, s>>>(
         A.nrows, A.ptr, A.col, A.val, x, xs, ep);
+    ++g_launches;
+    AIRG_LAUNCH_CHECK();
+    return AIRG_OK;
+  }
+  if (A.ew > 0) {
+    AIRG_CUDA(launch_pdl(spmv_ell_epi_kernel, (A.nrows + threads - 1) / threads, threads, s, A.nrows,
+                         A.ew, A.ecol, A.eval, x, xs, ep));
     ++g_launches;
     AIRG_LAUNCH_CHECK();
     return AIRG_OK;
@@ -281,6 +344,7 @@ static int launch_spmv(const Csr& A, const double* x, double xs, const Epi& ep, 
 }
 
 static int spmv_blocks(const Csr& A) {
+  if (A.ew > 0) return (int)(((long long)A.nrows + 255) / 256);
   return (int)(((long long)A.nrows * A.vs + 255) / 256);
 }
 
@@ -1020,6 +1084,8 @@ struct airg_plan {
   // captured graphs name these, never the caller's buffers
   double *sb = nullptr, *sx = nullptr, *vin = nullptr, *vout = nullptr;
   unsigned long long tick = 0;
+  bool ell_done = false;
+  std::vector<void*> ell_owned;  // ELL copies of the stencil operators (fast mode)
 };
 
 static int alloc_vec(double** p, long long n) {
@@ -1210,6 +1276,7 @@ int airg_plan_destroy(airg_plan* p) {
     if (q) dfree(q);
   if (p->iflag) dfree(p->iflag);
   if (p->nst) dfree(p->nst);
+  for (void* q : p->ell_owned) dfree(q);
 
   delete p;
   return AIRG_OK;
@@ -1556,13 +1623,80 @@ static int plan_streams(airg_plan* p) {
   return AIRG_OK;
 }
 
+// ---- ELL copies of fixed-width operators ------------------------------------
+__global__ void row_maxlen_kernel(int n, const int* __restrict__ ptr, int* __restrict__ out) {
+  int m = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    m = max(m, ptr[i + 1] - ptr[i]);
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+__global__ void csr_to_ell_pad_kernel(int n, int w, const int* __restrict__ ptr, const int* __restrict__ col,
+                                      const double* __restrict__ val, int* __restrict__ ecol,
+                                      double* __restrict__ eval) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int b = ptr[i], len = ptr[i + 1] - b;
+    const int pad = len > 0 ? col[b + len - 1] : 0;  // a valid column, value 0
+    for (int k = 0; k < w; ++k) {
+      ecol[(size_t)k * n + i] = k < len ? col[b + k] : pad;
+      eval[(size_t)k * n + i] = k < len ? val[b + k] : 0.0;
+    }
+  }
+}
+// Give A an ELL copy when its rows are short and nearly uniform (<= 4
+// entries, >= AIRG_ELL_FILL of the slots real): the top operator (3 per
+// row) and the finest A_fc (2 per row) of the advection hierarchies.  Off
+// by default: measured at 2048^2 (tools/vlevels.py) the finest A_fc took
+// 40.4 us in ELL vs 38.1 us in CSR and the finest R (fill 0.71) 34.7 vs
+// 31.0 us -- the CSR kernel's thread-per-row loads are already coalesced
+// for 2-3-entry rows, and the row-offset load it saves is not the
+// bottleneck.  AIRG_ELL_FILL=0.9 enables it.
+static int make_ell(airg_plan* p, Csr& A, cudaStream_t s) {
+  const double fill = getenv("AIRG_ELL_FILL") ? atof(getenv("AIRG_ELL_FILL")) : 2.0;
+  if (A.nrows == 0 || A.ew > 0 || fill > 1.0) return AIRG_OK;
+  int* d = nullptr;
+  AIRG_TRY(scratch(&d, 1, s));
+  AIRG_CUDA(cudaMemsetAsync(d, 0, sizeof(int), s));
+  row_maxlen_kernel<<<blocks_for(A.nrows, 256), 256, 0, s>>>(A.nrows, A.ptr, d);
+  AIRG_LAUNCH_CHECK();
+  int w = 0;
+  AIRG_CUDA(cudaMemcpyAsync(&w, d, sizeof(int), cudaMemcpyDeviceToHost, s));
+  AIRG_CUDA(cudaStreamSynchronize(s));
+  release(d, s);
+  if (w < 1 || w > 4 || (double)A.nnz < fill * (double)A.nrows * w) return AIRG_OK;
+  int* ecol = nullptr;
+  double* eval = nullptr;
+  AIRG_CUDA(dmalloc(&ecol, (size_t)w * A.nrows * sizeof(int)));
+  AIRG_CUDA(dmalloc(&eval, (size_t)w * A.nrows * sizeof(double)));
+  p->ell_owned.push_back(ecol);
+  p->ell_owned.push_back(eval);
+  csr_to_ell_pad_kernel<<<blocks_for(A.nrows, 256), 256, 0, s>>>(A.nrows, w, A.ptr, A.col, A.val, ecol,
+                                                                 eval);
+  AIRG_LAUNCH_CHECK();
+  A.ew = w;
+  A.ecol = ecol;
+  A.eval = eval;
+  return AIRG_OK;
+}
+
 // things a capture must not do (synchronous allocation) are done up front
 static int prepare_capture(airg_plan* p, cudaStream_t s) {
   if (!p->exact && p->ready_coarse && p->coarse_poly.kind == 1 &&
       p->coarse.nrows <= kDenseCoarseMax && p->dense_state == 0)
     AIRG_TRY(build_dense_coarse(p, s));
-  if (!p->exact)
+  if (!p->exact) {
     for (auto& L : p->lv) AIRG_TRY(prepare_chain(L, s));
+    if (!p->ell_done) {  // the finest level's stencil operators
+      p->ell_done = true;
+      if (p->ready_top) AIRG_TRY(make_ell(p, p->top, s));
+      if (!p->lv.empty()) {
+        AIRG_TRY(make_ell(p, p->lv[0].R, s));
+        AIRG_TRY(make_ell(p, p->lv[0].Afc, s));
+      }
+    }
+  }
   return AIRG_OK;
 }
 

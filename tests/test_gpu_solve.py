@@ -270,3 +270,17 @@ def test_fused_smoother_chain_partitions(G, hier64, kb, cap, monkeypatch):
     H2 = upload_hierarchy(hier64)
     ref = tonp(G.vcycle(H2, 0, r, G.SolveConfig()))
     assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+def test_ell_stencil_path_in_vcycle(G, monkeypatch):
+    """ELL copies of the finest level's stencil operators (off by default,
+    AIRG_ELL_FILL enables them): the fast-mode solve through the ELL
+    epilogue kernel stays within 1e-10 of the oracle."""
+    monkeypatch.setenv('AIRG_ELL_FILL', '0.5')
+    A = O.advection_2d(80, 72, *PI4)
+    Hh = O.setup(A, O.Cfg(poly_order=4))
+    x_o, hist_o, conv_o, its_o = O.richardson(Hh, np.zeros(A.nrows), np.ones(A.nrows))
+    H = upload_hierarchy(Hh)
+    x, st = G.richardson_solve(H, np.zeros(A.nrows), np.ones(A.nrows), G.SolveConfig())
+    assert st.iterations == its_o
+    assert rel(st.residual_history, hist_o) < 1e-10
