@@ -439,7 +439,15 @@ __device__ __forceinline__ int span_drop_lump_row(const uint2* bm, int nw, const
 // Numeric pass: warp per row, output length <= a.ncap (runtime: one kernel,
 // any class granularity; NW warps per CTA).
 template <int NW, int KP, int D>
-__global__ void __launch_bounds__(32 * NW) span_numeric_kernel(SpanNumArgs a) {
+// Occupancy: 8 CTAs of two warps per SM caps the kernel at 128 registers
+// (16 warps/SM); left free it took more and ran 12 warps/SM.  Measured on
+// the 2048^2 products of levels 4-9 (tools/span_micro.py): 104.5 -> 93.0 ms
+// despite a small spill of the deep-prefetch variant; capping harder (20 or
+// 32 warps/SM) spills more and measured 126-200 ms.
+#ifndef AIRG_SPAN_MINB
+#define AIRG_SPAN_MINB 8
+#endif
+__global__ void __launch_bounds__(32 * NW, (AIRG_SPAN_MINB * 2 / NW) > 0 ? (AIRG_SPAN_MINB * 2 / NW) : 1) span_numeric_kernel(SpanNumArgs a) {
   extern __shared__ uint4 span_smem4[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   unsigned char* base = (unsigned char*)span_smem4 + (size_t)w * span_num_bytes(a.ncap, a.wcap);
