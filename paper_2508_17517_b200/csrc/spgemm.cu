@@ -351,7 +351,14 @@ __device__ __forceinline__ void poly_power_walk(const PolyArgs& a, const PM& pm,
 }
 
 template <class PM, int KP>
-__global__ void __launch_bounds__(128) poly_assemble_kernel(PolyArgs a) {
+// KP = 8 (pattern rows of 129-511 entries): 6 CTAs per SM caps it at 85
+// registers (the shared-memory limit of the class is 6 CTAs too); left free
+// it took 96 and ran 5.  Polynomial phase 68.8-69.2 -> 67.1 ms on one box;
+// 8 CTAs (64 registers) spills and loses (78.9 ms).
+#ifndef AIRG_POLY_MINB8
+#define AIRG_POLY_MINB8 6
+#endif
+__global__ void __launch_bounds__(128, KP == 8 ? AIRG_POLY_MINB8 : 1) poly_assemble_kernel(PolyArgs a) {
   extern __shared__ unsigned char smraw[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int cap = a.cap;
