@@ -215,18 +215,27 @@ class _Timer:
         self.sink = sink
         self.phase = phase
 
+    def _stream(self):
+        # the setup stream, looked up once per setup (torch's current_stream()
+        # costs ~10 us of device-index bookkeeping per record)
+        import torch
+        st = self.sink.get('_stream')
+        if st is None:
+            st = self.sink['_stream'] = torch.cuda.current_stream()
+        return st
+
     def __enter__(self):
         import torch
         if self.sink is not None:
             self.e0 = torch.cuda.Event(enable_timing=True)
-            self.e0.record()
+            self.e0.record(self._stream())
         return self
 
     def __exit__(self, *exc):
         import torch
         if self.sink is not None:
             e1 = torch.cuda.Event(enable_timing=True)
-            e1.record()
+            e1.record(self._stream())
             self.sink.setdefault('_pending', []).append((self.phase, self.sink.get('_level'),
                                                          self.e0, e1))
         return False
@@ -502,4 +511,5 @@ def build_levels(A, cfg, level0, truncate_start, inj, polys, timings, keep_level
         level += 1
     _flush_timings(timings)
     timings.pop('_level', None)
+    timings.pop('_stream', None)
     return levels, current, coarse_solver, truncated_at

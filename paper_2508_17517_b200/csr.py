@@ -19,11 +19,17 @@ IDX = torch.int32
 VAL = torch.float64
 
 
+_HAVE_CUDA = False
+
+
 def _dev():
-    if not torch.cuda.is_available():
-        raise RuntimeError('paper_2508_17517_b200 needs a CUDA device (sm_100a); '
-                           'there is no CPU fallback')
-    return torch.device('cuda', torch.cuda.current_device())
+    global _HAVE_CUDA
+    if not _HAVE_CUDA:  # checked until a device is seen (then once per process)
+        if not torch.cuda.is_available():
+            raise RuntimeError('paper_2508_17517_b200 needs a CUDA device (sm_100a); '
+                               'there is no CPU fallback')
+        _HAVE_CUDA = True
+    return torch.device('cuda', torch._C._cuda_getDevice())
 
 
 def to_dev(a, dtype):
