@@ -350,18 +350,9 @@ static int ddc_pass_run(int n, const int* ptr, const int* col, const double* val
   if (nf > 0)
     ddc_ratio_kernel<8><<<group_blocks(nf, 8), 256, 0, s>>>(nf, 0, f_idx, ptr, col, val, labels, ratio, ibuf);
   AIRG_LAUNCH_CHECK();
+  // min / max / mean, read back with the zero-diagonal flag (one sync)
   int bad = 0;
   AIRG_CUDA(cudaMemcpyAsync(&bad, ibuf, sizeof(int), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
-  if (bad != 0x7fffffff) {
-    release(f_idx, s);
-    release(ratio, s);
-    release(ibuf, s);
-    set_error("zero diagonal in fine-fine block (fine row %d); splitting is not usable for "
-              "reduction", bad);
-    return AIRG_ERR_VALUE;
-  }
-  // min / max / mean
   double lo = 0, hi = 0, mean = 0;
   {
     double* mm = nullptr;
@@ -380,6 +371,14 @@ static int ddc_pass_run(int n, const int* ptr, const int* col, const double* val
     AIRG_CUDA(cudaStreamSynchronize(s));
     cudaFreeAsync(tmp, s);
     release(mm, s);
+    if (bad != 0x7fffffff) {
+      release(f_idx, s);
+      release(ratio, s);
+      release(ibuf, s);
+      set_error("zero diagonal in fine-fine block (fine row %d); splitting is not usable for "
+                "reduction", bad);
+      return AIRG_ERR_VALUE;
+    }
     lo = h[0];
     hi = h[1];
     double sm = 0;
