@@ -284,3 +284,38 @@ def test_ell_stencil_path_in_vcycle(G, monkeypatch):
     x, st = G.richardson_solve(H, np.zeros(A.nrows), np.ones(A.nrows), G.SolveConfig())
     assert st.iterations == its_o
     assert rel(st.residual_history, hist_o) < 1e-10
+
+
+def test_concurrent_solves_at_scale_with_cooperative_chains(G):
+    """Three threads x four solves on ONE 2048^2 hierarchy: the plans' fused
+    smoother chains are cooperative launches of up to 148 CTAs with ~190 KB of
+    shared memory each, so concurrent plans cannot be co-resident -- they must
+    serialise, not deadlock, and every solve is bitwise the single-thread one."""
+    import threading
+    import torch
+    A, b = G.build_advection_2d(G.AdvectionProblem(nx=2048, ny=2048, vx=PI4[0], vy=PI4[1]))
+    H = G.setup(A, G.SetupConfig())
+    x0 = torch.ones(A.nrows, dtype=torch.float64, device='cuda')
+    x_ref, st_ref = G.richardson_solve(H, b, x0, G.SolveConfig())
+    ref = tonp(x_ref).tobytes()
+    out, errs = {}, []
+
+    def run(i):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(4):
+                    x, st = G.richardson_solve(H, b, x0, G.SolveConfig())
+                s.synchronize()
+            out[i] = (tonp(x).tobytes() == ref, st.residual_history == st_ref.residual_history)
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(3)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not any(t.is_alive() for t in th), 'concurrent solves did not finish'
+    assert not errs, errs
+    assert all(a and h for a, h in out.values()) and len(out) == 3
