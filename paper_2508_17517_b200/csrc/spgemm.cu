@@ -673,11 +673,111 @@ static int max_row_len(int m, const int* p, int* out, cudaStream_t s) {
 // global memory.
 static const int kPolyBlockCap = getenv("AIRG_POLY_BLOCK_CAP") ? atoi(getenv("AIRG_POLY_BLOCK_CAP")) : 512;
 
+// Short pattern rows (<= G entries, G lanes per row, 32 / G rows per warp):
+// every power in registers.  Lane j owns pattern position j (column c_j) and
+// its cur / nxt / acc values and flags; a power walks the present positions
+// q in order, loads A's row of col_q G entries at a time and each lane picks
+// the entry with its column (distinct columns: at most one) -- the same
+// products added in the same order as the warp and CTA kernels, bitwise.
+template <int G>
+__global__ void __launch_bounds__(256) poly_small_kernel(PolyArgs a) {
+  const int lane = threadIdx.x & 31, j = lane & (G - 1), gbase = lane & ~(G - 1);
+  const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << gbase;
+  const long long groups = ((long long)gridDim.x * blockDim.x) / G;
+  for (long long g0 = ((long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / G; g0 < a.nrows;
+       g0 += groups) {  // warp-uniform trip count
+    const long long r = g0 + lane / G;
+    const bool live = r < a.nrows;
+    const int row = live ? (a.rows ? a.rows[r] : (int)r) : 0;
+    const int pb = live ? a.Pp[row] : 0, m = live ? a.Pp[row + 1] - pb : 0;
+    const int cj = j < m ? a.Pc[pb + j] : INT_MAX;
+    const int d = a.ncoef - 1;
+    double acc = 0.0, cur = 0.0, nxt = 0.0;
+    bool facc = false, fcur = false, fnxt = false;
+    if (cj == a.row0 + row) {  // c0 I (the diagonal is always in the pattern)
+      acc = add_rn(acc, a.coef[0]);
+      facc = true;
+    }
+    // lane j's value in a row of A (b..e): the entry with column c_j, if any
+    auto pick = [&](int b, int e, double& v) -> bool {
+      bool hit = false;
+      const int len = e - b;
+      const int lmax = __reduce_max_sync(0xffffffffu, len);
+      for (int t0 = 0; t0 < lmax; t0 += G) {
+        const int t = t0 + j;
+        const int ct = t < len ? __ldg(a.Ac + b + t) : -1;
+        const double vt = t < len ? __ldg(a.Av + b + t) : 0.0;
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+          const int ci = __shfl_sync(0xffffffffu, ct, i, G);
+          const double vi = __shfl_sync(0xffffffffu, vt, i, G);
+          if (ci == cj) {
+            v = vi;
+            hit = true;
+          }
+        }
+      }
+      return hit;
+    };
+    if (d >= 1) {
+      const double c1 = a.coef[1];
+      double v = 0.0;
+      const int ab = live ? a.Ap[row] : 0, ae = live ? a.Ap[row + 1] : 0;
+      if (pick(ab, ae, v) && cj != INT_MAX) {
+        acc = add_rn(acc, mul_rn(c1, v));
+        facc = true;
+        cur = v;
+        fcur = true;
+      }
+    }
+    const int mmax = __reduce_max_sync(0xffffffffu, m);
+    for (int k = 2; k <= d; ++k) {
+      nxt = 0.0;
+      fnxt = false;
+      for (int q = 0; q < mmax; ++q) {  // present positions in order
+        const bool pq = __shfl_sync(0xffffffffu, fcur, q, G) && q < m;
+        const double lq = __shfl_sync(0xffffffffu, cur, q, G);
+        const int colq = __shfl_sync(0xffffffffu, cj, q, G);
+        int b = 0, e = 0;
+        if (pq) {
+          const int rq = a.rowmap ? a.rowmap[colq] : colq;
+          b = a.Ap[rq];
+          e = a.Ap[rq + 1];
+        }
+        double v = 0.0;
+        if (pick(b, e, v) && cj != INT_MAX) {
+          nxt = add_rn(nxt, mul_rn(lq, v));
+          fnxt = true;
+        }
+      }
+      if (fnxt) {
+        acc = add_rn(acc, mul_rn(a.coef[k], nxt));
+        facc = true;
+      }
+      cur = nxt;
+      fcur = fnxt;
+    }
+    const bool keep = d == 0 ? facc : (facc && acc != 0.0);
+    if (j < m) {
+      a.out_val[pb + j] = acc;
+      a.out_keep[pb + j] = keep;
+    }
+    const int c = __popc(__ballot_sync(0xffffffffu, keep && j < m) & gmask);
+    if (live && j == 0) a.out_cnt[row] = c;
+  }
+}
+
+// class of a pattern row: register classes for <= 8 / <= 16 entries (plain
+// assembly only), else the pow2 caps x (bitmap | hash) position map
 __global__ void poly_class_kernel(int n, const int* __restrict__ Pp, const int* __restrict__ Pc,
-                                  int ncap, int* __restrict__ ids) {
+                                  int ncap, int reg, int* __restrict__ ids) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     const int b = Pp[i], m = Pp[i + 1] - b;
+    if (reg && m <= 16) {
+      ids[i] = 2 * ncap + (m <= 8 ? 0 : 1);
+      continue;
+    }
     int c = 0;
     while ((32 << c) < m) ++c;
     const bool bit = m == 0 || (long long)Pc[b + m - 1] - Pc[b] < kPolySpan;
@@ -744,25 +844,35 @@ static int launch_poly_class(PolyArgs b, cudaStream_t st) {
 static int run_poly_kernel(PolyArgs& a, int maxlen, cudaStream_t s) {
   int ncap = 1;
   while ((32 << (ncap - 1)) < maxlen) ++ncap;
-  if (2 * ncap > kMaxCls) {
+  if (2 * ncap + 2 > kMaxCls) {
     set_error("pattern row of %d entries exceeds the assembly classes", maxlen);
     return AIRG_ERR_VALUE;
   }
   int* ids = nullptr;
   AIRG_TRY(scratch(&ids, a.n > 0 ? a.n : 1, s));
-  if (a.n > 0) poly_class_kernel<<<blocks_for(a.n, 256), 256, 0, s>>>(a.n, a.Pp, a.Pc, ncap, ids);
+  const int reg = a.masked ? 0 : 1;  // register classes: plain assembly only
+  if (a.n > 0)
+    poly_class_kernel<<<blocks_for(a.n, 256), 256, 0, s>>>(a.n, a.Pp, a.Pc, ncap, reg, ids);
   AIRG_LAUNCH_CHECK();
   Classes cl;
-  AIRG_TRY(classify_ids(a.n, ids, 2 * ncap, cl, s));
+  AIRG_TRY(classify_ids(a.n, ids, 2 * ncap + 2, cl, s));
   Fork fk;
   AIRG_TRY(fk.begin(s));
-  for (int c = 0; c < 2 * ncap; ++c) {
+  for (int c = 0; c < 2 * ncap + 2; ++c) {
     const int nr = cl.count[c];
     if (!nr) continue;
     PolyArgs b = a;
-    b.cap = 32 << (c % ncap);
     b.rows = cl.list(c);
     b.nrows = nr;
+    if (c >= 2 * ncap) {
+      if (c == 2 * ncap)
+        poly_small_kernel<8><<<blocks_for((long long)nr * 8, 256), 256, 0, fk.stream(c)>>>(b);
+      else
+        poly_small_kernel<16><<<blocks_for((long long)nr * 16, 256), 256, 0, fk.stream(c)>>>(b);
+      AIRG_LAUNCH_CHECK();
+      continue;
+    }
+    b.cap = 32 << (c % ncap);
     if (c < ncap) AIRG_TRY(launch_poly_class<BitPos>(b, fk.stream(c)));
     else AIRG_TRY(launch_poly_class<HashPos>(b, fk.stream(c)));
   }

@@ -1,7 +1,8 @@
 """Bitwise parity of every masked-polynomial-assembly row class against the
 oracle (polynomial.py:372-416 / sparse.py:243-263).
 
-The library classes each pattern row by length (warp per row below 512
+The library classes each pattern row by length (all powers in registers,
+8 / 16 lanes per row, for rows of <= 8 / <= 16 entries; warp per row below 512
 entries -- its A rows held 1/2/4/8 x 32 entries per lane in the pipeline --,
 CTA per row from 512, CTA with a global-memory working set when it exceeds
 shared memory) and by column window (bitmap position map for windows
