@@ -678,6 +678,7 @@ static int launch_span_numeric(SpanNumArgs a, int ncap, int kd, cudaStream_t s) 
   }
   switch (kd) {
     case 82: return launch_span_numeric_t<8, 2>(a, s);
+    case 24: return launch_span_numeric_t<2, 4>(a, s);
     default: return launch_span_numeric_t<4, 4>(a, s);
   }
 }
@@ -730,7 +731,11 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
   release(tot, s);
   // mean B-row length of the span rows sets the numeric prefetch shape: rows
   // longer than 4 x 32 entries would run their tail with exposed latency
-  const int span_kd = tot_h[1] && tot_h[0] > 112ull * tot_h[1] ? 82 : 44;
+  // (KP, D) = (2, 4) up to 48 entries, (4, 4) up to 112, (8, 2) above
+  // (measured per level at 2048^2, tools/span_micro.py --kd: levels 3-4 5 %
+  // faster with (2, 4), levels 7-8 5-20 % with (8, 2))
+  const int span_kd = !tot_h[1] ? 44 : tot_h[0] > 112ull * tot_h[1] ? 82
+                    : tot_h[0] > 48ull * tot_h[1] ? 44 : 24;
   AIRG_TRY(scratch(&gbm, totw, s));
   // ---- pass 1 ----
   {
