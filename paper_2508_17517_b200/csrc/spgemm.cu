@@ -16,6 +16,7 @@
 // ref: sparse.py:222-352, polynomial.py:372-416, hierarchy.py:211-286
 #include "spgemm_core.cuh"
 #include <vector>
+#include <type_traits>
 #include <algorithm>
 
 namespace airg {
@@ -811,7 +812,10 @@ static int launch_poly_class(PolyArgs b, cudaStream_t st) {
     attr = true;
   }
   const size_t per = (PM::bytes(b.cap) + (size_t)b.cap * 27 + 15) & ~(size_t)15;
-  if (b.cap < kPolyBlockCap && per <= (size_t)smem_optin()) {
+  // hash-map rows (windows > kPolySpan) keep the CTA kernel from 256 entries:
+  // the warp kernel's probe loops lost there (upwind DG, configs[4])
+  const int block_cap = std::is_same<PM, BitPos>::value ? kPolyBlockCap : 256;
+  if (b.cap < block_cap && per <= (size_t)smem_optin()) {
     int warps = 4;
     while (warps > 1 && per * warps > (size_t)smem_optin()) warps >>= 1;
     // A-row entries held per lane in the pipeline: the class's row length
