@@ -163,6 +163,12 @@ typedef struct airg_csr_result airg_csr_result;
 int airg_result_info(airg_csr_result* r, int32_t* nrows_h, int32_t* ncols_h, int64_t* nnz_h);
 int airg_result_take(airg_csr_result* r, int32_t* ptr, int32_t* col, double* val, void* stream);
 int airg_result_free(airg_csr_result* r);
+/* Zero-copy hand-over: the result's three device buffers (library pool)
+ * become the caller's; each is returned with airg_buffer_free when the
+ * caller is done (val is NULL for a pattern-only result).  The result is
+ * ready on `stream` when this returns. */
+int airg_result_detach(airg_csr_result* r, int32_t** ptr, int32_t** col, double** val, void* stream);
+int airg_buffer_free(void* p, void* stream);
 
 /* numpy Generator(PCG64(SeedSequence(seed))) stream: out[i] = a + b*random()_i
  * (a=0,b=1: .random(n); a=-1,b=2: .uniform(-1,1,n)); the 128-bit state and

@@ -160,6 +160,8 @@ pp = C.POINTER(vp)
 sig('airg_result_info', vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i64))
 sig('airg_result_take', vp, vp, vp, vp, vp)
 sig('airg_result_free', vp)
+sig('airg_result_detach', vp, vp, vp, vp, vp)
+sig('airg_buffer_free', vp, vp)
 sig('airg_pcg64_fill', u64, u64, u64, u64, i64, f64, f64, vp, vp)
 sig('airg_random_unit', u64, u64, u64, u64, i64, vp, vp, vp)
 sig('airg_diagonal', i32, vp, vp, vp, vp, vp)

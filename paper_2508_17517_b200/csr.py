@@ -243,16 +243,49 @@ def new_result():
     return C.c_void_p()
 
 
+class _LibBuffer:
+    """A library-pool device buffer seen by torch without a copy
+    (__cuda_array_interface__; torch keeps this object alive as long as the
+    tensor).  Returned to the pool, on the then-current stream, when the last
+    tensor viewing it dies."""
+
+    __slots__ = ('ptr', 'n', 'typestr', '__weakref__')
+
+    def __init__(self, ptr, n, typestr):
+        self.ptr, self.n, self.typestr = ptr, n, typestr
+
+    @property
+    def __cuda_array_interface__(self):
+        return {'shape': (self.n,), 'typestr': self.typestr, 'data': (self.ptr, False),
+                'version': 3, 'strides': None}
+
+    def __del__(self):
+        try:
+            L.load().airg_buffer_free(C.c_void_p(self.ptr), L.stream_handle())
+        except Exception:  # interpreter shutdown
+            pass
+
+
+def _view(ptr, n, dtype):
+    typestr = {IDX: '<i4', VAL: '<f8'}[dtype]
+    return torch.as_tensor(_LibBuffer(ptr, n, typestr), device=_dev())
+
+
 def take(res, values=True):
-    """Copy a library-held airg_csr_result into fresh device tensors."""
+    """Adopt a library-held airg_csr_result as device tensors (zero-copy:
+    the result's pool buffers become the tensors' storage)."""
     nr, nc, nnz = C.c_int32(), C.c_int32(), C.c_int64()
     L.call('airg_result_info', res, C.byref(nr), C.byref(nc), C.byref(nnz))
-    p = empty(nr.value + 1, IDX)
-    c = empty(nnz.value, IDX)
-    v = empty(nnz.value, VAL) if values else None
-    L.call('airg_result_take', res, L.ptr(p), L.ptr(c), L.ptr(v), L.stream_handle())
-    if v is None:
-        v = torch.ones(nnz.value, dtype=VAL, device=p.device)
+    pp, pc, pv = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    L.call('airg_result_detach', res, C.byref(pp), C.byref(pc), C.byref(pv), L.stream_handle())
+    p = _view(pp.value, nr.value + 1, IDX)
+    c = _view(pc.value, nnz.value, IDX) if pc.value else empty(nnz.value, IDX)
+    if values and pv.value:
+        v = _view(pv.value, nnz.value, VAL)
+    else:
+        if pv.value:
+            L.load().airg_buffer_free(pv, L.stream_handle())
+        v = (torch.zeros if values else torch.ones)(nnz.value, dtype=VAL, device=p.device)
     return SparseMatrix(nr.value, nc.value, p, c, v)
 
 

@@ -160,6 +160,25 @@ int airg_result_take(airg_csr_result* r, int32_t* ptr, int32_t* col, double* val
   return AIRG_OK;
 }
 
+int airg_result_detach(airg_csr_result* r, int32_t** ptr, int32_t** col, double** val, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!r) {
+    set_error("null result");
+    return AIRG_ERR_ARG;
+  }
+  if (r->stream != s) AIRG_CUDA(cudaStreamSynchronize(r->stream));
+  *ptr = r->ptr;
+  *col = r->col;
+  *val = r->val;
+  delete r;
+  return AIRG_OK;
+}
+
+int airg_buffer_free(void* p, void* stream) {
+  if (p) cudaFreeAsync(p, (cudaStream_t)stream);
+  return AIRG_OK;
+}
+
 int airg_result_free(airg_csr_result* r) {
   if (!r) return AIRG_OK;
   release(r->ptr, r->stream);
