@@ -300,6 +300,11 @@ def count_cycle_bytes(H, include_top=True, coarse=None):
         p = lv.f_smoother
         d = len(p.coeffs) - 1 if p.coeffs is not None else 0
         tot += _spmat_bytes(lv.R) + 8 * lv.n + 8 * nc
+        if (lv.f_smoother_assembled is None and p.kind == 'arnoldi_coeff' and d == 0
+                and lv.A_fc.nrows > 0):
+            # fused: e[f] = c0 (r[f] - A_fc e_c) and the e[c] scatter in one pass
+            tot += _spmat_bytes(lv.A_fc) + 24 * nc + 16 * nf
+            continue
         tot += _spmat_bytes(lv.A_fc) + 8 * nc + 16 * nf
         if lv.f_smoother_assembled is not None:
             tot += 16 * nf + _spmat_bytes(lv.f_smoother_assembled)

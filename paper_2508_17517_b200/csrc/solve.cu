@@ -1567,6 +1567,20 @@ static int vcycle_rec(airg_plan* p, int level, const double* r, double* e, int f
     AIRG_TRY(launch_spmv(L.R, r, 1.0, ep, s, p->exact));
   }
   AIRG_TRY(vcycle_rec(p, level + 1, L.rc, L.ec, fits, s));
+  // degree-0 smoother (e.g. the finest level, whose A_ff is diagonal):
+  // e[f] = c0 (r[f] - A_fc e_c) straight from the A_fc launch's epilogue,
+  // no rhs vector, no second launch (fast mode; exact mode keeps the
+  // reference's two roundings)
+  if (fits == 1 && !p->exact && !L.has_asm && L.sm.kind == 0 && L.sm.coef.size() == 1 &&
+      L.Afc.nrows > 0) {
+    const double c0 = L.sm.coef[0];
+    Epi ep{e, L.f_idx, -c0, c0, r, L.f_idx, nullptr, nullptr};
+    ep.sc_src = L.ec;
+    ep.sc_idx = L.c_idx;
+    ep.sc_dst = e;
+    ep.sc_n = L.n_c;
+    return launch_spmv(L.Afc, L.ec, 1.0, ep, s, false);
+  }
   // rhs = r[f] - A_fc e_c, and (same launch) the scatter e[c] = e_c
   {
     Epi ep{L.rhs, nullptr, -1.0, 1.0, r, L.f_idx, nullptr, nullptr};

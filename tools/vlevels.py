@@ -44,8 +44,12 @@ ops.append((len(H.levels), 'coarse', 8 * Cm.nrows * Cm.nrows + 16 * Cm.nrows))
 for li in range(len(H.levels) - 1, -1, -1):
     lv = H.levels[li]
     nf, nc = lv.split.n_f, lv.split.n_c
-    ops.append((li, 'Afc', _spmat_bytes(lv.A_fc) + 8 * nc + 16 * nf + 16 * nc))
     d = len(lv.f_smoother.coeffs) - 1
+    fused0 = d == 0 and (len(ops) + 1 >= len(names) or 'axpby' not in names[len(ops) + 1])
+    if fused0:  # degree 0: e[f] = c0 (r[f] - A_fc e_c) in the A_fc launch
+        ops.append((li, 'Afc+e', _spmat_bytes(lv.A_fc) + 24 * nc + 16 * nf))
+        continue
+    ops.append((li, 'Afc', _spmat_bytes(lv.A_fc) + 8 * nc + 16 * nf + 16 * nc))
     if d == 0:
         ops.append((li, 'axpby', 24 * nf))
     elif 'chain_kernel' in names[len(ops)]:  # fused chain: one launch, the same (unfused) byte model
