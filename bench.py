@@ -539,9 +539,11 @@ def ours_arm(args, rank, world, local):
         raise SystemExit('the row-strip decomposition generates the FD operator only (--problem fd)')
     W = DistWorkload(args, world) if world > 1 else SerialWorkload(args)
     n = W.n
-    # grow both device pools once before warm-up (scaled to the per-GPU problem;
-    # 2048^2 peaks at ~4 GB library scratch and ~9 GB of torch-owned hierarchy)
-    G.reserve_memory(library_bytes=n * 1600, torch_bytes=n * 4000)
+    # grow both device pools once before warm-up (scaled to the per-GPU
+    # problem): the hierarchy's operators live in the library pool (zero-copy
+    # results) with the setup scratch; torch holds vectors and small tensors
+    G.reserve_memory(library_bytes=n * int(os.environ.get('AIRG_RES_LIB', 5600)),
+                     torch_bytes=n * int(os.environ.get('AIRG_RES_TORCH', 600)))
     info = {}
 
     def release():

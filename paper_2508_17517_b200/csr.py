@@ -8,6 +8,7 @@ device buffers); every operation is an sm_100a kernel in libairg.so.
 """
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -271,11 +272,23 @@ def _view(ptr, n, dtype):
     return torch.as_tensor(_LibBuffer(ptr, n, typestr), device=_dev())
 
 
+_TAKE_COPY = bool(os.environ.get('AIRG_TAKE_COPY'))
+
+
 def take(res, values=True):
     """Adopt a library-held airg_csr_result as device tensors (zero-copy:
-    the result's pool buffers become the tensors' storage)."""
+    the result's pool buffers become the tensors' storage; AIRG_TAKE_COPY=1
+    copies into torch-allocated tensors instead)."""
     nr, nc, nnz = C.c_int32(), C.c_int32(), C.c_int64()
     L.call('airg_result_info', res, C.byref(nr), C.byref(nc), C.byref(nnz))
+    if _TAKE_COPY:
+        p = empty(nr.value + 1, IDX)
+        c = empty(nnz.value, IDX)
+        v = empty(nnz.value, VAL) if values else None
+        L.call('airg_result_take', res, L.ptr(p), L.ptr(c), L.ptr(v), L.stream_handle())
+        if v is None:
+            v = torch.ones(nnz.value, dtype=VAL, device=p.device)
+        return SparseMatrix(nr.value, nc.value, p, c, v)
     pp, pc, pv = C.c_void_p(), C.c_void_p(), C.c_void_p()
     L.call('airg_result_detach', res, C.byref(pp), C.byref(pc), C.byref(pv), L.stream_handle())
     p = _view(pp.value, nr.value + 1, IDX)
