@@ -1086,7 +1086,41 @@ struct airg_plan {
   unsigned long long tick = 0;
   bool ell_done = false;
   std::vector<void*> ell_owned;  // ELL copies of the stencil operators (fast mode)
+  // plan build: operator nnz read back in ONE synchronisation (pinned slots
+  // filled by async copies, resolved by airg_plan_set_coarse)
+  int* nnz_h = nullptr;
+  int nnz_slots = 0, nnz_used = 0;
+  std::vector<std::pair<Csr*, int>> nnz_pend;
 };
+
+// An operator of the plan under construction: its nnz (ptr[nrows]) comes back
+// by an async copy into the plan's pinned slots; plan_finish_build fills
+// nnz and the lanes per row.
+static int plan_csr(airg_plan* p, Csr& c, int nrows, int ncols, const int* ptr, const int* col,
+                    const double* val) {
+  c = Csr();
+  c.nrows = nrows;
+  c.ncols = ncols;
+  c.ptr = ptr;
+  c.col = col;
+  c.val = val;
+  if (nrows <= 0) return AIRG_OK;
+  if (p->nnz_used >= p->nnz_slots) {
+    set_error("plan nnz slots exhausted");
+    return AIRG_ERR_ARG;
+  }
+  const int slot = p->nnz_used++;
+  AIRG_CUDA(cudaMemcpyAsync(p->nnz_h + slot, ptr + nrows, sizeof(int), cudaMemcpyDeviceToHost, 0));
+  p->nnz_pend.push_back({&c, slot});
+  return AIRG_OK;
+}
+
+// plan vectors: stream-ordered on the legacy stream, made visible to every
+// stream by the one synchronisation at the end of the build
+static int alloc_vec_async(double** q, long long n) {
+  AIRG_CUDA(cudaMallocFromPoolAsync((void**)q, (size_t)(n > 0 ? n : 1) * sizeof(double), lib_pool(), 0));
+  return AIRG_OK;
+}
 
 static int alloc_vec(double** p, long long n) {
   AIRG_CUDA(dmalloc(p, (n > 0 ? n : 1) * sizeof(double)));
@@ -1246,6 +1280,8 @@ int airg_plan_create(int nlevels, airg_plan** out) {
   airg_plan* p = new airg_plan();
   p->nlevels = nlevels;
   p->lv.resize(nlevels);
+  p->nnz_slots = 3 * nlevels + 4;
+  AIRG_CUDA(cudaHostAlloc((void**)&p->nnz_h, sizeof(int) * p->nnz_slots, cudaHostAllocDefault));
   p->norm_h = &p->norm_hv;
   AIRG_CUDA(dmalloc(&p->norm_d, sizeof(double)));
   AIRG_CUDA(dmalloc(&p->iflag, sizeof(int)));
@@ -1277,6 +1313,7 @@ int airg_plan_destroy(airg_plan* p) {
   if (p->iflag) dfree(p->iflag);
   if (p->nst) dfree(p->nst);
   for (void* q : p->ell_owned) dfree(q);
+  if (p->nnz_h) cudaFreeHost(p->nnz_h);
 
   delete p;
   return AIRG_OK;
@@ -1284,13 +1321,10 @@ int airg_plan_destroy(airg_plan* p) {
 
 int airg_plan_set_top(airg_plan* p, int n, const int32_t* ptr, const int32_t* col,
                       const double* val) {
-  p->top = make_csr(n, n, ptr, col, val, read_nnz(ptr, n));
-  AIRG_TRY(alloc_vec(&p->r, n));
-  AIRG_TRY(alloc_vec(&p->e, n));
-  const int nb = (int)((p->top.nrows * (long long)p->top.vs + 255) / 256);
-  p->nparts_cap = std::max(nb, 148 * 8);
-  AIRG_TRY(alloc_vec(&p->parts, p->nparts_cap));
-  p->ready_top = true;
+  AIRG_TRY(plan_csr(p, p->top, n, n, ptr, col, val));
+  AIRG_TRY(alloc_vec_async(&p->r, n));
+  AIRG_TRY(alloc_vec_async(&p->e, n));
+  p->ready_top = true;  // partials buffer sized at the end of the build
   return AIRG_OK;
 }
 
@@ -1309,21 +1343,21 @@ int airg_plan_set_level(airg_plan* p, int level, int n, int n_f, int n_c, const 
   L.n = n;
   L.n_f = n_f;
   L.n_c = n_c;
-  L.R = make_csr(n_c, n, R_ptr, R_col, R_val, read_nnz(R_ptr, n_c));
-  L.Afc = make_csr(n_f, n_c, Afc_ptr, Afc_col, Afc_val, read_nnz(Afc_ptr, n_f));
-  L.Aff = make_csr(n_f, n_f, Aff_ptr, Aff_col, Aff_val, read_nnz(Aff_ptr, n_f));
+  AIRG_TRY(plan_csr(p, L.R, n_c, n, R_ptr, R_col, R_val));
+  AIRG_TRY(plan_csr(p, L.Afc, n_f, n_c, Afc_ptr, Afc_col, Afc_val));
+  AIRG_TRY(plan_csr(p, L.Aff, n_f, n_f, Aff_ptr, Aff_col, Aff_val));
   L.has_asm = asm_nnz >= 0;
   if (L.has_asm) L.Asm = make_csr(n_f, n_f, asm_ptr, asm_col, asm_val, asm_nnz);
   L.f_idx = f_idx;
   L.c_idx = c_idx;
   AIRG_TRY(build_poly(L.sm, kind, ncoef, coef_h, 0, nullptr, nullptr, nullptr, diag_scale));
-  AIRG_TRY(alloc_vec(&L.rc, n_c));
-  AIRG_TRY(alloc_vec(&L.ec, n_c));
-  AIRG_TRY(alloc_vec(&L.rhs, n_f));
-  AIRG_TRY(alloc_vec(&L.ef, n_f));
-  AIRG_TRY(alloc_vec(&L.t0, n_f));
-  AIRG_TRY(alloc_vec(&L.t1, n_f));
-  AIRG_TRY(alloc_vec(&L.t2, n_f));
+  AIRG_TRY(alloc_vec_async(&L.rc, n_c));
+  AIRG_TRY(alloc_vec_async(&L.ec, n_c));
+  AIRG_TRY(alloc_vec_async(&L.rhs, n_f));
+  AIRG_TRY(alloc_vec_async(&L.ef, n_f));
+  AIRG_TRY(alloc_vec_async(&L.t0, n_f));
+  AIRG_TRY(alloc_vec_async(&L.t1, n_f));
+  AIRG_TRY(alloc_vec_async(&L.t2, n_f));
   return AIRG_OK;
 }
 
@@ -1331,15 +1365,24 @@ int airg_plan_set_coarse(airg_plan* p, int n, const int32_t* ptr, const int32_t*
                          const double* val, int kind, int ncoef, const double* coef_h, int nunits,
                          const int32_t* type_h, const double* p1_h, const double* p2_h,
                          const double* diag_scale) {
-  p->coarse = make_csr(n, n, ptr, col, val, read_nnz(ptr, n));
+  AIRG_TRY(plan_csr(p, p->coarse, n, n, ptr, col, val));
   AIRG_TRY(build_poly(p->coarse_poly, kind, ncoef, coef_h, nunits, type_h, p1_h, p2_h,
                       diag_scale));
-  AIRG_TRY(alloc_vec(&p->cw0, n));
-  AIRG_TRY(alloc_vec(&p->cw1, n));
-  AIRG_TRY(alloc_vec(&p->cw2, n));
-  AIRG_TRY(alloc_vec(&p->cw3, n));
+  AIRG_TRY(alloc_vec_async(&p->cw0, n));
+  AIRG_TRY(alloc_vec_async(&p->cw1, n));
+  AIRG_TRY(alloc_vec_async(&p->cw2, n));
+  AIRG_TRY(alloc_vec_async(&p->cw3, n));
+  // end of the build: one synchronisation resolves every operator's nnz and
+  // makes the stream-ordered allocations visible to all streams
+  AIRG_CUDA(cudaStreamSynchronize(0));
+  for (auto& pr : p->nnz_pend) {
+    pr.first->nnz = p->nnz_h[pr.second];
+    pr.first->vs = pick_vs(pr.first->nnz, pr.first->nrows);
+  }
+  p->nnz_pend.clear();
   if (!p->parts) {
-    p->nparts_cap = 148 * 8;
+    const int nb = p->ready_top ? (int)((p->top.nrows * (long long)p->top.vs + 255) / 256) : 0;
+    p->nparts_cap = std::max(nb, 148 * 8);
     AIRG_TRY(alloc_vec(&p->parts, p->nparts_cap));
   }
   p->ready_coarse = true;
