@@ -270,6 +270,10 @@ int airg_ap_onepoint(int m, int k, int nc, const int32_t* Ap, const int32_t* Ac,
 int airg_extract(int nr_sel, const int32_t* rows, const int32_t* p, const int32_t* c,
                  const double* v, const int32_t* colmap, int ncols_sel, airg_csr_result** out,
                  void* stream);
+/* the same with A's mean row length (nnz / rows) as a hint: lanes per row */
+int airg_extract_ex(int nr_sel, const int32_t* rows, const int32_t* p, const int32_t* c,
+                    const double* v, const int32_t* colmap, int ncols_sel, double mean_len,
+                    airg_csr_result** out, void* stream);
 /* map[i] = labels[i] == which ? pos[i] : -1 */
 int airg_label_colmap(int n, const int8_t* labels, int which, const int32_t* pos, int32_t* map,
                       void* stream);

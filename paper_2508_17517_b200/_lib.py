@@ -185,6 +185,7 @@ sig('airg_galerkin', i32, i32, vp, vp, vp, vp, vp, vp, vp, f64, C.c_int, pp, vp)
 sig('airg_ap_onepoint', i32, i32, i32, vp, vp, vp, vp, pp, vp)
 sig('airg_advection_dg', i32, i32, vp, C.c_int, C.c_int, pp, vp)
 sig('airg_extract', i32, vp, vp, vp, vp, vp, i32, pp, vp)
+sig('airg_extract_ex', i32, vp, vp, vp, vp, vp, i32, C.c_double, pp, vp)
 sig('airg_label_colmap', i32, vp, C.c_int, vp, vp, vp)
 sig('airg_restriction', i32, i32, vp, vp, vp, vp, vp, pp, vp)
 sig('airg_arnoldi', i32, vp, vp, vp, vp, C.c_int, vp, C.POINTER(i32), C.POINTER(f64), vp)

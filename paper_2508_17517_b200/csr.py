@@ -346,8 +346,8 @@ def _index_set(idx, limit, name):
 def extract_mapped(A, rows, colmap, ncols):
     """A[rows, :] with columns renumbered through ``colmap`` (-1 drops)."""
     r = new_result()
-    L.call('airg_extract', int(rows.numel()), L.ptr(rows), *_args(A), L.ptr(colmap), int(ncols),
-           C.byref(r), L.stream_handle())
+    L.call('airg_extract_ex', int(rows.numel()), L.ptr(rows), *_args(A), L.ptr(colmap), int(ncols),
+           A.nnz / max(A.nrows, 1), C.byref(r), L.stream_handle())
     return take(r)
 
 

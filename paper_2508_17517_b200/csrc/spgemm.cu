@@ -1160,25 +1160,39 @@ int airg_drop_lump(int m, int ncols, const int32_t* p, const int32_t* c, const d
   return AIRG_OK;
 }
 
-int airg_extract(int nr_sel, const int32_t* rows, const int32_t* p, const int32_t* c,
-                 const double* v, const int32_t* colmap, int ncols_sel, airg_csr_result** out,
-                 void* stream) {
+int airg_extract_ex(int nr_sel, const int32_t* rows, const int32_t* p, const int32_t* c,
+                    const double* v, const int32_t* colmap, int ncols_sel, double mean_len,
+                    airg_csr_result** out, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   airg_csr_result* r = new_result(nr_sel, ncols_sel, s);
   int* cnt = nullptr;
   AIRG_TRY(scratch(&cnt, nr_sel + 1, s));
-  const int nb = (int)(((long long)nr_sel * 8 + 255) / 256);
-  if (nr_sel > 0)
-    extract_kernel<8><<<nb, 256, 0, s>>>(nr_sel, rows, p, c, v, colmap, nullptr, nullptr, nullptr, cnt);
+  // lanes per row: ~2-4 entries per lane and round (8 without a hint)
+  const int vs = mean_len <= 0 ? 8 : mean_len <= 12 ? 4 : mean_len <= 48 ? 8 : mean_len <= 96 ? 16 : 32;
+  const int nb = (int)(((long long)nr_sel * vs + 255) / 256);
+  auto launch = [&](const int* optr, int* oc, double* ov, int* cn) {
+    switch (vs) {
+      case 4: extract_kernel<4><<<nb, 256, 0, s>>>(nr_sel, rows, p, c, v, colmap, optr, oc, ov, cn); break;
+      case 16: extract_kernel<16><<<nb, 256, 0, s>>>(nr_sel, rows, p, c, v, colmap, optr, oc, ov, cn); break;
+      case 32: extract_kernel<32><<<nb, 256, 0, s>>>(nr_sel, rows, p, c, v, colmap, optr, oc, ov, cn); break;
+      default: extract_kernel<8><<<nb, 256, 0, s>>>(nr_sel, rows, p, c, v, colmap, optr, oc, ov, cn);
+    }
+  };
+  if (nr_sel > 0) launch(nullptr, nullptr, nullptr, cnt);
   long long nnz = 0;
   AIRG_TRY(scan_counts(cnt, r->ptr, nr_sel, &nnz, s));
   AIRG_TRY(result_alloc_entries(r, nnz, true));
-  if (nr_sel > 0)
-    extract_kernel<8><<<nb, 256, 0, s>>>(nr_sel, rows, p, c, v, colmap, r->ptr, r->col, r->val, nullptr);
+  if (nr_sel > 0) launch(r->ptr, r->col, r->val, nullptr);
   AIRG_LAUNCH_CHECK();
   release(cnt, s);
   *out = r;
   return AIRG_OK;
+}
+
+int airg_extract(int nr_sel, const int32_t* rows, const int32_t* p, const int32_t* c,
+                 const double* v, const int32_t* colmap, int ncols_sel, airg_csr_result** out,
+                 void* stream) {
+  return airg_extract_ex(nr_sel, rows, p, c, v, colmap, ncols_sel, 0.0, out, stream);
 }
 
 int airg_label_colmap(int n, const int8_t* labels, int which, const int32_t* pos, int32_t* map,
