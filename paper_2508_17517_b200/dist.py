@@ -617,7 +617,7 @@ class _Ticker:
             self.sink[f'{key}@{self.level}'] = value
 
 
-def setup_distributed(comm, A, cfg, poly_inject=None, replicate_below=20000, force=False):
+def setup_distributed(comm, A, cfg, poly_inject=None, replicate_below=None, force=False):
     """AIRG setup (hierarchy.py:365-448) on a row-partitioned matrix.  Levels
     with more than ``replicate_below`` rows (and below the truncation start)
     are built distributed; the rest is built on every rank from the gathered
@@ -626,6 +626,9 @@ def setup_distributed(comm, A, cfg, poly_inject=None, replicate_below=20000, for
     from .amg_setup import (SETUP_PHASES, SEED_SMOOTHER, SEED_SPLIT, build_levels, derive_seed,
                             resolve_truncate_start, finalize_complexities, Hierarchy)
     cfg.validate()
+    if replicate_below is None:
+        import os
+        replicate_below = int(os.environ.get('AIRG_REPLICATE_BELOW', 20000))
     if cfg.inverse_type != 'arnoldi' or cfg.r_drop != 0:
         raise ValueError('the distributed setup supports inverse_type="arnoldi" with r_drop=0')
     inj = poly_inject or {}
