@@ -51,7 +51,8 @@ inline int num_sms() {
   return v;
 }
 
-inline int blocks_for(long long n, int threads, long long cap = 148LL * 64) {
+inline int blocks_for(long long n, int threads, long long cap = -1) {
+  if (cap < 0) cap = (long long)num_sms() * 64;
   long long b = (n + threads - 1) / threads;
   if (b < 1) b = 1;
   if (b > cap) b = cap;

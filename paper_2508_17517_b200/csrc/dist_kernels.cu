@@ -389,7 +389,7 @@ int airg_ddc_hist(int nf, const double* ratio, const double* edges_h, int nedges
   AIRG_CUDA(cudaFuncSetAttribute(ddc_hist_ext_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(200 * 1024)));
   if (nf > 0)
-    ddc_hist_ext_kernel<<<blocks_for(nf, 256, 148 * 2), 256, shm, s>>>(nf, ratio, de, nedges,
+    ddc_hist_ext_kernel<<<blocks_for(nf, 256, num_sms() * 2), 256, shm, s>>>(nf, ratio, de, nedges,
                                                                        (unsigned long long*)hist);
   AIRG_LAUNCH_CHECK();
   release(de, s);

@@ -436,7 +436,7 @@ static int dev_dot(long long n, const double* x, const double* y, double* out, d
 
 // dot-product partials: one per CTA of the cooperative kernel, which has
 // enough threads for one vs-lane group per row (the SpMV), at most 4 per SM
-static int arnoldi_parts(int n, int vs) { return blocks_for((long long)n * vs, 256, 148 * 4); }
+static int arnoldi_parts(int n, int vs) { return blocks_for((long long)n * vs, 256, num_sms() * 4); }
 
 static int arnoldi_multi(int n, const int* p, const int* c, const double* v, const double* b, int m,
                          double* H_h, int* k_h, double* beta_h, int vs, cudaStream_t s) {

@@ -819,7 +819,7 @@ static int newton_multi(const Poly& p, const Csr& A, const double* b, double* y,
   const int n = A.nrows;
   const int nunits = (int)p.utype.size();
   const int thr = 256;
-  const int nb = blocks_for(n, thr, 148 * 8);
+  const int nb = blocks_for(n, thr, num_sms() * 8);
   newton_init_kernel<<<nb, thr, 0, s>>>(n, b, t0, y, nst);
   ++g_launches;
   // SpMVs: the reference-order row kernel in exact mode; otherwise the
@@ -1258,7 +1258,7 @@ int airg_poly_apply(int kind, int n, const int32_t* ptr, const int32_t* col, con
   AIRG_TRY(build_poly(p, kind, ncoef, coef_h, nunits, type_h, p1_h, p2_h, diag_scale));
   Csr A = make_csr(n, n, ptr, col, val, read_nnz(ptr, n));
   double* w = nullptr;
-  const int nb = blocks_for(n, 256, 148 * 8);
+  const int nb = blocks_for(n, 256, num_sms() * 8);
   AIRG_TRY(scratch(&w, 4LL * (n > 0 ? n : 1) + nb + 8, s));
   double* parts = w + 4LL * (n > 0 ? n : 1);
   int* iflag = (int*)(parts + nb);
@@ -1382,7 +1382,7 @@ int airg_plan_set_coarse(airg_plan* p, int n, const int32_t* ptr, const int32_t*
   p->nnz_pend.clear();
   if (!p->parts) {
     const int nb = p->ready_top ? (int)((p->top.nrows * (long long)p->top.vs + 255) / 256) : 0;
-    p->nparts_cap = std::max(nb, 148 * 8);
+    p->nparts_cap = std::max(nb, num_sms() * 8);
     AIRG_TRY(alloc_vec(&p->parts, p->nparts_cap));
   }
   p->ready_coarse = true;
@@ -2523,7 +2523,7 @@ static int halo_nccl(airg_dplan* p, HaloX& h, double* x_ext, cudaStream_t s);
 static int dist_newton(airg_dplan* p, const double* in, double* out, cudaStream_t s) {
   DCoarse& D = p->dc;
   const int n = D.n_loc;
-  const int nb = blocks_for(n, 256, 148 * 4);
+  const int nb = blocks_for(n, 256, num_sms() * 4);
   AIRG_CUDA(launch_pdl(dn_init_kernel, nb, 256, s, n, in, D.u, out, D.state, D.red));
   for (size_t k = 0; k < D.utype.size(); ++k) {
     const int ty = D.utype[k];

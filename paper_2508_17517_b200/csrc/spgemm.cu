@@ -657,7 +657,7 @@ static int max_row_len(int m, const int* p, int* out, cudaStream_t s) {
   int* d = nullptr;
   AIRG_TRY(scratch(&d, 1, s));
   AIRG_CUDA(cudaMemsetAsync(d, 0, sizeof(int), s));
-  if (m > 0) max_rowlen_kernel<<<blocks_for(m, 256, 148 * 8), 256, 0, s>>>(m, p, d);
+  if (m > 0) max_rowlen_kernel<<<blocks_for(m, 256, num_sms() * 8), 256, 0, s>>>(m, p, d);
   AIRG_LAUNCH_CHECK();
   AIRG_CUDA(cudaMemcpyAsync(out, d, sizeof(int), cudaMemcpyDeviceToHost, s));
   AIRG_CUDA(cudaStreamSynchronize(s));
@@ -823,7 +823,7 @@ static int launch_poly_class(PolyArgs b, cudaStream_t st) {
     auto k = b.cap <= 32 ? poly_assemble_kernel<PM, 1>
            : b.cap <= 64 ? poly_assemble_kernel<PM, 2>
            : (b.cap <= 128 || !kp8) ? poly_assemble_kernel<PM, 4> : poly_assemble_kernel<PM, 8>;
-    k<<<blocks_for(b.nrows, warps, 148 * 32), warps * 32, per * warps, st>>>(b);
+    k<<<blocks_for(b.nrows, warps, num_sms() * 32), warps * 32, per * warps, st>>>(b);
     AIRG_LAUNCH_CHECK();
     return AIRG_OK;
   }
@@ -832,11 +832,11 @@ static int launch_poly_class(PolyArgs b, cudaStream_t st) {
   const int nt = b.cap >= 512 ? 256 : b.cap >= 256 ? nt256 : nt128;
   const size_t shm = block_bytes<PM>(b.cap);
   if (shm <= (size_t)smem_optin()) {
-    poly_assemble_block_kernel<PM><<<std::min(b.nrows, 148 * 16), nt, shm, st>>>(b);
+    poly_assemble_block_kernel<PM><<<std::min(b.nrows, num_sms() * 16), nt, shm, st>>>(b);
     AIRG_LAUNCH_CHECK();
     return AIRG_OK;
   }
-  const int grid = std::min(b.nrows, 148 * 2);
+  const int grid = std::min(b.nrows, num_sms() * 2);
   AIRG_TRY(scratch(&b.gmem, shm * grid, st));
   b.gstride = shm;
   poly_assemble_block_kernel<PM><<<grid, 256, 0, st>>>(b);

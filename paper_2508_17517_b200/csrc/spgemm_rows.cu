@@ -646,7 +646,7 @@ static int launch_span_numeric_nw(const SpanNumArgs& a, cudaStream_t s) {
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
     attr = shm;
   }
-  span_numeric_kernel<NW, KP, D><<<blocks_for(a.nrows, NW, 148 * 64), 32 * NW, shm, s>>>(a);
+  span_numeric_kernel<NW, KP, D><<<blocks_for(a.nrows, NW, num_sms() * 64), 32 * NW, shm, s>>>(a);
   AIRG_LAUNCH_CHECK();
   return AIRG_OK;
 }
@@ -691,7 +691,7 @@ static int launch_span_count(const SpanCountArgs& a, int span, cudaStream_t s) {
                                    kSpanMax));
     attr = true;
   }
-  span_count_kernel<NT><<<std::min(a.nrows, 148 * 16), NT, (size_t)span, s>>>(a);
+  span_count_kernel<NT><<<std::min(a.nrows, num_sms() * 16), NT, (size_t)span, s>>>(a);
   AIRG_LAUNCH_CHECK();
   return AIRG_OK;
 }
@@ -777,10 +777,10 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
           const int v = getenv("AIRG_COUNT_NT") ? atoi(getenv("AIRG_COUNT_NT")) : 256;
           return std::max(32, std::min(256, v)) & ~31;
         }();
-        spgemm_count_block_kernel<<<std::min(nr, 148 * 16), cnt_nt, (size_t)(1 << bits) * 4,
+        spgemm_count_block_kernel<<<std::min(nr, num_sms() * 16), cnt_nt, (size_t)(1 << bits) * 4,
                                     fk.stream(c)>>>(a);
       } else {
-        spgemm_count_kernel<<<blocks_for(nr, warps, 148 * 32), warps * 32, shm, fk.stream(c)>>>(a);
+        spgemm_count_kernel<<<blocks_for(nr, warps, num_sms() * 32), warps * 32, shm, fk.stream(c)>>>(a);
       }
       AIRG_LAUNCH_CHECK();
     }
@@ -871,7 +871,7 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
         // B row (~70-200 entries), so 128 threads beat 256 (38 vs 49 ms) for
         // the 512..1024 class; the long classes keep 256.
         const size_t shm = (size_t)(1 << cbits[c]) * 12 + 1024;
-        const int grid = std::min(nr, 148 * 32);
+        const int grid = std::min(nr, num_sms() * 32);
         static int nts[7] = {0, 0, 128, 128, 256, 256, 256};
         static bool parsed = false;
         if (!parsed) {  // AIRG_NT="t2,t3,t4,t5,t6" overrides (measurement only)
@@ -892,7 +892,7 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
 #undef AIRG_NUMBLK
       } else {
         const size_t shm = (size_t)cwarps[c] * ((1 << cbits[c]) * 12 + 1024);
-        spgemm_numeric_kernel<<<blocks_for(nr, cwarps[c], 148 * 32), cwarps[c] * 32, shm, st>>>(a);
+        spgemm_numeric_kernel<<<blocks_for(nr, cwarps[c], num_sms() * 32), cwarps[c] * 32, shm, st>>>(a);
       }
       AIRG_LAUNCH_CHECK();
     }
@@ -1120,11 +1120,11 @@ static int ap_onepoint(const Mat& A, int nc, const int* pcol, airg_csr_result** 
         cl.count[1], cl.list(1), A.p, A.c, A.v, pcol, rcol, rval, cnt);
   AIRG_LAUNCH_CHECK();
   if (cl.count[2])
-    ap_onepoint_kernel<256, kW0><<<blocks_for(cl.count[2], kW0, 148 * 4), 32 * kW0, shm0, fk.stream(2)>>>(
+    ap_onepoint_kernel<256, kW0><<<blocks_for(cl.count[2], kW0, num_sms() * 4), 32 * kW0, shm0, fk.stream(2)>>>(
         cl.count[2], cl.list(2), A.p, A.c, A.v, pcol, rcol, rval, cnt);
   AIRG_LAUNCH_CHECK();
   if (cl.count[3])
-    ap_onepoint_kernel<kApCap, kW1><<<blocks_for(cl.count[3], kW1, 148 * 4), 32 * kW1, shm1,
+    ap_onepoint_kernel<kApCap, kW1><<<blocks_for(cl.count[3], kW1, num_sms() * 4), 32 * kW1, shm1,
                                       fk.stream(3)>>>(cl.count[3], cl.list(3), A.p, A.c, A.v, pcol,
                                                       rcol, rval, cnt);
   AIRG_LAUNCH_CHECK();

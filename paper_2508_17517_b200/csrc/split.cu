@@ -414,7 +414,7 @@ static int ddc_pass_run(int n, const int* ptr, const int* col, const double* val
     }
     if (shm > 48 * 1024)
       AIRG_CUDA(cudaFuncSetAttribute(ddc_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-    ddc_hist_kernel<<<blocks_for(nf, 256, 148 * 2), 256, shm, s>>>(nf, ratio, de, nbins + 1, hist);
+    ddc_hist_kernel<<<blocks_for(nf, 256, num_sms() * 2), 256, shm, s>>>(nf, ratio, de, nbins + 1, hist);
     AIRG_LAUNCH_CHECK();
     std::vector<unsigned long long> hh(nbins + 2);
     AIRG_CUDA(cudaMemcpyAsync(hh.data(), hist, (nbins + 2) * sizeof(unsigned long long),
