@@ -769,7 +769,8 @@ __global__ void __launch_bounds__(256) poly_small_kernel(PolyArgs a) {
 }
 
 // class of a pattern row: register classes for <= 8 / <= 16 entries (plain
-// assembly only), else the pow2 caps x (bitmap | hash) position map
+// assembly only), else the pow2 caps x (bitmap | hash) position map; the top
+// cap class takes every longer row (its cap is the level's longest row)
 __global__ void poly_class_kernel(int n, const int* __restrict__ Pp, const int* __restrict__ Pc,
                                   int ncap, int reg, int* __restrict__ ids) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -780,7 +781,7 @@ __global__ void poly_class_kernel(int n, const int* __restrict__ Pp, const int* 
       continue;
     }
     int c = 0;
-    while ((32 << c) < m) ++c;
+    while (c < ncap - 1 && (32 << c) < m) ++c;
     const bool bit = m == 0 || (long long)Pc[b + m - 1] - Pc[b] < kPolySpan;
     ids[i] = c + (bit ? 0 : ncap);
   }
@@ -836,7 +837,9 @@ static int launch_poly_class(PolyArgs b, cudaStream_t st) {
     AIRG_LAUNCH_CHECK();
     return AIRG_OK;
   }
-  const int grid = std::min(b.nrows, num_sms() * 2);
+  // one working set per CTA, at most ~2 GB of them
+  const int grid = (int)std::max<long long>(
+      1, std::min<long long>(std::min(b.nrows, num_sms() * 2), (2ll << 30) / (long long)shm));
   AIRG_TRY(scratch(&b.gmem, shm * grid, st));
   b.gstride = shm;
   poly_assemble_block_kernel<PM><<<grid, 256, 0, st>>>(b);
@@ -846,12 +849,12 @@ static int launch_poly_class(PolyArgs b, cudaStream_t st) {
 }
 
 static int run_poly_kernel(PolyArgs& a, int maxlen, cudaStream_t s) {
+  // pow2 caps 32 .. 32 << (kPolyCaps - 1); rows beyond go to the top class
+  // with the longest row as its cap (global-memory working set), so any row
+  // length assembles, as the reference's does (polynomial.py:379-416)
+  constexpr int kPolyCaps = (kMaxCls - 2) / 2;
   int ncap = 1;
-  while ((32 << (ncap - 1)) < maxlen) ++ncap;
-  if (2 * ncap + 2 > kMaxCls) {
-    set_error("pattern row of %d entries exceeds the assembly classes", maxlen);
-    return AIRG_ERR_VALUE;
-  }
+  while (ncap < kPolyCaps && (32 << (ncap - 1)) < maxlen) ++ncap;
   int* ids = nullptr;
   AIRG_TRY(scratch(&ids, a.n > 0 ? a.n : 1, s));
   const int reg = a.masked ? 0 : 1;  // register classes: plain assembly only
@@ -877,6 +880,7 @@ static int run_poly_kernel(PolyArgs& a, int maxlen, cudaStream_t s) {
       continue;
     }
     b.cap = 32 << (c % ncap);
+    if (c % ncap == ncap - 1) b.cap = std::max(b.cap, maxlen);
     if (c < ncap) AIRG_TRY(launch_poly_class<BitPos>(b, fk.stream(c)));
     else AIRG_TRY(launch_poly_class<HashPos>(b, fk.stream(c)));
   }

@@ -89,3 +89,20 @@ def test_masked_product_all_classes():
     B = hub_matrix(6, 20000, HUBS[::-1])
     P = hub_matrix(7, 20000, HUBS)
     same(G.spgemm_fixed_sparsity(dev_csr(A), dev_csr(B), dev_csr(P)), O.spgemm_masked(A, B, P))
+
+
+# pattern rows beyond the largest pow2 cap class (32 << 10 = 32768 entries):
+# they share the top class, whose cap is the longest row (global-memory
+# working set), so any row length assembles as in the reference
+LONG_HUBS = [(30000, 33000, 60000),   # top class, just above 32768
+             (40000, 50000, 70000),   # top class, cap = this row's length
+             (20000, 20000, 50000)]   # cap 32768 class below it
+
+
+@pytest.mark.parametrize('order', [2, 5])
+def test_poly_assembly_rows_beyond_caps(order):
+    import paper_2508_17517_b200 as G
+    A = hub_matrix(8, 80000, LONG_HUBS)
+    rng = np.random.default_rng(10 + order)
+    p = O.Poly('arnoldi_coeff', order, order, coeffs=rng.standard_normal(order + 1))
+    same(G.assemble_fixed_sparsity(dev_poly(p), dev_csr(A)), O.assemble_poly(p, A))
