@@ -190,28 +190,44 @@ static int pmisr_run(int n, const int* cptr, const int* ccol, u128 s0, u128 inc,
                      signed char* labels, int* loops_h, cudaStream_t s) {
   double* w = nullptr;
   signed char* st = nullptr;
+  // rounds are enqueued kLubyBatch at a time, each counting the undecided
+  // rows left in its own slot, with one read-back per batch: a round after
+  // the last one finds no undecided row and changes nothing
+  static const int kLubyBatch = getenv("AIRG_LUBY_BATCH") ? std::max(1, atoi(getenv("AIRG_LUBY_BATCH"))) : 4;
   int* rem = nullptr;
   AIRG_TRY(scratch(&w, n, s));
   AIRG_TRY(scratch(&st, n, s));
-  AIRG_TRY(scratch(&rem, 1, s));
+  AIRG_TRY(scratch(&rem, kLubyBatch, s));
   AIRG_TRY(pcg64_fill(s0, inc, n, 0.0, 1.0, w, s));
   const int nb = blocks_for(n, 256);
   luby_weight_kernel<<<nb, 256, 0, s>>>(n, cptr, w);
   AIRG_CUDA(cudaMemsetAsync(st, 0, (size_t)n, s));
   int loops = 0;
-  int left = n;
-  while (left > 0) {
+  bool more = n > 0;
+  std::vector<int> left(kLubyBatch);
+  while (more) {
     if (max_loops >= 0 && loops >= max_loops) break;  // leftovers -> C in finish
-    // per-round new-F marker; earlier markers read as decided F
-    const signed char mark = (signed char)(3 + loops % 120);
-    if (loops > 0 && loops % 120 == 0) luby_normalise_kernel<<<nb, 256, 0, s>>>(n, st);
-    luby_select_kernel<<<nb, 256, 0, s>>>(n, cptr, ccol, w, st, mark);
-    AIRG_CUDA(cudaMemsetAsync(rem, 0, sizeof(int), s));
-    luby_block_kernel<<<nb, 256, 0, s>>>(n, cptr, ccol, st, mark, rem);
+    const int r = max_loops >= 0 ? std::min(kLubyBatch, max_loops - loops) : kLubyBatch;
+    AIRG_CUDA(cudaMemsetAsync(rem, 0, r * sizeof(int), s));
+    for (int q = 0; q < r; ++q) {
+      const int l = loops + q;
+      // per-round new-F marker; earlier markers read as decided F
+      const signed char mark = (signed char)(3 + l % 120);
+      if (l > 0 && l % 120 == 0) luby_normalise_kernel<<<nb, 256, 0, s>>>(n, st);
+      luby_select_kernel<<<nb, 256, 0, s>>>(n, cptr, ccol, w, st, mark);
+      luby_block_kernel<<<nb, 256, 0, s>>>(n, cptr, ccol, st, mark, rem + q);
+    }
     AIRG_LAUNCH_CHECK();
-    AIRG_CUDA(cudaMemcpyAsync(&left, rem, sizeof(int), cudaMemcpyDeviceToHost, s));
+    AIRG_CUDA(cudaMemcpyAsync(left.data(), rem, r * sizeof(int), cudaMemcpyDeviceToHost, s));
     AIRG_CUDA(cudaStreamSynchronize(s));
-    ++loops;
+    int q = 0;
+    while (q < r && left[q] > 0) ++q;
+    if (q < r) {
+      loops += q + 1;  // the round that left no undecided row
+      more = false;
+    } else {
+      loops += r;
+    }
   }
   luby_finish_kernel<<<nb, 256, 0, s>>>(n, st, labels, 1);
   AIRG_LAUNCH_CHECK();
@@ -265,28 +281,38 @@ int split_index(int n, const signed char* labels, int* pos, int* f_idx, int* c_i
 }
 
 // ---- DDC (splitting.py:162-207) --------------------------------------------
+// b = #{edges < r} per ratio (binary search over the edges in shared
+// memory); 32-bit shared bins, lanes of a warp with the same bin add once
+// (__match_any_sync: the ratios cluster in few bins, and same-address shared
+// atomics serialise), one global 64-bit add per non-empty bin and block
 __global__ void ddc_hist_kernel(int nf, const double* __restrict__ ratio, const double* __restrict__ edges,
                                 int nedges, unsigned long long* __restrict__ hist) {
-  extern __shared__ unsigned long long sh[];
-  double* se = (double*)(sh + nedges + 1);
-  for (int k = threadIdx.x; k <= nedges; k += blockDim.x) sh[k] = 0ull;
+  extern __shared__ unsigned long long sh64[];
+  unsigned* sh = (unsigned*)sh64;
+  double* se = (double*)(sh64 + nedges + 1);
+  for (int k = threadIdx.x; k <= nedges; k += blockDim.x) sh[k] = 0u;
   for (int k = threadIdx.x; k < nedges; k += blockDim.x) se[k] = edges[k];
   __syncthreads();
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nf;
-       t += (long long)gridDim.x * blockDim.x) {
-    const double r = ratio[t];
-    // b = #{edges < r}
-    int lo = 0, hi = nedges;
-    while (lo < hi) {
-      int mid = (lo + hi) >> 1;
-      if (se[mid] < r) lo = mid + 1;
-      else hi = mid;
+  const int lane = threadIdx.x & 31;
+  for (long long t0 = blockIdx.x * (long long)blockDim.x; t0 < nf; t0 += (long long)gridDim.x * blockDim.x) {
+    const long long t = t0 + threadIdx.x;
+    int b = -1;
+    if (t < nf) {
+      const double r = ratio[t];
+      int lo = 0, hi = nedges;
+      while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (se[mid] < r) lo = mid + 1;
+        else hi = mid;
+      }
+      b = lo;
     }
-    atomicAdd(sh + lo, 1ull);
+    const unsigned m = __match_any_sync(0xffffffffu, b);
+    if (b >= 0 && lane == __ffs(m) - 1) atomicAdd(sh + b, (unsigned)__popc(m));
   }
   __syncthreads();
   for (int k = threadIdx.x; k <= nedges; k += blockDim.x)
-    if (sh[k]) atomicAdd(hist + k, sh[k]);
+    if (sh[k]) atomicAdd(hist + k, (unsigned long long)sh[k]);
 }
 
 __global__ void ddc_convert_kernel(int nf, const int* __restrict__ f_idx, const double* __restrict__ ratio,
