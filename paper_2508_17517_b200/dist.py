@@ -653,6 +653,7 @@ def setup_distributed(comm, A, cfg, poly_inject=None, replicate_below=None, forc
         halo_a = Halo(comm, cur.rows, remote_cols(cur.M.col_indices, cur.rows, r))
         A_ext = with_cols(cur.M, halo_a.ext_cols(cur.M.col_indices), n + halo_a.n)
         lab_ext = halo_a.ext(labels)
+        tick('cf_split.halo')
         stats = []
         nf_glob = comm.sum_dev((lab_ext[:n] == 0).sum())
         for _ in range(cfg.ddc_its):
