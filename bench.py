@@ -151,7 +151,11 @@ def reference_arm(args, rank, world):
     ncpu, blas = cpu_cores_note()
     line = {
         'impl': 'reference', 'metric': METRIC, 'value': v, 'unit': 'DOF/s',
-        'n_gpus': world, 'steps': args.steps, 'warmup': args.warmup, 'ms_per_step': t * 1e3,
+        # whole-host time per step: the instances run concurrently, so one
+        # sample-step of the host takes n / value (each instance's own sample
+        # time is instance_ms_per_sample)
+        'n_gpus': world, 'steps': args.steps, 'warmup': args.warmup, 'ms_per_step': n / v * 1e3,
+        'instance_ms_per_sample': t * 1e3, 'samples_timed': procs * per,
         'higher_is_better': True, 'scaling': 'weak', 'vs_baseline': None, 'dtype': 'f64',
         'data': 'synthetic (2D upwind advection stencil, b=0, x0=1)',
         'config': {'workload': (f'AIRG pi/4 upwind DG Q1 advection {args.nx}x{args.nx} cells'
