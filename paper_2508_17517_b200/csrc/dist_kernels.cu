@@ -322,8 +322,7 @@ int airg_luby_round(int n, const int32_t* cptr, const int32_t* ccol_ext, const d
                                              rem);
   AIRG_LAUNCH_CHECK();
   if (remaining_h) {  // null: no convergence check this round (no host sync)
-    AIRG_CUDA(cudaMemcpyAsync(remaining_h, rem, sizeof(int), cudaMemcpyDeviceToHost, s));
-    AIRG_CUDA(cudaStreamSynchronize(s));
+    AIRG_CUDA(read_back(remaining_h, rem, sizeof(int), s));
   }
   release(rem, s);
   return AIRG_OK;
@@ -358,8 +357,9 @@ int airg_ddc_ratios(int nf, int row0, const int32_t* f_loc, const int32_t* ptr, 
   std::vector<double> h(3 * (size_t)np);
   AIRG_CUDA(cudaMemcpyAsync(bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
   if (nf > 0)
-    AIRG_CUDA(cudaMemcpyAsync(h.data(), parts, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
+    AIRG_CUDA(read_back(h.data(), parts, h.size() * sizeof(double), s));
+  else
+    AIRG_CUDA(cudaStreamSynchronize(s));
   double mn = INFINITY, mx = -INFINITY, sm = 0.0;
   for (int b = 0; nf > 0 && b < np; ++b) {
     mn = std::min(mn, h[3 * b]);
@@ -407,8 +407,7 @@ int airg_ddc_convert(int nf, const int32_t* f_loc, const double* ratio, double c
                                                                (signed char*)labels, c);
   AIRG_LAUNCH_CHECK();
   if (converted_h) {  // NULL: no host read (the caller counts the labels itself)
-    AIRG_CUDA(cudaMemcpyAsync(converted_h, c, sizeof(int), cudaMemcpyDeviceToHost, s));
-    AIRG_CUDA(cudaStreamSynchronize(s));
+    AIRG_CUDA(read_back(converted_h, c, sizeof(int), s));
   }
   release(c, s);
   return AIRG_OK;

@@ -459,8 +459,7 @@ static int arnoldi_multi(int n, const int* p, const int* c, const double* v, con
   const Gate second{ctl, ctl + 1};      // second sweep only
   double bb = 0;
   AIRG_TRY(dev_dot(n, b, b, dsc, nullptr, d, always, s));
-  AIRG_CUDA(cudaMemcpyAsync(&bb, dsc, sizeof(double), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
+  AIRG_CUDA(read_back(&bb, dsc, sizeof(double), s));
   const double beta = std::sqrt(bb);
   *beta_h = beta;
   if (beta == 0.0) {
@@ -489,8 +488,7 @@ static int arnoldi_multi(int n, const int* p, const int* c, const double* v, con
   }
   int ctlh[4];
   AIRG_CUDA(cudaMemcpyAsync(H_h, Hd, (size_t)(m + 1) * m * sizeof(double), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaMemcpyAsync(ctlh, ctl, sizeof ctlh, cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
+  AIRG_CUDA(read_back(ctlh, ctl, sizeof ctlh, s));
   *k_h = ctlh[2];
   release(V, s);
   release(w, s);
@@ -603,8 +601,7 @@ static int arnoldi_grid(int n, const int* p, const int* c, const double* v, cons
   const Gate always{nullptr, nullptr};
   double bb = 0;
   AIRG_TRY(dev_dot(n, b, b, sc, nullptr, d, always, s));
-  AIRG_CUDA(cudaMemcpyAsync(&bb, sc, sizeof(double), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
+  AIRG_CUDA(read_back(&bb, sc, sizeof(double), s));
   const double beta = std::sqrt(bb);
   *beta_h = beta;
   if (beta == 0.0) {
@@ -616,8 +613,7 @@ static int arnoldi_grid(int n, const int* p, const int* c, const double* v, cons
   AIRG_CUDA(cudaLaunchCooperativeKernel((const void*)arnoldi_grid_kernel, np, 256, args, 0, s));
   int k = 0;
   AIRG_CUDA(cudaMemcpyAsync(H_h, Hd, (size_t)(m + 1) * m * sizeof(double), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaMemcpyAsync(&k, info, sizeof(int), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
+  AIRG_CUDA(read_back(&k, info, sizeof(int), s));
   *k_h = k;
   for (void* q : {(void*)V, (void*)w, (void*)sc, (void*)Hd, (void*)info}) release(q, s);
   return AIRG_OK;
@@ -697,8 +693,7 @@ extern "C" int airg_arnoldi(int n, const int32_t* p, const int32_t* c, const dou
     int hi[2];
     AIRG_CUDA(cudaMemcpyAsync(H_h, H, (size_t)(m + 1) * m * sizeof(double), cudaMemcpyDeviceToHost, s));
     AIRG_CUDA(cudaMemcpyAsync(hi, info, sizeof hi, cudaMemcpyDeviceToHost, s));
-    AIRG_CUDA(cudaMemcpyAsync(beta_h, dinfo, sizeof(double), cudaMemcpyDeviceToHost, s));
-    AIRG_CUDA(cudaStreamSynchronize(s));
+    AIRG_CUDA(read_back(beta_h, dinfo, sizeof(double), s));
     for (void* q : {(void*)V, (void*)w, (void*)H, (void*)dinfo, (void*)info}) release(q, s);
     if (hi[1]) {
       set_error("cannot build a Krylov space from a zero vector");
@@ -707,8 +702,7 @@ extern "C" int airg_arnoldi(int n, const int32_t* p, const int32_t* c, const dou
     *k_h = hi[0];
   } else {
     int nnz = 0;
-    AIRG_CUDA(cudaMemcpyAsync(&nnz, p + n, sizeof(int), cudaMemcpyDeviceToHost, s));
-    AIRG_CUDA(cudaStreamSynchronize(s));
+    AIRG_CUDA(read_back(&nnz, p + n, sizeof(int), s));
     const int vs = arnoldi_vs(nnz, n);
     st = grid_arnoldi_ok(n, vs) ? arnoldi_grid(n, p, c, v, b, m, H_h, k_h, beta_h, vs, s)
                                 : arnoldi_multi(n, p, c, v, b, m, H_h, k_h, beta_h, vs, s);

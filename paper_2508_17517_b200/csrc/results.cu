@@ -17,8 +17,7 @@ int scan_counts(const int* in, int* out, int n, long long* total_h, cudaStream_t
   }
   if (total_h) {
     int t = 0;
-    AIRG_CUDA(cudaMemcpyAsync(&t, out + n, sizeof(int), cudaMemcpyDeviceToHost, s));
-    AIRG_CUDA(cudaStreamSynchronize(s));
+    AIRG_CUDA(read_back(&t, out + n, sizeof(int), s));
     *total_h = t;
   }
   return AIRG_OK;
@@ -36,8 +35,7 @@ int scan_counts64(const long long* in, long long* out, int n, long long* total_h
   }
   if (total_h) {
     long long t = 0;
-    AIRG_CUDA(cudaMemcpyAsync(&t, out + n, sizeof(long long), cudaMemcpyDeviceToHost, s));
-    AIRG_CUDA(cudaStreamSynchronize(s));
+    AIRG_CUDA(read_back(&t, out + n, sizeof(long long), s));
     *total_h = t;
   }
   return AIRG_OK;

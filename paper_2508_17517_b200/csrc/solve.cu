@@ -1210,8 +1210,7 @@ int airg_csr_to_ell(int nrows, const int32_t* ptr, const int32_t* col, const dou
   csr_to_ell_kernel<<<blocks_for(nrows, 256), 256, 0, s>>>(nrows, width, ptr, col, val, ell_col, ell_val, ovf);
   AIRG_LAUNCH_CHECK();
   int h = 0;
-  AIRG_CUDA(cudaMemcpyAsync(&h, ovf, sizeof(int), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
+  AIRG_CUDA(read_back(&h, ovf, sizeof(int), s));
   release(ovf, s);
   if (h) {
     set_error("a row is longer than the ELL width %d", width);
@@ -1243,8 +1242,7 @@ int airg_norm2(int n, const double* x, double* out_h, void* stream) {
   sumsq_kernel<<<nb, 256, 0, s>>>(n, x, parts);
   finish_norm_kernel<<<1, 1024, 0, s>>>(nb, parts, d);
   AIRG_LAUNCH_CHECK();
-  AIRG_CUDA(cudaMemcpyAsync(out_h, d, sizeof(double), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
+  AIRG_CUDA(read_back(out_h, d, sizeof(double), s));
   release(parts, s);
   return AIRG_OK;
 }
@@ -1455,8 +1453,7 @@ static int prepare_chain(LevelOps& L, cudaStream_t s) {
   release(cost, s);
   release(w, s);
   int need = 0;  // one read per level at plan build: the launch's shared bytes
-  AIRG_CUDA(cudaMemcpyAsync(&need, L.chain_part + 3 * G, sizeof(int), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
+  AIRG_CUDA(read_back(&need, L.chain_part + 3 * G, sizeof(int), s));
   L.chain_smem = std::min(chain_smem(), ((need + 1023) / 1024) * 1024 + 1024);
   L.chain_G = G;
   return AIRG_OK;
@@ -1568,8 +1565,7 @@ static int build_dense_coarse(airg_plan* p, cudaStream_t s) {
   ++g_launches;
   AIRG_LAUNCH_CHECK();
   int stopped = 0;
-  AIRG_CUDA(cudaMemcpyAsync(&stopped, p->iflag, sizeof(int), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
+  AIRG_CUDA(read_back(&stopped, p->iflag, sizeof(int), s));
   if (stopped & 1) {  // the reference stops per right-hand side (polynomial.py:312-355)
     dfree(p->coarseQ);
     p->coarseQ = nullptr;
@@ -1719,8 +1715,7 @@ static int make_ell(airg_plan* p, Csr& A, cudaStream_t s) {
   row_maxlen_kernel<<<blocks_for(A.nrows, 256), 256, 0, s>>>(A.nrows, A.ptr, d);
   AIRG_LAUNCH_CHECK();
   int w = 0;
-  AIRG_CUDA(cudaMemcpyAsync(&w, d, sizeof(int), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
+  AIRG_CUDA(read_back(&w, d, sizeof(int), s));
   release(d, s);
   if (w < 1 || w > 4 || (double)A.nnz < fill * (double)A.nrows * w) return AIRG_OK;
   int* ecol = nullptr;
@@ -1883,8 +1878,7 @@ static int residual_launch(airg_plan* p, const double* b, const double* x, cudaS
 static int residual_norm(airg_plan* p, const double* b, const double* x, double* rnorm,
                          cudaStream_t s) {
   AIRG_TRY(residual_launch(p, b, x, s));
-  AIRG_CUDA(cudaMemcpyAsync(p->norm_h, p->norm_d, sizeof(double), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
+  AIRG_CUDA(read_back(p->norm_h, p->norm_d, sizeof(double), s));
   *rnorm = *p->norm_h;
   return AIRG_OK;
 }
@@ -1936,8 +1930,7 @@ static int richardson_body(airg_plan* p, const double* b, double* x, double rtol
     finish_norm_kernel<<<1, 1024, 0, s>>>(nb, p->parts, p->norm_d);
     g_launches += 2;
     AIRG_LAUNCH_CHECK();
-    AIRG_CUDA(cudaMemcpyAsync(p->norm_h, p->norm_d, sizeof(double), cudaMemcpyDeviceToHost, s));
-    AIRG_CUDA(cudaStreamSynchronize(s));
+    AIRG_CUDA(read_back(p->norm_h, p->norm_d, sizeof(double), s));
     bnorm = *p->norm_h;
   }
   AIRG_TRY(residual_norm(p, b, x, &rnorm, s));
@@ -1959,8 +1952,7 @@ static int richardson_body(airg_plan* p, const double* b, double* x, double rtol
       AIRG_TRY(launch_axpby(n, x, nullptr, 1.0, x, nullptr, 1.0, p->e, t, p->exact));
       return residual_launch(p, b, x, t);
     }));
-    AIRG_CUDA(cudaMemcpyAsync(p->norm_h, p->norm_d, sizeof(double), cudaMemcpyDeviceToHost, s));
-    AIRG_CUDA(cudaStreamSynchronize(s));
+    AIRG_CUDA(read_back(p->norm_h, p->norm_d, sizeof(double), s));
     rnorm = *p->norm_h;
     ++its;
     history[its] = rnorm;
@@ -3111,13 +3103,11 @@ int airg_dplan_richardson(airg_dplan* p, const double* b, double* x, double rtol
     finish_sum_kernel<<<1, 1024, 0, s>>>(nb, p->parts, p->nrm_loc);
     AIRG_LAUNCH_CHECK();
     AIRG_TRY(norm_allreduce(p, s));
-    AIRG_CUDA(cudaMemcpyAsync(&p->norm_h, p->nrm_glob, sizeof(double), cudaMemcpyDeviceToHost, s));
-    AIRG_CUDA(cudaStreamSynchronize(s));
+    AIRG_CUDA(read_back(&p->norm_h, p->nrm_glob, sizeof(double), s));
   }
   const double bnorm = std::sqrt(p->norm_h);
   AIRG_TRY(dplan_residual(p, b, s));
-  AIRG_CUDA(cudaMemcpyAsync(&p->norm_h, p->nrm_glob, sizeof(double), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
+  AIRG_CUDA(read_back(&p->norm_h, p->nrm_glob, sizeof(double), s));
   double rn = std::sqrt(p->norm_h);
   history[0] = rn;
   const double thr = std::max(rtol * (bnorm > 0 ? bnorm : rn), atol);
@@ -3162,8 +3152,7 @@ int airg_dplan_richardson(airg_dplan* p, const double* b, double* x, double rtol
     } else {
       AIRG_TRY(iteration(s));
     }
-    AIRG_CUDA(cudaMemcpyAsync(&p->norm_h, p->nrm_glob, sizeof(double), cudaMemcpyDeviceToHost, s));
-    AIRG_CUDA(cudaStreamSynchronize(s));
+    AIRG_CUDA(read_back(&p->norm_h, p->nrm_glob, sizeof(double), s));
     rn = std::sqrt(p->norm_h);
     ++its;
     history[its] = rn;

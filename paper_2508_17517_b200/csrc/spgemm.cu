@@ -659,8 +659,7 @@ static int max_row_len(int m, const int* p, int* out, cudaStream_t s) {
   AIRG_CUDA(cudaMemsetAsync(d, 0, sizeof(int), s));
   if (m > 0) max_rowlen_kernel<<<blocks_for(m, 256, num_sms() * 8), 256, 0, s>>>(m, p, d);
   AIRG_LAUNCH_CHECK();
-  AIRG_CUDA(cudaMemcpyAsync(out, d, sizeof(int), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
+  AIRG_CUDA(read_back(out, d, sizeof(int), s));
   release(d, s);
   return AIRG_OK;
 }
@@ -1010,8 +1009,8 @@ int airg_spgemm_masked(int m, int k, int n, const int32_t* Ap, const int32_t* Ac
   int maxlen = 0;
   AIRG_TRY(max_row_len(m, Pp, &maxlen, s));
   int pnnz = 0;
-  if (m > 0) AIRG_CUDA(cudaMemcpyAsync(&pnnz, Pp + m, sizeof(int), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
+  if (m > 0) AIRG_CUDA(read_back(&pnnz, Pp + m, sizeof(int), s));
+  else AIRG_CUDA(cudaStreamSynchronize(s));
   double* pv = nullptr;
   unsigned char* keep = nullptr;
   int* cnt = nullptr;
@@ -1141,8 +1140,8 @@ int airg_drop_lump(int m, int ncols, const int32_t* p, const int32_t* c, const d
     return AIRG_ERR_VALUE;
   }
   int nnz = 0;
-  if (m > 0) AIRG_CUDA(cudaMemcpyAsync(&nnz, p + m, sizeof(int), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
+  if (m > 0) AIRG_CUDA(read_back(&nnz, p + m, sizeof(int), s));
+  else AIRG_CUDA(cudaStreamSynchronize(s));
   int *rcol = nullptr, *cnt = nullptr, *anyd = nullptr;
   double* rval = nullptr;
   const long long raw = (long long)nnz + m;
@@ -1157,8 +1156,7 @@ int airg_drop_lump(int m, int ncols, const int32_t* p, const int32_t* c, const d
   AIRG_LAUNCH_CHECK();
   AIRG_TRY(finish_raw(m, ncols, p, cnt, rcol, rval, out, s));
   int ad = 0;
-  AIRG_CUDA(cudaMemcpyAsync(&ad, anyd, sizeof(int), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
+  AIRG_CUDA(read_back(&ad, anyd, sizeof(int), s));
   if (changed_h) *changed_h = ad;
   for (void* q : {(void*)rcol, (void*)rval, (void*)cnt, (void*)anyd}) release(q, s);
   return AIRG_OK;
@@ -1214,8 +1212,8 @@ int airg_restriction(int n, int nc, const int32_t* zp, const int32_t* zc, const 
                      void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   int znnz = 0;
-  if (nc > 0) AIRG_CUDA(cudaMemcpyAsync(&znnz, zp + nc, sizeof(int), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
+  if (nc > 0) AIRG_CUDA(read_back(&znnz, zp + nc, sizeof(int), s));
+  else AIRG_CUDA(cudaStreamSynchronize(s));
   airg_csr_result* r = new_result(nc, n, s);
   AIRG_TRY(result_alloc_entries(r, (long long)znnz + nc, true));
   const double mean = nc > 0 ? (double)znnz / nc : 0.0;  // lanes per row: 4 entries per lane

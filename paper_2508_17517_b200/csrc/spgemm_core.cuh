@@ -448,9 +448,10 @@ static int classify(int m, const long long* size, const std::vector<long long>& 
   if (m > 0) classify_kernel<<<(m + 255) / 256, 256, 0, s>>>(m, size, dth, ncls, out.lists, cnt);
   AIRG_LAUNCH_CHECK();
   out.count.assign(ncls, 0);
-  AIRG_CUDA(cudaMemcpyAsync(out.count.data(), cnt, ncls * sizeof(int), cudaMemcpyDeviceToHost, s));
-  if (extra_dev) AIRG_CUDA(cudaMemcpyAsync(extra_h, extra_dev, sizeof(int), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
+  if (extra_dev)
+    AIRG_CUDA(read_back({{out.count.data(), cnt, ncls * sizeof(int)}, {extra_h, extra_dev, sizeof(int)}}, s));
+  else
+    AIRG_CUDA(read_back(out.count.data(), cnt, ncls * sizeof(int), s));
   out.m = m;
   release(dth, s);
   release(cnt, s);
@@ -467,9 +468,10 @@ static int classify_ids(int m, const int* ids, int ncls, Classes& out, cudaStrea
   if (m > 0) classify_ids_kernel<<<(m + 255) / 256, 256, 0, s>>>(m, ids, ncls, out.lists, cnt);
   AIRG_LAUNCH_CHECK();
   out.count.assign(ncls, 0);
-  AIRG_CUDA(cudaMemcpyAsync(out.count.data(), cnt, ncls * sizeof(int), cudaMemcpyDeviceToHost, s));
-  if (extra_dev) AIRG_CUDA(cudaMemcpyAsync(extra_h, extra_dev, sizeof(int), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
+  if (extra_dev)
+    AIRG_CUDA(read_back({{out.count.data(), cnt, ncls * sizeof(int)}, {extra_h, extra_dev, sizeof(int)}}, s));
+  else
+    AIRG_CUDA(read_back(out.count.data(), cnt, ncls * sizeof(int), s));
   out.m = m;
   release(cnt, s);
   return AIRG_OK;

@@ -786,8 +786,7 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
     }
     AIRG_TRY(fk.end(s));
     int novf = 0;
-    AIRG_CUDA(cudaMemcpyAsync(&novf, ovf_n, sizeof(int), cudaMemcpyDeviceToHost, s));
-    AIRG_CUDA(cudaStreamSynchronize(s));
+    AIRG_CUDA(read_back(&novf, ovf_n, sizeof(int), s));
     if (novf) {
       std::vector<int> rows(novf);
       AIRG_CUDA(cudaMemcpyAsync(rows.data(), ovf_rows, novf * sizeof(int), cudaMemcpyDeviceToHost, s));

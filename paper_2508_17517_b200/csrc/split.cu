@@ -219,8 +219,7 @@ static int pmisr_run(int n, const int* cptr, const int* ccol, u128 s0, u128 inc,
       luby_block_kernel<<<nb, 256, 0, s>>>(n, cptr, ccol, st, mark, rem + q);
     }
     AIRG_LAUNCH_CHECK();
-    AIRG_CUDA(cudaMemcpyAsync(left.data(), rem, r * sizeof(int), cudaMemcpyDeviceToHost, s));
-    AIRG_CUDA(cudaStreamSynchronize(s));
+    AIRG_CUDA(read_back(left.data(), rem, r * sizeof(int), s));
     int q = 0;
     while (q < r && left[q] > 0) ++q;
     if (q < r) {
@@ -394,8 +393,7 @@ static int ddc_pass_run(int n, const int* ptr, const int* col, const double* val
     const int pb = blocks_for(nf, 256, 1024);
     sum_kernel<<<pb, 256, 0, s>>>(nf, ratio, mm + 2);
     std::vector<double> h(2 + pb);
-    AIRG_CUDA(cudaMemcpyAsync(h.data(), mm, (2 + pb) * sizeof(double), cudaMemcpyDeviceToHost, s));
-    AIRG_CUDA(cudaStreamSynchronize(s));
+    AIRG_CUDA(read_back(h.data(), mm, (2 + pb) * sizeof(double), s));
     cudaFreeAsync(tmp, s);
     release(mm, s);
     if (bad != 0x7fffffff) {
@@ -472,8 +470,7 @@ static int ddc_pass_run(int n, const int* ptr, const int* col, const double* val
   if (convert_any && nf > 0) {
     ddc_convert_kernel<<<nb, 256, 0, s>>>(nf, f_idx, ratio, cut, all, labels, ibuf + 1);
     AIRG_LAUNCH_CHECK();
-    AIRG_CUDA(cudaMemcpyAsync(&converted, ibuf + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
-    AIRG_CUDA(cudaStreamSynchronize(s));
+    AIRG_CUDA(read_back(&converted, ibuf + 1, sizeof(int), s));
   }
   release(f_idx, s);
   release(ratio, s);
@@ -628,8 +625,7 @@ int airg_repair_split(int n, const int32_t* ptr, const int32_t* col, int8_t* lab
   repair_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, ptr, col, (const signed char*)labels, tmp, ch);
   AIRG_LAUNCH_CHECK();
   AIRG_CUDA(cudaMemcpyAsync(labels, tmp, (size_t)n, cudaMemcpyDeviceToDevice, s));
-  AIRG_CUDA(cudaMemcpyAsync(changed_h, ch, sizeof(int), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
+  AIRG_CUDA(read_back(changed_h, ch, sizeof(int), s));
   release(tmp, s);
   release(ch, s);
   return AIRG_OK;
@@ -646,8 +642,7 @@ int airg_prolong_onepoint(int n, const int32_t* ptr, const int32_t* col, const d
                                                         pos, pcol, bad);
   AIRG_LAUNCH_CHECK();
   int b = 0;
-  AIRG_CUDA(cudaMemcpyAsync(&b, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(cudaStreamSynchronize(s));
+  AIRG_CUDA(read_back(&b, bad, sizeof(int), s));
   release(bad, s);
   if (b != 0x7fffffff) {
     set_error("fine point %d has no coupling to any coarse point; the splitting is invalid for "
