@@ -487,8 +487,7 @@ static int arnoldi_multi(int n, const int* p, const int* c, const double* v, con
     AIRG_LAUNCH_CHECK();
   }
   int ctlh[4];
-  AIRG_CUDA(cudaMemcpyAsync(H_h, Hd, (size_t)(m + 1) * m * sizeof(double), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(read_back(ctlh, ctl, sizeof ctlh, s));
+  AIRG_CUDA(read_back({{H_h, Hd, (size_t)(m + 1) * m * sizeof(double)}, {ctlh, ctl, sizeof ctlh}}, s));
   *k_h = ctlh[2];
   release(V, s);
   release(w, s);
@@ -612,8 +611,7 @@ static int arnoldi_grid(int n, const int* p, const int* c, const double* v, cons
   void* args[] = {&a};
   AIRG_CUDA(cudaLaunchCooperativeKernel((const void*)arnoldi_grid_kernel, np, 256, args, 0, s));
   int k = 0;
-  AIRG_CUDA(cudaMemcpyAsync(H_h, Hd, (size_t)(m + 1) * m * sizeof(double), cudaMemcpyDeviceToHost, s));
-  AIRG_CUDA(read_back(&k, info, sizeof(int), s));
+  AIRG_CUDA(read_back({{H_h, Hd, (size_t)(m + 1) * m * sizeof(double)}, {&k, info, sizeof(int)}}, s));
   *k_h = k;
   for (void* q : {(void*)V, (void*)w, (void*)sc, (void*)Hd, (void*)info}) release(q, s);
   return AIRG_OK;
@@ -691,9 +689,8 @@ extern "C" int airg_arnoldi(int n, const int32_t* p, const int32_t* c, const dou
       arnoldi_cta_kernel<256, 16><<<1, 256, shm, s>>>(n, p, c, v, b, m, V, w, H, info, dinfo, vsm);
     AIRG_LAUNCH_CHECK();
     int hi[2];
-    AIRG_CUDA(cudaMemcpyAsync(H_h, H, (size_t)(m + 1) * m * sizeof(double), cudaMemcpyDeviceToHost, s));
-    AIRG_CUDA(cudaMemcpyAsync(hi, info, sizeof hi, cudaMemcpyDeviceToHost, s));
-    AIRG_CUDA(read_back(beta_h, dinfo, sizeof(double), s));
+    AIRG_CUDA(read_back({{H_h, H, (size_t)(m + 1) * m * sizeof(double)}, {hi, info, sizeof hi},
+                         {beta_h, dinfo, sizeof(double)}}, s));
     for (void* q : {(void*)V, (void*)w, (void*)H, (void*)dinfo, (void*)info}) release(q, s);
     if (hi[1]) {
       set_error("cannot build a Krylov space from a zero vector");

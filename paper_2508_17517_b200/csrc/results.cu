@@ -284,8 +284,7 @@ extern "C" int airg_random_unit(uint64_t state_hi, uint64_t state_lo, uint64_t i
   div_by_norm_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, np, parts, out, parts + np);
   AIRG_LAUNCH_CHECK();
   if (norm_h) {
-    AIRG_CUDA(cudaMemcpyAsync(norm_h, parts + np, sizeof(double), cudaMemcpyDeviceToHost, s));
-    AIRG_CUDA(cudaStreamSynchronize(s));
+    AIRG_CUDA(read_back(norm_h, parts + np, sizeof(double), s));
   }
   release(parts, s);
   return AIRG_OK;

@@ -725,9 +725,9 @@ static int spgemm_rows(const Mat& A, const Mat& B, int negate, int mode, double 
                                                                          cmin, words, span_min_ub(), tot);
   AIRG_LAUNCH_CHECK();
   unsigned long long tot_h[3] = {0, 0, 0};
-  AIRG_CUDA(cudaMemcpyAsync(tot_h, tot, sizeof(tot_h), cudaMemcpyDeviceToHost, s));
   long long totw = 0;
-  AIRG_TRY(scan_counts64(words, bmoff, m, &totw, s));  // synchronises (tot_h too)
+  AIRG_TRY(scan_counts64(words, bmoff, m, nullptr, s));
+  AIRG_CUDA(read_back({{tot_h, tot, sizeof(tot_h)}, {&totw, bmoff + m, sizeof(long long)}}, s));
   release(tot, s);
   // mean B-row length of the span rows sets the numeric prefetch shape: rows
   // longer than 4 x 32 entries would run their tail with exposed latency

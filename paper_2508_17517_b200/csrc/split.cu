@@ -378,7 +378,6 @@ static int ddc_pass_run(int n, const int* ptr, const int* col, const double* val
   AIRG_LAUNCH_CHECK();
   // min / max / mean, read back with the zero-diagonal flag (one sync)
   int bad = 0;
-  AIRG_CUDA(cudaMemcpyAsync(&bad, ibuf, sizeof(int), cudaMemcpyDeviceToHost, s));
   double lo = 0, hi = 0, mean = 0;
   {
     double* mm = nullptr;
@@ -393,7 +392,7 @@ static int ddc_pass_run(int n, const int* ptr, const int* col, const double* val
     const int pb = blocks_for(nf, 256, 1024);
     sum_kernel<<<pb, 256, 0, s>>>(nf, ratio, mm + 2);
     std::vector<double> h(2 + pb);
-    AIRG_CUDA(read_back(h.data(), mm, (2 + pb) * sizeof(double), s));
+    AIRG_CUDA(read_back({{h.data(), mm, (2 + pb) * sizeof(double)}, {&bad, ibuf, sizeof(int)}}, s));
     cudaFreeAsync(tmp, s);
     release(mm, s);
     if (bad != 0x7fffffff) {
@@ -442,9 +441,7 @@ static int ddc_pass_run(int n, const int* ptr, const int* col, const double* val
     ddc_hist_kernel<<<blocks_for(nf, 256, num_sms() * 2), 256, shm, s>>>(nf, ratio, de, nbins + 1, hist);
     AIRG_LAUNCH_CHECK();
     std::vector<unsigned long long> hh(nbins + 2);
-    AIRG_CUDA(cudaMemcpyAsync(hh.data(), hist, (nbins + 2) * sizeof(unsigned long long),
-                              cudaMemcpyDeviceToHost, s));
-    AIRG_CUDA(cudaStreamSynchronize(s));
+    AIRG_CUDA(read_back(hh.data(), hist, (nbins + 2) * sizeof(unsigned long long), s));
     release(de, s);
     release(hist, s);
     // above_k = #{ratio > edge_k} = sum_{b > k} hist[b]
