@@ -57,3 +57,7 @@ def test_reference_arm_rank0_prints_contract_line(capsys):
         assert k in line
     assert line['impl'] == 'reference' and line['value'] > 0
     assert line['e2e']['h2d_bytes_per_step'] == 0
+    # whole-host time per step: value = sample DOFs / ms_per_step
+    n = A.cpu_nx * A.cpu_nx
+    assert abs(line['ms_per_step'] - n / line['value'] * 1e3) <= 1e-9 * line['ms_per_step']
+    assert line['samples_timed'] >= line['steps']
