@@ -359,7 +359,14 @@ template <class PM, int KP>
 #ifndef AIRG_POLY_MINB8
 #define AIRG_POLY_MINB8 6
 #endif
-__global__ void __launch_bounds__(128, KP == 8 ? AIRG_POLY_MINB8 : 1) poly_assemble_kernel(PolyArgs a) {
+// KP = 4 (65-128 entries): 8 CTAs per SM caps it at 63 registers (80 free),
+// no spills; polynomial phase 61.7-62.4 -> 60.2-61.0 ms (7 compiles the same;
+// 10 CTAs = 48 registers spills, 66.8 ms)
+#ifndef AIRG_POLY_MINB4
+#define AIRG_POLY_MINB4 8
+#endif
+__global__ void __launch_bounds__(128, KP == 8 ? AIRG_POLY_MINB8 : KP == 4 ? AIRG_POLY_MINB4 : 1)
+    poly_assemble_kernel(PolyArgs a) {
   extern __shared__ unsigned char smraw[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int cap = a.cap;
