@@ -365,7 +365,13 @@ template <class PM, int KP>
 #ifndef AIRG_POLY_MINB4
 #define AIRG_POLY_MINB4 8
 #endif
-__global__ void __launch_bounds__(128, KP == 8 ? AIRG_POLY_MINB8 : KP == 4 ? AIRG_POLY_MINB4 : 1)
+// KP = 1 / 2 (<= 64 entries): the same 8-CTA cap (48-56 registers, from
+// 61-76; no spills): polynomial phase 60.5 -> 59.0-59.6 ms at 2048², the DG
+// problem's 0.65 -> 0.63 s
+#ifndef AIRG_POLY_MINB21
+#define AIRG_POLY_MINB21 8
+#endif
+__global__ void __launch_bounds__(128, KP == 8 ? AIRG_POLY_MINB8 : KP == 4 ? AIRG_POLY_MINB4 : AIRG_POLY_MINB21)
     poly_assemble_kernel(PolyArgs a) {
   extern __shared__ unsigned char smraw[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
