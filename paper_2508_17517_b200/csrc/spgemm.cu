@@ -695,10 +695,12 @@ static const int kPolyBlockCap = getenv("AIRG_POLY_BLOCK_CAP") ? atoi(getenv("AI
 template <int G>
 // occupancy cap of the register assembly classes: 5 / 6 CTAs per SM measured
 // within noise of the setup; left free
-#ifndef AIRG_PSMALL_MINB
-#define AIRG_PSMALL_MINB 1
+#ifdef AIRG_PSMALL_MINB
+#define AIRG_PSMALL_BOUNDS __launch_bounds__(256, AIRG_PSMALL_MINB)
+#else
+#define AIRG_PSMALL_BOUNDS __launch_bounds__(256)
 #endif
-__global__ void __launch_bounds__(256, AIRG_PSMALL_MINB) poly_small_kernel(PolyArgs a) {
+__global__ void AIRG_PSMALL_BOUNDS poly_small_kernel(PolyArgs a) {
   const int lane = threadIdx.x & 31, j = lane & (G - 1), gbase = lane & ~(G - 1);
   const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << gbase;
   const long long groups = ((long long)gridDim.x * blockDim.x) / G;

@@ -454,11 +454,14 @@ struct RegArgs {
 
 // occupancy cap (CTAs/SM) of the register SpGEMM classes: 5 (48 registers,
 // small spills) measured within 1 ms of the setup, 6 spills more; left free
-#ifndef AIRG_REG_MINB
-#define AIRG_REG_MINB 1
+// (an explicit 1 is not the same: it lets ptxas take 80+ registers)
+#ifdef AIRG_REG_MINB
+#define AIRG_REG_BOUNDS __launch_bounds__(256, AIRG_REG_MINB)
+#else
+#define AIRG_REG_BOUNDS __launch_bounds__(256)
 #endif
 template <int G>
-__global__ void __launch_bounds__(256, AIRG_REG_MINB) spgemm_reg_kernel(RegArgs a) {
+__global__ void AIRG_REG_BOUNDS spgemm_reg_kernel(RegArgs a) {
   const int lane = threadIdx.x & 31, j = lane & (G - 1), gbase = lane & ~(G - 1);
   const unsigned gmask = G == 32 ? kFull : ((1u << G) - 1u) << gbase;
   const long long groups = ((long long)gridDim.x * blockDim.x) / G;
